@@ -1,0 +1,143 @@
+/*
+ * ffmin_b200.h -- C ABI of the B200 force-field energy / gradient engine.
+ *
+ * This is the drop-in boundary for the reference's hot path.  The reference
+ * (ffmin, pure Python + NumPy/numba) reaches its kernels through
+ * `KernelBackend` objects (ffmin/kernels.py:984-1024) whose functions the
+ * energy layer calls once per oracle evaluation (ffmin/energy.py:114-174,
+ * 284-313).  Every entry point below replaces one of those calls; the
+ * Python host package paper_1810_03358_b200 binds them with ctypes and
+ * passes PyTorch / NumPy buffers as plain pointers.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; `stream` is a cudaStream_t (NULL =
+ *     legacy default stream) passed as void*;
+ *   - pointers named *_d are device (HBM) pointers, *_h host pointers;
+ *   - coordinates are float64 (n, 3) row-major, as MolecularSystem.coords
+ *     (ffmin/model.py:224-231); gradients come back in the same layout;
+ *   - every function returns 0 on success and a negative FFM_E* code on
+ *     failure; ffm_last_error() describes the last failure of the calling
+ *     thread.  Geometry problems are NOT errors at this level: like the
+ *     reference kernels (ffmin/kernels.py:11-14) they are reported through
+ *     status words (index of the first bad term / pair, -1 when clean) and
+ *     the host layer raises EnergyEvaluationError.
+ */
+#ifndef FFMIN_B200_H
+#define FFMIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FFM_OK 0
+#define FFM_EINVAL (-1)   /* bad argument / validation failure */
+#define FFM_ECUDA (-2)    /* CUDA runtime error */
+#define FFM_ENOMEM (-3)   /* device allocation failed */
+
+/* kernel precision: ffmin's dtype argument (ffmin/energy.py:90-179) */
+#define FFM_F64 0  /* all arithmetic in FP64 */
+#define FFM_F32 1  /* pair arithmetic in FP32, accumulation in FP64 */
+
+/* evaluation flags */
+#define FFM_ENERGY 1
+#define FFM_GRAD 2
+#define FFM_NO_NB 4     /* skip the nonbonded terms (all pairs + scaled 1-4) */
+#define FFM_NO_TERMS 8  /* skip the bonded terms (stretch, bend, torsion)    */
+
+/* status words (int64[8] per evaluation) */
+#define FFM_ST_NB_BAD_I 0   /* first coincident nonbonded pair, -1 clean */
+#define FFM_ST_NB_BAD_J 1
+#define FFM_ST_BOND 2       /* first degenerate bond term (grad only)   */
+#define FFM_ST_ANGLE 3      /* first degenerate angle term              */
+#define FFM_ST_DIHEDRAL 4   /* first degenerate dihedral term           */
+#define FFM_STATUS_WORDS 8
+
+/* energies: double[5] = stretch, bend, torsion, coulomb, vdw (kJ/mol),
+ * the fields of ffmin.energy.EnergyBreakdown (ffmin/energy.py:30-41). */
+#define FFM_NTERMS 5
+
+typedef struct ffm_system ffm_system_t;
+
+const char* ffm_version(void);
+const char* ffm_last_error(void);
+
+/* Upload one molecular system (parameters + topology) to `device`.
+ * Replaces MolecularSystem.arrays() (ffmin/model.py:259-319): q/sigma/eps
+ * per atom, and the nonbonded policy as a sparse list of the pairs whose
+ * scale is not 1 (excluded pairs with s = 0, 1-4 pairs with s = s14) instead
+ * of the dense (n, n) matrix.  cutoff <= 0 means no cutoff. */
+int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q_h,
+                      const double* sigma_h, const double* eps_h, int64_t nspecial,
+                      const int64_t* special_i_h, const int64_t* special_j_h,
+                      const double* special_s_h, double cutoff);
+
+/* Bonded term tables, as MolecularSystem.arrays() bond_idx/bond_K/bond_r0,
+ * ang_idx/ang_K/ang_t0 (radians), dih_idx/dih_V (ffmin/model.py:273-288). */
+int ffm_system_set_terms(ffm_system_t* sys, int64_t nbond, const int64_t* bond_idx_h,
+                         const double* bond_K_h, const double* bond_r0_h, int64_t nangle,
+                         const int64_t* ang_idx_h, const double* ang_K_h,
+                         const double* ang_t0_h, int64_t ndih, const int64_t* dih_idx_h,
+                         const double* dih_V_h);
+
+int ffm_system_destroy(ffm_system_t* sys);
+
+/* info[0..7] = n, padded n, super-unit S, blocks, units, special tiles,
+ * scaled pairs, device */
+int ffm_system_info(const ffm_system_t* sys, int64_t* info_h);
+
+/* Full evaluation on device buffers (no host synchronisation):
+ * replaces energy_total / energy_and_gradient (ffmin/energy.py:133-174) and
+ * the KernelBackend nb_energy / nb_grad / *_grad calls they make.
+ * grad_d (n*3, overwritten) may be NULL without FFM_GRAD. */
+int ffm_eval(ffm_system_t* sys, int precision, int flags, const double* coords_d,
+             double* grad_d, double* energies_d, int64_t* status_d, void* stream);
+
+/* Same, through host buffers: copies in, evaluates, copies out and
+ * synchronises -- the reference-facing call a NumPy caller makes. */
+int ffm_eval_host(ffm_system_t* sys, int precision, int flags, const double* coords_h,
+                  double* grad_h, double* energies_h, int64_t* status_h);
+
+/* Energies of `batch` candidate geometries of the same system
+ * (coords_d: [batch][n][3]); energies_d: [batch][5]; status_d: [batch][8].
+ * The batched evaluator behind the gradient-free drivers (probe_full in
+ * ffmin/optimizers/wiggle.py:118-127). */
+int ffm_eval_batch(ffm_system_t* sys, int precision, int64_t batch, const double* coords_d,
+                   double* energies_d, int64_t* status_d, void* stream);
+
+/* Exact energy change of `ncand` single-atom moves of the current geometry
+ * (ffmin/energy.py:284-313, exact_delta_atom_move): atoms_d[k] moves to
+ * newpos_d[k][3].  out_d[k][5] = (coulomb, vdw, stretch, bend, torsion)
+ * deltas, status_d[k][3] = (first coincident partner j, first degenerate
+ * angle row, first degenerate dihedral row), -1 when clean. */
+int ffm_atom_delta(ffm_system_t* sys, const double* coords_d, int64_t ncand,
+                   const int32_t* atoms_d, const double* newpos_d, double* out_d,
+                   int64_t* status_d, void* stream);
+
+/* ---- optimiser vector algebra on device vectors (ffmin/optimizers) ---- */
+
+/* out_d[0] = <x, y>, deterministic fixed-order reduction.  scratch_d holds
+ * ffm_vec_scratch_doubles() doubles. */
+int64_t ffm_vec_scratch_doubles(void);
+int ffm_dot(int64_t n, const double* x_d, const double* y_d, double* out_d,
+            double* scratch_d, void* stream);
+
+/* z = sa * (a * x + b * y); a/b read from a_d/b_d when non-NULL, else a_h/b_h;
+ * y_d may be NULL. */
+int ffm_axpby(int64_t n, const double* a_d, double a_h, double sa, const double* x_d,
+              const double* b_d, double b_h, const double* y_d, double* z_d, void* stream);
+
+/* L-BFGS two-loop recursion (ffmin/optimizers/lbfgs.py:53-75) in one
+ * cooperative kernel.  S_d/Y_d: ring buffers [m][n]; order_h[count] ring
+ * slots newest first; rho_h[count] = 1/<s,y> in the same order.  d_d gets
+ * the raw direction -H g (count >= 1; count = 0 is the caller's normalised
+ * antigradient). */
+int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const double* rho_h,
+                       const double* S_d, const double* Y_d, const double* g_d, double* d_d,
+                       double* scratch_d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FFMIN_B200_H */

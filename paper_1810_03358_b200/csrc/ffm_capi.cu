@@ -1,0 +1,639 @@
+// ffm_capi.cu -- the extern "C" boundary (include/ffmin_b200.h): system
+// plans resident in HBM, workspace management and launch sequencing.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/ffmin_b200.h"
+#include "ffm_kernels.h"
+
+using namespace ffm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define FFM_CUDA(call)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(FFM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+template <typename T>
+int upload(T** dst, const std::vector<T>& src) {
+  *dst = nullptr;
+  if (src.empty()) return FFM_OK;
+  if (cudaMalloc(dst, src.size() * sizeof(T)) != cudaSuccess)
+    return fail(FFM_ENOMEM, "cudaMalloc failed for a system table");
+  FFM_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return FFM_OK;
+}
+
+struct Work {
+  void* pos = nullptr;     // [batch][np] Vec4
+  int pos_batch = 0;
+  void* ipart = nullptr;   // [nunits][3][S]
+  void* jpart = nullptr;
+  double* epart = nullptr; // [batch][nunits][3]
+  int e_batch = 0;
+  double* term_e = nullptr;  // [batch][nterm_e]
+  int te_batch = 0;
+  double* term_f = nullptr;  // [nslots][3]
+};
+
+}  // namespace
+
+struct ffm_system {
+  int device = 0;
+  NbPlanDev plan{};
+  TermPlanDev tp{};
+  int nspt = 0;
+  // device tables
+  int2* d_unit_rc = nullptr;
+  int* d_unit_index = nullptr;
+  int* d_spt_ptr = nullptr;
+  int* d_spt_m = nullptr;
+  uint32_t* d_spt_mask = nullptr;
+  int* d_sp_ptr = nullptr;   // upper special rows (finder)
+  int* d_sp_j = nullptr;
+  double* d_sp_s = nullptr;
+  int* d_fsp_ptr = nullptr;  // full special rows (atom delta)
+  int* d_fsp_j = nullptr;
+  double* d_fsp_s = nullptr;
+  double* d_qt = nullptr;    // q sqrt(C), [np]
+  float2* d_lj32 = nullptr;  // [np]
+  double2* d_lj64 = nullptr;
+  double* d_q = nullptr;
+  double* d_sigma = nullptr;
+  double* d_eps = nullptr;
+  int* d_sc_idx = nullptr;
+  double* d_sc_s = nullptr;
+  // bonded
+  int* d_bond_idx = nullptr;
+  double* d_bond_K = nullptr;
+  double* d_bond_r0 = nullptr;
+  int* d_ang_idx = nullptr;
+  double* d_ang_K = nullptr;
+  double* d_ang_t0 = nullptr;
+  int* d_dih_idx = nullptr;
+  double* d_dih_V = nullptr;
+  int* d_slot_ptr = nullptr;
+  int* d_slot_idx = nullptr;
+  int* d_aterm_ptr = nullptr;
+  int* d_aterm_idx = nullptr;
+  // host copies needed to rebuild the term plan
+  std::vector<std::pair<int, int>> scaled;  // (i, j)
+  std::vector<double> scaled_s;
+  Work w[2];  // [precision]
+  // host-path staging
+  double* h_coords_d = nullptr;
+  double* h_grad_d = nullptr;
+  double* h_en_d = nullptr;
+  int64_t* h_st_d = nullptr;
+};
+
+namespace {
+
+void free_all(ffm_system* s) {
+  void* ptrs[] = {s->d_unit_rc, s->d_unit_index, s->d_spt_ptr, s->d_spt_m, s->d_spt_mask,
+                  s->d_sp_ptr, s->d_sp_j, s->d_sp_s, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
+                  s->d_qt, s->d_lj32, s->d_lj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
+                  s->d_sc_s, s->d_bond_idx, s->d_bond_K, s->d_bond_r0, s->d_ang_idx,
+                  s->d_ang_K, s->d_ang_t0, s->d_dih_idx, s->d_dih_V, s->d_slot_ptr,
+                  s->d_slot_idx, s->d_aterm_ptr, s->d_aterm_idx, s->h_coords_d, s->h_grad_d,
+                  s->h_en_d, s->h_st_d};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& w : s->w) {
+    void* wp[] = {w.pos, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
+    for (void* p : wp)
+      if (p) cudaFree(p);
+  }
+}
+
+// Super-unit edge: the largest S that still gives >= 2048 units (about 3.5
+// CTAs per SM slot at 4 CTAs/SM), so the hardware block scheduler balances
+// the triangle; never below 256.
+int choose_S(int64_t n) {
+  for (int S : {1024, 512, 256}) {
+    const int64_t nb = (n + S - 1) / S;
+    if (nb * (nb + 1) / 2 >= 2048) return S;
+  }
+  return 256;
+}
+
+// rebuild the term plan device view (after set_terms or creation)
+int build_terms(ffm_system* s, int64_t nbond, const int64_t* bidx, const double* bK,
+                const double* br0, int64_t nang, const int64_t* aidx, const double* aK,
+                const double* at0, int64_t ndih, const int64_t* didx, const double* dV) {
+  const int n = s->plan.n;
+  TermPlanDev& tp = s->tp;
+  auto chk = [&](int64_t v) { return v >= 0 && v < n; };
+  std::vector<int> bi(2 * nbond), ai(3 * nang), di(4 * ndih);
+  for (int64_t k = 0; k < 2 * nbond; ++k) {
+    if (!chk(bidx[k])) return fail(FFM_EINVAL, "bond index out of range");
+    bi[k] = (int)bidx[k];
+  }
+  for (int64_t k = 0; k < 3 * nang; ++k) {
+    if (!chk(aidx[k])) return fail(FFM_EINVAL, "angle index out of range");
+    ai[k] = (int)aidx[k];
+  }
+  for (int64_t k = 0; k < 4 * ndih; ++k) {
+    if (!chk(didx[k])) return fail(FFM_EINVAL, "dihedral index out of range");
+    di[k] = (int)didx[k];
+  }
+  for (void* p : {(void*)s->d_bond_idx, (void*)s->d_bond_K, (void*)s->d_bond_r0,
+                  (void*)s->d_ang_idx, (void*)s->d_ang_K, (void*)s->d_ang_t0,
+                  (void*)s->d_dih_idx, (void*)s->d_dih_V, (void*)s->d_slot_ptr,
+                  (void*)s->d_slot_idx, (void*)s->d_aterm_ptr, (void*)s->d_aterm_idx})
+    if (p) cudaFree(p);
+  int rc;
+  if ((rc = upload(&s->d_bond_idx, bi))) return rc;
+  if ((rc = upload(&s->d_bond_K, std::vector<double>(bK, bK + nbond)))) return rc;
+  if ((rc = upload(&s->d_bond_r0, std::vector<double>(br0, br0 + nbond)))) return rc;
+  if ((rc = upload(&s->d_ang_idx, ai))) return rc;
+  if ((rc = upload(&s->d_ang_K, std::vector<double>(aK, aK + nang)))) return rc;
+  if ((rc = upload(&s->d_ang_t0, std::vector<double>(at0, at0 + nang)))) return rc;
+  if ((rc = upload(&s->d_dih_idx, di))) return rc;
+  if ((rc = upload(&s->d_dih_V, std::vector<double>(dV, dV + 4 * ndih)))) return rc;
+
+  const int nsc = (int)s->scaled.size();
+  tp.n = n;
+  tp.nbond = (int)nbond;
+  tp.nangle = (int)nang;
+  tp.ndih = (int)ndih;
+  tp.nscaled = nsc;
+  tp.bond_idx = s->d_bond_idx;
+  tp.bond_K = s->d_bond_K;
+  tp.bond_r0 = s->d_bond_r0;
+  tp.ang_idx = s->d_ang_idx;
+  tp.ang_K = s->d_ang_K;
+  tp.ang_t0 = s->d_ang_t0;
+  tp.dih_idx = s->d_dih_idx;
+  tp.dih_V = s->d_dih_V;
+  tp.sc_idx = s->d_sc_idx;
+  tp.sc_s = s->d_sc_s;
+  tp.q = s->d_q;
+  tp.sigma = s->d_sigma;
+  tp.eps = s->d_eps;
+  tp.slot_angle0 = 2 * (int)nbond;
+  tp.slot_dih0 = tp.slot_angle0 + 3 * (int)nang;
+  tp.slot_sc0 = tp.slot_dih0 + 4 * (int)ndih;
+  tp.nslots = tp.slot_sc0 + 2 * nsc;
+  tp.e_angle0 = (int)nbond;
+  tp.e_dih0 = tp.e_angle0 + (int)nang;
+  tp.e_scc0 = tp.e_dih0 + (int)ndih;
+  tp.e_scv0 = tp.e_scc0 + nsc;
+  tp.nterm_e = tp.e_scv0 + nsc;
+
+  // atom -> slot CSR in slot order (fixed summation order of the gather)
+  std::vector<std::vector<int>> slots(n);
+  for (int t = 0; t < nbond; ++t)
+    for (int q = 0; q < 2; ++q) slots[bi[2 * t + q]].push_back(2 * t + q);
+  for (int t = 0; t < nang; ++t)
+    for (int q = 0; q < 3; ++q) slots[ai[3 * t + q]].push_back(tp.slot_angle0 + 3 * t + q);
+  for (int t = 0; t < ndih; ++t)
+    for (int q = 0; q < 4; ++q) slots[di[4 * t + q]].push_back(tp.slot_dih0 + 4 * t + q);
+  for (int t = 0; t < nsc; ++t) {
+    slots[s->scaled[t].first].push_back(tp.slot_sc0 + 2 * t);
+    slots[s->scaled[t].second].push_back(tp.slot_sc0 + 2 * t + 1);
+  }
+  std::vector<int> sptr(n + 1, 0), sidx;
+  for (int a = 0; a < n; ++a) {
+    std::sort(slots[a].begin(), slots[a].end());
+    sptr[a + 1] = sptr[a] + (int)slots[a].size();
+    sidx.insert(sidx.end(), slots[a].begin(), slots[a].end());
+  }
+  if ((rc = upload(&s->d_slot_ptr, sptr))) return rc;
+  if ((rc = upload(&s->d_slot_idx, sidx))) return rc;
+  // atom -> bonded term ids (ffmin/model.py:321-347 atom_terms)
+  std::vector<std::vector<int>> at(n);
+  for (int t = 0; t < nbond; ++t)
+    for (int q = 0; q < 2; ++q) at[bi[2 * t + q]].push_back(t);
+  for (int t = 0; t < nang; ++t)
+    for (int q = 0; q < 3; ++q) at[ai[3 * t + q]].push_back((int)nbond + t);
+  for (int t = 0; t < ndih; ++t)
+    for (int q = 0; q < 4; ++q) at[di[4 * t + q]].push_back((int)(nbond + nang) + t);
+  std::vector<int> aptr(n + 1, 0), aidx2;
+  for (int a = 0; a < n; ++a) {
+    aptr[a + 1] = aptr[a] + (int)at[a].size();
+    aidx2.insert(aidx2.end(), at[a].begin(), at[a].end());
+  }
+  if ((rc = upload(&s->d_aterm_ptr, aptr))) return rc;
+  if ((rc = upload(&s->d_aterm_idx, aidx2))) return rc;
+  // term workspaces are sized by the term plan: drop them
+  for (auto& w : s->w) {
+    if (w.term_e) cudaFree(w.term_e);
+    if (w.term_f) cudaFree(w.term_f);
+    w.term_e = nullptr;
+    w.term_f = nullptr;
+    w.te_batch = 0;
+  }
+  return FFM_OK;
+}
+
+// allocate / grow the workspace of one precision
+int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
+  Work& w = s->w[prec];
+  const bool f64 = prec == FFM_F64;
+  const NbPlanDev& p = s->plan;
+  const size_t tsz = f64 ? 8 : 4;
+  if (w.pos_batch < batch) {
+    if (w.pos) cudaFree(w.pos);
+    w.pos = nullptr;
+    const size_t bytes = (size_t)batch * p.np * 4 * tsz;
+    if (cudaMalloc(&w.pos, bytes) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for packed coordinates");
+    w.pos_batch = batch;
+    FFM_CUDA(launch_pad(p.n, p.np, batch, f64, w.pos, 0));
+    FFM_CUDA(cudaDeviceSynchronize());
+  }
+  if (grad && !w.ipart) {
+    const size_t bytes = (size_t)p.nunits * 3 * p.S * tsz;
+    if (cudaMalloc(&w.ipart, bytes) != cudaSuccess || cudaMalloc(&w.jpart, bytes) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for gradient partials");
+  }
+  if (w.e_batch < batch) {
+    if (w.epart) cudaFree(w.epart);
+    w.epart = nullptr;
+    if (cudaMalloc(&w.epart, (size_t)batch * p.nunits * 3 * sizeof(double)) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for energy partials");
+    w.e_batch = batch;
+  }
+  if (w.te_batch < batch) {
+    if (w.term_e) cudaFree(w.term_e);
+    w.term_e = nullptr;
+    const size_t ne = std::max(1, s->tp.nterm_e);
+    if (cudaMalloc(&w.term_e, (size_t)batch * ne * sizeof(double)) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for term energies");
+    w.te_batch = batch;
+  }
+  if (grad && !w.term_f) {
+    const size_t nsl = std::max(1, s->tp.nslots);
+    if (cudaMalloc(&w.term_f, nsl * 3 * sizeof(double)) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for term forces");
+  }
+  return FFM_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ffm_version(void) { return "ffmin_b200 0.1.0 (sm_100a)"; }
+const char* ffm_last_error(void) { return g_err.c_str(); }
+
+int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q_h,
+                      const double* sigma_h, const double* eps_h, int64_t nspecial,
+                      const int64_t* special_i_h, const int64_t* special_j_h,
+                      const double* special_s_h, double cutoff) {
+  if (!out) return fail(FFM_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || n > (1LL << 26)) return fail(FFM_EINVAL, "atom count out of range");
+  if (n > 0 && (!q_h || !sigma_h || !eps_h)) return fail(FFM_EINVAL, "parameter array is NULL");
+  if (nspecial < 0 || (nspecial > 0 && (!special_i_h || !special_j_h || !special_s_h)))
+    return fail(FFM_EINVAL, "special pair arrays are NULL");
+  FFM_CUDA(cudaSetDevice(device));
+  DeviceGuard guard(device);
+  auto* s = new ffm_system();
+  s->device = device;
+  NbPlanDev& p = s->plan;
+  p.n = (int)n;
+  p.S = choose_S(n);
+  p.nb = (int)std::max<int64_t>(1, (n + p.S - 1) / p.S);
+  p.np = p.nb * p.S;
+  p.nunits = p.nb * (p.nb + 1) / 2;
+  p.has_cutoff = cutoff > 0.0 ? 1 : 0;
+  p.cut2 = cutoff > 0.0 ? cutoff * cutoff : 0.0;
+  int rc;
+#define FFM_TRY(x)     \
+  do {                 \
+    rc = (x);          \
+    if (rc) {          \
+      free_all(s);     \
+      delete s;        \
+      return rc;       \
+    }                  \
+  } while (0)
+
+  // ---- per-atom records (padding atoms keep zero charge / LJ)
+  std::vector<double> qt(p.np, 0.0), qv(q_h, q_h + n), sg(sigma_h, sigma_h + n),
+      ep(eps_h, eps_h + n);
+  std::vector<float2> lj32(p.np, make_float2(0.f, 0.f));
+  std::vector<double2> lj64(p.np, make_double2(0.0, 0.0));
+  const double sqc = std::sqrt(kCoulomb);
+  for (int64_t a = 0; a < n; ++a) {
+    if (!(sigma_h[a] > 0.0) || !(eps_h[a] >= 0.0) || !std::isfinite(q_h[a]))
+      FFM_TRY(fail(FFM_EINVAL, "atom parameters invalid (sigma > 0, eps >= 0, finite q)"));
+    qt[a] = q_h[a] * sqc;
+    const double se = 2.0 * std::sqrt(eps_h[a]);
+    const double s3 = sigma_h[a] * sigma_h[a] * sigma_h[a];
+    lj64[a] = make_double2(se * s3 * s3, se * s3);
+    lj32[a] = make_float2((float)lj64[a].x, (float)lj64[a].y);
+  }
+  FFM_TRY(upload(&s->d_qt, qt));
+  FFM_TRY(upload(&s->d_lj32, lj32));
+  FFM_TRY(upload(&s->d_lj64, lj64));
+  FFM_TRY(upload(&s->d_q, qv));
+  FFM_TRY(upload(&s->d_sigma, sg));
+  FFM_TRY(upload(&s->d_eps, ep));
+
+  // ---- special pairs: canonical (i < j), sorted, unique
+  std::vector<std::tuple<int, int, double>> sp;
+  sp.reserve(nspecial);
+  for (int64_t k = 0; k < nspecial; ++k) {
+    int64_t i = special_i_h[k], j = special_j_h[k];
+    if (i == j || i < 0 || j < 0 || i >= n || j >= n)
+      FFM_TRY(fail(FFM_EINVAL, "special pair index out of range or i == j"));
+    if (i > j) std::swap(i, j);
+    if (!std::isfinite(special_s_h[k]))
+      FFM_TRY(fail(FFM_EINVAL, "special pair scale not finite"));
+    if (special_s_h[k] == 1.0) continue;  // same as the default
+    sp.emplace_back((int)i, (int)j, special_s_h[k]);
+  }
+  std::sort(sp.begin(), sp.end());
+  for (size_t k = 1; k < sp.size(); ++k)
+    if (std::get<0>(sp[k]) == std::get<0>(sp[k - 1]) && std::get<1>(sp[k]) == std::get<1>(sp[k - 1]))
+      FFM_TRY(fail(FFM_EINVAL, "duplicate special pair"));
+
+  // upper rows (finder) and full rows (atom delta)
+  std::vector<int> sp_ptr(n + 1, 0), sp_j;
+  std::vector<double> sp_s;
+  std::vector<std::vector<std::pair<int, double>>> full(n);
+  for (auto& e : sp) {
+    sp_ptr[std::get<0>(e) + 1]++;
+    full[std::get<0>(e)].emplace_back(std::get<1>(e), std::get<2>(e));
+    full[std::get<1>(e)].emplace_back(std::get<0>(e), std::get<2>(e));
+  }
+  for (int64_t a = 0; a < n; ++a) sp_ptr[a + 1] += sp_ptr[a];
+  for (auto& e : sp) {
+    sp_j.push_back(std::get<1>(e));
+    sp_s.push_back(std::get<2>(e));
+  }
+  std::vector<int> fptr(n + 1, 0), fj;
+  std::vector<double> fs;
+  for (int64_t a = 0; a < n; ++a) {
+    std::sort(full[a].begin(), full[a].end());
+    fptr[a + 1] = fptr[a] + (int)full[a].size();
+    for (auto& e : full[a]) {
+      fj.push_back(e.first);
+      fs.push_back(e.second);
+    }
+  }
+  if (n == 0) sp_ptr.assign(1, 0), fptr.assign(1, 0);
+  FFM_TRY(upload(&s->d_sp_ptr, sp_ptr));
+  FFM_TRY(upload(&s->d_sp_j, sp_j));
+  FFM_TRY(upload(&s->d_sp_s, sp_s));
+  FFM_TRY(upload(&s->d_fsp_ptr, fptr));
+  FFM_TRY(upload(&s->d_fsp_j, fj));
+  FFM_TRY(upload(&s->d_fsp_s, fs));
+
+  // ---- tile masks for the dense sweep, and the scaled list
+  const int nsub = p.np / kIB, njbt = p.np / kJB;
+  std::map<int64_t, std::vector<uint32_t>> tiles;
+  for (auto& e : sp) {
+    const int i = std::get<0>(e), j = std::get<1>(e);
+    const int64_t key = (int64_t)(i / kIB) * njbt + j / kJB;
+    auto& m = tiles[key];
+    if (m.empty()) m.assign(kIB, 0u);
+    m[i % kIB] |= 1u << (j % kJB);
+    if (std::get<2>(e) != 0.0) {
+      s->scaled.emplace_back(i, j);
+      s->scaled_s.push_back(std::get<2>(e));
+    }
+  }
+  std::vector<int> spt_ptr(nsub + 1, 0), spt_m;
+  std::vector<uint32_t> spt_mask;
+  for (auto& kv : tiles) {
+    const int k = (int)(kv.first / njbt), m = (int)(kv.first % njbt);
+    spt_ptr[k + 1]++;
+    spt_m.push_back(m);
+    spt_mask.insert(spt_mask.end(), kv.second.begin(), kv.second.end());
+  }
+  for (int k = 0; k < nsub; ++k) spt_ptr[k + 1] += spt_ptr[k];
+  s->nspt = (int)spt_m.size();
+  FFM_TRY(upload(&s->d_spt_ptr, spt_ptr));
+  FFM_TRY(upload(&s->d_spt_m, spt_m));
+  FFM_TRY(upload(&s->d_spt_mask, spt_mask));
+  std::vector<int> scidx;
+  for (auto& e : s->scaled) {
+    scidx.push_back(e.first);
+    scidx.push_back(e.second);
+  }
+  FFM_TRY(upload(&s->d_sc_idx, scidx));
+  FFM_TRY(upload(&s->d_sc_s, s->scaled_s));
+
+  // ---- units: off-diagonal first (full work), diagonal last (half work)
+  std::vector<int2> urc;
+  std::vector<int> uidx((size_t)p.nb * p.nb, -1);
+  for (int r = 0; r < p.nb; ++r)
+    for (int c = r + 1; c < p.nb; ++c) urc.push_back(make_int2(r, c));
+  for (int r = 0; r < p.nb; ++r) urc.push_back(make_int2(r, r));
+  for (size_t u = 0; u < urc.size(); ++u) uidx[(size_t)urc[u].x * p.nb + urc[u].y] = (int)u;
+  FFM_TRY(upload(&s->d_unit_rc, urc));
+  FFM_TRY(upload(&s->d_unit_index, uidx));
+  p.unit_rc = s->d_unit_rc;
+  p.spt_ptr = s->d_spt_ptr;
+  p.spt_m = s->d_spt_m;
+  p.spt_mask = s->d_spt_mask;
+
+  s->tp.has_cutoff = p.has_cutoff;
+  s->tp.cutoff = cutoff > 0.0 ? cutoff : 0.0;
+  FFM_TRY(build_terms(s, 0, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0,
+                      nullptr, nullptr));
+#undef FFM_TRY
+  *out = s;
+  return FFM_OK;
+}
+
+int ffm_system_set_terms(ffm_system_t* s, int64_t nbond, const int64_t* bond_idx_h,
+                         const double* bond_K_h, const double* bond_r0_h, int64_t nangle,
+                         const int64_t* ang_idx_h, const double* ang_K_h,
+                         const double* ang_t0_h, int64_t ndih, const int64_t* dih_idx_h,
+                         const double* dih_V_h) {
+  if (!s) return fail(FFM_EINVAL, "system is NULL");
+  if (nbond < 0 || nangle < 0 || ndih < 0) return fail(FFM_EINVAL, "negative term count");
+  if ((nbond && (!bond_idx_h || !bond_K_h || !bond_r0_h)) ||
+      (nangle && (!ang_idx_h || !ang_K_h || !ang_t0_h)) || (ndih && (!dih_idx_h || !dih_V_h)))
+    return fail(FFM_EINVAL, "term array is NULL");
+  DeviceGuard guard(s->device);
+  return build_terms(s, nbond, bond_idx_h, bond_K_h, bond_r0_h, nangle, ang_idx_h, ang_K_h,
+                     ang_t0_h, ndih, dih_idx_h, dih_V_h);
+}
+
+int ffm_system_destroy(ffm_system_t* s) {
+  if (!s) return FFM_OK;
+  DeviceGuard guard(s->device);
+  cudaDeviceSynchronize();
+  free_all(s);
+  delete s;
+  return FFM_OK;
+}
+
+int ffm_system_info(const ffm_system_t* s, int64_t* info) {
+  if (!s || !info) return fail(FFM_EINVAL, "NULL argument");
+  info[0] = s->plan.n;
+  info[1] = s->plan.np;
+  info[2] = s->plan.S;
+  info[3] = s->plan.nb;
+  info[4] = s->plan.nunits;
+  info[5] = s->nspt;
+  info[6] = (int64_t)s->scaled.size();
+  info[7] = s->device;
+  return FFM_OK;
+}
+
+int ffm_eval(ffm_system_t* s, int precision, int flags, const double* coords_d,
+             double* grad_d, double* energies_d, int64_t* status_d, void* stream) {
+  if (!s || !energies_d || !status_d) return fail(FFM_EINVAL, "NULL argument");
+  if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
+  const bool grad = (flags & FFM_GRAD) != 0;
+  if (grad && !grad_d) return fail(FFM_EINVAL, "grad_d is NULL with FFM_GRAD");
+  if (s->plan.n > 0 && !coords_d) return fail(FFM_EINVAL, "coords_d is NULL");
+  DeviceGuard guard(s->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = ensure_work(s, precision, 1, grad);
+  if (rc) return rc;
+  Work& w = s->w[precision];
+  const bool f64 = precision == FFM_F64;
+  const bool do_nb = !(flags & FFM_NO_NB), do_terms = !(flags & FFM_NO_TERMS);
+  const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
+  TermPlanDev tp = s->tp;  // the term types this call evaluates
+  if (!do_terms) tp.nbond = tp.nangle = tp.ndih = 0;
+  if (!do_nb) tp.nscaled = 0;
+  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, status_d, st));
+  if (do_nb) FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipart, w.jpart, w.epart, 1, st));
+  FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
+  if (grad && s->plan.n > 0)
+    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart,
+                             w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
+                             s->tp.slot_sc0, do_nb, do_terms, grad_d, st));
+  FFM_CUDA(launch_reduce(do_nb ? s->plan.nunits : 0, tp, 1, w.epart, w.term_e, energies_d,
+                         status_d, st));
+  FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
+                         s->d_sp_j, s->d_sp_s, status_d, st));
+  return FFM_OK;
+}
+
+int ffm_eval_host(ffm_system_t* s, int precision, int flags, const double* coords_h,
+                  double* grad_h, double* energies_h, int64_t* status_h) {
+  if (!s || !energies_h || !status_h) return fail(FFM_EINVAL, "NULL argument");
+  const bool grad = (flags & FFM_GRAD) != 0;
+  if (grad && !grad_h) return fail(FFM_EINVAL, "grad_h is NULL with FFM_GRAD");
+  DeviceGuard guard(s->device);
+  const size_t cb = (size_t)std::max(1, s->plan.n) * 3 * sizeof(double);
+  if (!s->h_coords_d) {
+    if (cudaMalloc(&s->h_coords_d, cb) != cudaSuccess || cudaMalloc(&s->h_grad_d, cb) != cudaSuccess ||
+        cudaMalloc(&s->h_en_d, FFM_NTERMS * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&s->h_st_d, FFM_STATUS_WORDS * sizeof(int64_t)) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for host-path staging");
+  }
+  const size_t nb = (size_t)s->plan.n * 3 * sizeof(double);
+  if (nb) FFM_CUDA(cudaMemcpyAsync(s->h_coords_d, coords_h, nb, cudaMemcpyHostToDevice, 0));
+  int rc = ffm_eval(s, precision, flags, s->h_coords_d, grad ? s->h_grad_d : nullptr,
+                    s->h_en_d, s->h_st_d, nullptr);
+  if (rc) return rc;
+  if (grad && nb) FFM_CUDA(cudaMemcpyAsync(grad_h, s->h_grad_d, nb, cudaMemcpyDeviceToHost, 0));
+  FFM_CUDA(cudaMemcpyAsync(energies_h, s->h_en_d, FFM_NTERMS * sizeof(double),
+                           cudaMemcpyDeviceToHost, 0));
+  FFM_CUDA(cudaMemcpyAsync(status_h, s->h_st_d, FFM_STATUS_WORDS * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, 0));
+  FFM_CUDA(cudaStreamSynchronize(0));
+  return FFM_OK;
+}
+
+int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* coords_d,
+                   double* energies_d, int64_t* status_d, void* stream) {
+  if (!s || !energies_d || !status_d) return fail(FFM_EINVAL, "NULL argument");
+  if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
+  if (batch < 1 || batch > 65535) return fail(FFM_EINVAL, "batch must be in [1, 65535]");
+  if (s->plan.n > 0 && !coords_d) return fail(FFM_EINVAL, "coords_d is NULL");
+  DeviceGuard guard(s->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = ensure_work(s, precision, (int)batch, false);
+  if (rc) return rc;
+  Work& w = s->w[precision];
+  const bool f64 = precision == FFM_F64;
+  const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
+  const int B = (int)batch;
+  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, B, f64, coords_d, s->d_qt, w.pos, status_d, st));
+  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, nullptr, nullptr, w.epart, B, st));
+  FFM_CUDA(launch_terms(s->tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
+  FFM_CUDA(launch_reduce(s->plan.nunits, s->tp, B, w.epart, w.term_e, energies_d, status_d, st));
+  FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
+                         s->d_sp_s, status_d, st));
+  return FFM_OK;
+}
+
+int ffm_atom_delta(ffm_system_t* s, const double* coords_d, int64_t ncand,
+                   const int32_t* atoms_d, const double* newpos_d, double* out_d,
+                   int64_t* status_d, void* stream) {
+  if (!s) return fail(FFM_EINVAL, "system is NULL");
+  if (ncand < 0 || ncand > (1LL << 30)) return fail(FFM_EINVAL, "bad candidate count");
+  if (ncand == 0) return FFM_OK;
+  if (!coords_d || !atoms_d || !newpos_d || !out_d || !status_d)
+    return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(s->device);
+  FFM_CUDA(launch_atom_delta(s->tp, coords_d, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
+                             s->d_aterm_ptr, s->d_aterm_idx, (int)ncand, atoms_d, newpos_d,
+                             out_d, status_d, static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+int64_t ffm_vec_scratch_doubles(void) {
+  return (int64_t)std::max<size_t>(two_loop_scratch_doubles(), (size_t)vec_reduce_blocks());
+}
+
+int ffm_dot(int64_t n, const double* x_d, const double* y_d, double* out_d, double* scratch_d,
+            void* stream) {
+  if (n < 0 || !out_d || !scratch_d || (n > 0 && (!x_d || !y_d)))
+    return fail(FFM_EINVAL, "bad dot arguments");
+  FFM_CUDA(launch_dot(n, x_d, y_d, scratch_d, out_d, static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+int ffm_axpby(int64_t n, const double* a_d, double a_h, double sa, const double* x_d,
+              const double* b_d, double b_h, const double* y_d, double* z_d, void* stream) {
+  if (n < 0 || (n > 0 && (!x_d || !z_d))) return fail(FFM_EINVAL, "bad axpby arguments");
+  if (n == 0) return FFM_OK;
+  FFM_CUDA(launch_axpby(n, a_d, a_h, sa, x_d, b_d, b_h, y_d, z_d,
+                        static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const double* rho_h,
+                       const double* S_d, const double* Y_d, const double* g_d, double* d_d,
+                       double* scratch_d, void* stream) {
+  if (n < 1 || count < 1 || count > kMaxLbfgsPairs || !order_h || !rho_h || !S_d || !Y_d ||
+      !g_d || !d_d || !scratch_d)
+    return fail(FFM_EINVAL, "bad two-loop arguments");
+  FFM_CUDA(launch_lbfgs_two_loop(n, count, order_h, rho_h, S_d, Y_d, g_d, d_d, scratch_d,
+                                 static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+}  // extern "C"

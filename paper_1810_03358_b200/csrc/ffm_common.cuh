@@ -1,0 +1,122 @@
+// ffm_common.cuh -- shared definitions for the B200 force-field kernels.
+//
+// Packed-arithmetic layer: the O(N^2) pair kernel is issue-slot bound on the
+// FP32 pipe, so its inner loop is written on Blackwell's packed f32x2
+// instructions (FADD2/FMUL2/FFMA2: two FP32 lanes per issue slot, same
+// 128 FMA/clk/SM pipe rate, see profiles/r01_pipes_microbench.txt).  The
+// same kernel templates instantiate on double with a plain two-lane struct,
+// so FP32 and FP64 modes share one tiling/reduction structure.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ffm {
+
+// ffmin/constants.py:10, 13, 16
+constexpr double kCoulomb = 1389.38757;
+constexpr double kRmin = 1e-12;
+constexpr double kDegenerateEps = 1e-12;
+
+// Pair-kernel tiling:
+//   a warp tile is 128 i-atoms (4 per lane, two packed pairs) x 32 j-atoms;
+//   a CTA is 4 warps and owns one super-unit of S x S atoms.
+constexpr int kWarps = 4;
+constexpr int kThreads = kWarps * 32;
+constexpr int kIB = 128;  // i-sub-block
+constexpr int kJB = 32;   // j-block
+
+// ------------------------------------------------------------ packed math
+template <typename T> struct Pk;
+
+template <> struct Pk<float> {
+  using V = uint64_t;  // two fp32 lanes in one 64-bit register pair
+  static __device__ __forceinline__ V make(float a, float b) {
+    V r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+  }
+  static __device__ __forceinline__ V bc(float a) { return make(a, a); }
+  static __device__ __forceinline__ float lo(V v) {
+    return __uint_as_float((unsigned)(v & 0xffffffffull));
+  }
+  static __device__ __forceinline__ float hi(V v) { return __uint_as_float((unsigned)(v >> 32)); }
+  static __device__ __forceinline__ V add(V a, V b) {
+    V d;
+    asm("add.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  }
+  static __device__ __forceinline__ V mul(V a, V b) {
+    V d;
+    asm("mul.rn.ftz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+  }
+  static __device__ __forceinline__ V fma(V a, V b, V c) {
+    V d;
+    asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+  }
+  // MUFU.RSQ on each lane (no packed form exists)
+  static __device__ __forceinline__ V rsqrt(V v) {
+    float a, b;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+    float ra, rb;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(a));
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(b));
+    return make(ra, rb);
+  }
+  static __device__ __forceinline__ V zero() { return 0ull; }
+};
+
+struct D2 {
+  double x, y;
+};
+
+template <> struct Pk<double> {
+  using V = D2;
+  static __device__ __forceinline__ V make(double a, double b) { return {a, b}; }
+  static __device__ __forceinline__ V bc(double a) { return {a, a}; }
+  static __device__ __forceinline__ double lo(V v) { return v.x; }
+  static __device__ __forceinline__ double hi(V v) { return v.y; }
+  static __device__ __forceinline__ V add(V a, V b) { return {a.x + b.x, a.y + b.y}; }
+  static __device__ __forceinline__ V mul(V a, V b) { return {a.x * b.x, a.y * b.y}; }
+  static __device__ __forceinline__ V fma(V a, V b, V c) {
+    return {::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y)};
+  }
+  // MUFU.RSQ64H seed + one Newton step: relative error ~1e-14
+  static __device__ __forceinline__ double rsqrt1(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double h = x * y;
+    double e = ::fma(-h, y, 1.0);
+    return ::fma(0.5 * y, e, y);
+  }
+  static __device__ __forceinline__ V rsqrt(V v) { return {rsqrt1(v.x), rsqrt1(v.y)}; }
+  static __device__ __forceinline__ V zero() { return {0.0, 0.0}; }
+};
+
+// Atom records in HBM (padded to the super-unit size):
+//   pos[a] = (x, y, z, q~)   with q~ = q * sqrt(C) so q~_i q~_j = C q_i q_j
+//   lj[a]  = (a_i, b_i)      with a_i = 2 sqrt(eps_i) sigma_i^6,
+//                                 b_i = 2 sqrt(eps_i) sigma_i^3
+// so the geometric-mean LJ of ffmin/kernels.py:340-344 factorises:
+//   4 eps_ij (sig_ij/r)^12 = a_i a_j / r^12,  4 eps_ij (sig_ij/r)^6 = b_i b_j / r^6.
+template <typename T> struct Vec4T;
+template <> struct Vec4T<float> { using type = float4; };
+template <> struct Vec4T<double> { using type = double4; };
+template <typename T> struct Vec2T;
+template <> struct Vec2T<float> { using type = float2; };
+template <> struct Vec2T<double> { using type = double2; };
+
+// Status words written by the kernels (device int64[kStatusWords]).
+enum StatusSlot : int {
+  kStNbBadI = 0,      // first coincident nonbonded pair (i, j), -1 clean
+  kStNbBadJ = 1,
+  kStBond = 2,        // first degenerate bond term, -1 clean
+  kStAngle = 3,
+  kStDihedral = 4,
+  kStNbSuspect = 5,   // set when the pair sweep saw a possible coincidence
+  kStNbKey = 6,       // scratch: min (i * n + j) over coincident pairs
+  kStWords = 8
+};
+
+}  // namespace ffm

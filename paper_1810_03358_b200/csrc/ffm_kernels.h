@@ -1,0 +1,69 @@
+// ffm_kernels.h -- host-side launch wrappers shared by the C-ABI layer.
+#pragma once
+#include "ffm_common.cuh"
+#include "ffm_plan.cuh"
+
+namespace ffm {
+
+size_t nb_smem_bytes(int S, bool fp64, bool grad);
+
+// all-pairs sweep over every super-unit; batch > 1 only without GRAD
+cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
+                      const void* lj, void* ipart, void* jpart, double* epart, int batch,
+                      cudaStream_t st);
+
+// coords (fp64, [batch][n][3]) -> padded pos records of the chosen precision;
+// also resets the status words of every batch entry.
+cudaError_t launch_pack(int n, int np, int batch, bool fp64, const double* coords,
+                        const double* qt, void* pos, int64_t* status, cudaStream_t st);
+
+// fills the padding atoms (zero charge / LJ, far apart) once per buffer
+cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, cudaStream_t st);
+
+// bonded + scaled-pair terms in FP64; writes term energies, slot forces
+cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,
+                         double* term_e, double* term_f, int64_t* status, cudaStream_t st);
+
+// gradient[a] = sum of nonbonded partials + incident term slots, fixed order
+// use_nb: add the pair partials and the scaled-pair slots; use_terms: add
+// the bonded slots (slots below slot_sc0)
+cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
+                            const void* ipart, const void* jpart, const int* slot_ptr,
+                            const int* slot_idx, const double* term_f, int slot_sc0,
+                            bool use_nb, bool use_terms, double* grad, cudaStream_t st);
+
+// energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
+// coincidences for the finder
+cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
+                          const double* term_e, double* energies, int64_t* status,
+                          cudaStream_t st);
+
+// exact first coincident pair (reference loop order), only when flagged;
+// then converts the status sentinels to -1.
+cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
+                          const int* sp_ptr, const int* sp_j, const double* sp_s,
+                          int64_t* status, cudaStream_t st);
+
+// exact single-atom move deltas (ffmin/energy.py:284-313) for a batch of
+// candidate moves: out[k][5] = (coulomb, vdw, stretch, bend, torsion) deltas;
+// status[k][3] = (bad nonbonded partner j, bad angle row, bad dihedral row)
+cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
+                              const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
+                              const int* aterm_ptr, const int* aterm_idx, int ncand,
+                              const int* atoms, const double* newpos, double* out,
+                              int64_t* status, cudaStream_t st);
+
+// ---- vector algebra (ffm_vec.cu) ----
+int vec_reduce_blocks();
+cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,
+                       double* out, cudaStream_t st);
+cudaError_t launch_axpby(int64_t n, const double* a_dev, double a_host, double sa,
+                         const double* x, const double* b_dev, double b_host,
+                         const double* y, double* z, cudaStream_t st);
+constexpr int kMaxLbfgsPairs = 32;
+size_t two_loop_scratch_doubles();
+cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const double* rho,
+                                  const double* S, const double* Y, const double* g,
+                                  double* q, double* scratch, cudaStream_t st);
+
+}  // namespace ffm

@@ -1,0 +1,338 @@
+// ffm_pairs.cu -- the O(N^2) nonbonded energy / gradient sweep.
+//
+// Restates ffmin/kernels.py:285-356 (_loop_nb_energy / _loop_nb_grad) for
+// sm_100a.  Each unordered pair i < j is evaluated once (Newton's third law):
+//
+//   * a warp owns a 128 x 32 tile: every lane holds 4 i-atoms in registers
+//     (two packed f32x2 pairs) and walks the 32 j-atoms of the tile along a
+//     rotated diagonal, j = (lane + t) mod 32, reading them from shared memory
+//     without bank conflicts; the j-gradient accumulator travels with j
+//     through one lane shuffle per step, so no atomics are needed;
+//   * a CTA (4 warps) owns an S x S super-unit of the upper triangle; its
+//     i-gradient rows are reduced across warps in shared memory and its
+//     j-gradient columns accumulate in shared memory, and both are written
+//     once per unit to a partial buffer;
+//   * a gather kernel (ffm_terms.cu) sums the partials of every atom in a
+//     fixed order, so results are bit-identical run to run.
+//
+// Exclusions (1-2, 1-3) and scaled 1-4 pairs are removed from the dense sweep
+// by per-tile bitmasks (only tiles near the diagonal of a chain carry any);
+// the scaled ones are evaluated exactly by the sparse term kernel.
+#include "ffm_kernels.h"
+
+namespace ffm {
+
+template <typename T>
+__device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
+
+template <>
+__device__ __forceinline__ Pk<float>::V shfl_rot<float>(Pk<float>::V v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
+}
+template <>
+__device__ __forceinline__ Pk<double>::V shfl_rot<double>(Pk<double>::V v, int src) {
+  return {__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
+}
+
+// One 128 x 32 warp tile.  MASKED tiles carry per-lane activity bitmasks
+// (diagonal i < j condition and/or special pairs); inactive pairs are
+// neutralised (r2 -> 1, coefficients -> 0) so they contribute exactly zero.
+template <typename T, bool GRAD, bool CUTOFF, bool MASKED>
+__device__ __forceinline__ void warp_tile(
+    const typename Vec4T<T>::type* __restrict__ J,
+    const typename Vec2T<T>::type* __restrict__ L, int lane,
+    const typename Pk<T>::V (&xi)[2], const typename Pk<T>::V (&yi)[2],
+    const typename Pk<T>::V (&zi)[2], const typename Pk<T>::V (&qi)[2],
+    const typename Pk<T>::V (&ai)[2], const typename Pk<T>::V (&bi)[2],
+    typename Pk<T>::V (&F)[2][3], typename Pk<T>::V& ec2,
+    typename Pk<T>::V& ev2, T* __restrict__ jacc, int jacc_stride,
+    const uint32_t (&mk)[4], T cut2, T& minr2) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  V gx = P::zero(), gy = P::zero(), gz = P::zero();
+  const int src = (lane + 1) & 31;
+#pragma unroll 4
+  for (int t = 0; t < 32; ++t) {
+    const int jj = (lane + t) & 31;
+    const auto pj = J[jj];  // (-x, -y, -z, q~)
+    const auto lj = L[jj];  // (a, -b)
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      V dx = P::add(xi[pp], P::bc(pj.x));
+      V dy = P::add(yi[pp], P::bc(pj.y));
+      V dz = P::add(zi[pp], P::bc(pj.z));
+      V r2 = P::mul(dx, dx);
+      r2 = P::fma(dy, dy, r2);
+      r2 = P::fma(dz, dz, r2);
+      V A = P::mul(ai[pp], P::bc(lj.x));
+      V nB = P::mul(bi[pp], P::bc(lj.y));
+      V Q = P::mul(qi[pp], P::bc(pj.w));
+      if (MASKED) {
+        const bool a0 = (mk[2 * pp] >> jj) & 1u;
+        const bool a1 = (mk[2 * pp + 1] >> jj) & 1u;
+        r2 = P::make(a0 ? P::lo(r2) : T(1), a1 ? P::hi(r2) : T(1));
+        A = P::make(a0 ? P::lo(A) : T(0), a1 ? P::hi(A) : T(0));
+        nB = P::make(a0 ? P::lo(nB) : T(0), a1 ? P::hi(nB) : T(0));
+        Q = P::make(a0 ? P::lo(Q) : T(0), a1 ? P::hi(Q) : T(0));
+      }
+      if constexpr (sizeof(T) == 8) {
+        // FP64 mode tracks the closest pair exactly (coincidence check of
+        // ffmin/kernels.py:330-332 happens before the cutoff test)
+        minr2 = fmin(minr2, fmin(P::lo(r2), P::hi(r2)));
+      }
+      if (CUTOFF) {
+        const bool c0 = P::lo(r2) <= cut2;
+        const bool c1 = P::hi(r2) <= cut2;
+        A = P::make(c0 ? P::lo(A) : T(0), c1 ? P::hi(A) : T(0));
+        nB = P::make(c0 ? P::lo(nB) : T(0), c1 ? P::hi(nB) : T(0));
+        Q = P::make(c0 ? P::lo(Q) : T(0), c1 ? P::hi(Q) : T(0));
+      }
+      const V ri = P::rsqrt(r2);
+      const V i2 = P::mul(ri, ri);
+      const V i4 = P::mul(i2, i2);
+      const V i6 = P::mul(i4, i2);
+      const V u = P::mul(A, i6);     // A / r^6
+      const V v = P::add(u, nB);     // A / r^6 - B
+      ev2 = P::fma(v, i6, ev2);      // A / r^12 - B / r^6
+      const V ecp = P::mul(Q, ri);   // C q_i q_j / r
+      ec2 = P::add(ec2, ecp);
+      if (GRAD) {
+        // g = -(dE/dr)/r = (C q q / r + 12 A / r^12 - 6 B / r^6) / r^2
+        const V pw = P::add(u, v);   // 2 A / r^6 - B
+        const V k = P::mul(pw, i6);
+        const V w = P::fma(k, P::bc(T(6)), ecp);
+        const V g = P::mul(w, i2);
+        // F_i = -grad_i = g (x_i - x_j);  grad_j += g (x_i - x_j)
+        F[pp][0] = P::fma(g, dx, F[pp][0]);
+        F[pp][1] = P::fma(g, dy, F[pp][1]);
+        F[pp][2] = P::fma(g, dz, F[pp][2]);
+        gx = P::fma(g, dx, gx);
+        gy = P::fma(g, dy, gy);
+        gz = P::fma(g, dz, gz);
+      }
+    }
+    if (GRAD && t < 31) {
+      gx = shfl_rot<T>(gx, src);
+      gy = shfl_rot<T>(gy, src);
+      gz = shfl_rot<T>(gz, src);
+    }
+  }
+  if (GRAD) {
+    // after 31 rotations lane l holds the column of j = (l + 31) mod 32
+    const int jj = (lane + 31) & 31;
+    jacc[jj] += P::lo(gx) + P::hi(gx);
+    jacc[jacc_stride + jj] += P::lo(gy) + P::hi(gy);
+    jacc[2 * jacc_stride + jj] += P::lo(gz) + P::hi(gz);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kWarps; ++w) s += red[w];
+  return s;
+}
+
+__device__ __forceinline__ double block_min(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = red[0];
+  for (int w = 1; w < kWarps; ++w) s = fmin(s, red[w]);
+  return s;
+}
+
+// grid = (nunits, batch).  ipart/jpart: [nunits][3][S] gradient partials
+// (GRAD only); epart: [batch][nunits][3] = (coulomb, vdw, min r^2).
+template <typename T, bool GRAD, bool CUTOFF>
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
+nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
+                const typename Vec2T<T>::type* __restrict__ lj,
+                T* __restrict__ ipart, T* __restrict__ jpart,
+                double* __restrict__ epart) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  using V4 = typename Vec4T<T>::type;
+  using V2 = typename Vec2T<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kWarps];
+  const int S = plan.S;
+  V4* sj = reinterpret_cast<V4*>(smem_raw);
+  V2* sl = reinterpret_cast<V2*>(sj + S);
+  T* jacc = reinterpret_cast<T*>(sl + S);  // [3][S]      (GRAD)
+  T* ired = jacc + 3 * S;                  // [kWarps][3][kIB] (GRAD)
+
+  const int u = blockIdx.x;
+  const int bidx = blockIdx.y;
+  pos += (size_t)bidx * plan.np;
+  const int2 rc = plan.unit_rc[u];
+  const int i0 = rc.x * S, j0 = rc.y * S;
+  const bool diag = rc.x == rc.y;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  for (int a = tid; a < S; a += kThreads) {
+    V4 p = pos[j0 + a];
+    p.x = -p.x;
+    p.y = -p.y;
+    p.z = -p.z;
+    sj[a] = p;
+    V2 l = lj[j0 + a];
+    l.y = -l.y;
+    sl[a] = l;
+    if (GRAD) {
+      jacc[a] = T(0);
+      jacc[S + a] = T(0);
+      jacc[2 * S + a] = T(0);
+    }
+  }
+  __syncthreads();
+
+  double Ec = 0.0, Ev = 0.0;
+  T minr2 = T(1e30);
+  const T cut2 = T(plan.cut2);
+  const int nsub = S / kIB, njb = S / kJB;
+  for (int ks = 0; ks < nsub; ++ks) {
+    const int ib = i0 + ks * kIB;
+    V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const V4 p0 = pos[ib + lane + 64 * pp];
+      const V4 p1 = pos[ib + lane + 64 * pp + 32];
+      const V2 l0 = lj[ib + lane + 64 * pp];
+      const V2 l1 = lj[ib + lane + 64 * pp + 32];
+      xi[pp] = P::make(p0.x, p1.x);
+      yi[pp] = P::make(p0.y, p1.y);
+      zi[pp] = P::make(p0.z, p1.z);
+      qi[pp] = P::make(p0.w, p1.w);
+      ai[pp] = P::make(l0.x, l1.x);
+      bi[pp] = P::make(l0.y, l1.y);
+    }
+    V F[2][3];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
+    V ec2 = P::zero(), ev2 = P::zero();
+    const int kk = ib / kIB;
+    const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];
+
+    for (int m = warp; m < njb; m += kWarps) {
+      const int jb = j0 + m * kJB;
+      if (diag && jb + kJB <= ib) continue;  // whole tile has j < i
+      bool masked = diag && jb < ib + kIB;   // straddles the diagonal
+      uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
+      if (masked) {
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int d = ib + lane + 32 * p - jb;  // pair active iff jj > d
+          mk[p] = d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
+        }
+      }
+      const int mg = jb / kJB;
+      for (int e = e_beg; e < e_end; ++e) {
+        if (plan.spt_m[e] == mg) {
+          masked = true;
+#pragma unroll
+          for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)e * kIB + 32 * p + lane];
+          break;
+        }
+      }
+      T* jc = jacc + m * kJB;
+      if (masked)
+        warp_tile<T, GRAD, CUTOFF, true>(sj + m * kJB, sl + m * kJB, lane, xi, yi, zi, qi,
+                                         ai, bi, F, ec2, ev2, jc, S, mk, cut2, minr2);
+      else
+        warp_tile<T, GRAD, CUTOFF, false>(sj + m * kJB, sl + m * kJB, lane, xi, yi, zi,
+                                          qi, ai, bi, F, ec2, ev2, jc, S, mk, cut2, minr2);
+      Ec += double(P::lo(ec2)) + double(P::hi(ec2));
+      Ev += double(P::lo(ev2)) + double(P::hi(ev2));
+      ec2 = P::zero();
+      ev2 = P::zero();
+    }
+    if (GRAD) {
+      // cross-warp reduction of the i-rows of this sub-block (fixed order)
+      T* my = ired + warp * 3 * kIB;
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          my[c * kIB + lane + 64 * pp] = P::lo(F[pp][c]);
+          my[c * kIB + lane + 64 * pp + 32] = P::hi(F[pp][c]);
+        }
+      }
+      __syncthreads();
+      {
+        const int a = tid;  // kThreads == kIB
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          T s = T(0);
+#pragma unroll
+          for (int w = 0; w < kWarps; ++w) s += ired[w * 3 * kIB + c * kIB + a];
+          // F = -gradient
+          ipart[((size_t)u * 3 + c) * S + ks * kIB + a] = -s;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (GRAD) {
+    __syncthreads();
+    for (int a = tid; a < S; a += kThreads) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) jpart[((size_t)u * 3 + c) * S + a] = jacc[c * S + a];
+    }
+  }
+  const double ec = block_sum<T>(Ec, red);
+  const double ev = block_sum<T>(Ev, red);
+  const double mr = block_min(double(minr2), red);
+  if (tid == 0) {
+    double* e = epart + ((size_t)bidx * plan.nunits + u) * 3;
+    e[0] = ec;
+    e[1] = ev;
+    e[2] = mr;
+  }
+}
+
+size_t nb_smem_bytes(int S, bool fp64, bool grad) {
+  const size_t t = fp64 ? 8 : 4;
+  size_t b = (size_t)S * (4 * t + 2 * t);
+  if (grad) b += (size_t)3 * S * t + (size_t)kWarps * 3 * kIB * t;
+  return b;
+}
+
+template <typename T, bool GRAD, bool CUTOFF>
+static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const void* lj,
+                               void* ipart, void* jpart, double* epart, int batch,
+                               cudaStream_t st) {
+  const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD);
+  auto k = nb_units_kernel<T, GRAD, CUTOFF>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(plan.nunits, batch);
+  k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
+                                  static_cast<const typename Vec2T<T>::type*>(lj),
+                                  static_cast<T*>(ipart), static_cast<T*>(jpart), epart);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
+                      const void* lj, void* ipart, void* jpart, double* epart, int batch,
+                      cudaStream_t st) {
+  const bool cut = plan.has_cutoff != 0;
+#define FFM_NB(T, G, C) return launch_nb_t<T, G, C>(plan, pos, lj, ipart, jpart, epart, batch, st)
+  if (fp64) {
+    if (grad) { if (cut) FFM_NB(double, true, true); else FFM_NB(double, true, false); }
+    else { if (cut) FFM_NB(double, false, true); else FFM_NB(double, false, false); }
+  } else {
+    if (grad) { if (cut) FFM_NB(float, true, true); else FFM_NB(float, true, false); }
+    else { if (cut) FFM_NB(float, false, true); else FFM_NB(float, false, false); }
+  }
+#undef FFM_NB
+}
+
+}  // namespace ffm

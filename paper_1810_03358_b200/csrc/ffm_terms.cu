@@ -1,0 +1,614 @@
+// ffm_terms.cu -- everything around the pair sweep: coordinate packing,
+// bonded terms and scaled 1-4 pairs (FP64), the deterministic gradient
+// gather, the energy reduction, the coincident-pair finder and the exact
+// single-atom move deltas used by the gradient-free method.
+#include <cfloat>
+#include "ffm_kernels.h"
+
+namespace ffm {
+
+constexpr long long kSentinel = 0x7fffffffffffffffLL;
+
+// ------------------------------------------------------------------ packing
+template <typename T>
+__global__ void pack_kernel(int n, int np, int batch, const double* __restrict__ coords,
+                            const double* __restrict__ qt,
+                            typename Vec4T<T>::type* __restrict__ pos,
+                            int64_t* __restrict__ status) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < (int64_t)n * batch) {
+    const int64_t b = k / n, a = k - b * n;
+    const double* c = coords + 3 * k;
+    typename Vec4T<T>::type p;
+    p.x = T(c[0]);
+    p.y = T(c[1]);
+    p.z = T(c[2]);
+    p.w = T(qt[a]);
+    pos[b * np + a] = p;
+  }
+  if (status && k < batch) {
+    int64_t* s = status + k * kStWords;
+    s[kStNbBadI] = -1;
+    s[kStNbBadJ] = -1;
+    s[kStBond] = kSentinel;
+    s[kStAngle] = kSentinel;
+    s[kStDihedral] = kSentinel;
+    s[kStNbSuspect] = 0;
+    s[kStNbKey] = kSentinel;
+    s[7] = 0;
+  }
+}
+
+template <typename T>
+__global__ void pad_kernel(int n, int np, int batch, typename Vec4T<T>::type* __restrict__ pos) {
+  const int npad = np - n;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= (int64_t)npad * batch) return;
+  const int64_t b = k / npad, a = k - b * npad;
+  // zero charge and LJ (set in lj/qt), far from everything and 10 A apart
+  typename Vec4T<T>::type p;
+  p.x = T(1.0e4 + 10.0 * (double)a);
+  p.y = T(1.0e4);
+  p.z = T(1.0e4);
+  p.w = T(0);
+  pos[b * np + n + a] = p;
+}
+
+cudaError_t launch_pack(int n, int np, int batch, bool fp64, const double* coords,
+                        const double* qt, void* pos, int64_t* status, cudaStream_t st) {
+  const int64_t tot = (int64_t)n * batch > batch ? (int64_t)n * batch : batch;
+  const int blocks = (int)((tot + 255) / 256);
+  if (fp64)
+    pack_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+                                                static_cast<double4*>(pos), status);
+  else
+    pack_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+                                               static_cast<float4*>(pos), status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, cudaStream_t st) {
+  const int64_t tot = (int64_t)(np - n) * batch;
+  if (tot <= 0) return cudaSuccess;
+  const int blocks = (int)((tot + 255) / 256);
+  if (fp64)
+    pad_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<double4*>(pos));
+  else
+    pad_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<float4*>(pos));
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- term physics
+struct P3 {
+  double x, y, z;
+};
+__device__ __forceinline__ P3 ld3(const double* c, int i) { return {c[3 * i], c[3 * i + 1], c[3 * i + 2]}; }
+__device__ __forceinline__ P3 sub(P3 a, P3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ double dot(P3 a, P3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ P3 cross(P3 a, P3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__device__ __forceinline__ void st3(double* f, P3 v) {
+  f[0] = v.x;
+  f[1] = v.y;
+  f[2] = v.z;
+}
+
+// ffmin/kernels.py:52-86: K (r - r0)^2; grad variant checks r < RMIN.
+__device__ bool bond_term(P3 ci, P3 cj, double K, double r0, bool grad, double* e, P3* gi) {
+  const P3 d = sub(ci, cj);
+  const double r = sqrt(dot(d, d));
+  if (grad && r < kRmin) return false;
+  const double dv = r - r0;
+  *e = K * dv * dv;
+  if (grad) {
+    const double c = 2.0 * K * dv / r;
+    *gi = {c * d.x, c * d.y, c * d.z};
+  }
+  return true;
+}
+
+// ffmin/kernels.py:89-161: K (theta - theta0)^2 at apex j.
+__device__ bool angle_term(P3 ci, P3 cj, P3 ck, double K, double t0, bool grad, double* e,
+                           P3* gi, P3* gk) {
+  const P3 a = sub(ci, cj), b = sub(ck, cj);
+  const double na = sqrt(dot(a, a)), nb = sqrt(dot(b, b));
+  if (na < kDegenerateEps || nb < kDegenerateEps) return false;
+  double u = dot(a, b) / (na * nb);
+  u = u > 1.0 ? 1.0 : (u < -1.0 ? -1.0 : u);
+  if (!grad) {
+    const double d = acos(u) - t0;
+    *e = K * d * d;
+    return true;
+  }
+  const double sin_th = sqrt(1.0 - u * u);
+  if (sin_th < kDegenerateEps) return false;
+  const double d = acos(u) - t0;
+  *e = K * d * d;
+  const double pref = -2.0 * K * d / sin_th;
+  const double nab = na * nb, naa = na * na, nbb = nb * nb;
+  *gi = {pref * (b.x / nab - u * a.x / naa), pref * (b.y / nab - u * a.y / naa),
+         pref * (b.z / nab - u * a.z / naa)};
+  *gk = {pref * (a.x / nab - u * b.x / nbb), pref * (a.y / nab - u * b.y / nbb),
+         pref * (a.z / nab - u * b.z / nbb)};
+  return true;
+}
+
+// ffmin/kernels.py:164-282: OPLS cosine series on the atan2 dihedral.
+__device__ bool dihedral_term(P3 ci, P3 cj, P3 ck, P3 cl, const double* V, bool grad,
+                              double* e, P3* g) {
+  const P3 b1 = sub(cj, ci), b2 = sub(ck, cj), b3 = sub(cl, ck);
+  const P3 n1 = cross(b1, b2), n2 = cross(b2, b3);
+  const double n1sq = dot(n1, n1), n2sq = dot(n2, n2);
+  const double n1n = sqrt(n1sq), n2n = sqrt(n2sq);
+  const double b2sq = dot(b2, b2), b2n = sqrt(b2sq);
+  if (n1n < kDegenerateEps || n2n < kDegenerateEps || b2n < kDegenerateEps) return false;
+  const P3 m = cross(n1, n2);
+  const double y = dot(m, b2) / b2n;
+  const double x = dot(n1, n2);
+  const double phi = atan2(y, x);
+  *e = 0.5 * (V[0] * (1.0 + cos(phi)) + V[1] * (1.0 - cos(2.0 * phi)) +
+              V[2] * (1.0 + cos(3.0 * phi)) + V[3] * (1.0 - cos(4.0 * phi)));
+  if (!grad) return true;
+  const double dedphi = 0.5 * (-V[0] * sin(phi) + 2.0 * V[1] * sin(2.0 * phi) -
+                               3.0 * V[2] * sin(3.0 * phi) + 4.0 * V[3] * sin(4.0 * phi));
+  const P3 cI = {-(b2n / n1sq) * n1.x, -(b2n / n1sq) * n1.y, -(b2n / n1sq) * n1.z};
+  const P3 cL = {(b2n / n2sq) * n2.x, (b2n / n2sq) * n2.y, (b2n / n2sq) * n2.z};
+  const double p = dot(b1, b2) / b2sq;
+  const double s = dot(b3, b2) / b2sq;
+  const P3 cJ = {-(1.0 + p) * cI.x + s * cL.x, -(1.0 + p) * cI.y + s * cL.y,
+                 -(1.0 + p) * cI.z + s * cL.z};
+  const P3 cK = {-(1.0 + s) * cL.x + p * cI.x, -(1.0 + s) * cL.y + p * cI.y,
+                 -(1.0 + s) * cL.z + p * cI.z};
+  g[0] = {dedphi * cI.x, dedphi * cI.y, dedphi * cI.z};
+  g[1] = {dedphi * cJ.x, dedphi * cJ.y, dedphi * cJ.z};
+  g[2] = {dedphi * cK.x, dedphi * cK.y, dedphi * cK.z};
+  g[3] = {dedphi * cL.x, dedphi * cL.y, dedphi * cL.z};
+  return true;
+}
+
+// One scaled (0 < s < 1) nonbonded pair, ffmin/kernels.py:316-353 with the
+// pair's own scale.  Returns false on coincidence.
+__device__ bool scaled_pair(P3 ci, P3 cj, double qi, double qj, double sgi, double sgj,
+                            double epi, double epj, double s, bool has_cut, double cutoff,
+                            bool grad, double* ec, double* ev, P3* gi) {
+  const P3 d = sub(ci, cj);
+  const double r = sqrt(dot(d, d));
+  *ec = 0.0;
+  *ev = 0.0;
+  *gi = {0.0, 0.0, 0.0};
+  if (r < kRmin) return false;
+  if (has_cut && r > cutoff) return true;
+  const double qq = s * qi * qj;
+  *ec = kCoulomb * qq / r;
+  double dedr_over_r = -kCoulomb * qq / (r * r * r);
+  const double eps_ij = sqrt(epi * epj);
+  if (eps_ij > 0.0) {
+    const double sig = sqrt(sgi * sgj);
+    const double t = sig / r;
+    const double x6 = t * t * t * t * t * t;
+    *ev = 4.0 * s * eps_ij * (x6 * x6 - x6);
+    dedr_over_r += 4.0 * s * eps_ij * (-12.0 * x6 * x6 + 6.0 * x6) / (r * r);
+  }
+  if (grad) *gi = {dedr_over_r * d.x, dedr_over_r * d.y, dedr_over_r * d.z};
+  return true;
+}
+
+__device__ __forceinline__ void amin(int64_t* p, int64_t v) {
+  atomicMin(reinterpret_cast<long long*>(p), (long long)v);
+}
+
+// one thread per term over [bonds | angles | dihedrals | scaled pairs]
+__global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict__ coords,
+                             double* __restrict__ term_e, double* __restrict__ term_f,
+                             int64_t* __restrict__ status) {
+  const int b = blockIdx.y;
+  coords += (size_t)b * tp.n * 3;
+  term_e += (size_t)b * tp.nterm_e;
+  status += (size_t)b * kStWords;
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < tp.nbond) {
+    const int i = tp.bond_idx[2 * t], j = tp.bond_idx[2 * t + 1];
+    double e = 0.0;
+    P3 gi = {0, 0, 0};
+    if (!bond_term(ld3(coords, i), ld3(coords, j), tp.bond_K[t], tp.bond_r0[t], grad, &e, &gi))
+      amin(status + kStBond, t);
+    term_e[t] = e;
+    if (grad) {
+      st3(term_f + 3 * (2 * t), gi);
+      st3(term_f + 3 * (2 * t + 1), {-gi.x, -gi.y, -gi.z});
+    }
+    return;
+  }
+  t -= tp.nbond;
+  if (t < tp.nangle) {
+    const int i = tp.ang_idx[3 * t], j = tp.ang_idx[3 * t + 1], k = tp.ang_idx[3 * t + 2];
+    double e = 0.0;
+    P3 gi = {0, 0, 0}, gk = {0, 0, 0};
+    if (!angle_term(ld3(coords, i), ld3(coords, j), ld3(coords, k), tp.ang_K[t], tp.ang_t0[t],
+                    grad, &e, &gi, &gk)) {
+      amin(status + kStAngle, t);
+      e = 0.0;
+      gi = gk = {0, 0, 0};
+    }
+    term_e[tp.e_angle0 + t] = e;
+    if (grad) {
+      double* f = term_f + 3 * (tp.slot_angle0 + 3 * t);
+      st3(f, gi);
+      st3(f + 3, {-(gi.x + gk.x), -(gi.y + gk.y), -(gi.z + gk.z)});
+      st3(f + 6, gk);
+    }
+    return;
+  }
+  t -= tp.nangle;
+  if (t < tp.ndih) {
+    const int* id = tp.dih_idx + 4 * t;
+    double e = 0.0;
+    P3 g[4] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    if (!dihedral_term(ld3(coords, id[0]), ld3(coords, id[1]), ld3(coords, id[2]),
+                       ld3(coords, id[3]), tp.dih_V + 4 * t, grad, &e, g)) {
+      amin(status + kStDihedral, t);
+      e = 0.0;
+      g[0] = g[1] = g[2] = g[3] = {0, 0, 0};
+    }
+    term_e[tp.e_dih0 + t] = e;
+    if (grad) {
+      double* f = term_f + 3 * (tp.slot_dih0 + 4 * t);
+      for (int q = 0; q < 4; ++q) st3(f + 3 * q, g[q]);
+    }
+    return;
+  }
+  t -= tp.ndih;
+  if (t < tp.nscaled) {
+    const int i = tp.sc_idx[2 * t], j = tp.sc_idx[2 * t + 1];
+    double ec, ev;
+    P3 gi;
+    if (!scaled_pair(ld3(coords, i), ld3(coords, j), tp.q[i], tp.q[j], tp.sigma[i],
+                     tp.sigma[j], tp.eps[i], tp.eps[j], tp.sc_s[t], tp.has_cutoff != 0,
+                     tp.cutoff, grad, &ec, &ev, &gi))
+      status[kStNbSuspect] = 1;
+    term_e[tp.e_scc0 + t] = ec;
+    term_e[tp.e_scv0 + t] = ev;
+    if (grad) {
+      double* f = term_f + 3 * (tp.slot_sc0 + 2 * t);
+      st3(f, gi);
+      st3(f + 3, {-gi.x, -gi.y, -gi.z});
+    }
+  }
+}
+
+cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,
+                         double* term_e, double* term_f, int64_t* status, cudaStream_t st) {
+  const int tot = tp.nbond + tp.nangle + tp.ndih + tp.nscaled;
+  if (tot == 0) return cudaSuccess;
+  dim3 grid((tot + 127) / 128, batch);
+  terms_kernel<<<grid, 128, 0, st>>>(tp, grad, coords, term_e, term_f, status);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- gradient gather
+template <typename T>
+__global__ void assemble_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
+                                const T* __restrict__ ipart, const T* __restrict__ jpart,
+                                const int* __restrict__ slot_ptr,
+                                const int* __restrict__ slot_idx,
+                                const double* __restrict__ term_f, int slot_sc0, bool use_nb,
+                                bool use_terms, double* __restrict__ grad) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const int b = a / S, off = a - b * S;
+  double gx = 0.0, gy = 0.0, gz = 0.0;
+  if (use_nb) {
+    for (int c = b; c < nb; ++c) {  // i-side: units (b, c)
+      const size_t base = (size_t)unit_index[b * nb + c] * 3 * S + off;
+      gx += (double)ipart[base];
+      gy += (double)ipart[base + S];
+      gz += (double)ipart[base + 2 * S];
+    }
+    for (int r = 0; r <= b; ++r) {  // j-side: units (r, b)
+      const size_t base = (size_t)unit_index[r * nb + b] * 3 * S + off;
+      gx += (double)jpart[base];
+      gy += (double)jpart[base + S];
+      gz += (double)jpart[base + 2 * S];
+    }
+  }
+  for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
+    const int k = slot_idx[s];
+    if (k < slot_sc0 ? !use_terms : !use_nb) continue;
+    const double* f = term_f + 3 * (size_t)k;
+    gx += f[0];
+    gy += f[1];
+    gz += f[2];
+  }
+  grad[3 * a] = gx;
+  grad[3 * a + 1] = gy;
+  grad[3 * a + 2] = gz;
+}
+
+cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
+                            const void* ipart, const void* jpart, const int* slot_ptr,
+                            const int* slot_idx, const double* term_f, int slot_sc0,
+                            bool use_nb, bool use_terms, double* grad, cudaStream_t st) {
+  const int blocks = (n + 127) / 128;
+  if (fp64)
+    assemble_kernel<double><<<blocks, 128, 0, st>>>(
+        n, S, nb, unit_index, static_cast<const double*>(ipart),
+        static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
+        use_terms, grad);
+  else
+    assemble_kernel<float><<<blocks, 128, 0, st>>>(
+        n, S, nb, unit_index, static_cast<const float*>(ipart),
+        static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
+        use_terms, grad);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------- energy reduction
+constexpr int kRedThreads = 1024;
+
+__device__ double tree_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = sh[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+__device__ double tree_min(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = sh[threadIdx.x];
+    for (int o = 16; o > 0; o >>= 1) s = fmin(s, __shfl_xor_sync(0xffffffffu, s, o));
+  }
+  return s;
+}
+
+// one block per batch entry; every partial is summed in a fixed order
+__global__ void __launch_bounds__(kRedThreads)
+reduce_kernel(int nunits, TermPlanDev tp, const double* __restrict__ epart,
+              const double* __restrict__ term_e, double* __restrict__ energies,
+              int64_t* __restrict__ status) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x;
+  epart += (size_t)b * nunits * 3;
+  term_e += (size_t)b * tp.nterm_e;
+  double ec = 0.0, ev = 0.0, mr = DBL_MAX, es = 0.0, eb = 0.0, et = 0.0;
+  for (int u = threadIdx.x; u < nunits; u += kRedThreads) {
+    ec += epart[3 * u];
+    ev += epart[3 * u + 1];
+    mr = fmin(mr, epart[3 * u + 2]);
+  }
+  for (int t = threadIdx.x; t < tp.nbond; t += kRedThreads) es += term_e[t];
+  for (int t = threadIdx.x; t < tp.nangle; t += kRedThreads) eb += term_e[tp.e_angle0 + t];
+  for (int t = threadIdx.x; t < tp.ndih; t += kRedThreads) et += term_e[tp.e_dih0 + t];
+  for (int t = threadIdx.x; t < tp.nscaled; t += kRedThreads) {
+    ec += term_e[tp.e_scc0 + t];
+    ev += term_e[tp.e_scv0 + t];
+  }
+  ec = tree_sum(ec, sh);
+  ev = tree_sum(ev, sh);
+  es = tree_sum(es, sh);
+  eb = tree_sum(eb, sh);
+  et = tree_sum(et, sh);
+  mr = tree_min(mr, sh);
+  if (threadIdx.x == 0) {
+    double* E = energies + 5 * (size_t)b;
+    E[0] = es;
+    E[1] = eb;
+    E[2] = et;
+    E[3] = ec;
+    E[4] = ev;
+    int64_t* s = status + (size_t)b * kStWords;
+    if (!isfinite(ec) || !isfinite(ev) || mr < kRmin * kRmin) s[kStNbSuspect] = 1;
+  }
+}
+
+cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
+                          const double* term_e, double* energies, int64_t* status,
+                          cudaStream_t st) {
+  reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, tp, epart, term_e, energies, status);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ pair finder
+// Exact restatement of the coincidence test of ffmin/kernels.py:294-302 over
+// the whole upper triangle; only runs when the sweep flagged a suspect.
+template <typename T>
+__global__ void finder_kernel(int n, int np, const typename Vec4T<T>::type* __restrict__ pos,
+                              const int* __restrict__ sp_ptr, const int* __restrict__ sp_j,
+                              const double* __restrict__ sp_s, int64_t* __restrict__ status) {
+  const int b = blockIdx.y;
+  int64_t* s = status + (size_t)b * kStWords;
+  if (s[kStNbSuspect] == 0) return;
+  pos += (size_t)b * np;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const auto pi = pos[i];
+  int cur = sp_ptr[i];
+  const int end = sp_ptr[i + 1];
+  for (int j = i + 1; j < n; ++j) {
+    while (cur < end && sp_j[cur] < j) ++cur;
+    if (cur < end && sp_j[cur] == j && sp_s[cur] == 0.0) continue;
+    const auto pj = pos[j];
+    const double dx = (double)pi.x - (double)pj.x, dy = (double)pi.y - (double)pj.y,
+                 dz = (double)pi.z - (double)pj.z;
+    if (sqrt(dx * dx + dy * dy + dz * dz) < kRmin) {
+      amin(s + kStNbKey, (int64_t)i * n + j);
+      break;
+    }
+  }
+}
+
+__global__ void finalize_kernel(int n, int batch, int64_t* __restrict__ status) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  int64_t* s = status + (size_t)b * kStWords;
+  if (s[kStNbKey] != kSentinel) {
+    s[kStNbBadI] = s[kStNbKey] / n;
+    s[kStNbBadJ] = s[kStNbKey] % n;
+  }
+  for (int k = kStBond; k <= kStDihedral; ++k)
+    if (s[k] == kSentinel) s[k] = -1;
+}
+
+cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
+                          const int* sp_ptr, const int* sp_j, const double* sp_s,
+                          int64_t* status, cudaStream_t st) {
+  dim3 grid((n + 127) / 128, batch);
+  if (n == 0) {
+  } else if (fp64)
+    finder_kernel<double><<<grid, 128, 0, st>>>(n, np, static_cast<const double4*>(pos),
+                                                sp_ptr, sp_j, sp_s, status);
+  else
+    finder_kernel<float><<<grid, 128, 0, st>>>(n, np, static_cast<const float4*>(pos), sp_ptr,
+                                               sp_j, sp_s, status);
+  finalize_kernel<<<(batch + 127) / 128, 128, 0, st>>>(n, batch, status);
+  return cudaGetLastError();
+}
+
+// -------------------------------------------------------- single-atom moves
+constexpr int kDeltaThreads = 256;
+
+__device__ __forceinline__ P3 pick(const double* c, int atom, P3 np, int i) {
+  return i == atom ? np : ld3(c, i);
+}
+
+// one block per candidate move.  Nonbonded part restates
+// ffmin/kernels.py:419-454 (_loop_nb_atom_delta), bonded parts 457-593.
+__global__ void __launch_bounds__(kDeltaThreads)
+atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
+                  const int* __restrict__ fsp_ptr, const int* __restrict__ fsp_j,
+                  const double* __restrict__ fsp_s, const int* __restrict__ aterm_ptr,
+                  const int* __restrict__ aterm_idx, const int* __restrict__ atoms,
+                  const double* __restrict__ newpos, double* __restrict__ out,
+                  int64_t* __restrict__ status) {
+  __shared__ double sh[32];
+  __shared__ long long bad[3];
+  const int k = blockIdx.x;
+  const int a = atoms[k];
+  const P3 np = {newpos[3 * k], newpos[3 * k + 1], newpos[3 * k + 2]};
+  const P3 ca = ld3(coords, a);
+  if (threadIdx.x < 3) bad[threadIdx.x] = kSentinel;
+  __syncthreads();
+  const int sb = fsp_ptr[a], se = fsp_ptr[a + 1];
+  double dec = 0.0, dev = 0.0;
+  for (int j = threadIdx.x; j < tp.n; j += kDeltaThreads) {
+    if (j == a) continue;
+    // binary search of the (short, sorted) special row of atom a
+    double s = 1.0;
+    int lo = sb, hi = se;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (fsp_j[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    if (lo < se && fsp_j[lo] == j) s = fsp_s[lo];
+    if (s == 0.0) continue;
+    const P3 cj = ld3(coords, j);
+    const P3 o = sub(ca, cj), nn = sub(np, cj);
+    const double ro = sqrt(dot(o, o)), rn = sqrt(dot(nn, nn));
+    if (ro < kRmin || rn < kRmin) {
+      atomicMin(&bad[0], (long long)j);
+      continue;
+    }
+    const double qq = s * tp.q[a] * tp.q[j];
+    const double eps_ij = sqrt(tp.eps[a] * tp.eps[j]);
+    const double sig = sqrt(tp.sigma[a] * tp.sigma[j]);
+    const bool in_old = !tp.has_cutoff || ro <= tp.cutoff;
+    const bool in_new = !tp.has_cutoff || rn <= tp.cutoff;
+    if (in_old) {
+      dec -= kCoulomb * qq / ro;
+      if (eps_ij > 0.0) {
+        const double t = sig / ro, x = t * t * t * t * t * t;
+        dev -= 4.0 * s * eps_ij * (x * x - x);
+      }
+    }
+    if (in_new) {
+      dec += kCoulomb * qq / rn;
+      if (eps_ij > 0.0) {
+        const double t = sig / rn, x = t * t * t * t * t * t;
+        dev += 4.0 * s * eps_ij * (x * x - x);
+      }
+    }
+  }
+  // bonded terms touching the atom
+  double db = 0.0, da = 0.0, dd = 0.0;
+  for (int q = aterm_ptr[a] + threadIdx.x; q < aterm_ptr[a + 1]; q += kDeltaThreads) {
+    int t = aterm_idx[q];
+    if (t < tp.nbond) {
+      const int i = tp.bond_idx[2 * t], j = tp.bond_idx[2 * t + 1];
+      P3 d = sub(ld3(coords, i), ld3(coords, j));
+      const double dold = sqrt(dot(d, d)) - tp.bond_r0[t];
+      d = sub(pick(coords, a, np, i), pick(coords, a, np, j));
+      const double dnew = sqrt(dot(d, d)) - tp.bond_r0[t];
+      db += tp.bond_K[t] * (dnew * dnew - dold * dold);
+      continue;
+    }
+    t -= tp.nbond;
+    if (t < tp.nangle) {
+      const int i = tp.ang_idx[3 * t], j = tp.ang_idx[3 * t + 1], kk = tp.ang_idx[3 * t + 2];
+      double eo, en;
+      P3 g0, g1;
+      if (!angle_term(ld3(coords, i), ld3(coords, j), ld3(coords, kk), tp.ang_K[t],
+                      tp.ang_t0[t], false, &eo, &g0, &g1) ||
+          !angle_term(pick(coords, a, np, i), pick(coords, a, np, j),
+                      pick(coords, a, np, kk), tp.ang_K[t], tp.ang_t0[t], false, &en, &g0,
+                      &g1)) {
+        atomicMin(&bad[1], (long long)t);
+        continue;
+      }
+      da += en - eo;
+      continue;
+    }
+    t -= tp.nangle;
+    const int* id = tp.dih_idx + 4 * t;
+    double eo, en;
+    P3 g[4];
+    if (!dihedral_term(ld3(coords, id[0]), ld3(coords, id[1]), ld3(coords, id[2]),
+                       ld3(coords, id[3]), tp.dih_V + 4 * t, false, &eo, g) ||
+        !dihedral_term(pick(coords, a, np, id[0]), pick(coords, a, np, id[1]),
+                       pick(coords, a, np, id[2]), pick(coords, a, np, id[3]),
+                       tp.dih_V + 4 * t, false, &en, g)) {
+      atomicMin(&bad[2], (long long)t);
+      continue;
+    }
+    dd += en - eo;
+  }
+  dec = tree_sum(dec, sh);
+  dev = tree_sum(dev, sh);
+  db = tree_sum(db, sh);
+  da = tree_sum(da, sh);
+  dd = tree_sum(dd, sh);
+  if (threadIdx.x == 0) {
+    double* o = out + 5 * (size_t)k;
+    o[0] = dec;
+    o[1] = dev;
+    o[2] = db;
+    o[3] = da;
+    o[4] = dd;
+    int64_t* s = status + 3 * (size_t)k;
+    for (int q = 0; q < 3; ++q) s[q] = bad[q] == kSentinel ? -1 : (int64_t)bad[q];
+  }
+}
+
+cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
+                              const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
+                              const int* aterm_ptr, const int* aterm_idx, int ncand,
+                              const int* atoms, const double* newpos, double* out,
+                              int64_t* status, cudaStream_t st) {
+  if (ncand <= 0) return cudaSuccess;
+  atom_delta_kernel<<<ncand, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s,
+                                                     aterm_ptr, aterm_idx, atoms, newpos, out,
+                                                     status);
+  return cudaGetLastError();
+}
+
+}  // namespace ffm

@@ -1,0 +1,228 @@
+// ffm_vec.cu -- optimiser vector algebra kept resident in HBM.
+//
+// The reference drivers do their vector algebra in NumPy on the host
+// (ffmin/optimizers/*.py); here x, g, s, y and the search directions never
+// leave the device.  All reductions use a fixed grid and a fixed combination
+// order, so every dot product -- and therefore every optimiser trace -- is
+// bit-identical run to run.
+#include <cooperative_groups.h>
+#include "ffm_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace ffm {
+
+constexpr int kVecBlocks = 296;  // 2 per SM on 148 SMs
+constexpr int kVecThreads = 256;
+
+int vec_reduce_blocks() { return kVecBlocks; }
+
+__device__ __forceinline__ double block_sum256(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kVecThreads / 32; ++w) s += sh[w];
+  __syncthreads();
+  return s;  // thread 0
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+dot_partial_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                   double* __restrict__ part) {
+  __shared__ double sh[kVecThreads / 32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < n;
+       i += (int64_t)kVecBlocks * kVecThreads)
+    acc = fma(x[i], y[i], acc);
+  const double s = block_sum256(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+dot_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double sh[kVecThreads / 32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kVecBlocks; i += kVecThreads) acc += part[i];
+  const double s = block_sum256(acc, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,
+                       double* out, cudaStream_t st) {
+  dot_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, x, y, part);
+  dot_final_kernel<<<1, kVecThreads, 0, st>>>(part, out);
+  return cudaGetLastError();
+}
+
+// z = sa * (a * x + b * y); a, b from device pointers when given.  y may be
+// null (then b is ignored).
+__global__ void axpby_kernel(int64_t n, const double* __restrict__ a_dev, double a_host,
+                             double sa, const double* __restrict__ x,
+                             const double* __restrict__ b_dev, double b_host,
+                             const double* __restrict__ y, double* __restrict__ z) {
+  const double a = a_dev ? *a_dev : a_host;
+  const double b = b_dev ? *b_dev : b_host;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = a * x[i];
+    if (y) v = fma(b, y[i], v);
+    z[i] = sa * v;
+  }
+}
+
+cudaError_t launch_axpby(int64_t n, const double* a_dev, double a_host, double sa,
+                         const double* x, const double* b_dev, double b_host,
+                         const double* y, double* z, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 4 * kVecBlocks) blocks = 4 * kVecBlocks;
+  if (blocks < 1) blocks = 1;
+  axpby_kernel<<<(int)blocks, 256, 0, st>>>(n, a_dev, a_host, sa, x, b_dev, b_host, y, z);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------- L-BFGS two-loop
+// ffmin/optimizers/lbfgs.py:53-75 (Algorithm 3): one cooperative kernel with
+// 2 m + 1 grid-wide phases and no host round trip.  S and Y are ring buffers
+// [m][n]; the host passes the ring order (newest first) and rho_i.  Partial
+// sums rotate through three scratch rows so a row is never rewritten while a
+// slower block may still be reading it.
+struct TwoLoopArgs {
+  int64_t n;
+  int count;
+  int idx[kMaxLbfgsPairs];     // ring slots, newest first
+  double rho[kMaxLbfgsPairs];  // 1 / <s_i, y_i>, same order
+  const double* S;
+  const double* Y;
+  const double* g;
+  double* q;     // output: the raw quasi-Newton direction -H g
+  double* part;  // scratch [5][kVecBlocks]
+};
+
+__device__ __forceinline__ double grid_sum(const double* part) {
+  double s = 0.0;  // every block sums every partial in the same order
+  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b];
+  return s;
+}
+
+__global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double sh[kVecThreads / 32];
+  __shared__ double bc;
+  const int64_t n = A.n;
+  const int64_t stride = (int64_t)gridDim.x * kVecThreads;
+  const int64_t i0 = (int64_t)blockIdx.x * kVecThreads + threadIdx.x;
+  const int G = gridDim.x;
+  double* rot = A.part;  // rows 0..2 rotate
+  double* psy = A.part + 3 * kVecBlocks;
+  double* pyy = A.part + 4 * kVecBlocks;
+  double alpha[kMaxLbfgsPairs];
+  int p = 0;
+
+  {  // phase 0: q = g;  <s_0, g>, <s_0, y_0>, <y_0, y_0>  (index 0 = newest)
+    const double* s0 = A.S + (int64_t)A.idx[0] * n;
+    const double* y0 = A.Y + (int64_t)A.idx[0] * n;
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int64_t i = i0; i < n; i += stride) {
+      const double v = A.g[i];
+      A.q[i] = v;
+      a = fma(s0[i], v, a);
+      b = fma(s0[i], y0[i], b);
+      c = fma(y0[i], y0[i], c);
+    }
+    a = block_sum256(a, sh);
+    b = block_sum256(b, sh);
+    c = block_sum256(c, sh);
+    if (threadIdx.x == 0) {
+      rot[blockIdx.x] = a;
+      psy[blockIdx.x] = b;
+      pyy[blockIdx.x] = c;
+    }
+  }
+  grid.sync();
+  if (threadIdx.x == 0) bc = grid_sum(psy) / grid_sum(pyy);
+  __syncthreads();
+  const double gamma = bc;  // <s,y>/<y,y> of the newest pair (H0 scaling)
+
+  // first loop, newest -> oldest: alpha_k = rho_k <s_k, q>;  q -= alpha_k y_k
+  for (int k = 0; k < A.count; ++k) {
+    __syncthreads();
+    if (threadIdx.x == 0) bc = A.rho[k] * grid_sum(rot + (p % 3) * kVecBlocks);
+    __syncthreads();
+    alpha[k] = bc;
+    const bool last = k + 1 == A.count;
+    const double* y = A.Y + (int64_t)A.idx[k] * n;
+    // next dot: <s_{k+1}, q>, or after scaling by gamma <y_oldest, q>
+    const double* w = last ? A.Y + (int64_t)A.idx[A.count - 1] * n
+                           : A.S + (int64_t)A.idx[k + 1] * n;
+    double acc = 0.0;
+    for (int64_t i = i0; i < n; i += stride) {
+      double v = fma(-alpha[k], y[i], A.q[i]);
+      if (last) v *= gamma;
+      A.q[i] = v;
+      acc = fma(w[i], v, acc);
+    }
+    acc = block_sum256(acc, sh);
+    ++p;
+    if (threadIdx.x == 0) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
+    grid.sync();
+  }
+  // second loop, oldest -> newest: beta = rho_k <y_k, q>;  q += (alpha_k - beta) s_k
+  for (int k = A.count - 1; k >= 0; --k) {
+    __syncthreads();
+    if (threadIdx.x == 0) bc = A.rho[k] * grid_sum(rot + (p % 3) * kVecBlocks);
+    __syncthreads();
+    const double coef = alpha[k] - bc;
+    const double* s = A.S + (int64_t)A.idx[k] * n;
+    if (k == 0) {
+      for (int64_t i = i0; i < n; i += stride) A.q[i] = -fma(coef, s[i], A.q[i]);
+      break;
+    }
+    const double* y2 = A.Y + (int64_t)A.idx[k - 1] * n;
+    double acc = 0.0;
+    for (int64_t i = i0; i < n; i += stride) {
+      const double v = fma(coef, s[i], A.q[i]);
+      A.q[i] = v;
+      acc = fma(y2[i], v, acc);
+    }
+    acc = block_sum256(acc, sh);
+    ++p;
+    if (threadIdx.x == 0) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
+    grid.sync();
+  }
+  (void)G;
+}
+
+size_t two_loop_scratch_doubles() { return 5 * (size_t)kVecBlocks; }
+
+cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const double* rho,
+                                  const double* S, const double* Y, const double* g,
+                                  double* q, double* scratch, cudaStream_t st) {
+  if (count < 1 || count > kMaxLbfgsPairs) return cudaErrorInvalidValue;
+  TwoLoopArgs a;
+  a.n = n;
+  a.count = count;
+  for (int k = 0; k < count; ++k) {
+    a.idx[k] = idx[k];
+    a.rho[k] = rho[k];
+  }
+  a.S = S;
+  a.Y = Y;
+  a.g = g;
+  a.q = q;
+  a.part = scratch;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, two_loop_kernel, kVecThreads, 0);
+  int blocks = sms * (per_sm < 2 ? per_sm : 2);
+  const int64_t need = (n + kVecThreads - 1) / kVecThreads;
+  if (blocks > need) blocks = (int)need;
+  if (blocks > kVecBlocks) blocks = kVecBlocks;
+  if (blocks < 1) blocks = 1;
+  void* args[] = {&a};
+  return cudaLaunchCooperativeKernel((void*)two_loop_kernel, blocks, kVecThreads, args, 0, st);
+}
+
+}  // namespace ffm

@@ -1,0 +1,182 @@
+"""Objective oracles: the only interface optimizers see (mirrors ffmin/oracle.py).
+
+Call accounting is identical to the reference: value(), gradient() and
+value_and_gradient() each bump their counters, a fused call bumps both.
+
+Two molecular oracles:
+  * ``MolecularOracle``      -- NumPy in / NumPy out, the reference-facing
+    drop-in (every call is one host->device->host round trip);
+  * ``DeviceMolecularOracle`` -- coordinates and gradients stay in HBM as
+    torch tensors; only the 5 energy terms and 8 status words (104 bytes)
+    come back per evaluation.  The device-resident optimisers use this one.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .energy import energy_and_gradient, energy_total, raise_status
+from .engine import engine_for, precision_of
+
+
+class ObjectiveOracle:
+    """Base class; subclasses implement _value/_gradient/_value_and_gradient."""
+
+    #: vectors this oracle consumes: "host" (NumPy) or "device" (torch cuda)
+    space = "host"
+
+    def __init__(self, n):
+        self.n = int(n)
+        self.value_calls = 0
+        self.grad_calls = 0
+
+    def reset_counters(self):
+        self.value_calls = 0
+        self.grad_calls = 0
+
+    def value(self, x) -> float:
+        self.value_calls += 1
+        return float(self._value(self._coerce(x)))
+
+    def gradient(self, x):
+        self.grad_calls += 1
+        return self._out(self._gradient(self._coerce(x)))
+
+    def value_and_gradient(self, x):
+        self.value_calls += 1
+        self.grad_calls += 1
+        f, g = self._value_and_gradient(self._coerce(x))
+        return float(f), self._out(g)
+
+    def _coerce(self, x):
+        return np.asarray(x, dtype=np.float64)
+
+    def _out(self, g):
+        return np.asarray(g, dtype=np.float64)
+
+    def _value_and_gradient(self, x):
+        return self._value(x), self._gradient(x)
+
+    def _value(self, x):
+        raise NotImplementedError
+
+    def _gradient(self, x):
+        raise NotImplementedError
+
+
+class FunctionOracle(ObjectiveOracle):
+    """Wrap plain callables f(x) and optionally g(x) (ffmin/oracle.py:53-73)."""
+
+    def __init__(self, n, f, grad=None, value_and_grad=None):
+        super().__init__(n)
+        self._f = f
+        self._g = grad
+        self._fg = value_and_grad
+
+    def _value(self, x):
+        return self._f(x)
+
+    def _gradient(self, x):
+        if self._g is None:
+            raise NotImplementedError("no gradient supplied for this oracle")
+        return self._g(x)
+
+    def _value_and_gradient(self, x):
+        if self._fg is not None:
+            return self._fg(x)
+        return super()._value_and_gradient(x)
+
+
+class MolecularOracle(ObjectiveOracle):
+    """Total force-field energy of flattened coordinates, host buffers
+    (ffmin/oracle.py:76-103)."""
+
+    def __init__(self, system, dtype=np.float64, backend=None):
+        super().__init__(3 * system.natoms)
+        self.system = system
+        self.dtype = np.dtype(dtype)
+        self.backend = backend
+
+    def system_at(self, x):
+        return self.system.with_coords(np.asarray(x, dtype=np.float64))
+
+    def _value(self, x):
+        return energy_total(self.system_at(x), self.dtype, self.backend).total
+
+    def _gradient(self, x):
+        _, g = energy_and_gradient(self.system_at(x), self.dtype, self.backend)
+        return g
+
+    def _value_and_gradient(self, x):
+        bd, g = energy_and_gradient(self.system_at(x), self.dtype, self.backend)
+        return bd.total, g
+
+
+class DeviceMolecularOracle(ObjectiveOracle):
+    """Device-resident molecular oracle: x and gradients are cuda float64
+    tensors of length 3n; f comes back as a Python float.
+
+    ``last_breakdown`` keeps the 5 terms of the latest evaluation; errors
+    are raised exactly as by the energy layer.
+    """
+
+    space = "device"
+
+    def __init__(self, system, dtype=np.float64, device=None):
+        super().__init__(3 * system.natoms)
+        self.system = system
+        self.dtype = np.dtype(dtype)
+        self.precision = precision_of(self.dtype)
+        self.engine = engine_for(system.topology, device)
+        self.device = self.engine.device
+        self._en, self._st = self.engine.new_outputs()
+        self._host = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
+                                 pin_memory=True)
+        self._stage = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
+                                  device=self.device)
+        self.last_breakdown = None
+        self.evaluations = 0
+
+    def initial_point(self):
+        return torch.from_numpy(np.ascontiguousarray(self.system.coords).reshape(-1)).to(
+            self.device)
+
+    def _coerce(self, x):
+        if isinstance(x, torch.Tensor):
+            if x.device != self.device or x.dtype != torch.float64:
+                x = x.to(device=self.device, dtype=torch.float64)
+            return x.contiguous()
+        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(
+            self.device)
+
+    def _out(self, g):
+        return g
+
+    def _run(self, x, grad):
+        n = self.system.natoms
+        g = torch.empty(3 * n, dtype=torch.float64, device=self.device) if grad else None
+        self.engine.eval(x.view(n, 3), self.precision, grad=None if g is None else g.view(n, 3),
+                         energies=self._en, status=self._st)
+        # one 104-byte readback: 5 energies + 8 status words
+        self._stage[:N.FFM_NTERMS].copy_(self._en)
+        self._stage[N.FFM_NTERMS:].copy_(self._st.view(torch.float64))
+        self._host.copy_(self._stage)
+        vals = self._host.numpy()
+        en = vals[:N.FFM_NTERMS].copy()
+        st = vals[N.FFM_NTERMS:].view(np.int64).copy()
+        self.evaluations += 1
+        raise_status(self.system, st, grad=grad)
+        self.last_breakdown = en
+        f = float(en[0]) + float(en[1]) + float(en[2]) + float(en[3]) + float(en[4])
+        return f, g
+
+    def _value(self, x):
+        return self._run(x, False)[0]
+
+    def _gradient(self, x):
+        return self._run(x, True)[1]
+
+    def _value_and_gradient(self, x):
+        return self._run(x, True)

@@ -1,0 +1,197 @@
+"""Generate the golden vectors that pin the CPU oracle and the B200 path.
+
+Runs ONLY in the build container, where the reference package is importable
+from /root/reference (never on the GPU box).  It builds each case with the
+reference's own constructors, evaluates it with the reference's own energy
+layer (numba backend, the reference default; numpy backend where noted),
+and stores inputs and outputs in tests/golden/golden_v1.npz.
+
+    python tests/golden/make_golden.py
+
+Cases (reference call sites in brackets):
+  chain10      make_chain_system(10, 42)           [tests/conftest.py chain10]
+  chain14      make_chain_system(14, 3)            [tests/test_kernels_backends.py]
+  cloud24      two_cluster_system(5, 24, 12.0)     [tests/test_kernels_backends.py]
+  cloud24c7    same with a 7 A cutoff              [kernels nb_* with cutoff 7]
+  explicit8    excluded + scaled policy, 8 atoms   [tests/test_energy.py]
+  chain200     make_chain_system(200, 1, 0.25)
+  globule1500  paper_1810_03358_b200.synth.make_globule_system(1500), rebuilt
+               as an ffmin system
+  chain12cut   make_chain_system(12, 4, cutoff=4.0)
+plus error cases (coincident pair, degenerate angle / dihedral), single-atom
+move deltas, float32 evaluations, and an L-BFGS run on the 500-atom chain of
+BASELINE.json configs[0].
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+REPO = Path(__file__).resolve().parents[2]
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, "/root/reference/pkg/tests")
+
+import ffmin  # noqa: E402
+from ffmin.energy import EnergyEvaluationError, energy_and_gradient, energy_total  # noqa: E402
+from ffmin.energy import exact_delta_atom_move  # noqa: E402
+from ffmin.kernels import NUMBA_BACKEND, NUMPY_BACKEND  # noqa: E402
+from ffmin.model import AngleTerm, AtomSpec, BondTerm, DihedralTerm  # noqa: E402
+from ffmin.model import MolecularSystem, NonbondedPolicy  # noqa: E402
+from ffmin.optimizers import StopCriteria, lbfgs, make_linesearch  # noqa: E402
+from ffmin.oracle import MolecularOracle  # noqa: E402
+from ffmin.synth import make_chain_system  # noqa: E402
+
+import paper_1810_03358_b200.synth as our_synth  # noqa: E402
+
+OUT = Path(__file__).resolve().parent / "golden_v1.npz"
+store = {}
+
+
+def put_system(name, s):
+    p = s.arrays()
+    nb = s.nonbonded
+    ex, sc = sorted(nb.excluded), sorted(nb.scaled14)
+    store[f"{name}/coords"] = s.coords
+    for k in ("q", "sigma", "epsilon", "bond_idx", "bond_K", "bond_r0", "ang_idx", "ang_K",
+              "ang_t0", "dih_idx", "dih_V"):
+        store[f"{name}/{k}"] = np.asarray(p[k])
+    store[f"{name}/excluded"] = np.array(ex, np.int64).reshape(-1, 2)
+    store[f"{name}/scaled14"] = np.array(sc, np.int64).reshape(-1, 2)
+    store[f"{name}/s14"] = np.array(nb.s14)
+    store[f"{name}/cutoff"] = np.array(-1.0 if nb.cutoff is None else nb.cutoff)
+
+
+def put_eval(name, s, tag="", backend=None):
+    for dt, suffix in ((np.float64, "f64"), (np.float32, "f32")):
+        bd = energy_total(s, dt, backend)
+        store[f"{name}/energy_{suffix}{tag}"] = np.array(
+            [bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        bd2, g = energy_and_gradient(s, dt, backend)
+        store[f"{name}/grad_{suffix}{tag}"] = np.asarray(g, np.float64)
+        store[f"{name}/egrad_{suffix}{tag}"] = np.array(
+            [bd2.stretch, bd2.bend, bd2.torsion, bd2.coulomb, bd2.vdw])
+
+
+def two_cluster(seed, n, gap):
+    from conftest import two_cluster_system
+    return two_cluster_system(seed=seed, n=n, gap=gap)
+
+
+def main():
+    t0 = time.time()
+    cases = {}
+    cases["chain10"] = make_chain_system(10, seed=42, strain=0.3)
+    cases["chain14"] = make_chain_system(14, seed=3, strain=0.3)
+    cases["cloud24"] = two_cluster(5, 24, 12.0)
+    c24 = cases["cloud24"]
+    cases["cloud24c7"] = MolecularSystem(atoms=c24.atoms, coords=c24.coords,
+                                         nonbonded=NonbondedPolicy.no_exclusions(7.0))
+    rng = np.random.default_rng(11)
+    atoms = tuple(AtomSpec(i, f"A{i}", q=float(rng.uniform(-0.5, 0.5)),
+                           sigma=float(rng.uniform(2.8, 3.6)),
+                           epsilon=float(rng.uniform(0.1, 0.9))) for i in range(8))
+    cases["explicit8"] = MolecularSystem(
+        atoms=atoms, coords=rng.uniform(0.0, 6.0, (8, 3)),
+        nonbonded=NonbondedPolicy(excluded=frozenset({(0, 1), (2, 3)}),
+                                  scaled14=frozenset({(0, 3)}), s14=0.5))
+    cases["chain200"] = make_chain_system(200, seed=1, strain=0.25)
+    cases["chain12cut"] = make_chain_system(12, seed=4, strain=0.3, cutoff=4.0)
+
+    # our array-built globule, rebuilt as a reference system
+    g = our_synth.make_globule_system(1500, seed=0)
+    t = g.topology
+    ref_g = MolecularSystem(
+        atoms=tuple(AtomSpec(i, f"C{i}", float(t.q[i]), float(t.sigma[i]), float(t.epsilon[i]))
+                    for i in range(t.natoms)),
+        coords=g.coords,
+        bonds=tuple(BondTerm(int(i), int(j), float(k), float(r))
+                    for (i, j), k, r in zip(t.bond_idx, t.bond_K, t.bond_r0)),
+        angles=tuple(AngleTerm(int(i), int(j), int(k), float(kk), float(a))
+                     for (i, j, k), kk, a in zip(t.ang_idx, t.ang_K, t.ang_t0)),
+        dihedrals=tuple(DihedralTerm(int(i), int(j), int(k), int(l), *map(float, v))
+                        for (i, j, k, l), v in zip(t.dih_idx, t.dih_V)),
+        nonbonded=ffmin.build_default_exclusions(
+            t.natoms, tuple(BondTerm(int(i), int(j), 1.0, 1.0) for i, j in t.bond_idx), 0.5))
+    cases["globule1500"] = ref_g
+
+    # our chain generator must reproduce the reference draw for draw
+    for seed, n, strain in ((42, 10, 0.3), (3, 14, 0.3), (1, 200, 0.25), (0, 500, 0.3)):
+        a = make_chain_system(n, seed=seed, strain=strain)
+        b = our_synth.make_chain_system(n, seed=seed, strain=strain)
+        pa = a.arrays()
+        tb = b.topology
+        assert np.array_equal(a.coords, b.coords), "chain coords differ"
+        for k, v in (("q", tb.q), ("sigma", tb.sigma), ("epsilon", tb.epsilon),
+                     ("bond_K", tb.bond_K), ("bond_r0", tb.bond_r0), ("ang_K", tb.ang_K),
+                     ("ang_t0", tb.ang_t0), ("dih_V", tb.dih_V)):
+            assert np.array_equal(pa[k], v), f"chain {k} differs (seed {seed})"
+        assert a.nonbonded.excluded == b.nonbonded.excluded
+        assert a.nonbonded.scaled14 == b.nonbonded.scaled14
+    store["meta/chain_generator_identical"] = np.array(1)
+
+    for name, s in cases.items():
+        put_system(name, s)
+        put_eval(name, s)
+        if name in ("chain14", "cloud24"):
+            put_eval(name, s, "_np", NUMPY_BACKEND)
+    store["meta/cases"] = np.array(list(cases), dtype=object).astype(str)
+
+    # error cases
+    c = c24.coords.copy()
+    c[3] = c[11]
+    bad = c24.with_coords(c)
+    put_system("coincident", bad)
+    store["coincident/expect"] = np.array(NUMBA_BACKEND.nb_energy(
+        bad.coords, *[bad.arrays()[k] for k in ("q", "sigma", "epsilon", "scale")],
+        0.0)[2:], np.int64)
+    chain = make_chain_system(10, seed=5, strain=0.2)
+    cc = chain.coords.copy()
+    cc[4] = cc[5] + 0.5 * (cc[5] - cc[6]) / np.linalg.norm(cc[5] - cc[6]) * 1.5  # collinear 4-5-6
+    put_system("collinear", chain.with_coords(cc))
+    msgs = []
+    for fn in (energy_total, energy_and_gradient):
+        try:
+            fn(chain.with_coords(cc))
+            msgs.append("")
+        except EnergyEvaluationError as e:
+            msgs.append(str(e))
+    store["collinear/messages"] = np.array(msgs)
+
+    # single-atom move deltas (exact, O(n))
+    for name in ("chain14", "cloud24", "chain200"):
+        s = cases[name]
+        rng = np.random.default_rng(7)
+        atoms_ = rng.integers(0, s.natoms, 6)
+        deltas = rng.uniform(-0.3, 0.3, (6, 3))
+        vals = [exact_delta_atom_move(s, int(a), d) for a, d in zip(atoms_, deltas)]
+        store[f"{name}/delta_atoms"] = atoms_
+        store[f"{name}/delta_moves"] = deltas
+        store[f"{name}/delta_values"] = np.array(vals)
+
+    # L-BFGS, 500-atom chain (BASELINE.json configs[0]), bounded run
+    s500 = make_chain_system(500, seed=0, strain=0.3)
+    put_system("lbfgs500", s500)
+    stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
+    t1 = time.time()
+    res = lbfgs(MolecularOracle(s500), s500.coords.ravel(), m=3,
+                linesearch=make_linesearch("par"), stop=stop)
+    store["lbfgs500/seconds"] = np.array(time.time() - t1)
+    store["lbfgs500/f_trace"] = np.array([r.f for r in res.trace.records])
+    store["lbfgs500/gn_trace"] = np.array([r.grad_norm for r in res.trace.records])
+    store["lbfgs500/calls"] = np.array([[r.value_calls, r.grad_calls] for r in res.trace.records])
+    store["lbfgs500/final"] = np.array([res.f, res.grad_norm, res.iterations])
+    store["lbfgs500/x"] = res.x
+    store["lbfgs500/status"] = np.array(res.status)
+
+    np.savez_compressed(OUT, **store)
+    print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB) in {time.time() - t0:.1f}s")
+
+
+if __name__ == "__main__":
+    main()
