@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Headline benchmark: all-pairs LJ + Coulomb energy + analytic gradient.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A "step" is one energy + gradient evaluation (one oracle value_and_gradient
+call) of a 100,000-atom synthetic protein-like system (BASELINE.json metric
+"pair-interactions/sec (energy+grad) at N=10k/100k"), FP32 pair arithmetic
+with FP64 accumulation; the FP64 mode is measured alongside.  value = pair
+interactions (N(N-1)/2 per step) per second, whole job, inputs resident in
+HBM; e2e = the same through the public host API (energy_and_gradient on
+pinned NumPy coordinates, copies inside the timed region).
+
+N > 1 (torchrun): the pair triangle is row-sharded over the ranks
+(paper_1810_03358_b200.parallel), gradients/energies all-reduced over
+NVLink with NCCL; strong scaling, timing = max over ranks.
+
+--impl reference times the reference algorithm on the host: the C
+restatement in oracle/ (the reference itself is Python + numba and cannot
+be installed here), all host threads, a bounded row slice per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "pair-interactions/sec (energy+grad)"
+NATOMS = 100_000
+FLOP_PER_PAIR = 38  # 27 FP32 ops (10 of them FMA -> +10) + 1 rsqrt, DESIGN.md
+FMA_SLOTS_PER_PAIR = 26  # FP32 lane-ops on the FMA pipe per pair (13 FFMA2/FMUL2/FADD2)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--natoms", type=int, default=NATOMS)
+    p.add_argument("--no-extras", action="store_true", help="skip the secondary configs")
+    return p.parse_args()
+
+
+def peaks():
+    d = {}
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    # FP32 FMA peak measured on this pool (profiles/r01_pipes_microbench.txt):
+    # 123.2 FMA/clk/SM at 1965 MHz nominal -> 35.83 TFMA/s
+    fma = 35.83e12
+    return d, fma
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    n = args.natoms
+    s = make_globule_system(n, seed=0)
+    A = O.Arrays.from_system(s)
+    threads = O.host_threads()
+    total_pairs = n * (n - 1) // 2
+    # rows [i0, i1) hold sum_{i0 <= i < i1} (n - 1 - i) pairs; five slices of
+    # equal pair count cover the triangle, one slice per step
+    rows = np.arange(n)
+    cum = np.concatenate([[0], np.cumsum(n - 1 - rows)])
+    edges = [int(np.searchsorted(cum, total_pairs * k / 5)) for k in range(6)]
+    edges[-1] = n
+    slices = [(edges[k], edges[k + 1]) for k in range(5)]
+
+    def step(k):
+        i0, i1 = slices[k % 5]
+        t0 = time.perf_counter()
+        O.nb_eval(A, s.coords, True, threads=threads, rows=(i0, i1))
+        O.bonded(A, s.coords, True)
+        return time.perf_counter() - t0, int(cum[i1] - cum[i0])
+
+    for k in range(args.warmup):
+        step(k)
+    tot_t, tot_p = 0.0, 0
+    for k in range(args.steps):
+        dt, npairs = step(k)
+        tot_t += dt
+        tot_p += npairs
+    value = tot_p / tot_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "pairs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"energy+gradient, {n}-atom synthetic protein-like globule",
+                   "natoms": n, "sample": "one fifth of the pair triangle (row slice) per step"},
+        "cpu_baseline": {"value": value, "unit": "pairs/s", "cores": threads, "kind": "port",
+                         "sample": "row slices of the 100k-atom energy+gradient, 1/5 triangle each"},
+        "e2e": {"value": value, "unit": "pairs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.parallel import ShardedSystem, init_from_env
+    from paper_1810_03358_b200.synth import make_globule_system
+    import torch.distributed as dist
+
+    rank, world, local = init_from_env("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = args.natoms
+    s = make_globule_system(n, seed=0)
+    lib = N.load()
+    if world > 1:
+        eng = ShardedSystem(s.topology, device=local)
+        handle = eng.engine.handle
+    else:
+        eng = DeviceSystem(s.topology, local)
+        handle = eng.handle
+    pairs = n * (n - 1) / 2
+    rng = np.random.default_rng(1234)
+    base = np.ascontiguousarray(s.coords)
+    # a fresh geometry per step (small jitter), resident in HBM
+    steps_coords = [torch.from_numpy(base + rng.normal(scale=0.01, size=base.shape)).to(dev)
+                    for _ in range(4)]
+    grad = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    en, st = eng.new_outputs()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def time_device(prec, steps, warmup):
+        for k in range(warmup):
+            eng.eval(steps_coords[k % 4], prec, grad=grad, energies=en, status=st)
+        barrier()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(steps)]
+        nb_ms = []
+        l0 = lib.ffm_launch_count()
+        for k in range(steps):
+            flush.zero_()  # L2 flush between timed steps (outside the events)
+            ev[k][0].record()
+            eng.eval(steps_coords[k % 4], prec, grad=grad, energies=en, status=st,
+                     flags=N.FFM_ENERGY | N.FFM_GRAD | N.FFM_TIME_NB)
+            ev[k][1].record()
+            ms = np.zeros(1, np.float32)
+            N.check(lib.ffm_system_nb_ms(handle, ms.ctypes.data), "nb_ms")
+            nb_ms.append(float(ms[0]))
+        barrier()
+        launches = lib.ffm_launch_count() - l0
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        tot = float(np.sum(step_ms))
+        if world > 1:
+            t = torch.tensor([tot, float(np.mean(nb_ms))], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot, nbm = t.tolist()
+        else:
+            nbm = float(np.mean(nb_ms))
+        assert int(st[0]) == -1, "coincident atoms in the benchmark system"
+        return tot / steps, nbm, launches
+
+    with ClockSampler(local) as clk:
+        ms32, nb32, launches = time_device(N.FFM_F32, args.steps, args.warmup)
+    clocks = clk.summary()
+    ms64, nb64, _ = time_device(N.FFM_F64, max(3, args.steps // 2), 2)
+    value = pairs / (ms32 * 1e-3)
+
+    # ---- e2e through the public API, host buffers (pinned), FP32 mode
+    pinned = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    if world > 1:
+        from paper_1810_03358_b200.parallel import ShardedMolecularOracle
+
+        orc = ShardedMolecularOracle(s, np.float32, device=local)
+    e2e_times = []
+    for k in range(args.warmup + args.steps):
+        pinned.numpy()[:] = steps_coords[k % 4].cpu().numpy()
+        host = pinned.numpy()
+        barrier()
+        t0 = time.perf_counter()
+        if world > 1:
+            f, g = orc.value_and_gradient(host.reshape(-1))
+        else:
+            bd, g = energy_and_gradient(s.with_coords(host), np.float32)
+        t1 = time.perf_counter()
+        if k >= args.warmup:
+            e2e_times.append(t1 - t0)
+    e2e_s = float(np.mean(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+
+    measured, fma_peak = peaks()
+    flop_peak = 2 * fma_peak
+    nb_pairs_per_rank = pairs / world
+    achieved = nb_pairs_per_rank * FLOP_PER_PAIR / (nb32 * 1e-3)
+    # FMA-pipe fraction: FP32 lane-op slots used per second over the pipe's
+    # 128 lane-ops / clk / SM (= fma_peak per second)
+    fma_frac = nb_pairs_per_rank * FMA_SLOTS_PER_PAIR / (nb32 * 1e-3) / fma_peak
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms32,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (pair arithmetic; fp64 accumulation)", "data": "synthetic",
+        "config": {"workload": f"energy+gradient of a {n}-atom synthetic protein-like globule "
+                               "(LJ + Coulomb all pairs, bonded terms, 1-2/1-3 excluded, 1-4 scaled)",
+                   "natoms": n, "pairs_per_step": int(pairs), "parallelism": f"row-shard x{world}",
+                   "l2": "flushed (256 MB write) between timed steps",
+                   "inputs": "fresh jittered geometry per step, resident in HBM"},
+        "value_f64": pairs / (ms64 * 1e-3), "ms_per_step_f64": ms64,
+        "e2e": {"value": pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": n * 3 * 8,
+                "d2h_bytes_per_step": n * 3 * 8 + 5 * 8 + 8 * 8,
+                "api": "paper_1810_03358_b200.energy.energy_and_gradient(system, np.float32)"
+                       if world == 1 else "parallel.ShardedMolecularOracle.value_and_gradient"},
+        "roofline": {"bound": "fp32-fma-pipe", "kernel": "nb_units_kernel<float,GRAD>",
+                     "achieved": achieved / 1e12, "peak": flop_peak / 1e12, "unit": "TFLOP/s",
+                     "frac": achieved / flop_peak, "traffic": None,
+                     "flop_per_pair": FLOP_PER_PAIR, "fma_pipe_frac": fma_frac,
+                     "nb_ms": nb32, "nb_ms_f64": nb64,
+                     "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt"},
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+    }
+
+    if rank == 0 and world == 1:
+        line["cpu_baseline"] = cpu_baseline(s)
+    if not args.no_extras:
+        extras = run_extras(rank, world, local)
+        if rank == 0:
+            line["extras"] = extras
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def cpu_baseline(s):
+    import oracle as O
+
+    A = O.Arrays.from_system(s)
+    threads = O.host_threads()
+    n = s.natoms
+    t0 = time.perf_counter()
+    O.nb_eval(A, s.coords, True, threads=threads)
+    O.bonded(A, s.coords, True)
+    dt = time.perf_counter() - t0
+    return {"value": n * (n - 1) / 2 / dt, "unit": "pairs/s", "cores": threads, "kind": "port",
+            "sample": f"one full {n}-atom energy+gradient (oracle/ffmin_oracle.c, "
+                      f"{threads} threads), {dt:.2f} s"}
+
+
+def run_extras(rank, world, local):
+    """Secondary BASELINE configs, bounded (about a minute)."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    out = {}
+    dev = torch.device("cuda", local)
+    if world == 1:
+        # configs[1]: single evaluation sweep, N = 3k / 10k / 30k, FP64 and FP32
+        sweep = {}
+        for n in (3000, 10000, 30000):
+            s = make_globule_system(n, seed=0)
+            eng = DeviceSystem(s.topology, local)
+            c = torch.from_numpy(np.ascontiguousarray(s.coords)).to(dev)
+            g = torch.empty_like(c)
+            en, st = eng.new_outputs()
+            for prec, tag in ((N.FFM_F32, "f32"), (N.FFM_F64, "f64")):
+                for _ in range(3):
+                    eng.eval(c, prec, grad=g, energies=en, status=st)
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                reps = 20
+                e0.record()
+                for _ in range(reps):
+                    eng.eval(c, prec, grad=g, energies=en, status=st)
+                e1.record()
+                torch.cuda.synchronize()
+                ms = e0.elapsed_time(e1) / reps
+                sweep[f"{n}_{tag}"] = {"ms": ms, "pairs_per_s": n * (n - 1) / 2 / (ms * 1e-3)}
+            eng.close()
+        out["sweep_energy_grad"] = sweep
+        # configs[3]: 1024 candidate geometries of a 5k-atom system per step
+        s = make_globule_system(5000, seed=0)
+        eng = DeviceSystem(s.topology, local)
+        B = 1024
+        rng = np.random.default_rng(0)
+        batch = torch.from_numpy(s.coords[None] + rng.normal(scale=0.02, size=(B,) + s.coords.shape)).to(dev)
+        en, st = eng.new_outputs(B)
+        for _ in range(2):
+            eng.eval_batch(batch, N.FFM_F32, energies=en, status=st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            eng.eval_batch(batch, N.FFM_F32, energies=en, status=st)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        out["batched_candidates"] = {"candidates": B, "natoms": 5000, "ms_per_step": ms,
+                                     "pairs_per_s": B * 5000 * 4999 / 2 / (ms * 1e-3),
+                                     "precision": "f32", "what": "energy only"}
+        eng.close()
+        # configs[0]: L-BFGS on the 500-atom chain, against the reference run
+        out["lbfgs500"] = lbfgs500()
+    return out
+
+
+def lbfgs500():
+    import torch
+
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import StopCriteria, lbfgs, make_linesearch
+    from paper_1810_03358_b200.synth import make_chain_system
+
+    G = np.load(ROOT / "tests" / "golden" / "golden_v1.npz")
+    s = make_chain_system(500, seed=0, strain=0.3)
+    stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
+    lbfgs(MolecularOracle(s), s.coords.ravel(), m=3, linesearch=make_linesearch("par"),
+          stop=StopCriteria(max_iterations=5, gradient_norm_rtol=0.0))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = lbfgs(MolecularOracle(s), s.coords.ravel(), m=3, linesearch=make_linesearch("par"),
+                stop=stop)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    ref_f = float(G["lbfgs500/final"][0])
+    return {"iterations": res.iterations, "status": res.status, "f": res.f, "ref_f": ref_f,
+            "rel_diff_f": abs(res.f - ref_f) / abs(ref_f), "seconds": dt,
+            "ref_seconds_numba_1core": float(G["lbfgs500/seconds"]),
+            "oracle_calls": [res.trace.records[-1].value_calls, res.trace.records[-1].grad_calls],
+            "ref_oracle_calls": G["lbfgs500/calls"][-1].tolist()}
+
+
+if __name__ == "__main__":
+    main()

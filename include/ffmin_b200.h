@@ -45,6 +45,7 @@ extern "C" {
 #define FFM_GRAD 2
 #define FFM_NO_NB 4     /* skip the nonbonded terms (all pairs + scaled 1-4) */
 #define FFM_NO_TERMS 8  /* skip the bonded terms (stretch, bend, torsion)    */
+#define FFM_TIME_NB 16  /* record CUDA events around the pair sweep          */
 
 /* status words (int64[8] per evaluation) */
 #define FFM_ST_NB_BAD_I 0   /* first coincident nonbonded pair, -1 clean */
@@ -82,6 +83,21 @@ int ffm_system_set_terms(ffm_system_t* sys, int64_t nbond, const int64_t* bond_i
                          const double* dih_V_h);
 
 int ffm_system_destroy(ffm_system_t* sys);
+
+/* Row sharding over `nranks` GPUs (one process per GPU): this handle then
+ * evaluates only its share of the S x S super-units of the pair triangle
+ * (units dealt round-robin, heaviest first) and, on rank 0 only, the O(N)
+ * bonded / 1-4 terms.  Gradients and energies of an evaluation are partial
+ * sums; the caller all-reduces them (NCCL over NVLink in
+ * paper_1810_03358_b200.parallel).  nranks = 1 restores the full sweep. */
+int ffm_system_set_shard(ffm_system_t* sys, int rank, int nranks);
+
+/* Device time of the pair sweep of the last FFM_TIME_NB evaluation
+ * (CUDA events on the evaluation's stream; synchronises on them). */
+int ffm_system_nb_ms(ffm_system_t* sys, float* ms_h);
+
+/* Number of kernels this library has launched in the process. */
+long long ffm_launch_count(void);
 
 /* info[0..7] = n, padded n, super-unit S, blocks, units, special tiles,
  * scaled pairs, device */

@@ -22,8 +22,12 @@ SOURCES = ("ffm_pairs.cu", "ffm_terms.cu", "ffm_vec.cu", "ffm_capi.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
 )
+# per-file extras: the bonded terms are evaluated without FMA contraction so
+# that degeneracy thresholds (ffmin/kernels.py:130-140) see the same roundoff
+# as the reference's CPU arithmetic
+EXTRA = {"ffm_terms.cu": ("-fmad=false",)}
 
 
 def nvcc_path() -> str:
@@ -46,15 +50,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = LIB_DIR / (Path(src).stem + ".o")
+        cmd = [nvcc_path(), *NVCC_FLAGS, *EXTRA.get(src, ()), "-c", "-o", str(obj),
+               str(CSRC / src)]
+        _run(cmd, verbose)
+        objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
+    _run([nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
+          *objs], verbose)
+    os.replace(tmp, LIB)
+    for o in objs:
+        os.remove(o)
+    return LIB
+
+
+def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
-    os.replace(tmp, LIB)
-    return LIB
 
 
 if __name__ == "__main__":

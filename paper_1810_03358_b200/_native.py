@@ -18,6 +18,9 @@ FFM_F64 = 0
 FFM_F32 = 1
 FFM_ENERGY = 1
 FFM_GRAD = 2
+FFM_NO_NB = 4
+FFM_NO_TERMS = 8
+FFM_TIME_NB = 16
 FFM_NTERMS = 5
 FFM_STATUS_WORDS = 8
 ST_NB_BAD_I, ST_NB_BAD_J, ST_BOND, ST_ANGLE, ST_DIHEDRAL = 0, 1, 2, 3, 4
@@ -34,7 +37,10 @@ SIGNATURES = {
     "ffm_system_create": (_I, [C.POINTER(_P), _I, _I64, _P, _P, _P, _I64, _P, _P, _P, _D]),
     "ffm_system_set_terms": (_I, [_P, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P]),
     "ffm_system_destroy": (_I, [_P]),
+    "ffm_system_set_shard": (_I, [_P, _I, _I]),
     "ffm_system_info": (_I, [_P, _P]),
+    "ffm_system_nb_ms": (_I, [_P, _P]),
+    "ffm_launch_count": (C.c_longlong, []),
     "ffm_eval": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "ffm_eval_host": (_I, [_P, _I, _I, _P, _P, _P, _P]),
     "ffm_eval_batch": (_I, [_P, _I, _I64, _P, _P, _P, _P]),

@@ -14,6 +14,8 @@
 
 using namespace ffm;
 
+std::atomic<long long> ffm::g_launch_count{0};
+
 namespace {
 
 thread_local std::string g_err;
@@ -41,7 +43,8 @@ int upload(T** dst, const std::vector<T>& src) {
 }
 
 struct Work {
-  void* pos = nullptr;     // [batch][np] Vec4
+  void* pos = nullptr;     // [batch][np] Vec4 (j side)
+  void* ipos = nullptr;    // [batch][4][np/2] pairs (i side)
   int pos_batch = 0;
   void* ipart = nullptr;   // [nunits][3][S]
   void* jpart = nullptr;
@@ -74,6 +77,8 @@ struct ffm_system {
   double* d_qt = nullptr;    // q sqrt(C), [np]
   float2* d_lj32 = nullptr;  // [np]
   double2* d_lj64 = nullptr;
+  float* d_ilj32 = nullptr;  // LJ in the i-side pair layout, [2][np/2] pairs
+  double* d_ilj64 = nullptr;
   double* d_q = nullptr;
   double* d_sigma = nullptr;
   double* d_eps = nullptr;
@@ -92,10 +97,16 @@ struct ffm_system {
   int* d_slot_idx = nullptr;
   int* d_aterm_ptr = nullptr;
   int* d_aterm_idx = nullptr;
+  // row sharding (ffm_system_set_shard): units u with u % nranks == rank
+  int rank = 0, nranks = 1;
+  int* d_unit_list = nullptr;
   // host copies needed to rebuild the term plan
   std::vector<std::pair<int, int>> scaled;  // (i, j)
   std::vector<double> scaled_s;
   Work w[2];  // [precision]
+  // FFM_TIME_NB: events around the pair sweep of the last evaluation
+  cudaEvent_t ev_nb0 = nullptr, ev_nb1 = nullptr;
+  bool timed = false;
   // host-path staging
   double* h_coords_d = nullptr;
   double* h_grad_d = nullptr;
@@ -108,15 +119,17 @@ namespace {
 void free_all(ffm_system* s) {
   void* ptrs[] = {s->d_unit_rc, s->d_unit_index, s->d_spt_ptr, s->d_spt_m, s->d_spt_mask,
                   s->d_sp_ptr, s->d_sp_j, s->d_sp_s, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
-                  s->d_qt, s->d_lj32, s->d_lj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
+                  s->d_qt, s->d_lj32, s->d_lj64, s->d_ilj32, s->d_ilj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
                   s->d_sc_s, s->d_bond_idx, s->d_bond_K, s->d_bond_r0, s->d_ang_idx,
                   s->d_ang_K, s->d_ang_t0, s->d_dih_idx, s->d_dih_V, s->d_slot_ptr,
                   s->d_slot_idx, s->d_aterm_ptr, s->d_aterm_idx, s->h_coords_d, s->h_grad_d,
-                  s->h_en_d, s->h_st_d};
+                  s->h_en_d, s->h_st_d, s->d_unit_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
+  if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
-    void* wp[] = {w.pos, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
+    void* wp[] = {w.pos, w.ipos, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
     for (void* p : wp)
       if (p) cudaFree(p);
   }
@@ -251,24 +264,31 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   const size_t tsz = f64 ? 8 : 4;
   if (w.pos_batch < batch) {
     if (w.pos) cudaFree(w.pos);
-    w.pos = nullptr;
+    if (w.ipos) cudaFree(w.ipos);
+    w.pos = w.ipos = nullptr;
     const size_t bytes = (size_t)batch * p.np * 4 * tsz;
-    if (cudaMalloc(&w.pos, bytes) != cudaSuccess)
+    if (cudaMalloc(&w.pos, bytes) != cudaSuccess || cudaMalloc(&w.ipos, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for packed coordinates");
     w.pos_batch = batch;
-    FFM_CUDA(launch_pad(p.n, p.np, batch, f64, w.pos, 0));
+    FFM_CUDA(launch_pad(p.n, p.np, batch, f64, w.pos, w.ipos, 0));
     FFM_CUDA(cudaDeviceSynchronize());
   }
+  // partial slots of units another rank owns are never written: they must
+  // read as zero in the gather and the energy reduction
   if (grad && !w.ipart) {
     const size_t bytes = (size_t)p.nunits * 3 * p.S * tsz;
     if (cudaMalloc(&w.ipart, bytes) != cudaSuccess || cudaMalloc(&w.jpart, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for gradient partials");
+    FFM_CUDA(cudaMemset(w.ipart, 0, bytes));
+    FFM_CUDA(cudaMemset(w.jpart, 0, bytes));
   }
   if (w.e_batch < batch) {
     if (w.epart) cudaFree(w.epart);
     w.epart = nullptr;
-    if (cudaMalloc(&w.epart, (size_t)batch * p.nunits * 3 * sizeof(double)) != cudaSuccess)
+    const size_t bytes = (size_t)batch * p.nunits * 3 * sizeof(double);
+    if (cudaMalloc(&w.epart, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for energy partials");
+    FFM_CUDA(cudaMemset(w.epart, 0, bytes));
     w.e_batch = batch;
   }
   if (w.te_batch < batch) {
@@ -328,6 +348,8 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   p.np = p.nb * p.S;
   p.nunits = p.nb * (p.nb + 1) / 2;
   p.has_cutoff = cutoff > 0.0 ? 1 : 0;
+  p.unit_list = nullptr;
+  p.nlaunch = p.nunits;
   p.cut2 = cutoff > 0.0 ? cutoff * cutoff : 0.0;
   int rc;
 #define FFM_TRY(x)     \
@@ -358,6 +380,13 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_qt, qt));
   FFM_TRY(upload(&s->d_lj32, lj32));
   FFM_TRY(upload(&s->d_lj64, lj64));
+  if (cudaMalloc(&s->d_ilj32, (size_t)p.np * 2 * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&s->d_ilj64, (size_t)p.np * 2 * sizeof(double)) != cudaSuccess)
+    FFM_TRY(fail(FFM_ENOMEM, "cudaMalloc failed for LJ records"));
+  if (launch_ilj(p.np, false, s->d_lj32, s->d_ilj32, 0) != cudaSuccess ||
+      launch_ilj(p.np, true, s->d_lj64, s->d_ilj64, 0) != cudaSuccess ||
+      cudaDeviceSynchronize() != cudaSuccess)
+    FFM_TRY(fail(FFM_ECUDA, "building the LJ pair records failed"));
   FFM_TRY(upload(&s->d_q, qv));
   FFM_TRY(upload(&s->d_sigma, sg));
   FFM_TRY(upload(&s->d_eps, ep));
@@ -494,6 +523,53 @@ int ffm_system_destroy(ffm_system_t* s) {
   return FFM_OK;
 }
 
+int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
+  if (!s || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(FFM_EINVAL, "bad shard (rank, nranks)");
+  DeviceGuard guard(s->device);
+  FFM_CUDA(cudaDeviceSynchronize());
+  if (s->d_unit_list) cudaFree(s->d_unit_list);
+  s->d_unit_list = nullptr;
+  s->rank = rank;
+  s->nranks = nranks;
+  if (nranks == 1) {
+    s->plan.unit_list = nullptr;
+    s->plan.nlaunch = s->plan.nunits;
+  } else {
+    // units are ordered heavy (off-diagonal) first: dealing them round-robin
+    // gives every rank the same work to within one unit
+    std::vector<int> mine;
+    for (int u = rank; u < s->plan.nunits; u += nranks) mine.push_back(u);
+    int rc = upload(&s->d_unit_list, mine);
+    if (rc) return rc;
+    s->plan.unit_list = s->d_unit_list;
+    s->plan.nlaunch = (int)mine.size();
+  }
+  // drop the partial buffers so stale slots of other ranks read as zero
+  for (auto& w : s->w) {
+    for (void** p : {&w.ipart, &w.jpart})
+      if (*p) {
+        cudaFree(*p);
+        *p = nullptr;
+      }
+    if (w.epart) cudaFree(w.epart);
+    w.epart = nullptr;
+    w.e_batch = 0;
+  }
+  return FFM_OK;
+}
+
+int ffm_system_nb_ms(ffm_system_t* s, float* ms) {
+  if (!s || !ms) return fail(FFM_EINVAL, "NULL argument");
+  if (!s->timed) return fail(FFM_EINVAL, "last evaluation was not timed (FFM_TIME_NB)");
+  DeviceGuard guard(s->device);
+  FFM_CUDA(cudaEventSynchronize(s->ev_nb1));
+  FFM_CUDA(cudaEventElapsedTime(ms, s->ev_nb0, s->ev_nb1));
+  return FFM_OK;
+}
+
+long long ffm_launch_count(void) { return g_launch_count.load(); }
+
 int ffm_system_info(const ffm_system_t* s, int64_t* info) {
   if (!s || !info) return fail(FFM_EINVAL, "NULL argument");
   info[0] = s->plan.n;
@@ -523,10 +599,24 @@ int ffm_eval(ffm_system_t* s, int precision, int flags, const double* coords_d,
   const bool do_nb = !(flags & FFM_NO_NB), do_terms = !(flags & FFM_NO_TERMS);
   const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
   TermPlanDev tp = s->tp;  // the term types this call evaluates
-  if (!do_terms) tp.nbond = tp.nangle = tp.ndih = 0;
-  if (!do_nb) tp.nscaled = 0;
-  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, status_d, st));
-  if (do_nb) FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipart, w.jpart, w.epart, 1, st));
+  if (!do_terms || s->rank != 0) tp.nbond = tp.nangle = tp.ndih = 0;  // O(N) terms: rank 0
+  if (!do_nb || s->rank != 0) tp.nscaled = 0;
+  const void* ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
+  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
+                       status_d, st));
+  const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
+  if (time_nb) {
+    if (!s->ev_nb0) {
+      FFM_CUDA(cudaEventCreate(&s->ev_nb0));
+      FFM_CUDA(cudaEventCreate(&s->ev_nb1));
+    }
+    FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
+  }
+  if (do_nb)
+    FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.ipart, w.jpart, w.epart,
+                       1, st));
+  if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
+  s->timed = time_nb;
   FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
   if (grad && s->plan.n > 0)
     FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart,
@@ -580,10 +670,15 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   const bool f64 = precision == FFM_F64;
   const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
   const int B = (int)batch;
-  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, B, f64, coords_d, s->d_qt, w.pos, status_d, st));
-  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, nullptr, nullptr, w.epart, B, st));
-  FFM_CUDA(launch_terms(s->tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
-  FFM_CUDA(launch_reduce(s->plan.nunits, s->tp, B, w.epart, w.term_e, energies_d, status_d, st));
+  const void* ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
+  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, B, f64, coords_d, s->d_qt, w.pos, w.ipos,
+                       status_d, st));
+  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, w.ipos, ilj, nullptr, nullptr, w.epart,
+                     B, st));
+  TermPlanDev tp = s->tp;
+  if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
+  FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
+  FFM_CUDA(launch_reduce(s->plan.nunits, tp, B, w.epart, w.term_e, energies_d, status_d, st));
   FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                          s->d_sp_s, status_d, st));
   return FFM_OK;

@@ -19,8 +19,8 @@ constexpr double kDegenerateEps = 1e-12;
 
 // Pair-kernel tiling:
 //   a warp tile is 128 i-atoms (4 per lane, two packed pairs) x 32 j-atoms;
-//   a CTA is 4 warps and owns one super-unit of S x S atoms.
-constexpr int kWarps = 4;
+//   a CTA is 8 warps and owns one super-unit of S x S atoms.
+constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kIB = 128;  // i-sub-block
 constexpr int kJB = 32;   // j-block

@@ -3,22 +3,34 @@
 #include "ffm_common.cuh"
 #include "ffm_plan.cuh"
 
+#include <atomic>
+
 namespace ffm {
+
+// every kernel launch of the engine, for the benchmark's gpu_launches claim
+extern std::atomic<long long> g_launch_count;
+inline void count_launch(long long k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
 
 size_t nb_smem_bytes(int S, bool fp64, bool grad);
 
-// all-pairs sweep over every super-unit; batch > 1 only without GRAD
+// all-pairs sweep over every super-unit; batch > 1 only without GRAD.
+// pos/lj: j-side records; ipos/ilj: the same data in the i-side pair layout
 cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
-                      const void* lj, void* ipart, void* jpart, double* epart, int batch,
-                      cudaStream_t st);
+                      const void* lj, const void* ipos, const void* ilj, void* ipart,
+                      void* jpart, double* epart, int batch, cudaStream_t st);
 
-// coords (fp64, [batch][n][3]) -> padded pos records of the chosen precision;
-// also resets the status words of every batch entry.
+// coords (fp64, [batch][n][3]) -> padded pos / ipos records of the chosen
+// precision; also resets the status words of every batch entry.
 cudaError_t launch_pack(int n, int np, int batch, bool fp64, const double* coords,
-                        const double* qt, void* pos, int64_t* status, cudaStream_t st);
+                        const double* qt, void* pos, void* ipos, int64_t* status,
+                        cudaStream_t st);
 
 // fills the padding atoms (zero charge / LJ, far apart) once per buffer
-cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, cudaStream_t st);
+cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipos,
+                       cudaStream_t st);
+
+// LJ (a, b) records -> i-side pair layout (once per system)
+cudaError_t launch_ilj(int np, bool fp64, const void* lj, void* ilj, cudaStream_t st);
 
 // bonded + scaled-pair terms in FP64; writes term energies, slot forces
 cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,

@@ -34,7 +34,24 @@ __device__ __forceinline__ Pk<double>::V shfl_rot<double>(Pk<double>::V v, int s
   return {__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src)};
 }
 
-// One 128 x 32 warp tile.  MASKED tiles carry per-lane activity bitmasks
+// i-side pair loads: 64-bit (fp32 pair) / 128-bit (fp64 pair) straight into
+// the packed registers
+template <typename T>
+__device__ __forceinline__ typename Pk<T>::V ld_pair(const T* __restrict__ base, int64_t r);
+template <>
+__device__ __forceinline__ Pk<float>::V ld_pair<float>(const float* __restrict__ base, int64_t r) {
+  return __ldg(reinterpret_cast<const unsigned long long*>(base) + r);
+}
+template <>
+__device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restrict__ base,
+                                                          int64_t r) {
+  const double2 d = __ldg(reinterpret_cast<const double2*>(base) + r);
+  return {d.x, d.y};
+}
+
+// One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
+// j-block, so step t of lane l reads entry l + t (atom (l + t) mod 32) with
+// an immediate offset.  MASKED tiles carry per-lane activity bitmasks
 // (diagonal i < j condition and/or special pairs); inactive pairs are
 // neutralised (r2 -> 1, coefficients -> 0) so they contribute exactly zero.
 template <typename T, bool GRAD, bool CUTOFF, bool MASKED>
@@ -51,11 +68,12 @@ __device__ __forceinline__ void warp_tile(
   using V = typename P::V;
   V gx = P::zero(), gy = P::zero(), gz = P::zero();
   const int src = (lane + 1) & 31;
-#pragma unroll 4
+  J += lane;
+  L += lane;
+#pragma unroll 8
   for (int t = 0; t < 32; ++t) {
-    const int jj = (lane + t) & 31;
-    const auto pj = J[jj];  // (-x, -y, -z, q~)
-    const auto lj = L[jj];  // (a, -b)
+    const auto pj = J[t];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
+    const auto lj = L[t];  // (a, -b)
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       V dx = P::add(xi[pp], P::bc(pj.x));
@@ -68,6 +86,7 @@ __device__ __forceinline__ void warp_tile(
       V nB = P::mul(bi[pp], P::bc(lj.y));
       V Q = P::mul(qi[pp], P::bc(pj.w));
       if (MASKED) {
+        const int jj = (lane + t) & 31;
         const bool a0 = (mk[2 * pp] >> jj) & 1u;
         const bool a1 = (mk[2 * pp + 1] >> jj) & 1u;
         r2 = P::make(a0 ? P::lo(r2) : T(1), a1 ? P::hi(r2) : T(1));
@@ -111,18 +130,17 @@ __device__ __forceinline__ void warp_tile(
         gz = P::fma(g, dz, gz);
       }
     }
-    if (GRAD && t < 31) {
+    if (GRAD) {  // the j column moves one lane down with its atom
       gx = shfl_rot<T>(gx, src);
       gy = shfl_rot<T>(gy, src);
       gz = shfl_rot<T>(gz, src);
     }
   }
   if (GRAD) {
-    // after 31 rotations lane l holds the column of j = (l + 31) mod 32
-    const int jj = (lane + 31) & 31;
-    jacc[jj] += P::lo(gx) + P::hi(gx);
-    jacc[jacc_stride + jj] += P::lo(gy) + P::hi(gy);
-    jacc[2 * jacc_stride + jj] += P::lo(gz) + P::hi(gz);
+    // after 32 rotations lane l holds the column of j = l again
+    jacc[lane] += P::lo(gx) + P::hi(gx);
+    jacc[jacc_stride + lane] += P::lo(gy) + P::hi(gy);
+    jacc[2 * jacc_stride + lane] += P::lo(gz) + P::hi(gz);
   }
 }
 
@@ -152,10 +170,10 @@ __device__ __forceinline__ double block_min(double v, double* red) {
 // grid = (nunits, batch).  ipart/jpart: [nunits][3][S] gradient partials
 // (GRAD only); epart: [batch][nunits][3] = (coulomb, vdw, min r^2).
 template <typename T, bool GRAD, bool CUTOFF>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 4 : 2)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1)
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
-                const typename Vec2T<T>::type* __restrict__ lj,
-                T* __restrict__ ipart, T* __restrict__ jpart,
+                const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
+                const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,
                 double* __restrict__ epart) {
   using P = Pk<T>;
   using V = typename P::V;
@@ -164,34 +182,34 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kWarps];
   const int S = plan.S;
-  V4* sj = reinterpret_cast<V4*>(smem_raw);
-  V2* sl = reinterpret_cast<V2*>(sj + S);
-  T* jacc = reinterpret_cast<T*>(sl + S);  // [3][S]      (GRAD)
-  T* ired = jacc + 3 * S;                  // [kWarps][3][kIB] (GRAD)
+  V4* sj = reinterpret_cast<V4*>(smem_raw);   // [2S]: each j-block stored twice
+  V2* sl = reinterpret_cast<V2*>(sj + 2 * S);  // [2S]
+  T* jacc = reinterpret_cast<T*>(sl + 2 * S);  // [3][S]      (GRAD)
+  T* ired = jacc + 3 * S;                      // [kWarps][3][kIB] (GRAD)
 
-  const int u = blockIdx.x;
+  const int u = plan.unit_list ? plan.unit_list[blockIdx.x] : blockIdx.x;
   const int bidx = blockIdx.y;
   pos += (size_t)bidx * plan.np;
+  ipos += (size_t)bidx * 4 * plan.np;
+  const int64_t half = plan.np >> 1;
   const int2 rc = plan.unit_rc[u];
   const int i0 = rc.x * S, j0 = rc.y * S;
   const bool diag = rc.x == rc.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  for (int a = tid; a < S; a += kThreads) {
-    V4 p = pos[j0 + a];
+  for (int e = tid; e < 2 * S; e += kThreads) {
+    const int a = j0 + (e >> 6) * kJB + (e & 31);
+    V4 p = pos[a];
     p.x = -p.x;
     p.y = -p.y;
     p.z = -p.z;
-    sj[a] = p;
-    V2 l = lj[j0 + a];
+    sj[e] = p;
+    V2 l = lj[a];
     l.y = -l.y;
-    sl[a] = l;
-    if (GRAD) {
-      jacc[a] = T(0);
-      jacc[S + a] = T(0);
-      jacc[2 * S + a] = T(0);
-    }
+    sl[e] = l;
   }
+  if (GRAD)
+    for (int a = tid; a < 3 * S; a += kThreads) jacc[a] = T(0);
   __syncthreads();
 
   double Ec = 0.0, Ev = 0.0;
@@ -200,25 +218,22 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   const int nsub = S / kIB, njb = S / kJB;
   for (int ks = 0; ks < nsub; ++ks) {
     const int ib = i0 + ks * kIB;
+    const int kk = ib / kIB;
     V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
-      const V4 p0 = pos[ib + lane + 64 * pp];
-      const V4 p1 = pos[ib + lane + 64 * pp + 32];
-      const V2 l0 = lj[ib + lane + 64 * pp];
-      const V2 l1 = lj[ib + lane + 64 * pp + 32];
-      xi[pp] = P::make(p0.x, p1.x);
-      yi[pp] = P::make(p0.y, p1.y);
-      zi[pp] = P::make(p0.z, p1.z);
-      qi[pp] = P::make(p0.w, p1.w);
-      ai[pp] = P::make(l0.x, l1.x);
-      bi[pp] = P::make(l0.y, l1.y);
+      const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
+      xi[pp] = ld_pair<T>(ipos, r);
+      yi[pp] = ld_pair<T>(ipos, half + r);
+      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+      ai[pp] = ld_pair<T>(ilj, r);
+      bi[pp] = ld_pair<T>(ilj, half + r);
     }
     V F[2][3];
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
     V ec2 = P::zero(), ev2 = P::zero();
-    const int kk = ib / kIB;
     const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];
 
     for (int m = warp; m < njb; m += kWarps) {
@@ -243,12 +258,14 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
         }
       }
       T* jc = jacc + m * kJB;
+      const V4* J = sj + m * 2 * kJB;
+      const V2* L = sl + m * 2 * kJB;
       if (masked)
-        warp_tile<T, GRAD, CUTOFF, true>(sj + m * kJB, sl + m * kJB, lane, xi, yi, zi, qi,
-                                         ai, bi, F, ec2, ev2, jc, S, mk, cut2, minr2);
+        warp_tile<T, GRAD, CUTOFF, true>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jc,
+                                         S, mk, cut2, minr2);
       else
-        warp_tile<T, GRAD, CUTOFF, false>(sj + m * kJB, sl + m * kJB, lane, xi, yi, zi,
-                                          qi, ai, bi, F, ec2, ev2, jc, S, mk, cut2, minr2);
+        warp_tile<T, GRAD, CUTOFF, false>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jc,
+                                          S, mk, cut2, minr2);
       Ec += double(P::lo(ec2)) + double(P::hi(ec2));
       Ev += double(P::lo(ev2)) + double(P::hi(ev2));
       ec2 = P::zero();
@@ -266,26 +283,20 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
         }
       }
       __syncthreads();
-      {
-        const int a = tid;  // kThreads == kIB
+      for (int x = tid; x < 3 * kIB; x += kThreads) {
+        const int c = x / kIB, a = x - c * kIB;
+        T s = T(0);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          T s = T(0);
-#pragma unroll
-          for (int w = 0; w < kWarps; ++w) s += ired[w * 3 * kIB + c * kIB + a];
-          // F = -gradient
-          ipart[((size_t)u * 3 + c) * S + ks * kIB + a] = -s;
-        }
+        for (int w = 0; w < kWarps; ++w) s += ired[w * 3 * kIB + x];
+        // F = -gradient
+        ipart[((size_t)u * 3 + c) * S + ks * kIB + a] = -s;
       }
       __syncthreads();
     }
   }
   if (GRAD) {
     __syncthreads();
-    for (int a = tid; a < S; a += kThreads) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) jpart[((size_t)u * 3 + c) * S + a] = jacc[c * S + a];
-    }
+    for (int x = tid; x < 3 * S; x += kThreads) jpart[(size_t)u * 3 * S + x] = jacc[x];
   }
   const double ec = block_sum<T>(Ec, red);
   const double ev = block_sum<T>(Ev, red);
@@ -300,31 +311,34 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
 
 size_t nb_smem_bytes(int S, bool fp64, bool grad) {
   const size_t t = fp64 ? 8 : 4;
-  size_t b = (size_t)S * (4 * t + 2 * t);
+  size_t b = (size_t)2 * S * (4 * t + 2 * t);
   if (grad) b += (size_t)3 * S * t + (size_t)kWarps * 3 * kIB * t;
   return b;
 }
 
 template <typename T, bool GRAD, bool CUTOFF>
 static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const void* lj,
-                               void* ipart, void* jpart, double* epart, int batch,
-                               cudaStream_t st) {
+                               const void* ipos, const void* ilj, void* ipart, void* jpart,
+                               double* epart, int batch, cudaStream_t st) {
   const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD);
   auto k = nb_units_kernel<T, GRAD, CUTOFF>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(plan.nunits, batch);
-  k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
+  if (plan.nlaunch == 0) return cudaSuccess;
+  dim3 grid(plan.nlaunch, batch);
+  count_launch(), k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
                                   static_cast<const typename Vec2T<T>::type*>(lj),
+                                  static_cast<const T*>(ipos), static_cast<const T*>(ilj),
                                   static_cast<T*>(ipart), static_cast<T*>(jpart), epart);
   return cudaGetLastError();
 }
 
 cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
-                      const void* lj, void* ipart, void* jpart, double* epart, int batch,
-                      cudaStream_t st) {
+                      const void* lj, const void* ipos, const void* ilj, void* ipart,
+                      void* jpart, double* epart, int batch, cudaStream_t st) {
   const bool cut = plan.has_cutoff != 0;
-#define FFM_NB(T, G, C) return launch_nb_t<T, G, C>(plan, pos, lj, ipart, jpart, epart, batch, st)
+#define FFM_NB(T, G, C) \
+  return launch_nb_t<T, G, C>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, batch, st)
   if (fp64) {
     if (grad) { if (cut) FFM_NB(double, true, true); else FFM_NB(double, true, false); }
     else { if (cut) FFM_NB(double, false, true); else FFM_NB(double, false, false); }

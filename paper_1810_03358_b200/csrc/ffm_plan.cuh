@@ -18,6 +18,8 @@ struct NbPlanDev {
   int nb;       // np / S
   int nunits;   // nb * (nb + 1) / 2
   const int2* unit_rc;       // [nunits] (row block, column block)
+  const int* unit_list;      // units this launch evaluates (row sharding), or null = all
+  int nlaunch;               // number of CTAs along x (= nunits without sharding)
   const int* spt_ptr;        // [np/128 + 1] special tiles per i-sub-block
   const int* spt_m;          // [nspt] global j-block index of the tile
   const uint32_t* spt_mask;  // [nspt][128] bit jj set: pair (i, jb+jj) special

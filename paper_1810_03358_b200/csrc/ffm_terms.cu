@@ -10,21 +10,44 @@ namespace ffm {
 constexpr long long kSentinel = 0x7fffffffffffffffLL;
 
 // ------------------------------------------------------------------ packing
+// Two copies of the positions are written per evaluation:
+//   pos  [batch][np]       Vec4 (x, y, z, q~)        -- j side, staged to smem
+//   ipos [batch][4][np/2]  pairs (T, T) per component -- i side, loaded as
+//        64/128-bit pairs straight into the packed registers of the pair
+//        kernel: record r = k*64 + pp*32 + lane holds atoms
+//        (128k + 64pp + lane, 128k + 64pp + lane + 32).
+__device__ __forceinline__ int64_t ipos_index(int a, int np, int c) {
+  const int k = a >> 7, i = a & 127;
+  const int r = k * 64 + (i >> 6) * 32 + (i & 31);
+  return ((int64_t)c * (np >> 1) + r) * 2 + ((i >> 5) & 1);
+}
+
+template <typename T>
+__device__ __forceinline__ void put_atom(typename Vec4T<T>::type* pos, T* ipos, int np, int a,
+                                         T x, T y, T z, T w) {
+  typename Vec4T<T>::type p;
+  p.x = x;
+  p.y = y;
+  p.z = z;
+  p.w = w;
+  pos[a] = p;
+  ipos[ipos_index(a, np, 0)] = x;
+  ipos[ipos_index(a, np, 1)] = y;
+  ipos[ipos_index(a, np, 2)] = z;
+  ipos[ipos_index(a, np, 3)] = w;
+}
+
 template <typename T>
 __global__ void pack_kernel(int n, int np, int batch, const double* __restrict__ coords,
                             const double* __restrict__ qt,
-                            typename Vec4T<T>::type* __restrict__ pos,
+                            typename Vec4T<T>::type* __restrict__ pos, T* __restrict__ ipos,
                             int64_t* __restrict__ status) {
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < (int64_t)n * batch) {
     const int64_t b = k / n, a = k - b * n;
     const double* c = coords + 3 * k;
-    typename Vec4T<T>::type p;
-    p.x = T(c[0]);
-    p.y = T(c[1]);
-    p.z = T(c[2]);
-    p.w = T(qt[a]);
-    pos[b * np + a] = p;
+    put_atom<T>(pos + b * np, ipos + b * 4 * (int64_t)np, np, (int)a, T(c[0]), T(c[1]),
+                T(c[2]), T(qt[a]));
   }
   if (status && k < batch) {
     int64_t* s = status + k * kStWords;
@@ -40,41 +63,65 @@ __global__ void pack_kernel(int n, int np, int batch, const double* __restrict__
 }
 
 template <typename T>
-__global__ void pad_kernel(int n, int np, int batch, typename Vec4T<T>::type* __restrict__ pos) {
+__global__ void pad_kernel(int n, int np, int batch, typename Vec4T<T>::type* __restrict__ pos,
+                           T* __restrict__ ipos) {
   const int npad = np - n;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (int64_t)npad * batch) return;
   const int64_t b = k / npad, a = k - b * npad;
   // zero charge and LJ (set in lj/qt), far from everything and 10 A apart
-  typename Vec4T<T>::type p;
-  p.x = T(1.0e4 + 10.0 * (double)a);
-  p.y = T(1.0e4);
-  p.z = T(1.0e4);
-  p.w = T(0);
-  pos[b * np + n + a] = p;
+  put_atom<T>(pos + b * np, ipos + b * 4 * (int64_t)np, np, n + (int)a,
+              T(1.0e4 + 10.0 * (double)a), T(1.0e4), T(1.0e4), T(0));
 }
 
 cudaError_t launch_pack(int n, int np, int batch, bool fp64, const double* coords,
-                        const double* qt, void* pos, int64_t* status, cudaStream_t st) {
+                        const double* qt, void* pos, void* ipos, int64_t* status,
+                        cudaStream_t st) {
   const int64_t tot = (int64_t)n * batch > batch ? (int64_t)n * batch : batch;
   const int blocks = (int)((tot + 255) / 256);
   if (fp64)
-    pack_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
-                                                static_cast<double4*>(pos), status);
+    count_launch(), pack_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+                                                static_cast<double4*>(pos),
+                                                static_cast<double*>(ipos), status);
   else
-    pack_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
-                                               static_cast<float4*>(pos), status);
+    count_launch(), pack_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+                                               static_cast<float4*>(pos),
+                                               static_cast<float*>(ipos), status);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, cudaStream_t st) {
+cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipos,
+                       cudaStream_t st) {
   const int64_t tot = (int64_t)(np - n) * batch;
   if (tot <= 0) return cudaSuccess;
   const int blocks = (int)((tot + 255) / 256);
   if (fp64)
-    pad_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<double4*>(pos));
+    count_launch(), pad_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<double4*>(pos),
+                                               static_cast<double*>(ipos));
   else
-    pad_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<float4*>(pos));
+    count_launch(), pad_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<float4*>(pos),
+                                              static_cast<float*>(ipos));
+  return cudaGetLastError();
+}
+
+// LJ (a, b) in the i-side pair layout, built once per system
+template <typename T>
+__global__ void ilj_kernel(int np, const typename Vec2T<T>::type* __restrict__ lj,
+                           T* __restrict__ ilj) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= np) return;
+  ilj[ipos_index(a, np, 0)] = lj[a].x;
+  ilj[ipos_index(a, np, 1)] = lj[a].y;
+}
+
+cudaError_t launch_ilj(int np, bool fp64, const void* lj, void* ilj, cudaStream_t st) {
+  const int blocks = (np + 255) / 256;
+  if (fp64)
+    count_launch(), ilj_kernel<double><<<blocks, 256, 0, st>>>(np, static_cast<const double2*>(lj),
+                                               static_cast<double*>(ilj));
+  else
+    count_launch(), ilj_kernel<float><<<blocks, 256, 0, st>>>(np, static_cast<const float2*>(lj),
+                                              static_cast<float*>(ilj));
   return cudaGetLastError();
 }
 
@@ -282,7 +329,7 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
   const int tot = tp.nbond + tp.nangle + tp.ndih + tp.nscaled;
   if (tot == 0) return cudaSuccess;
   dim3 grid((tot + 127) / 128, batch);
-  terms_kernel<<<grid, 128, 0, st>>>(tp, grad, coords, term_e, term_f, status);
+  count_launch(); terms_kernel<<<grid, 128, 0, st>>>(tp, grad, coords, term_e, term_f, status);
   return cudaGetLastError();
 }
 
@@ -331,12 +378,12 @@ cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_ind
                             bool use_nb, bool use_terms, double* grad, cudaStream_t st) {
   const int blocks = (n + 127) / 128;
   if (fp64)
-    assemble_kernel<double><<<blocks, 128, 0, st>>>(
+    count_launch(), assemble_kernel<double><<<blocks, 128, 0, st>>>(
         n, S, nb, unit_index, static_cast<const double*>(ipart),
         static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
         use_terms, grad);
   else
-    assemble_kernel<float><<<blocks, 128, 0, st>>>(
+    count_launch(), assemble_kernel<float><<<blocks, 128, 0, st>>>(
         n, S, nb, unit_index, static_cast<const float*>(ipart),
         static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
         use_terms, grad);
@@ -353,7 +400,7 @@ __device__ double tree_sum(double v, double* sh) {
   __syncthreads();
   double s = 0.0;
   if (threadIdx.x < 32) {
-    s = sh[threadIdx.x];
+    s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   }
   return s;  // valid in thread 0
@@ -364,9 +411,9 @@ __device__ double tree_min(double v, double* sh) {
   __syncthreads();
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
   __syncthreads();
-  double s = 0.0;
+  double s = DBL_MAX;
   if (threadIdx.x < 32) {
-    s = sh[threadIdx.x];
+    s = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : DBL_MAX;
     for (int o = 16; o > 0; o >>= 1) s = fmin(s, __shfl_xor_sync(0xffffffffu, s, o));
   }
   return s;
@@ -415,7 +462,7 @@ reduce_kernel(int nunits, TermPlanDev tp, const double* __restrict__ epart,
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
                           const double* term_e, double* energies, int64_t* status,
                           cudaStream_t st) {
-  reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, tp, epart, term_e, energies, status);
+  count_launch(); reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, tp, epart, term_e, energies, status);
   return cudaGetLastError();
 }
 
@@ -466,12 +513,12 @@ cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
   dim3 grid((n + 127) / 128, batch);
   if (n == 0) {
   } else if (fp64)
-    finder_kernel<double><<<grid, 128, 0, st>>>(n, np, static_cast<const double4*>(pos),
+    count_launch(), finder_kernel<double><<<grid, 128, 0, st>>>(n, np, static_cast<const double4*>(pos),
                                                 sp_ptr, sp_j, sp_s, status);
   else
-    finder_kernel<float><<<grid, 128, 0, st>>>(n, np, static_cast<const float4*>(pos), sp_ptr,
+    count_launch(), finder_kernel<float><<<grid, 128, 0, st>>>(n, np, static_cast<const float4*>(pos), sp_ptr,
                                                sp_j, sp_s, status);
-  finalize_kernel<<<(batch + 127) / 128, 128, 0, st>>>(n, batch, status);
+  count_launch(); finalize_kernel<<<(batch + 127) / 128, 128, 0, st>>>(n, batch, status);
   return cudaGetLastError();
 }
 
@@ -605,7 +652,7 @@ cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* atoms, const double* newpos, double* out,
                               int64_t* status, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
-  atom_delta_kernel<<<ncand, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s,
+  count_launch(), atom_delta_kernel<<<ncand, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s,
                                                      aterm_ptr, aterm_idx, atoms, newpos, out,
                                                      status);
   return cudaGetLastError();

@@ -51,8 +51,8 @@ dot_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
 
 cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,
                        double* out, cudaStream_t st) {
-  dot_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, x, y, part);
-  dot_final_kernel<<<1, kVecThreads, 0, st>>>(part, out);
+  count_launch(); dot_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, x, y, part);
+  count_launch(); dot_final_kernel<<<1, kVecThreads, 0, st>>>(part, out);
   return cudaGetLastError();
 }
 
@@ -78,7 +78,7 @@ cudaError_t launch_axpby(int64_t n, const double* a_dev, double a_host, double s
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4 * kVecBlocks) blocks = 4 * kVecBlocks;
   if (blocks < 1) blocks = 1;
-  axpby_kernel<<<(int)blocks, 256, 0, st>>>(n, a_dev, a_host, sa, x, b_dev, b_host, y, z);
+  count_launch(); axpby_kernel<<<(int)blocks, 256, 0, st>>>(n, a_dev, a_host, sa, x, b_dev, b_host, y, z);
   return cudaGetLastError();
 }
 
@@ -222,6 +222,7 @@ cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const do
   if (blocks > kVecBlocks) blocks = kVecBlocks;
   if (blocks < 1) blocks = 1;
   void* args[] = {&a};
+  count_launch();
   return cudaLaunchCooperativeKernel((void*)two_loop_kernel, blocks, kVecThreads, args, 0, st);
 }
 

@@ -3,12 +3,9 @@
 Call accounting is identical to the reference: value(), gradient() and
 value_and_gradient() each bump their counters, a fused call bumps both.
 
-Two molecular oracles:
-  * ``MolecularOracle``      -- NumPy in / NumPy out, the reference-facing
-    drop-in (every call is one host->device->host round trip);
-  * ``DeviceMolecularOracle`` -- coordinates and gradients stay in HBM as
-    torch tensors; only the 5 energy terms and 8 status words (104 bytes)
-    come back per evaluation.  The device-resident optimisers use this one.
+``MolecularOracle`` evaluates on the device and takes either NumPy arrays
+(reference-facing) or cuda tensors (device-resident); the optimisers always
+drive it with device vectors.
 """
 
 from __future__ import annotations
@@ -17,7 +14,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .energy import energy_and_gradient, energy_total, raise_status
+from .energy import raise_status
 from .engine import engine_for, precision_of
 
 
@@ -90,44 +87,28 @@ class FunctionOracle(ObjectiveOracle):
 
 
 class MolecularOracle(ObjectiveOracle):
-    """Total force-field energy of flattened coordinates, host buffers
-    (ffmin/oracle.py:76-103)."""
+    """Total force-field energy as a function of flattened coordinates
+    (ffmin/oracle.py:76-103), evaluated on the device.
 
-    def __init__(self, system, dtype=np.float64, backend=None):
-        super().__init__(3 * system.natoms)
-        self.system = system
-        self.dtype = np.dtype(dtype)
-        self.backend = backend
-
-    def system_at(self, x):
-        return self.system.with_coords(np.asarray(x, dtype=np.float64))
-
-    def _value(self, x):
-        return energy_total(self.system_at(x), self.dtype, self.backend).total
-
-    def _gradient(self, x):
-        _, g = energy_and_gradient(self.system_at(x), self.dtype, self.backend)
-        return g
-
-    def _value_and_gradient(self, x):
-        bd, g = energy_and_gradient(self.system_at(x), self.dtype, self.backend)
-        return bd.total, g
-
-
-class DeviceMolecularOracle(ObjectiveOracle):
-    """Device-resident molecular oracle: x and gradients are cuda float64
-    tensors of length 3n; f comes back as a Python float.
-
-    ``last_breakdown`` keeps the 5 terms of the latest evaluation; errors
-    are raised exactly as by the energy layer.
+    Accepts NumPy arrays (reference-facing: gradients come back as float64
+    NumPy arrays, f as a Python float) or cuda float64 tensors (device-
+    resident: gradients stay in HBM).  ``space == "device"``, so every
+    optimiser driven by it keeps x, g and its vector algebra on the GPU;
+    only the 5 energy terms and 8 status words (104 bytes) come back per
+    evaluation.  dtype selects the kernel precision; values and gradients
+    at the oracle boundary are always float64, as in the reference.
     """
 
     space = "device"
 
-    def __init__(self, system, dtype=np.float64, device=None):
+    def __init__(self, system, dtype=np.float64, backend=None, device=None):
         super().__init__(3 * system.natoms)
+        from .energy import _check_backend
+
+        _check_backend(backend)
         self.system = system
         self.dtype = np.dtype(dtype)
+        self.backend = backend
         self.precision = precision_of(self.dtype)
         self.engine = engine_for(system.topology, device)
         self.device = self.engine.device
@@ -136,22 +117,33 @@ class DeviceMolecularOracle(ObjectiveOracle):
                                  pin_memory=True)
         self._stage = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
                                   device=self.device)
+        self._host_io = False
         self.last_breakdown = None
         self.evaluations = 0
 
+    def system_at(self, x):
+        if isinstance(x, torch.Tensor):
+            x = x.detach().cpu().numpy()
+        return self.system.with_coords(np.asarray(x, dtype=np.float64))
+
     def initial_point(self):
+        """x0 of the wrapped system as a device vector."""
         return torch.from_numpy(np.ascontiguousarray(self.system.coords).reshape(-1)).to(
             self.device)
 
     def _coerce(self, x):
         if isinstance(x, torch.Tensor):
+            self._host_io = False
             if x.device != self.device or x.dtype != torch.float64:
                 x = x.to(device=self.device, dtype=torch.float64)
-            return x.contiguous()
+            return x.reshape(-1).contiguous()
+        self._host_io = True
         return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(
             self.device)
 
     def _out(self, g):
+        if self._host_io:
+            return g.cpu().numpy()
         return g
 
     def _run(self, x, grad):
@@ -169,6 +161,7 @@ class DeviceMolecularOracle(ObjectiveOracle):
         self.evaluations += 1
         raise_status(self.system, st, grad=grad)
         self.last_breakdown = en
+        # EnergyBreakdown.total order (ffmin/energy.py:38-41)
         f = float(en[0]) + float(en[1]) + float(en[2]) + float(en[3]) + float(en[4])
         return f, g
 
@@ -180,3 +173,7 @@ class DeviceMolecularOracle(ObjectiveOracle):
 
     def _value_and_gradient(self, x):
         return self._run(x, True)
+
+
+# the device-resident oracle is the molecular oracle
+DeviceMolecularOracle = MolecularOracle

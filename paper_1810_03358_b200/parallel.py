@@ -1,0 +1,166 @@
+"""Row-sharded evaluation over the GPUs of one node (one process per GPU).
+
+The pair triangle is cut into S x S super-units (csrc/ffm_capi.cu); rank r
+of W evaluates the units u = r, r + W, r + 2W, ... (heaviest first, so every
+rank gets the same work to within one unit) and rank 0 also the O(N) bonded
+and 1-4 terms.  Each rank therefore produces a *partial* gradient over all
+atoms and partial energies; one NCCL all-reduce (SUM) of the packed
+[gradient | energies] vector over NVLink completes them on every rank, and
+one tiny all-reduce (MIN) merges the error words.  Coordinates are
+replicated: every rank runs the same optimiser on the same all-reduced
+numbers, so no broadcast is needed per step.
+
+The reduction logic (``ShardCombiner``) is independent of CUDA and is
+exercised with the gloo backend on CPU tensors in tests/test_parallel_cpu.py.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+
+INT64_MAX = np.iinfo(np.int64).max
+
+
+def shard_units(nunits: int, rank: int, world: int):
+    """The unit indices rank `rank` evaluates (mirrors ffm_system_set_shard)."""
+    return list(range(rank, nunits, world))
+
+
+def unit_order(nb: int):
+    """(r, c) of every unit in evaluation order: off-diagonal first, then the
+    diagonal (mirrors ffm_system_create)."""
+    off = [(r, c) for r in range(nb) for c in range(r + 1, nb)]
+    return off + [(r, r) for r in range(nb)]
+
+
+class ShardCombiner:
+    """All-reduce of one rank's partial evaluation."""
+
+    def __init__(self, n, device, group=None):
+        self.n = n
+        self.group = group
+        self.buf = torch.empty(3 * n + N.FFM_NTERMS, dtype=torch.float64, device=device)
+        self.keys = torch.empty(4, dtype=torch.int64, device=device)
+
+    def combine(self, grad, energies, status):
+        """grad (3n,) or None, energies (5,), status (8,) int64 -- local
+        partials in, global values out (in place on grad/energies/status)."""
+        n3 = 3 * self.n
+        if grad is not None:
+            self.buf[:n3].copy_(grad.reshape(-1))
+        else:
+            self.buf[:n3].zero_()
+        self.buf[n3:].copy_(energies)
+        dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=self.group)
+        if grad is not None:
+            grad.reshape(-1).copy_(self.buf[:n3])
+        energies.copy_(self.buf[n3:])
+        # error words: first coincident pair as one key i * n + j, first bad
+        # bonded terms; sentinel INT64_MAX for "clean"
+        st = status
+        big = torch.full_like(st[:1], INT64_MAX)
+        key = torch.where(st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1] >= 0,
+                          st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1] * self.n + st[N.ST_NB_BAD_J:N.ST_NB_BAD_J + 1],
+                          big)
+        self.keys[0:1].copy_(key)
+        for k, slot in enumerate((N.ST_BOND, N.ST_ANGLE, N.ST_DIHEDRAL), start=1):
+            v = st[slot:slot + 1]
+            self.keys[k:k + 1].copy_(torch.where(v >= 0, v, big))
+        dist.all_reduce(self.keys, op=dist.ReduceOp.MIN, group=self.group)
+        k0 = self.keys[0:1]
+        clean = k0 == INT64_MAX
+        st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1].copy_(torch.where(clean, -1, k0 // self.n))
+        st[N.ST_NB_BAD_J:N.ST_NB_BAD_J + 1].copy_(torch.where(clean, -1, k0 % self.n))
+        for k, slot in enumerate((N.ST_BOND, N.ST_ANGLE, N.ST_DIHEDRAL), start=1):
+            v = self.keys[k:k + 1]
+            st[slot:slot + 1].copy_(torch.where(v == INT64_MAX, -1, v))
+        return grad, energies, status
+
+
+class ShardedSystem:
+    """This rank's engine handle (a private DeviceSystem with a shard) plus
+    the combiner; evaluates like engine.DeviceSystem.eval, globally."""
+
+    def __init__(self, topo, group=None, device=None):
+        from .engine import DeviceSystem
+
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.engine = DeviceSystem(topo, device)
+        N.check(self.engine.lib.ffm_system_set_shard(self.engine.handle, self.rank, self.world),
+                "ffm_system_set_shard")
+        self.n = topo.natoms
+        self.device = self.engine.device
+        self.combiner = ShardCombiner(self.n, self.device, group)
+
+    def new_outputs(self):
+        return self.engine.new_outputs()
+
+    def eval(self, coords, precision=N.FFM_F64, grad=None, energies=None, status=None,
+             flags=None):
+        energies, status = self.engine.eval(coords, precision, grad=grad, energies=energies,
+                                            status=status, flags=flags)
+        self.combiner.combine(grad, energies, status)
+        return energies, status
+
+
+class ShardedMolecularOracle:
+    """MolecularOracle over row-sharded GPUs: same interface and call
+    accounting, every rank sees identical (all-reduced) values."""
+
+    space = "device"
+
+    def __init__(self, system, dtype=np.float64, group=None, device=None):
+        from .engine import precision_of
+        from .oracle import MolecularOracle
+
+        self._base = MolecularOracle.__new__(MolecularOracle)
+        MolecularOracle.__init__(self._base, system, dtype, device=device)
+        self._base.engine = ShardedSystem(system.topology, group, device)
+        self.system = system
+        self.n = 3 * system.natoms
+        self.device = self._base.device
+        self.precision = precision_of(dtype)
+
+    def __getattr__(self, name):
+        return getattr(self._base, name)
+
+    @property
+    def value_calls(self):
+        return self._base.value_calls
+
+    @property
+    def grad_calls(self):
+        return self._base.grad_calls
+
+    def value(self, x):
+        return self._base.value(x)
+
+    def gradient(self, x):
+        return self._base.gradient(x)
+
+    def value_and_gradient(self, x):
+        return self._base.value_and_gradient(x)
+
+
+def init_from_env(backend="nccl"):
+    """torchrun-style initialisation (RANK / WORLD_SIZE / LOCAL_RANK /
+    MASTER_ADDR); returns (rank, world, local_rank)."""
+    import os
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local

@@ -1,0 +1,222 @@
+"""Parity of the B200 energy / gradient path with the oracle and the
+reference golden vectors.  GPU only (-m gpu).
+
+Tolerances:
+  FP64 mode: energies within 1e-10 relative, gradients within 1e-10 of
+             max|g| -- the north star asks for 1e-6;
+  FP32 mode: energies within 1e-5 relative, gradients within 1e-4 of max|g|
+             (pair arithmetic in FP32, accumulation in FP64), compared with
+             the FP64 reference.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import golden_system, oracle_arrays
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["chain10", "chain14", "cloud24", "cloud24c7", "explicit8", "chain200", "chain12cut",
+         "globule1500"]
+
+
+@pytest.fixture(scope="module")
+def E():
+    import paper_1810_03358_b200.energy as energy
+
+    return energy
+
+
+def _rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-12))
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp64_matches_reference(golden, E, name):
+    s = golden_system(golden, name)
+    bd, g = E.energy_and_gradient(s, np.float64)
+    ref_e, ref_g = golden[f"{name}/egrad_f64"], golden[f"{name}/grad_f64"]
+    got = [bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw]
+    np.testing.assert_allclose(got, ref_e, rtol=1e-10, atol=1e-9)
+    assert np.max(np.abs(g - ref_g)) <= 1e-10 * np.max(np.abs(ref_g))
+    assert g.dtype == np.float64
+    bd2 = E.energy_total(s, np.float64)
+    np.testing.assert_allclose([bd2.stretch, bd2.bend, bd2.torsion, bd2.coulomb, bd2.vdw],
+                               golden[f"{name}/energy_f64"], rtol=1e-10, atol=1e-9)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fp32_mode_tracks_fp64_reference(golden, E, name):
+    s = golden_system(golden, name)
+    bd, g = E.energy_and_gradient(s, np.float32)
+    assert g.dtype == np.float32 and isinstance(bd.total, float)
+    ref_e, ref_g = golden[f"{name}/egrad_f64"], golden[f"{name}/grad_f64"]
+    got = [bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw]
+    np.testing.assert_allclose(got, ref_e, rtol=1e-5, atol=1e-4)
+    assert np.max(np.abs(g - ref_g)) <= 1e-4 * np.max(np.abs(ref_g))
+
+
+@pytest.mark.parametrize("name", ["chain200", "globule1500"])
+def test_repeated_calls_bit_identical(golden, E, name):
+    s = golden_system(golden, name)
+    for dt in (np.float64, np.float32):
+        a, ga = E.energy_and_gradient(s, dt)
+        b, gb = E.energy_and_gradient(s, dt)
+        assert a == b and np.array_equal(ga, gb)
+
+
+def test_coincident_pair_error(golden, E):
+    s = golden_system(golden, "coincident")
+    for dt in (np.float64, np.float32):
+        with pytest.raises(E.EnergyEvaluationError, match=r"nonbonded pair \(3,11\)"):
+            E.energy_total(s, dt)
+        with pytest.raises(E.EnergyEvaluationError, match=r"nonbonded pair \(3,11\)"):
+            E.energy_and_gradient(s, dt)
+
+
+def test_degenerate_terms_raise_reference_messages(golden, E):
+    s = golden_system(golden, "collinear")
+    msgs = golden["collinear/messages"].tolist()
+    with pytest.raises(E.EnergyEvaluationError) as ei:
+        E.energy_total(s)
+    assert str(ei.value) == msgs[0]
+    with pytest.raises(E.EnergyEvaluationError) as ei:
+        E.energy_and_gradient(s)
+    assert str(ei.value) == msgs[1]
+
+
+@pytest.mark.parametrize("name", ["chain14", "cloud24", "chain200"])
+def test_exact_atom_deltas(golden, E, name):
+    s = golden_system(golden, name)
+    for a, d, want in zip(golden[f"{name}/delta_atoms"], golden[f"{name}/delta_moves"],
+                          golden[f"{name}/delta_values"]):
+        got = E.exact_delta_atom_move(s, int(a), d)
+        assert got == pytest.approx(float(want), rel=1e-10, abs=1e-10)
+
+
+def test_landmarks_and_constant(E):
+    from paper_1810_03358_b200.model import AtomSpec, MolecularSystem, NonbondedPolicy
+
+    def pair(r, q=0.0, sigma=3.0, eps=0.1):
+        return MolecularSystem(atoms=(AtomSpec(0, "a", q, sigma, eps), AtomSpec(1, "b", q, sigma, eps)),
+                               coords=np.array([[0.0, 0, 0], [r, 0, 0]]),
+                               nonbonded=NonbondedPolicy.no_exclusions())
+
+    assert E.energy_coulomb(pair(1.0, q=1.0, eps=0.0)) == pytest.approx(1389.38757, abs=1e-5)
+    sig, eps = 3.4, 0.9
+    assert abs(E.energy_vdw(pair(sig, sigma=sig, eps=eps))) <= 1e-10 * eps
+    assert E.energy_vdw(pair(2 ** (1 / 6) * sig, sigma=sig, eps=eps)) == pytest.approx(-eps, rel=1e-10)
+    assert E.energy_vdw(pair(0.3 * 3.5, sigma=3.5, eps=0.276)) > 1e6
+
+
+def test_batch_equals_single_evaluations(golden):
+    import torch
+
+    from paper_1810_03358_b200.engine import engine_for
+
+    s = golden_system(golden, "globule1500")
+    eng = engine_for(s.topology)
+    rng = np.random.default_rng(3)
+    B = 7
+    batch = s.coords[None] + rng.normal(scale=0.05, size=(B,) + s.coords.shape)
+    for prec in (0, 1):
+        en, st = eng.eval_batch(torch.from_numpy(batch).cuda(), prec)
+        en = en.cpu().numpy()
+        for b in range(B):
+            e1, st1, _ = eng.eval_host(batch[b], prec)
+            np.testing.assert_allclose(en[b], e1, rtol=1e-12, atol=1e-9)
+        assert np.all(st.cpu().numpy()[:, 0] == -1)
+
+
+def test_kernel_backend_dropin(golden):
+    """The 'cuda' KernelBackend answers the reference kernel signatures."""
+    from paper_1810_03358_b200.kernels import get_backend
+
+    kb = get_backend()
+    assert kb.name == "cuda"
+    s = golden_system(golden, "cloud24")
+    p = s.arrays()
+    c = np.ascontiguousarray(s.coords)
+    A, _ = oracle_arrays(golden, "cloud24")
+    ec, ev, _, _, gref = O.nb_eval(A, c, True)
+    out = kb.nb_energy(c, p["q"], p["sigma"], p["epsilon"], p["scale"], 0.0)
+    assert out[2:] == (-1, -1)
+    assert out[0] == pytest.approx(ec, rel=1e-11) and out[1] == pytest.approx(ev, rel=1e-11)
+    gout = np.zeros_like(c)
+    r = kb.nb_grad(c, p["q"], p["sigma"], p["epsilon"], p["scale"], 0.0, gout)
+    assert r[2:] == (-1, -1)
+    assert np.max(np.abs(gout - gref)) <= 1e-10 * np.max(np.abs(gref))
+    # the reference call with a 7 A cutoff (fresh parameter arrays -> fresh plan)
+    A7, _ = oracle_arrays(golden, "cloud24c7")
+    s7 = golden_system(golden, "cloud24c7")
+    p7 = s7.arrays()
+    ec7, ev7, _, _, _ = O.nb_eval(A7, c, False)
+    out = kb.nb_energy(c, p7["q"], p7["sigma"], p7["epsilon"], p7["scale"], 7.0)
+    assert out[0] == pytest.approx(ec7, rel=1e-11) and out[1] == pytest.approx(ev7, rel=1e-11)
+    # bonded kernels on the chain
+    s = golden_system(golden, "chain14")
+    p = s.arrays()
+    c = np.ascontiguousarray(s.coords)
+    A, _ = oracle_arrays(golden, "chain14")
+    (es, eb, et), _, gb = O.bonded(A, c, True)
+    g = np.zeros_like(c)
+    e, bad = kb.bond_grad(c, p["bond_idx"], p["bond_K"], p["bond_r0"], g)
+    e2, bad2 = kb.angle_grad(c, p["ang_idx"], p["ang_K"], p["ang_t0"], g)
+    e3, bad3 = kb.dihedral_grad(c, p["dih_idx"], p["dih_V"], g)
+    assert (bad, bad2, bad3) == (-1, -1, -1)
+    assert (e, e2, e3) == pytest.approx((es, eb, et), rel=1e-12)
+    assert np.max(np.abs(g - gb)) <= 1e-11 * np.max(np.abs(gb))
+    # coincident pair through the kernel API
+    s = golden_system(golden, "coincident")
+    p = s.arrays()
+    out = kb.nb_energy(np.ascontiguousarray(s.coords), p["q"], p["sigma"], p["epsilon"],
+                       p["scale"], 0.0)
+    assert out[2:] == (3, 11)
+
+
+def test_missing_native_library_fails_loudly(tmp_path):
+    from paper_1810_03358_b200 import _native
+
+    with pytest.raises(ImportError, match="missing"):
+        _native.load(tmp_path / "nope.so")
+
+
+# ------------------------------------------------------- full-size checks
+
+@pytest.mark.parametrize("n", [30000, 100000])
+def test_full_size_against_threaded_oracle(n):
+    """BASELINE sizes: the whole FP32 / FP64 gradient against the C oracle
+    run on all host cores."""
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(n, seed=1)
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    assert err is None
+    gmax = np.max(np.abs(g_ref))
+    for dt, et, gt in ((np.float64, 1e-10, 1e-10), (np.float32, 1e-5, 1e-4)):
+        bd, g = energy_and_gradient(s, dt)
+        got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        assert _rel(got, e_ref) <= et, (dt, got, e_ref)
+        assert np.max(np.abs(g - g_ref)) <= gt * gmax
+
+
+def test_full_size_properties():
+    """Size-independent properties at N = 100k: translation invariance,
+    Newton's third law (net gradient ~ 0), FP32 ~ FP64."""
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(100000, seed=2)
+    bd, g = energy_and_gradient(s, np.float64)
+    gm = g.reshape(-1, 3)
+    assert np.linalg.norm(gm.sum(axis=0)) <= 1e-9 * np.linalg.norm(g)
+    bd2, _ = energy_and_gradient(s.with_coords(s.coords + np.array([3.25, -1.5, 0.75])),
+                                 np.float64)
+    assert bd2.total == pytest.approx(bd.total, rel=1e-9)
+    bd3, g3 = energy_and_gradient(s, np.float32)
+    assert bd3.total == pytest.approx(bd.total, rel=1e-5)
+    assert np.max(np.abs(g3 - g)) <= 1e-4 * np.max(np.abs(g))
