@@ -46,6 +46,10 @@ class HostOps:
         """a x + b y (new vector)."""
         return a * x if y is None else a * x + b * y
 
+    def div(self, x, a):
+        """x / a (the reference normalises by division)."""
+        return x / a
+
     def all_finite(self, x) -> bool:
         return bool(np.all(np.isfinite(x)))
 
@@ -128,6 +132,9 @@ class DeviceOps:
                                         float(b), None if y is None else self._p(y),
                                         self._p(z), self._s()), "ffm_axpby")
         return z
+
+    def div(self, x, a):
+        return self.lincomb(1.0 / a, x)
 
     def all_finite(self, x) -> bool:
         return bool(self.torch.isfinite(x).all().item())
