@@ -214,6 +214,38 @@ def main():
                                            r.trace.records[-1].grad_calls])
         print(name, r.status, r.f, r.grad_norm, r.iterations, time.time() - t1)
 
+    # every driver on a strained 30-atom chain, 40 iterations (trace parity)
+    from ffmin.optimizers import (cg, fgm, gradient_descent_fixed, heavy_ball,
+                                  nesterov_momentum, nesterov_strongly_convex, ofgm,
+                                  steepest_descent)
+    s30 = make_chain_system(30, seed=8, strain=0.3)
+    put_system("drv30", s30)
+    x30 = s30.coords.ravel()
+    st40 = StopCriteria(max_iterations=40, gradient_norm_rtol=0.0)
+    runs = {
+        "sd_h": lambda o: steepest_descent(o, x30, make_linesearch("h"), st40),
+        "sd_par": lambda o: steepest_descent(o, x30, make_linesearch("par"), st40),
+        "gd": lambda o: gradient_descent_fixed(o, x30, 4000.0, st40),
+        "hb": lambda o: heavy_ball(o, x30, 1.0 / 4000.0, 0.5, st40),
+        "nag": lambda o: nesterov_momentum(o, x30, 4000.0, st40),
+        "nagsc": lambda o: nesterov_strongly_convex(o, x30, 4000.0, 40.0, st40),
+        "fgm": lambda o: fgm(o, x30, make_linesearch("par"), st40),
+        "ofgm_L": lambda o: ofgm(o, x30, 40, L=4000.0, stop=st40),
+        "ofgm_ls": lambda o: ofgm(o, x30, 40, linesearch=make_linesearch("h"), stop=st40),
+        "lbfgs": lambda o: lbfgs(o, x30, m=4, linesearch=make_linesearch("h"), stop=st40),
+    }
+    for v in ("fr", "prp", "prp+", "hs", "cd", "ls", "dy"):
+        runs["cg_" + v] = (lambda v: lambda o: cg(o, x30, v, make_linesearch("par"), st40))(v)
+    for name, fn in runs.items():
+        r = fn(MolecularOracle(s30))
+        store[f"drv30/{name}/f"] = np.array([rec.f for rec in r.trace.records])
+        store[f"drv30/{name}/gn"] = np.array([rec.grad_norm for rec in r.trace.records])
+        store[f"drv30/{name}/calls"] = np.array([[rec.value_calls, rec.grad_calls]
+                                                 for rec in r.trace.records])
+        store[f"drv30/{name}/x"] = r.x
+        store[f"drv30/{name}/status"] = np.array(r.status)
+    store["drv30/names"] = np.array(list(runs))
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB) in {time.time() - t0:.1f}s")
 

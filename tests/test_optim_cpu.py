@@ -136,3 +136,22 @@ def test_lbfgs_clears_memory_once_then_fails():
     stub = Flaky()
     res = lbfgs(orc, np.ones(3), m=3, linesearch=stub)
     assert res.status == LINESEARCH_FAILURE and res.iterations == 1 and stub.calls == 3
+
+
+DRIVERS = ["sd_h", "sd_par", "gd", "hb", "nag", "nagsc", "fgm", "ofgm_L", "ofgm_ls", "lbfgs",
+           "cg_fr", "cg_prp", "cg_prp+", "cg_hs", "cg_cd", "cg_ls", "cg_dy"]
+
+
+@pytest.mark.parametrize("name", DRIVERS)
+def test_every_driver_reproduces_reference_trace(golden, name):
+    """Host vector space + C oracle: each driver's 40-iteration trace on the
+    30-atom chain equals the reference's bit for bit."""
+    from drivers_common import driver_runs, trace
+
+    A, c = oracle_arrays(golden, "drv30")
+    res = driver_runs(c.reshape(-1))[name](c_oracle(A))
+    f, calls = trace(res)
+    assert np.array_equal(f, golden[f"drv30/{name}/f"])
+    assert np.array_equal(calls, golden[f"drv30/{name}/calls"])
+    assert np.array_equal(res.x, golden[f"drv30/{name}/x"])
+    assert res.status == str(golden[f"drv30/{name}/status"])

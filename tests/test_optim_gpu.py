@@ -110,3 +110,27 @@ def test_device_results_stay_on_device():
                 stop=StopCriteria(max_iterations=20, gradient_norm_rtol=0.0))
     assert isinstance(res.x, torch.Tensor) and res.x.is_cuda
     assert res.f < res.trace.records[0].f
+
+
+DRIVERS = ["sd_h", "sd_par", "gd", "hb", "nag", "nagsc", "fgm", "ofgm_L", "ofgm_ls", "lbfgs",
+           "cg_fr", "cg_prp", "cg_prp+", "cg_hs", "cg_cd", "cg_ls", "cg_dy"]
+FIXED_STEP = {"gd", "hb", "nag", "nagsc", "ofgm_L"}
+
+
+@pytest.mark.parametrize("name", DRIVERS)
+def test_every_driver_on_device_tracks_reference(golden, name):
+    """The same drivers with x, g and directions in HBM (FP64): traces agree
+    with the reference to 1e-7 -- all 40 iterations for the fixed-step
+    methods, the first 10 for line-searched ones (a line search may take a
+    different branch once two probe energies tie to roundoff)."""
+    from drivers_common import driver_runs, trace
+
+    from paper_1810_03358_b200.oracle import MolecularOracle
+
+    s = golden_system(golden, "drv30")
+    res = driver_runs(s.coords.ravel())[name](MolecularOracle(s))
+    f, _ = trace(res)
+    ref = golden[f"drv30/{name}/f"]
+    k = len(ref) if name in FIXED_STEP else 11
+    np.testing.assert_allclose(f[:k], ref[:k], rtol=1e-7)
+    assert res.status == str(golden[f"drv30/{name}/status"])
