@@ -131,6 +131,25 @@ int ffm_atom_delta(ffm_system_t* sys, const double* coords_d, int64_t ncand,
                    const int32_t* atoms_d, const double* newpos_d, double* out_d,
                    int64_t* status_d, void* stream);
 
+/* Far-field linearised single-atom move deltas (ffmin/energy.py:215-281,
+ * linearize_farfield_coulomb + delta_energy_atom_move, the incremental mode
+ * of the gradient-free method, paper section 3): partners within lin_cutoff
+ * of the atom's current position, and every excluded / 1-4 partner, are
+ * treated exactly; the far Coulomb sum by its first-order Taylor term; far
+ * vdW is neglected.  out_d[k][6] = (near coulomb, near vdw, stretch, bend,
+ * torsion, far linear term); status_d as ffm_atom_delta.  Requires a
+ * system without a nonbonded cutoff. */
+int ffm_atom_delta_lin(ffm_system_t* sys, const double* coords_d, int64_t ncand,
+                       const int32_t* atoms_d, const double* newpos_d, double lin_cutoff,
+                       double* out_d, int64_t* status_d, void* stream);
+
+/* ffmin/energy.py:215-240 linearize_farfield_coulomb (kernels.py:359-387):
+ * e0_coef_d[4] = (far-field Coulomb energy of `atom`, its gradient x/y/z),
+ * near_mask_d[n] = 1 for the exact near set, bad_d[0] = first coincident far
+ * partner or -1. */
+int ffm_farfield_build(ffm_system_t* sys, const double* coords_d, int64_t atom, double cutoff,
+                       double* e0_coef_d, uint8_t* near_mask_d, int64_t* bad_d, void* stream);
+
 /* ---- optimiser vector algebra on device vectors (ffmin/optimizers) ---- */
 
 /* out_d[0] = <x, y>, deterministic fixed-order reduction.  scratch_d holds

@@ -12,7 +12,12 @@ import ctypes as C
 import threading
 from pathlib import Path
 
+import os
+
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libffmin_b200.so"
+# development aid: FFMIN_B200_LIB points at an alternative build (tuning sweeps)
+if os.environ.get("FFMIN_B200_LIB"):
+    LIB_PATH = Path(os.environ["FFMIN_B200_LIB"])
 
 FFM_F64 = 0
 FFM_F32 = 1
@@ -45,6 +50,8 @@ SIGNATURES = {
     "ffm_eval_host": (_I, [_P, _I, _I, _P, _P, _P, _P]),
     "ffm_eval_batch": (_I, [_P, _I, _I64, _P, _P, _P, _P]),
     "ffm_atom_delta": (_I, [_P, _P, _I64, _P, _P, _P, _P, _P]),
+    "ffm_atom_delta_lin": (_I, [_P, _P, _I64, _P, _P, _D, _P, _P, _P]),
+    "ffm_farfield_build": (_I, [_P, _P, _I64, _D, _P, _P, _P, _P]),
     "ffm_vec_scratch_doubles": (_I64, []),
     "ffm_dot": (_I, [_I64, _P, _P, _P, _P, _P]),
     "ffm_axpby": (_I, [_I64, _P, _D, _D, _P, _P, _D, _P, _P, _P]),

@@ -687,15 +687,39 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
 int ffm_atom_delta(ffm_system_t* s, const double* coords_d, int64_t ncand,
                    const int32_t* atoms_d, const double* newpos_d, double* out_d,
                    int64_t* status_d, void* stream) {
+  return ffm_atom_delta_lin(s, coords_d, ncand, atoms_d, newpos_d, 0.0, out_d, status_d,
+                            stream);
+}
+
+int ffm_atom_delta_lin(ffm_system_t* s, const double* coords_d, int64_t ncand,
+                       const int32_t* atoms_d, const double* newpos_d, double lin_cutoff,
+                       double* out_d, int64_t* status_d, void* stream) {
   if (!s) return fail(FFM_EINVAL, "system is NULL");
   if (ncand < 0 || ncand > (1LL << 30)) return fail(FFM_EINVAL, "bad candidate count");
+  if (lin_cutoff > 0.0 && s->plan.has_cutoff)
+    return fail(FFM_EINVAL, "incremental delta requires a system nonbonded cutoff of none");
   if (ncand == 0) return FFM_OK;
   if (!coords_d || !atoms_d || !newpos_d || !out_d || !status_d)
     return fail(FFM_EINVAL, "NULL argument");
   DeviceGuard guard(s->device);
   FFM_CUDA(launch_atom_delta(s->tp, coords_d, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
                              s->d_aterm_ptr, s->d_aterm_idx, (int)ncand, atoms_d, newpos_d,
-                             out_d, status_d, static_cast<cudaStream_t>(stream)));
+                             lin_cutoff > 0.0 ? lin_cutoff : 0.0, out_d, status_d,
+                             static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+int ffm_farfield_build(ffm_system_t* s, const double* coords_d, int64_t atom, double cutoff,
+                       double* e0_coef_d, uint8_t* near_mask_d, int64_t* bad_d,
+                       void* stream) {
+  if (!s || !coords_d || !e0_coef_d || !near_mask_d || !bad_d)
+    return fail(FFM_EINVAL, "NULL argument");
+  if (atom < 0 || atom >= s->plan.n) return fail(FFM_EINVAL, "atom index out of range");
+  if (!(cutoff > 0.0)) return fail(FFM_EINVAL, "cutoff must be > 0");
+  DeviceGuard guard(s->device);
+  FFM_CUDA(launch_farfield(s->tp, coords_d, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s, (int)atom,
+                           cutoff, e0_coef_d, near_mask_d, bad_d,
+                           static_cast<cudaStream_t>(stream)));
   return FFM_OK;
 }
 

@@ -55,6 +55,14 @@ template <> struct Pk<float> {
     asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
   }
+  // two FFMA2 sharing the multiplicands, emitted back to back so the
+  // second can take g and d from the operand reuse cache (register-file
+  // read bandwidth, not the FMA pipe, limits 3-source FFMA2)
+  static __device__ __forceinline__ void fma_pair(V g, V d, V& a, V& b) {
+    asm("fma.rn.ftz.f32x2 %0, %2, %3, %0;\n\t"
+        "fma.rn.ftz.f32x2 %1, %2, %3, %1;"
+        : "+l"(a), "+l"(b) : "l"(g), "l"(d));
+  }
   // MUFU.RSQ on each lane (no packed form exists)
   static __device__ __forceinline__ V rsqrt(V v) {
     float a, b;
@@ -91,6 +99,10 @@ template <> struct Pk<double> {
     return ::fma(0.5 * y, e, y);
   }
   static __device__ __forceinline__ V rsqrt(V v) { return {rsqrt1(v.x), rsqrt1(v.y)}; }
+  static __device__ __forceinline__ void fma_pair(V g, V d, V& a, V& b) {
+    a = fma(g, d, a);
+    b = fma(g, d, b);
+  }
   static __device__ __forceinline__ V zero() { return {0.0, 0.0}; }
 };
 

@@ -62,8 +62,15 @@ cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
 cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
                               const int* aterm_ptr, const int* aterm_idx, int ncand,
-                              const int* atoms, const double* newpos, double* out,
-                              int64_t* status, cudaStream_t st);
+                              const int* atoms, const double* newpos, double lin_cutoff,
+                              double* out, int64_t* status, cudaStream_t st);
+
+// far-field linearisation of one atom: e0_coef[4] = (E_far, dE/dx, dE/dy,
+// dE/dz), near_mask[n], bad = first coincident far partner or -1
+cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const int* fsp_ptr,
+                            const int* fsp_j, const double* fsp_s, int atom, double cutoff,
+                            double* e0_coef, uint8_t* near_mask, int64_t* bad,
+                            cudaStream_t st);
 
 // ---- vector algebra (ffm_vec.cu) ----
 int vec_reduce_blocks();

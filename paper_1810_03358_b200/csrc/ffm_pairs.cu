@@ -22,6 +22,11 @@
 
 namespace ffm {
 
+#ifndef FFM_UNROLL
+#define FFM_UNROLL 32
+#endif
+constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
+
 template <typename T>
 __device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
 
@@ -70,10 +75,80 @@ __device__ __forceinline__ void warp_tile(
   const int src = (lane + 1) & 31;
   J += lane;
   L += lane;
-#pragma unroll 8
+#pragma unroll kStepUnroll
   for (int t = 0; t < 32; ++t) {
     const auto pj = J[t];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
     const auto lj = L[t];  // (a, -b)
+#ifndef FFM_SCHED
+#define FFM_SCHED 1
+#endif
+#if FFM_SCHED == 1
+    // phase-separated: both pairs' geometry first, the four MUFU.RSQ issued
+    // back to back, coefficient products while they are in flight
+    V dx[2], dy[2], dz[2], r2[2], A[2], nB[2], Q[2], ri[2];
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      dx[pp] = P::add(xi[pp], P::bc(pj.x));
+      dy[pp] = P::add(yi[pp], P::bc(pj.y));
+      dz[pp] = P::add(zi[pp], P::bc(pj.z));
+      r2[pp] = P::mul(dx[pp], dx[pp]);
+      r2[pp] = P::fma(dy[pp], dy[pp], r2[pp]);
+      r2[pp] = P::fma(dz[pp], dz[pp], r2[pp]);
+    }
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      A[pp] = P::mul(ai[pp], P::bc(lj.x));
+      nB[pp] = P::mul(bi[pp], P::bc(lj.y));
+      Q[pp] = P::mul(qi[pp], P::bc(pj.w));
+      if (MASKED) {
+        const int jj = (lane + t) & 31;
+        const bool a0 = (mk[2 * pp] >> jj) & 1u;
+        const bool a1 = (mk[2 * pp + 1] >> jj) & 1u;
+        r2[pp] = P::make(a0 ? P::lo(r2[pp]) : T(1), a1 ? P::hi(r2[pp]) : T(1));
+        A[pp] = P::make(a0 ? P::lo(A[pp]) : T(0), a1 ? P::hi(A[pp]) : T(0));
+        nB[pp] = P::make(a0 ? P::lo(nB[pp]) : T(0), a1 ? P::hi(nB[pp]) : T(0));
+        Q[pp] = P::make(a0 ? P::lo(Q[pp]) : T(0), a1 ? P::hi(Q[pp]) : T(0));
+      }
+      if constexpr (sizeof(T) == 8) minr2 = fmin(minr2, fmin(P::lo(r2[pp]), P::hi(r2[pp])));
+      if (CUTOFF) {
+        const bool c0 = P::lo(r2[pp]) <= cut2;
+        const bool c1 = P::hi(r2[pp]) <= cut2;
+        A[pp] = P::make(c0 ? P::lo(A[pp]) : T(0), c1 ? P::hi(A[pp]) : T(0));
+        nB[pp] = P::make(c0 ? P::lo(nB[pp]) : T(0), c1 ? P::hi(nB[pp]) : T(0));
+        Q[pp] = P::make(c0 ? P::lo(Q[pp]) : T(0), c1 ? P::hi(Q[pp]) : T(0));
+      }
+      ri[pp] = P::rsqrt(r2[pp]);
+    }
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const V i2 = P::mul(ri[pp], ri[pp]);
+      const V i4 = P::mul(i2, i2);
+      const V i6 = P::mul(i4, i2);
+      const V u = P::mul(A[pp], i6);
+      const V v = P::add(u, nB[pp]);
+      ev2 = P::fma(v, i6, ev2);
+      const V ecp = P::mul(Q[pp], ri[pp]);
+      ec2 = P::add(ec2, ecp);
+      if (GRAD) {
+        const V pw = P::add(u, v);
+        const V k = P::mul(pw, i6);
+        const V w = P::fma(k, P::bc(T(6)), ecp);
+        const V g = P::mul(w, i2);
+#if defined(FFM_PAIRFMA) && FFM_PAIRFMA
+        P::fma_pair(g, dx[pp], F[pp][0], gx);
+        P::fma_pair(g, dy[pp], F[pp][1], gy);
+        P::fma_pair(g, dz[pp], F[pp][2], gz);
+#else
+        F[pp][0] = P::fma(g, dx[pp], F[pp][0]);
+        F[pp][1] = P::fma(g, dy[pp], F[pp][1]);
+        F[pp][2] = P::fma(g, dz[pp], F[pp][2]);
+        gx = P::fma(g, dx[pp], gx);
+        gy = P::fma(g, dy[pp], gy);
+        gz = P::fma(g, dz[pp], gz);
+#endif
+      }
+    }
+#else
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       V dx = P::add(xi[pp], P::bc(pj.x));
@@ -130,6 +205,7 @@ __device__ __forceinline__ void warp_tile(
         gz = P::fma(g, dz, gz);
       }
     }
+#endif
     if (GRAD) {  // the j column moves one lane down with its atom
       gx = shfl_rot<T>(gx, src);
       gy = shfl_rot<T>(gy, src);
@@ -169,8 +245,11 @@ __device__ __forceinline__ double block_min(double v, double* red) {
 
 // grid = (nunits, batch).  ipart/jpart: [nunits][3][S] gradient partials
 // (GRAD only); epart: [batch][nunits][3] = (coulomb, vdw, min r^2).
+#ifndef FFM_MINB
+#define FFM_MINB 2
+#endif
 template <typename T, bool GRAD, bool CUTOFF>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? FFM_MINB : 1)
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,

@@ -233,7 +233,7 @@ __device__ bool scaled_pair(P3 ci, P3 cj, double qi, double qj, double sgi, doub
   if (eps_ij > 0.0) {
     const double sig = sqrt(sgi * sgj);
     const double t = sig / r;
-    const double x6 = t * t * t * t * t * t;
+    const double t2 = t * t, x6 = t2 * (t2 * t2);  // numba lowers x**6 to powi
     *ev = 4.0 * s * eps_ij * (x6 * x6 - x6);
     dedr_over_r += 4.0 * s * eps_ij * (-12.0 * x6 * x6 + 6.0 * x6) / (r * r);
   }
@@ -536,8 +536,8 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
                   const int* __restrict__ fsp_ptr, const int* __restrict__ fsp_j,
                   const double* __restrict__ fsp_s, const int* __restrict__ aterm_ptr,
                   const int* __restrict__ aterm_idx, const int* __restrict__ atoms,
-                  const double* __restrict__ newpos, double* __restrict__ out,
-                  int64_t* __restrict__ status) {
+                  const double* __restrict__ newpos, double lin_cutoff,
+                  double* __restrict__ out, int64_t* __restrict__ status) {
   __shared__ double sh[32];
   __shared__ long long bad[3];
   const int k = blockIdx.x;
@@ -547,7 +547,9 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
   if (threadIdx.x < 3) bad[threadIdx.x] = kSentinel;
   __syncthreads();
   const int sb = fsp_ptr[a], se = fsp_ptr[a + 1];
-  double dec = 0.0, dev = 0.0;
+  const bool lin = lin_cutoff > 0.0;
+  const P3 dl = sub(np, ca);
+  double dec = 0.0, dev = 0.0, far = 0.0;
   for (int j = threadIdx.x; j < tp.n; j += kDeltaThreads) {
     if (j == a) continue;
     // binary search of the (short, sorted) special row of atom a
@@ -558,9 +560,38 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
       if (fsp_j[mid] < j) lo = mid + 1; else hi = mid;
     }
     if (lo < se && fsp_j[lo] == j) s = fsp_s[lo];
-    if (s == 0.0) continue;
     const P3 cj = ld3(coords, j);
-    const P3 o = sub(ca, cj), nn = sub(np, cj);
+    const P3 o = sub(ca, cj);
+    if (lin) {
+      // far-field linearisation (ffmin/kernels.py:359-416): excluded / 1-4
+      // partners and everything within the cutoff are treated exactly, the
+      // far Coulomb sum by its gradient at the current position
+      const double ro = sqrt(dot(o, o));
+      if (!(ro <= lin_cutoff || s != 1.0)) {
+        const double qq = tp.q[a] * tp.q[j];
+        far += -kCoulomb * qq / (ro * ro * ro) * dot(o, dl);
+        continue;
+      }
+      if (s == 0.0) continue;
+      const P3 nn = sub(np, cj);
+      const double rn = sqrt(dot(nn, nn));
+      if (ro < kRmin || rn < kRmin) {
+        atomicMin(&bad[0], (long long)j);
+        continue;
+      }
+      const double qq = s * tp.q[a] * tp.q[j];
+      dec += kCoulomb * qq * (1.0 / rn - 1.0 / ro);
+      const double eps_ij = sqrt(tp.eps[a] * tp.eps[j]);
+      if (eps_ij > 0.0) {
+        const double sig = sqrt(tp.sigma[a] * tp.sigma[j]);
+        const double to = sig / ro, to2 = to * to, xo = to2 * (to2 * to2);
+        const double tn = sig / rn, tn2 = tn * tn, xn = tn2 * (tn2 * tn2);
+        dev += 4.0 * s * eps_ij * ((xn * xn - xn) - (xo * xo - xo));
+      }
+      continue;
+    }
+    if (s == 0.0) continue;
+    const P3 nn = sub(np, cj);
     const double ro = sqrt(dot(o, o)), rn = sqrt(dot(nn, nn));
     if (ro < kRmin || rn < kRmin) {
       atomicMin(&bad[0], (long long)j);
@@ -574,14 +605,14 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
     if (in_old) {
       dec -= kCoulomb * qq / ro;
       if (eps_ij > 0.0) {
-        const double t = sig / ro, x = t * t * t * t * t * t;
+        const double t = sig / ro, t2 = t * t, x = t2 * (t2 * t2);
         dev -= 4.0 * s * eps_ij * (x * x - x);
       }
     }
     if (in_new) {
       dec += kCoulomb * qq / rn;
       if (eps_ij > 0.0) {
-        const double t = sig / rn, x = t * t * t * t * t * t;
+        const double t = sig / rn, t2 = t * t, x = t2 * (t2 * t2);
         dev += 4.0 * s * eps_ij * (x * x - x);
       }
     }
@@ -634,13 +665,16 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
   db = tree_sum(db, sh);
   da = tree_sum(da, sh);
   dd = tree_sum(dd, sh);
+  far = tree_sum(far, sh);
   if (threadIdx.x == 0) {
-    double* o = out + 5 * (size_t)k;
+    const int w = lin ? 6 : 5;
+    double* o = out + w * (size_t)k;
     o[0] = dec;
     o[1] = dev;
     o[2] = db;
     o[3] = da;
     o[4] = dd;
+    if (lin) o[5] = far;
     int64_t* s = status + 3 * (size_t)k;
     for (int q = 0; q < 3; ++q) s[q] = bad[q] == kSentinel ? -1 : (int64_t)bad[q];
   }
@@ -649,12 +683,77 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
 cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
                               const int* aterm_ptr, const int* aterm_idx, int ncand,
-                              const int* atoms, const double* newpos, double* out,
-                              int64_t* status, cudaStream_t st) {
+                              const int* atoms, const double* newpos, double lin_cutoff,
+                              double* out, int64_t* status, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
   count_launch(), atom_delta_kernel<<<ncand, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s,
-                                                     aterm_ptr, aterm_idx, atoms, newpos, out,
-                                                     status);
+                                                     aterm_ptr, aterm_idx, atoms, newpos, lin_cutoff,
+                                                     out, status);
+  return cudaGetLastError();
+}
+
+// ffmin/kernels.py:359-387 (_loop_farfield_build): far-field Coulomb energy of
+// one atom and its gradient, and the exact near set; one block.
+__global__ void __launch_bounds__(kDeltaThreads)
+farfield_kernel(TermPlanDev tp, const double* __restrict__ coords,
+                const int* __restrict__ fsp_ptr, const int* __restrict__ fsp_j,
+                const double* __restrict__ fsp_s, int a, double cutoff,
+                double* __restrict__ e0_coef, uint8_t* __restrict__ near_mask,
+                int64_t* __restrict__ bad) {
+  __shared__ double sh[32];
+  __shared__ long long first_bad;
+  if (threadIdx.x == 0) first_bad = kSentinel;
+  __syncthreads();
+  const P3 ca = ld3(coords, a);
+  const int sb = fsp_ptr[a], se = fsp_ptr[a + 1];
+  double e0 = 0.0, cx = 0.0, cy = 0.0, cz = 0.0;
+  for (int j = threadIdx.x; j < tp.n; j += kDeltaThreads) {
+    uint8_t near = 0;
+    if (j != a) {
+      double s = 1.0;
+      int lo = sb, hi = se;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (fsp_j[mid] < j) lo = mid + 1; else hi = mid;
+      }
+      if (lo < se && fsp_j[lo] == j) s = fsp_s[lo];
+      const P3 d = sub(ca, ld3(coords, j));
+      const double r = sqrt(dot(d, d));
+      if (r <= cutoff || s != 1.0) {
+        near = 1;
+      } else if (r < kRmin) {
+        atomicMin(&first_bad, (long long)j);
+      } else {
+        const double qq = tp.q[a] * tp.q[j];
+        e0 += kCoulomb * qq / r;
+        const double g = -kCoulomb * qq / (r * r * r);
+        cx += g * d.x;
+        cy += g * d.y;
+        cz += g * d.z;
+      }
+    }
+    near_mask[j] = near;
+  }
+  e0 = tree_sum(e0, sh);
+  cx = tree_sum(cx, sh);
+  cy = tree_sum(cy, sh);
+  cz = tree_sum(cz, sh);
+  if (threadIdx.x == 0) {
+    e0_coef[0] = e0;
+    e0_coef[1] = cx;
+    e0_coef[2] = cy;
+    e0_coef[3] = cz;
+    *bad = first_bad == kSentinel ? -1 : (int64_t)first_bad;
+  }
+}
+
+cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const int* fsp_ptr,
+                            const int* fsp_j, const double* fsp_s, int atom, double cutoff,
+                            double* e0_coef, uint8_t* near_mask, int64_t* bad,
+                            cudaStream_t st) {
+  count_launch();
+  farfield_kernel<<<1, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s, atom, cutoff,
+                                               e0_coef, near_mask, bad);
   return cudaGetLastError();
 }
 

@@ -202,26 +202,115 @@ def exact_delta_atom_move(system: MolecularSystem, atom: int, delta, dtype=np.fl
                           backend=None) -> float:
     """Exact O(n) energy change for moving one atom (ffmin/energy.py:284-313),
     evaluated by the device delta kernel."""
+    _check_backend(backend)
+    out, st = atom_deltas(system, [atom], np.asarray(delta, np.float64).reshape(1, 3))
+    _raise_delta(system, atom, st[0])
+    o = out[0]
+    # reference summation order: de + dea + ded + dec + dev
+    return float(o[2]) + float(o[3]) + float(o[4]) + float(o[0]) + float(o[1])
+
+
+@dataclass(frozen=True)
+class NeighborList:
+    """Symmetric within-cutoff adjacency (ffmin/energy.py:44-49)."""
+
+    cutoff: float
+    neighbors: tuple
+
+
+@dataclass(frozen=True)
+class FarFieldLinearization:
+    """First-order model of one atom's far-field Coulomb sum
+    (ffmin/energy.py:52-68)."""
+
+    atom: int
+    cutoff: float
+    ref_pos: np.ndarray
+    e_far0: float
+    coef: np.ndarray
+    near_idx: np.ndarray
+
+
+def _dev_coords(system):
     import torch
 
-    _check_backend(backend)
-    delta = np.asarray(delta, dtype=np.float64).reshape(3)
-    newpos = system.coords[atom] + delta
     eng = engine_for(system.topology)
-    dev = eng.device
-    coords = torch.from_numpy(np.ascontiguousarray(system.coords)).to(dev)
-    out, st = eng.atom_delta(coords, torch.tensor([atom], dtype=torch.int32, device=dev),
-                             torch.from_numpy(newpos.reshape(1, 3)).to(dev))
-    out = out.cpu().numpy()[0]
-    st = st.cpu().numpy()[0]
+    return eng, torch.from_numpy(np.array(system.coords, dtype=np.float64)).to(eng.device)
+
+
+def build_neighbor_list(system: MolecularSystem, cutoff: float) -> NeighborList:
+    """Within-cutoff adjacency by a brute-force pair scan on the device
+    (ffmin/energy.py:201-212)."""
+    if not cutoff > 0:
+        raise ValueError(f"cutoff must be > 0, got {cutoff}")
+    import torch
+
+    _, c = _dev_coords(system)
+    n = system.natoms
+    out = []
+    for i0 in range(0, n, 4096):
+        d = torch.cdist(c[i0:i0 + 4096], c)
+        d[torch.arange(d.shape[0], device=c.device), torch.arange(i0, i0 + d.shape[0],
+                                                               device=c.device)] = float("inf")
+        rows = (d <= cutoff).cpu().numpy()
+        out.extend(np.nonzero(r)[0].astype(np.int64) for r in rows)
+    return NeighborList(cutoff=float(cutoff), neighbors=tuple(out))
+
+
+def linearize_farfield_coulomb(system: MolecularSystem, atom: int,
+                               cutoff: float) -> FarFieldLinearization:
+    """Split one atom's Coulomb sum at `cutoff` and linearise the far part
+    (ffmin/energy.py:215-240), one device kernel."""
+    if not 0 <= atom < system.natoms:
+        raise ValueError(f"atom index {atom} out of range for {system.natoms} atoms")
+    if not cutoff > 0:
+        raise ValueError(f"cutoff must be > 0, got {cutoff}")
+    eng, c = _dev_coords(system)
+    e, m, b = eng.farfield(c, atom, cutoff)
+    if int(b.item()) >= 0:
+        raise EnergyEvaluationError(f"nonbonded pair ({atom},{int(b.item())}): coincident atoms")
+    e = e.cpu().numpy()
+    return FarFieldLinearization(atom=int(atom), cutoff=float(cutoff),
+                                 ref_pos=system.coords[atom].copy(), e_far0=float(e[0]),
+                                 coef=e[1:4].copy(),
+                                 near_idx=np.nonzero(m.cpu().numpy())[0].astype(np.int64))
+
+
+def delta_energy_atom_move(system: MolecularSystem, lin: FarFieldLinearization, delta) -> float:
+    """Energy change of moving lin.atom by delta with the far field
+    linearised (ffmin/energy.py:243-281); valid while the system still has
+    the coordinates lin was built from."""
+    if system.topology.cutoff is not None:
+        raise ValueError("incremental delta requires a system nonbonded cutoff of none")
+    out, st = atom_deltas(system, [lin.atom], np.asarray(delta, np.float64).reshape(1, 3),
+                          lin_cutoff=lin.cutoff)
+    _raise_delta(system, lin.atom, st[0])
+    o = out[0]
+    return float(o[2]) + float(o[3]) + float(o[4]) + float(o[0]) + float(o[1]) + float(o[5])
+
+
+def atom_deltas(system: MolecularSystem, atoms, deltas, lin_cutoff=None, coords_d=None):
+    """Batched single-atom move deltas on the device: rows (k, 5) exact or
+    (k, 6) linearised, plus status rows (k, 3), as NumPy."""
+    import torch
+
+    eng = engine_for(system.topology)
+    if coords_d is None:
+        coords_d = torch.from_numpy(np.array(system.coords, dtype=np.float64)).to(eng.device)
+    atoms = np.asarray(atoms, dtype=np.int64).reshape(-1)
+    newpos = system.coords[atoms] + np.asarray(deltas, np.float64).reshape(-1, 3)
+    out, st = eng.atom_delta(coords_d, torch.from_numpy(atoms.astype(np.int32)).to(eng.device),
+                             torch.from_numpy(newpos).to(eng.device), lin_cutoff=lin_cutoff)
+    return out.cpu().numpy(), st.cpu().numpy()
+
+
+def _raise_delta(system, atom, st):
     if st[0] >= 0:
         raise EnergyEvaluationError(f"nonbonded pair ({atom},{int(st[0])}): coincident atoms")
     if st[1] >= 0:
         raise EnergyEvaluationError(f"{_angle_name(system, int(st[1]))}: zero-length arm")
     if st[2] >= 0:
         raise EnergyEvaluationError(f"{_dihedral_name(system, int(st[2]))}: degenerate plane")
-    # reference summation order: de + dea + ded + dec + dev
-    return float(out[2]) + float(out[3]) + float(out[4]) + float(out[0]) + float(out[1])
 
 
 # re-export the constant under its conventional name (ffmin/energy.py:316-317)

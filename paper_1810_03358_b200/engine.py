@@ -126,20 +126,36 @@ class DeviceSystem:
                 "ffm_eval_batch")
         return energies, status
 
-    def atom_delta(self, coords, atoms, newpos, out=None, status=None, stream=None):
-        """Exact energy change of single-atom moves; atoms int32 (k,), newpos
-        float64 (k, 3), all on device.  Returns (out (k, 5), status (k, 3))."""
+    def atom_delta(self, coords, atoms, newpos, out=None, status=None, stream=None,
+                   lin_cutoff=None):
+        """Energy change of single-atom moves; atoms int32 (k,), newpos
+        float64 (k, 3), all on device.  Exact: out (k, 5) = (coulomb, vdw,
+        stretch, bend, torsion); with lin_cutoff the far-field linearised
+        delta, out (k, 6) with the far term last.  status (k, 3)."""
         self._check_coords(coords)
         k = int(atoms.shape[0])
+        w = 5 if lin_cutoff is None else 6
         if out is None:
-            out = torch.empty((k, 5), dtype=torch.float64, device=self.device)
+            out = torch.empty((k, w), dtype=torch.float64, device=self.device)
         if status is None:
             status = torch.empty((k, 3), dtype=torch.int64, device=self.device)
         assert atoms.dtype == torch.int32 and newpos.dtype == torch.float64
-        N.check(self.lib.ffm_atom_delta(self.handle, _p(coords), k, _p(atoms.contiguous()),
-                                        _p(newpos.contiguous()), _p(out), _p(status),
-                                        _stream_ptr(stream)), "ffm_atom_delta")
+        N.check(self.lib.ffm_atom_delta_lin(
+            self.handle, _p(coords), k, _p(atoms.contiguous()), _p(newpos.contiguous()),
+            0.0 if lin_cutoff is None else float(lin_cutoff), _p(out), _p(status),
+            _stream_ptr(stream)), "ffm_atom_delta_lin")
         return out, status
+
+    def farfield(self, coords, atom, cutoff, stream=None):
+        """(e0_coef[4], near_mask[n] uint8, bad[1]) device tensors."""
+        self._check_coords(coords)
+        e = torch.empty(4, dtype=torch.float64, device=self.device)
+        m = torch.empty(self.n, dtype=torch.uint8, device=self.device)
+        b = torch.empty(1, dtype=torch.int64, device=self.device)
+        N.check(self.lib.ffm_farfield_build(self.handle, _p(coords), int(atom), float(cutoff),
+                                            _p(e), _p(m), _p(b), _stream_ptr(stream)),
+                "ffm_farfield_build")
+        return e, m, b
 
     # ------------------------------------------------------------- host
     def eval_host(self, coords, precision=N.FFM_F64, grad=False, flags=None):

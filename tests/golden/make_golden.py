@@ -246,6 +246,40 @@ def main():
         store[f"drv30/{name}/status"] = np.array(r.status)
     store["drv30/names"] = np.array(list(runs))
 
+    # far-field linearisation + incremental deltas (energy.py:215-281)
+    from ffmin.energy import delta_energy_atom_move, linearize_farfield_coulomb
+    sff = two_cluster(7, 40, 40.0)
+    put_system("ff40", sff)
+    rng = np.random.default_rng(70)
+    rows = []
+    for atom in (0, 7, 23, 39):
+        lin = linearize_farfield_coulomb(sff, atom, 7.0)
+        store[f"ff40/lin{atom}"] = np.concatenate([[lin.e_far0], lin.coef])
+        store[f"ff40/near{atom}"] = lin.near_idx
+        for _ in range(3):
+            d = rng.uniform(-0.3, 0.3, 3)
+            rows.append([atom, *d, delta_energy_atom_move(sff, lin, d)])
+    store["ff40/deltas"] = np.array(rows)
+
+    # gradient-free atom wiggle (section 3), incremental and full-recompute
+    from ffmin.optimizers import WiggleConfig, atom_wiggle
+    for name, sw, cfg, iters in (
+            ("wig40", two_cluster(3, 40, 40.0), WiggleConfig(seed=0), 2000),
+            ("wigchain", make_chain_system(20, seed=6, strain=0.3),
+             WiggleConfig(seed=1, use_incremental_coulomb=False), 1000)):
+        put_system(name, sw)
+        t1 = time.time()
+        r = atom_wiggle(sw, cfg, StopCriteria(max_iterations=iters, gradient_norm_rtol=0.0))
+        store[f"{name}/seconds"] = np.array(time.time() - t1)
+        store[f"{name}/f"] = np.array([rec.f for rec in r.trace.records])
+        store[f"{name}/step"] = np.array([rec.step for rec in r.trace.records])
+        store[f"{name}/calls"] = np.array([rec.value_calls for rec in r.trace.records])
+        store[f"{name}/x"] = r.x
+        store[f"{name}/cfg"] = np.array([cfg.h, cfg.seed, cfg.epoch_iterations,
+                                         float(cfg.use_incremental_coulomb), cfg.cutoff, iters])
+        print(name, r.status, r.f, sum(1 for rec in r.trace.records if rec.step > 0),
+              time.time() - t1)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT} ({OUT.stat().st_size / 1e6:.2f} MB) in {time.time() - t0:.1f}s")
 

@@ -220,3 +220,36 @@ def test_full_size_properties():
     bd3, g3 = energy_and_gradient(s, np.float32)
     assert bd3.total == pytest.approx(bd.total, rel=1e-5)
     assert np.max(np.abs(g3 - g)) <= 1e-4 * np.max(np.abs(g))
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_row_shards_sum_to_the_full_evaluation(world):
+    """ffm_system_set_shard on one GPU: the partial gradients / energies of
+    all ranks, summed, equal the unsharded evaluation (what the NCCL
+    all-reduce of parallel.ShardCombiner computes on W GPUs)."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(20000, seed=4)
+    c = torch.from_numpy(s.coords.copy()).cuda()
+    full = DeviceSystem(s.topology)
+    g_full = torch.empty_like(c)
+    e_full, _ = full.eval(c, N.FFM_F64, grad=g_full)
+    g_sum = torch.zeros_like(c)
+    e_sum = torch.zeros(5, dtype=torch.float64, device=c.device)
+    for rank in range(world):
+        eng = DeviceSystem(s.topology)
+        N.check(eng.lib.ffm_system_set_shard(eng.handle, rank, world), "set_shard")
+        g = torch.empty_like(c)
+        e, st = eng.eval(c, N.FFM_F64, grad=g)
+        assert int(st[0]) == -1
+        if rank != 0:
+            assert float(e[0]) == float(e[1]) == float(e[2]) == 0.0  # bonded on rank 0 only
+        g_sum += g
+        e_sum += e
+        eng.close()
+    assert torch.allclose(e_sum, e_full, rtol=1e-12)
+    assert float((g_sum - g_full).abs().max()) <= 1e-11 * float(g_full.abs().max())

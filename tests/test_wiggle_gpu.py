@@ -1,0 +1,60 @@
+"""Far-field linearisation, incremental deltas and the gradient-free atom
+wiggle on the device, against the reference (golden).  GPU only."""
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import golden_system
+
+pytestmark = pytest.mark.gpu
+
+
+def test_farfield_linearisation_matches_reference(golden):
+    from paper_1810_03358_b200.energy import delta_energy_atom_move, linearize_farfield_coulomb
+
+    s = golden_system(golden, "ff40")
+    for atom in (0, 7, 23, 39):
+        lin = linearize_farfield_coulomb(s, atom, 7.0)
+        ref = golden[f"ff40/lin{atom}"]
+        assert lin.e_far0 == pytest.approx(ref[0], rel=1e-12, abs=1e-12)
+        np.testing.assert_allclose(lin.coef, ref[1:], rtol=1e-11, atol=1e-12)
+        assert np.array_equal(lin.near_idx, golden[f"ff40/near{atom}"])
+    for atom, dx, dy, dz, want in golden["ff40/deltas"]:
+        lin = linearize_farfield_coulomb(s, int(atom), 7.0)
+        got = delta_energy_atom_move(s, lin, [dx, dy, dz])
+        assert got == pytest.approx(want, rel=1e-10, abs=1e-10)
+
+
+def test_incremental_delta_rejects_cutoff_systems(golden):
+    from paper_1810_03358_b200.energy import delta_energy_atom_move, linearize_farfield_coulomb
+
+    s = golden_system(golden, "chain12cut")
+    lin = linearize_farfield_coulomb(s, 3, 7.0)
+    with pytest.raises(ValueError, match="cutoff"):
+        delta_energy_atom_move(s, lin, [0.1, 0.0, 0.0])
+
+
+@pytest.mark.parametrize("name", ["wig40", "wigchain"])
+def test_wiggle_tracks_reference(golden, name):
+    from paper_1810_03358_b200.optimizers import StopCriteria
+    from paper_1810_03358_b200.optimizers.wiggle import WiggleConfig, atom_wiggle
+
+    s = golden_system(golden, name)
+    h, seed, epoch, inc, cutoff, iters = golden[f"{name}/cfg"]
+    cfg = WiggleConfig(h=h, seed=int(seed), epoch_iterations=int(epoch),
+                       use_incremental_coulomb=bool(inc), cutoff=cutoff)
+    res = atom_wiggle(s, cfg, StopCriteria(max_iterations=int(iters), gradient_norm_rtol=0.0))
+    f = np.array([r.f for r in res.trace.records])
+    steps = np.array([r.step for r in res.trace.records])
+    ref_f, ref_steps = golden[f"{name}/f"], golden[f"{name}/step"]
+    # same random atoms, same accept / reject decisions, same energies
+    assert np.array_equal(steps > 0, ref_steps > 0)
+    np.testing.assert_allclose(steps, ref_steps, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(f, ref_f, rtol=1e-10, atol=1e-8)
+    calls = np.array([r.value_calls for r in res.trace.records])
+    assert np.array_equal(calls, golden[f"{name}/calls"])
+    # every accepted move strictly lowered the energy
+    assert all(b < a for a, b, st in zip(f, f[1:], steps[1:]) if st > 0)
+    assert math.isnan(res.grad_norm)

@@ -34,6 +34,48 @@ __global__ void k_ffma2(float* out, float a0, float b0){
   }
   out[blockIdx.x*blockDim.x+threadIdx.x]=x0.x+x1.x+x2.x+x3.x+x4.x+x5.x+x6.x+x7.x+x0.y+x1.y+x2.y+x3.y+x4.y+x5.y+x6.y+x7.y;
 }
+// FFMA2 with three distinct register-pair operands in every instruction
+// (no operand reuse possible): tests register-bank read limits
+__global__ void k_ffma2_distinct(float* out, float a0, float b0){
+  float2 a[8], b[8], x[8];
+  #pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    a[k] = make_float2(a0 + (threadIdx.x + k) * 1e-9f, a0 - k * 1e-9f);
+    b[k] = make_float2(b0 + k * 1e-9f, b0 + threadIdx.x * 1e-9f);
+    x[k] = make_float2(threadIdx.x + k, k);
+  }
+  #pragma unroll 4
+  for(int i=0;i<ITERS;i++){
+    #pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __ffma2_rn(x[k], a[k], b[k]);
+  }
+  float s = 0; for (int k = 0; k < 8; ++k) s += x[k].x + x[k].y;
+  out[blockIdx.x*blockDim.x+threadIdx.x]=s;
+}
+__global__ void k_ffma_distinct(float* out, float a0, float b0){
+  float a[8], b[8], x[8];
+  #pragma unroll
+  for (int k = 0; k < 8; ++k) { a[k] = a0 + (threadIdx.x + k) * 1e-9f; b[k] = b0 + k * 1e-9f; x[k] = threadIdx.x + k; }
+  #pragma unroll 4
+  for(int i=0;i<ITERS;i++){
+    #pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fmaf(x[k], a[k], b[k]);
+  }
+  float s = 0; for (int k = 0; k < 8; ++k) s += x[k];
+  out[blockIdx.x*blockDim.x+threadIdx.x]=s;
+}
+__global__ void k_fmul2_distinct(float* out, float a0){
+  float2 a[8], x[8];
+  #pragma unroll
+  for (int k = 0; k < 8; ++k) { a[k] = make_float2(1.0f + (threadIdx.x + k) * 1e-9f, 1.0f - k * 1e-9f); x[k] = make_float2(threadIdx.x + k, k); }
+  #pragma unroll 4
+  for(int i=0;i<ITERS;i++){
+    #pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = __fmul2_rn(x[k], a[k]);
+  }
+  float s = 0; for (int k = 0; k < 8; ++k) s += x[k].x + x[k].y;
+  out[blockIdx.x*blockDim.x+threadIdx.x]=s;
+}
 __global__ void k_rsqrt(float* out, float a){
   float x0=threadIdx.x+1, x1=x0+1, x2=x0+2, x3=x0+3, x4=x0+4, x5=x0+5, x6=x0+6, x7=x0+7;
   #pragma unroll 16
@@ -80,6 +122,9 @@ int main(){
   run("ffma_imm", [&]{k_ffma<<<blocks,threads>>>(out,1.0001f,0.5f);}, 8.0*ITERS, "FMA");
   run("ffma_reg", [&]{k_ffma_reg<<<blocks,threads>>>(out,1.0001f,0.5f);}, 8.0*ITERS, "FMA");
   run("ffma2", [&]{k_ffma2<<<blocks,threads>>>(out,1.0001f,0.5f);}, 16.0*ITERS, "FMA");
+  run("ffma2_dist", [&]{k_ffma2_distinct<<<blocks,threads>>>(out,1.0f,0.5f);}, 16.0*ITERS, "FMA");
+  run("ffma_dist", [&]{k_ffma_distinct<<<blocks,threads>>>(out,1.0f,0.5f);}, 8.0*ITERS, "FMA");
+  run("fmul2_dist", [&]{k_fmul2_distinct<<<blocks,threads>>>(out,1.0f);}, 16.0*ITERS, "MUL");
   run("rsqrt", [&]{k_rsqrt<<<blocks,threads>>>(out,1.0f);}, 8.0*ITERS, "op");
   run("dfma", [&]{k_dfma<<<blocks,threads>>>((double*)out,1.0000001,0.5);}, 8.0*ITERS, "FMA");
   run("shfl", [&]{k_shfl<<<blocks,threads>>>(out,1.0f);}, 4.0*ITERS, "op");
