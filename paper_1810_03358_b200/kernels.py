@@ -214,17 +214,37 @@ def dihedral_delta(coords, atom, newpos, didx, V, rows):
     return _rows_delta(coords, atom, newpos, "dihedral", (didx, V), rows)
 
 
-def _not_yet(name):
-    def f(*args, **kwargs):
-        raise NotImplementedError(
-            f"cuda backend: {name} (far-field linearisation, wiggle incremental mode) is "
-            "not implemented on the device yet; use exact deltas (nb_atom_delta)")
-    f.__name__ = name
-    return f
+def farfield_build(coords, q, scale, atom, cutoff):
+    """ffmin/kernels.py:359-387: (e0, cx, cy, cz, near_mask uint8, bad)."""
+    n = coords.shape[0]
+    eng = _engine((q, scale), lambda: _topology(n, q, None, np.zeros(n), scale, -1.0), n)
+    import torch
+
+    c = torch.from_numpy(_f64coords(coords)).to(eng.device)
+    e, m, b = eng.farfield(c, int(atom), float(cutoff))
+    e = e.cpu().numpy()
+    return float(e[0]), float(e[1]), float(e[2]), float(e[3]), m.cpu().numpy(), int(b.item())
 
 
-farfield_build = _not_yet("farfield_build")
-near_nb_delta = _not_yet("near_nb_delta")
+def near_nb_delta(coords, q, sigma, epsilon, scale, atom, newpos, near_idx):
+    """ffmin/kernels.py:390-416: exact nonbonded change of moving `atom`
+    against the partners in near_idx only -- the exact delta kernel on a
+    plan whose other atoms carry no charge and no LJ."""
+    n = coords.shape[0]
+    near = np.zeros(n, bool)
+    near[np.asarray(near_idx, np.int64)] = True
+    near[int(atom)] = True
+    qn = np.where(near, np.asarray(q, np.float64), 0.0)
+    en = np.where(near, np.asarray(epsilon, np.float64), 0.0)
+    eng = DeviceSystem(_topology(n, qn, sigma, en, scale, -1.0))
+    try:
+        out, st = _delta(eng, coords, atom, newpos)
+    finally:
+        eng.close()
+    if st[0] >= 0:
+        return 0.0, 0.0, int(st[0])
+    return float(out[0]), float(out[1]), -1
+
 
 _CUDA_FNS = {
     "bond_energy": bond_energy, "bond_grad": bond_grad,

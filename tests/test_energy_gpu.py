@@ -253,3 +253,33 @@ def test_row_shards_sum_to_the_full_evaluation(world):
         eng.close()
     assert torch.allclose(e_sum, e_full, rtol=1e-12)
     assert float((g_sum - g_full).abs().max()) <= 1e-11 * float(g_full.abs().max())
+
+
+def test_kernel_backend_farfield_functions(golden):
+    from paper_1810_03358_b200.kernels import get_backend
+
+    kb = get_backend("cuda")
+    s = golden_system(golden, "ff40")
+    p = s.arrays()
+    c = np.ascontiguousarray(s.coords)
+    for atom in (0, 23):
+        e0, cx, cy, cz, near, bad = kb.farfield_build(c, p["q"], p["scale"], atom, 7.0)
+        ref = golden[f"ff40/lin{atom}"]
+        assert bad == -1
+        np.testing.assert_allclose([e0, cx, cy, cz], ref, rtol=1e-11, atol=1e-12)
+        assert np.array_equal(np.nonzero(near)[0], golden[f"ff40/near{atom}"])
+        newpos = c[atom] + np.array([0.1, -0.2, 0.05])
+        dec, dev, bad = kb.near_nb_delta(c, p["q"], p["sigma"], p["epsilon"], p["scale"],
+                                         atom, newpos, np.nonzero(near)[0])
+        A, _ = oracle_arrays(golden, "ff40")
+        # oracle: exact delta restricted to the near set
+        import oracle as OO
+        mask = np.zeros(A.n, bool)
+        mask[np.nonzero(near)[0]] = True
+        mask[atom] = True
+        A.q = np.where(mask, A.q, 0.0)
+        A.eps = np.where(mask, A.eps, 0.0)
+        parts, b2 = OO.atom_delta(A, c, atom, newpos - c[atom])
+        assert bad == b2 == -1
+        assert dec == pytest.approx(parts[0], rel=1e-10, abs=1e-10)
+        assert dev == pytest.approx(parts[1], rel=1e-10, abs=1e-10)
