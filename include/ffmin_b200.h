@@ -46,6 +46,8 @@ extern "C" {
 #define FFM_NO_NB 4     /* skip the nonbonded terms (all pairs + scaled 1-4) */
 #define FFM_NO_TERMS 8  /* skip the bonded terms (stretch, bend, torsion)    */
 #define FFM_TIME_NB 16  /* record CUDA events around the pair sweep          */
+#define FFM_NO_GRAPH 32 /* issue the kernels directly instead of replaying a
+                         * captured CUDA graph of the same call              */
 
 /* status words (int64[8] per evaluation) */
 #define FFM_ST_NB_BAD_I 0   /* first coincident nonbonded pair, -1 clean */
@@ -103,7 +105,10 @@ long long ffm_launch_count(void);
  * scaled pairs, device */
 int ffm_system_info(const ffm_system_t* sys, int64_t* info_h);
 
-/* Full evaluation on device buffers (no host synchronisation):
+/* Full evaluation on device buffers (no host synchronisation).  The first
+ * call with a given (precision, flags, buffer addresses) captures its seven
+ * kernels into a CUDA graph; later identical calls replay it with one
+ * launch (keep input/output buffers fixed to benefit).
  * replaces energy_total / energy_and_gradient (ffmin/energy.py:133-174) and
  * the KernelBackend nb_energy / nb_grad / *_grad calls they make.
  * grad_d (n*3, overwritten) may be NULL without FFM_GRAD. */
@@ -157,6 +162,11 @@ int ffm_farfield_build(ffm_system_t* sys, const double* coords_d, int64_t atom, 
 int64_t ffm_vec_scratch_doubles(void);
 int ffm_dot(int64_t n, const double* x_d, const double* y_d, double* out_d,
             double* scratch_d, void* stream);
+
+/* out_d[q] = <xs_h[q], ys_h[q]> for q < k <= 8 in one pass (host arrays of
+ * device pointers), same fixed-order reduction as ffm_dot. */
+int ffm_dots(int64_t n, int k, const double* const* xs_h, const double* const* ys_h,
+             double* out_d, double* scratch_d, void* stream);
 
 /* z = sa * (a * x + b * y); a/b read from a_d/b_d when non-NULL, else a_h/b_h;
  * y_d may be NULL. */

@@ -26,6 +26,7 @@ FFM_GRAD = 2
 FFM_NO_NB = 4
 FFM_NO_TERMS = 8
 FFM_TIME_NB = 16
+FFM_NO_GRAPH = 32
 FFM_NTERMS = 5
 FFM_STATUS_WORDS = 8
 ST_NB_BAD_I, ST_NB_BAD_J, ST_BOND, ST_ANGLE, ST_DIHEDRAL = 0, 1, 2, 3, 4
@@ -54,6 +55,7 @@ SIGNATURES = {
     "ffm_farfield_build": (_I, [_P, _P, _I64, _D, _P, _P, _P, _P]),
     "ffm_vec_scratch_doubles": (_I64, []),
     "ffm_dot": (_I, [_I64, _P, _P, _P, _P, _P]),
+    "ffm_dots": (_I, [_I64, _I, _P, _P, _P, _P, _P]),
     "ffm_axpby": (_I, [_I64, _P, _D, _D, _P, _P, _D, _P, _P, _P]),
     "ffm_lbfgs_two_loop": (_I, [_I64, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
 }

@@ -104,6 +104,18 @@ struct ffm_system {
   std::vector<std::pair<int, int>> scaled;  // (i, j)
   std::vector<double> scaled_s;
   Work w[2];  // [precision]
+  // captured evaluation sequences (CUDA graphs), keyed by the call's
+  // arguments; invalidated whenever a workspace buffer moves
+  struct GraphEntry {
+    int prec, flags;
+    const void *coords, *grad, *energies, *status;
+    long long gen;
+    long long kernels;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
+  long long gen = 0;
+  cudaStream_t cap_stream = nullptr;
   // FFM_TIME_NB: events around the pair sweep of the last evaluation
   cudaEvent_t ev_nb0 = nullptr, ev_nb1 = nullptr;
   bool timed = false;
@@ -126,6 +138,9 @@ void free_all(ffm_system* s) {
                   s->h_en_d, s->h_st_d, s->d_unit_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+  s->graphs.clear();
+  if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
   if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
@@ -133,6 +148,12 @@ void free_all(ffm_system* s) {
     for (void* p : wp)
       if (p) cudaFree(p);
   }
+}
+
+void drop_graphs(ffm_system* s) {
+  for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
+  s->graphs.clear();
+  s->gen++;
 }
 
 // Super-unit edge: the largest S that still gives >= 2048 units (about 3.5
@@ -259,6 +280,23 @@ int build_terms(ffm_system* s, int64_t nbond, const int64_t* bidx, const double*
 // allocate / grow the workspace of one precision
 int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   Work& w = s->w[prec];
+  struct Bump {
+    ffm_system* s;
+    Work* w;
+    void* p[8];
+    Bump(ffm_system* s_, Work* w_) : s(s_), w(w_) {
+      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, nullptr};
+      for (int i = 0; i < 8; ++i) p[i] = q[i];
+    }
+    ~Bump() {
+      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, nullptr};
+      for (int i = 0; i < 8; ++i)
+        if (q[i] != p[i]) {
+          drop_graphs(s);
+          break;
+        }
+    }
+  } bump(s, &w);
   const bool f64 = prec == FFM_F64;
   const NbPlanDev& p = s->plan;
   const size_t tsz = f64 ? 8 : 4;
@@ -294,7 +332,7 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   if (w.te_batch < batch) {
     if (w.term_e) cudaFree(w.term_e);
     w.term_e = nullptr;
-    const size_t ne = std::max(1, s->tp.nterm_e);
+    const size_t ne = (size_t)std::max(1, term_blocks(s->tp)) * 5;
     if (cudaMalloc(&w.term_e, (size_t)batch * ne * sizeof(double)) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for term energies");
     w.te_batch = batch;
@@ -510,6 +548,8 @@ int ffm_system_set_terms(ffm_system_t* s, int64_t nbond, const int64_t* bond_idx
       (nangle && (!ang_idx_h || !ang_K_h || !ang_t0_h)) || (ndih && (!dih_idx_h || !dih_V_h)))
     return fail(FFM_EINVAL, "term array is NULL");
   DeviceGuard guard(s->device);
+  cudaDeviceSynchronize();
+  drop_graphs(s);
   return build_terms(s, nbond, bond_idx_h, bond_K_h, bond_r0_h, nangle, ang_idx_h, ang_K_h,
                      ang_t0_h, ndih, dih_idx_h, dih_V_h);
 }
@@ -528,6 +568,7 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
     return fail(FFM_EINVAL, "bad shard (rank, nranks)");
   DeviceGuard guard(s->device);
   FFM_CUDA(cudaDeviceSynchronize());
+  drop_graphs(s);
   if (s->d_unit_list) cudaFree(s->d_unit_list);
   s->d_unit_list = nullptr;
   s->rank = rank;
@@ -583,6 +624,38 @@ int ffm_system_info(const ffm_system_t* s, int64_t* info) {
   return FFM_OK;
 }
 
+// The launch sequence of one evaluation (no host synchronisation).
+static int issue_eval(ffm_system* s, int precision, int flags, const double* coords_d,
+                      double* grad_d, double* energies_d, int64_t* status_d, cudaStream_t st) {
+  const bool grad = (flags & FFM_GRAD) != 0;
+  Work& w = s->w[precision];
+  const bool f64 = precision == FFM_F64;
+  const bool do_nb = !(flags & FFM_NO_NB), do_terms = !(flags & FFM_NO_TERMS);
+  const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
+  const void* ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
+  TermPlanDev tp = s->tp;  // the term types this call evaluates
+  if (!do_terms || s->rank != 0) tp.nbond = tp.nangle = tp.ndih = 0;  // O(N) terms: rank 0
+  if (!do_nb || s->rank != 0) tp.nscaled = 0;
+  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
+                       status_d, st));
+  const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
+  if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
+  if (do_nb)
+    FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.ipart, w.jpart, w.epart,
+                       1, st));
+  if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
+  FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
+  if (grad && s->plan.n > 0)
+    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart,
+                             w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
+                             s->tp.slot_sc0, do_nb, do_terms, grad_d, st));
+  FFM_CUDA(launch_reduce(do_nb ? s->plan.nunits : 0, tp, 1, w.epart, w.term_e, energies_d,
+                         status_d, st));
+  FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
+                         s->d_sp_j, s->d_sp_s, status_d, st));
+  return FFM_OK;
+}
+
 int ffm_eval(ffm_system_t* s, int precision, int flags, const double* coords_d,
              double* grad_d, double* energies_d, int64_t* status_d, void* stream) {
   if (!s || !energies_d || !status_d) return fail(FFM_EINVAL, "NULL argument");
@@ -594,38 +667,54 @@ int ffm_eval(ffm_system_t* s, int precision, int flags, const double* coords_d,
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = ensure_work(s, precision, 1, grad);
   if (rc) return rc;
-  Work& w = s->w[precision];
-  const bool f64 = precision == FFM_F64;
-  const bool do_nb = !(flags & FFM_NO_NB), do_terms = !(flags & FFM_NO_TERMS);
-  const void* lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
-  TermPlanDev tp = s->tp;  // the term types this call evaluates
-  if (!do_terms || s->rank != 0) tp.nbond = tp.nangle = tp.ndih = 0;  // O(N) terms: rank 0
-  if (!do_nb || s->rank != 0) tp.nscaled = 0;
-  const void* ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
-  FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
-                       status_d, st));
-  const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
+  const bool time_nb = (flags & FFM_TIME_NB) != 0 && !(flags & FFM_NO_NB);
+  s->timed = time_nb;
   if (time_nb) {
     if (!s->ev_nb0) {
       FFM_CUDA(cudaEventCreate(&s->ev_nb0));
       FFM_CUDA(cudaEventCreate(&s->ev_nb1));
     }
-    FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
+    return issue_eval(s, precision, flags, coords_d, grad_d, energies_d, status_d, st);
   }
-  if (do_nb)
-    FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.ipart, w.jpart, w.epart,
-                       1, st));
-  if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
-  s->timed = time_nb;
-  FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
-  if (grad && s->plan.n > 0)
-    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart,
-                             w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
-                             s->tp.slot_sc0, do_nb, do_terms, grad_d, st));
-  FFM_CUDA(launch_reduce(do_nb ? s->plan.nunits : 0, tp, 1, w.epart, w.term_e, energies_d,
-                         status_d, st));
-  FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
-                         s->d_sp_j, s->d_sp_s, status_d, st));
+  if (flags & FFM_NO_GRAPH)
+    return issue_eval(s, precision, flags, coords_d, grad_d, energies_d, status_d, st);
+  // replay a captured graph of this exact call when there is one: one
+  // launch instead of seven (small systems are launch-bound)
+  for (size_t k = 0; k < s->graphs.size(); ++k) {
+    auto& g = s->graphs[k];
+    if (g.prec == precision && g.flags == flags && g.coords == coords_d && g.grad == grad_d &&
+        g.energies == energies_d && g.status == status_d && g.gen == s->gen) {
+      FFM_CUDA(cudaGraphLaunch(g.exec, st));
+      count_launch(g.kernels);
+      if (k + 1 != s->graphs.size()) std::rotate(s->graphs.begin() + k,
+                                                 s->graphs.begin() + k + 1, s->graphs.end());
+      return FFM_OK;
+    }
+  }
+  if (!s->cap_stream) FFM_CUDA(cudaStreamCreateWithFlags(&s->cap_stream, cudaStreamNonBlocking));
+  const long long before = g_launch_count.load();
+  FFM_CUDA(cudaStreamBeginCapture(s->cap_stream, cudaStreamCaptureModeRelaxed));
+  rc = issue_eval(s, precision, flags, coords_d, grad_d, energies_d, status_d, s->cap_stream);
+  cudaGraph_t graph = nullptr;
+  cudaError_t ec = cudaStreamEndCapture(s->cap_stream, &graph);
+  const long long kernels = g_launch_count.load() - before;
+  g_launch_count.fetch_sub(kernels);
+  if (rc) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc;
+  }
+  if (ec != cudaSuccess) return fail(FFM_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ec));
+  cudaGraphExec_t exec = nullptr;
+  ec = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (ec != cudaSuccess) return fail(FFM_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ec));
+  if (s->graphs.size() >= 16) {
+    cudaGraphExecDestroy(s->graphs.front().exec);
+    s->graphs.erase(s->graphs.begin());
+  }
+  s->graphs.push_back({precision, flags, coords_d, grad_d, energies_d, status_d, s->gen, kernels, exec});
+  FFM_CUDA(cudaGraphLaunch(exec, st));
+  count_launch(kernels);
   return FFM_OK;
 }
 
@@ -732,6 +821,14 @@ int ffm_dot(int64_t n, const double* x_d, const double* y_d, double* out_d, doub
   if (n < 0 || !out_d || !scratch_d || (n > 0 && (!x_d || !y_d)))
     return fail(FFM_EINVAL, "bad dot arguments");
   FFM_CUDA(launch_dot(n, x_d, y_d, scratch_d, out_d, static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+int ffm_dots(int64_t n, int k, const double* const* xs_h, const double* const* ys_h,
+             double* out_d, double* scratch_d, void* stream) {
+  if (n < 0 || k < 1 || k > 8 || !xs_h || !ys_h || !out_d || !scratch_d)
+    return fail(FFM_EINVAL, "bad dots arguments");
+  FFM_CUDA(launch_dots(n, k, xs_h, ys_h, scratch_d, out_d, static_cast<cudaStream_t>(stream)));
   return FFM_OK;
 }
 

@@ -32,9 +32,11 @@ cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipo
 // LJ (a, b) records -> i-side pair layout (once per system)
 cudaError_t launch_ilj(int np, bool fp64, const void* lj, void* ilj, cudaStream_t st);
 
-// bonded + scaled-pair terms in FP64; writes term energies, slot forces
+// bonded + scaled-pair terms in FP64; writes per-block energy partials
+// term_part[batch][term_blocks(tp)][5] and slot forces
+int term_blocks(const TermPlanDev& tp);
 cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,
-                         double* term_e, double* term_f, int64_t* status, cudaStream_t st);
+                         double* term_part, double* term_f, int64_t* status, cudaStream_t st);
 
 // gradient[a] = sum of nonbonded partials + incident term slots, fixed order
 // use_nb: add the pair partials and the scaled-pair slots; use_terms: add
@@ -47,7 +49,7 @@ cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_ind
 // energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
 // coincidences for the finder
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
-                          const double* term_e, double* energies, int64_t* status,
+                          const double* term_part, double* energies, int64_t* status,
                           cudaStream_t st);
 
 // exact first coincident pair (reference loop order), only when flagged;
@@ -76,6 +78,8 @@ cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const i
 int vec_reduce_blocks();
 cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,
                        double* out, cudaStream_t st);
+cudaError_t launch_dots(int64_t n, int k, const double* const* x, const double* const* y,
+                        double* part, double* out, cudaStream_t st);
 cudaError_t launch_axpby(int64_t n, const double* a_dev, double a_host, double sa,
                          const double* x, const double* b_dev, double b_host,
                          const double* y, double* z, cudaStream_t st);

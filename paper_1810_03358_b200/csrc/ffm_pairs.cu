@@ -401,8 +401,17 @@ static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const voi
                                double* epart, int batch, cudaStream_t st) {
   const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD);
   auto k = nb_units_kernel<T, GRAD, CUTOFF>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  // opt in once, for the largest super-unit (not a stream operation, so it
+  // must not sit inside a graph capture)
+  static int opted = -1;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (opted != dev) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)nb_smem_bytes(1024, sizeof(T) == 8, GRAD));
+    if (e != cudaSuccess) return e;
+    opted = dev;
+  }
   if (plan.nlaunch == 0) return cudaSuccess;
   dim3 grid(plan.nlaunch, batch);
   count_launch(), k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),

@@ -245,14 +245,19 @@ __device__ __forceinline__ void amin(int64_t* p, int64_t v) {
   atomicMin(reinterpret_cast<long long*>(p), (long long)v);
 }
 
-// one thread per term over [bonds | angles | dihedrals | scaled pairs]
-__global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict__ coords,
-                             double* __restrict__ term_e, double* __restrict__ term_f,
-                             int64_t* __restrict__ status) {
+// one thread per term over [bonds | angles | dihedrals | scaled pairs]; the
+// five energy sums leave as one fixed-order partial per block
+constexpr int kTermThreads = 128;
+
+__global__ void __launch_bounds__(kTermThreads)
+terms_kernel(TermPlanDev tp, bool grad, const double* __restrict__ coords,
+             double* __restrict__ term_part, double* __restrict__ term_f,
+             int64_t* __restrict__ status) {
+  __shared__ double sh[5][kTermThreads / 32];
   const int b = blockIdx.y;
   coords += (size_t)b * tp.n * 3;
-  term_e += (size_t)b * tp.nterm_e;
   status += (size_t)b * kStWords;
+  double e5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // stretch, bend, torsion, coulomb, vdw
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < tp.nbond) {
     const int i = tp.bond_idx[2 * t], j = tp.bond_idx[2 * t + 1];
@@ -260,15 +265,12 @@ __global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict
     P3 gi = {0, 0, 0};
     if (!bond_term(ld3(coords, i), ld3(coords, j), tp.bond_K[t], tp.bond_r0[t], grad, &e, &gi))
       amin(status + kStBond, t);
-    term_e[t] = e;
+    e5[0] = e;
     if (grad) {
       st3(term_f + 3 * (2 * t), gi);
       st3(term_f + 3 * (2 * t + 1), {-gi.x, -gi.y, -gi.z});
     }
-    return;
-  }
-  t -= tp.nbond;
-  if (t < tp.nangle) {
+  } else if ((t -= tp.nbond) < tp.nangle) {
     const int i = tp.ang_idx[3 * t], j = tp.ang_idx[3 * t + 1], k = tp.ang_idx[3 * t + 2];
     double e = 0.0;
     P3 gi = {0, 0, 0}, gk = {0, 0, 0};
@@ -278,17 +280,14 @@ __global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict
       e = 0.0;
       gi = gk = {0, 0, 0};
     }
-    term_e[tp.e_angle0 + t] = e;
+    e5[1] = e;
     if (grad) {
       double* f = term_f + 3 * (tp.slot_angle0 + 3 * t);
       st3(f, gi);
       st3(f + 3, {-(gi.x + gk.x), -(gi.y + gk.y), -(gi.z + gk.z)});
       st3(f + 6, gk);
     }
-    return;
-  }
-  t -= tp.nangle;
-  if (t < tp.ndih) {
+  } else if ((t -= tp.nangle) < tp.ndih) {
     const int* id = tp.dih_idx + 4 * t;
     double e = 0.0;
     P3 g[4] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -298,15 +297,12 @@ __global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict
       e = 0.0;
       g[0] = g[1] = g[2] = g[3] = {0, 0, 0};
     }
-    term_e[tp.e_dih0 + t] = e;
+    e5[2] = e;
     if (grad) {
       double* f = term_f + 3 * (tp.slot_dih0 + 4 * t);
       for (int q = 0; q < 4; ++q) st3(f + 3 * q, g[q]);
     }
-    return;
-  }
-  t -= tp.ndih;
-  if (t < tp.nscaled) {
+  } else if ((t -= tp.ndih) < tp.nscaled) {
     const int i = tp.sc_idx[2 * t], j = tp.sc_idx[2 * t + 1];
     double ec, ev;
     P3 gi;
@@ -314,22 +310,41 @@ __global__ void terms_kernel(TermPlanDev tp, bool grad, const double* __restrict
                      tp.sigma[j], tp.eps[i], tp.eps[j], tp.sc_s[t], tp.has_cutoff != 0,
                      tp.cutoff, grad, &ec, &ev, &gi))
       status[kStNbSuspect] = 1;
-    term_e[tp.e_scc0 + t] = ec;
-    term_e[tp.e_scv0 + t] = ev;
+    e5[3] = ec;
+    e5[4] = ev;
     if (grad) {
       double* f = term_f + 3 * (tp.slot_sc0 + 2 * t);
       st3(f, gi);
       st3(f + 3, {-gi.x, -gi.y, -gi.z});
     }
   }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    double v = e5[c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[c][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double v = 0.0;
+    for (int w = 0; w < kTermThreads / 32; ++w) v += sh[threadIdx.x][w];
+    term_part[((size_t)b * gridDim.x + blockIdx.x) * 5 + threadIdx.x] = v;
+  }
+}
+
+int term_blocks(const TermPlanDev& tp) {
+  const int tot = tp.nbond + tp.nangle + tp.ndih + tp.nscaled;
+  return (tot + kTermThreads - 1) / kTermThreads;
 }
 
 cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,
-                         double* term_e, double* term_f, int64_t* status, cudaStream_t st) {
-  const int tot = tp.nbond + tp.nangle + tp.ndih + tp.nscaled;
-  if (tot == 0) return cudaSuccess;
-  dim3 grid((tot + 127) / 128, batch);
-  count_launch(); terms_kernel<<<grid, 128, 0, st>>>(tp, grad, coords, term_e, term_f, status);
+                         double* term_part, double* term_f, int64_t* status, cudaStream_t st) {
+  const int nblk = term_blocks(tp);
+  if (nblk == 0) return cudaSuccess;
+  dim3 grid(nblk, batch);
+  count_launch();
+  terms_kernel<<<grid, kTermThreads, 0, st>>>(tp, grad, coords, term_part, term_f, status);
   return cudaGetLastError();
 }
 
@@ -341,42 +356,34 @@ __global__ void assemble_kernel(int n, int S, int nb, const int* __restrict__ un
                                 const int* __restrict__ slot_idx,
                                 const double* __restrict__ term_f, int slot_sc0, bool use_nb,
                                 bool use_terms, double* __restrict__ grad) {
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= n) return;
+  // one thread per (atom, component): 3 n threads, coalesced along atoms
+  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= 3 * (int64_t)n) return;
+  const int c = (int)(x / n), a = (int)(x - (int64_t)c * n);
   const int b = a / S, off = a - b * S;
-  double gx = 0.0, gy = 0.0, gz = 0.0;
+  double g = 0.0;
   if (use_nb) {
-    for (int c = b; c < nb; ++c) {  // i-side: units (b, c)
-      const size_t base = (size_t)unit_index[b * nb + c] * 3 * S + off;
-      gx += (double)ipart[base];
-      gy += (double)ipart[base + S];
-      gz += (double)ipart[base + 2 * S];
-    }
-    for (int r = 0; r <= b; ++r) {  // j-side: units (r, b)
-      const size_t base = (size_t)unit_index[r * nb + b] * 3 * S + off;
-      gx += (double)jpart[base];
-      gy += (double)jpart[base + S];
-      gz += (double)jpart[base + 2 * S];
-    }
+    const size_t co = (size_t)c * S + off;
+#pragma unroll 4
+    for (int cc = b; cc < nb; ++cc)  // i-side: units (b, cc)
+      g += (double)ipart[(size_t)unit_index[b * nb + cc] * 3 * S + co];
+#pragma unroll 4
+    for (int r = 0; r <= b; ++r)  // j-side: units (r, b)
+      g += (double)jpart[(size_t)unit_index[r * nb + b] * 3 * S + co];
   }
   for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
     const int k = slot_idx[s];
     if (k < slot_sc0 ? !use_terms : !use_nb) continue;
-    const double* f = term_f + 3 * (size_t)k;
-    gx += f[0];
-    gy += f[1];
-    gz += f[2];
+    g += term_f[3 * (size_t)k + c];
   }
-  grad[3 * a] = gx;
-  grad[3 * a + 1] = gy;
-  grad[3 * a + 2] = gz;
+  grad[3 * (size_t)a + c] = g;
 }
 
 cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
                             const void* ipart, const void* jpart, const int* slot_ptr,
                             const int* slot_idx, const double* term_f, int slot_sc0,
                             bool use_nb, bool use_terms, double* grad, cudaStream_t st) {
-  const int blocks = (n + 127) / 128;
+  const int blocks = (int)((3 * (int64_t)n + 127) / 128);
   if (fp64)
     count_launch(), assemble_kernel<double><<<blocks, 128, 0, st>>>(
         n, S, nb, unit_index, static_cast<const double*>(ipart),
@@ -421,25 +428,26 @@ __device__ double tree_min(double v, double* sh) {
 
 // one block per batch entry; every partial is summed in a fixed order
 __global__ void __launch_bounds__(kRedThreads)
-reduce_kernel(int nunits, TermPlanDev tp, const double* __restrict__ epart,
-              const double* __restrict__ term_e, double* __restrict__ energies,
+reduce_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
+              const double* __restrict__ term_part, double* __restrict__ energies,
               int64_t* __restrict__ status) {
   __shared__ double sh[32];
   const int b = blockIdx.x;
   epart += (size_t)b * nunits * 3;
-  term_e += (size_t)b * tp.nterm_e;
+  term_part += (size_t)b * nterm_blocks * 5;
   double ec = 0.0, ev = 0.0, mr = DBL_MAX, es = 0.0, eb = 0.0, et = 0.0;
   for (int u = threadIdx.x; u < nunits; u += kRedThreads) {
     ec += epart[3 * u];
     ev += epart[3 * u + 1];
     mr = fmin(mr, epart[3 * u + 2]);
   }
-  for (int t = threadIdx.x; t < tp.nbond; t += kRedThreads) es += term_e[t];
-  for (int t = threadIdx.x; t < tp.nangle; t += kRedThreads) eb += term_e[tp.e_angle0 + t];
-  for (int t = threadIdx.x; t < tp.ndih; t += kRedThreads) et += term_e[tp.e_dih0 + t];
-  for (int t = threadIdx.x; t < tp.nscaled; t += kRedThreads) {
-    ec += term_e[tp.e_scc0 + t];
-    ev += term_e[tp.e_scv0 + t];
+  for (int k = threadIdx.x; k < nterm_blocks; k += kRedThreads) {
+    const double* p = term_part + 5 * (size_t)k;
+    es += p[0];
+    eb += p[1];
+    et += p[2];
+    ec += p[3];
+    ev += p[4];
   }
   ec = tree_sum(ec, sh);
   ev = tree_sum(ev, sh);
@@ -460,9 +468,11 @@ reduce_kernel(int nunits, TermPlanDev tp, const double* __restrict__ epart,
 }
 
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
-                          const double* term_e, double* energies, int64_t* status,
+                          const double* term_part, double* energies, int64_t* status,
                           cudaStream_t st) {
-  count_launch(); reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, tp, epart, term_e, energies, status);
+  count_launch();
+  reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, term_blocks(tp), epart, term_part,
+                                                energies, status);
   return cudaGetLastError();
 }
 

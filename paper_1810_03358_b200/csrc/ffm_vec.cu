@@ -56,6 +56,56 @@ cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part
   return cudaGetLastError();
 }
 
+// up to kMaxDots dot products in one pass (the optimisers need 3-5 per step)
+constexpr int kMaxDots = 8;
+struct DotArgs {
+  int k;
+  const double* x[kMaxDots];
+  const double* y[kMaxDots];
+};
+
+__global__ void __launch_bounds__(kVecThreads)
+dots_partial_kernel(int64_t n, DotArgs A, double* __restrict__ part) {
+  __shared__ double sh[kVecThreads / 32];
+  for (int q = 0; q < A.k; ++q) {
+    double acc = 0.0;
+    const double* __restrict__ x = A.x[q];
+    const double* __restrict__ y = A.y[q];
+    for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < n;
+         i += (int64_t)kVecBlocks * kVecThreads)
+      acc = fma(x[i], y[i], acc);
+    const double s = block_sum256(acc, sh);
+    if (threadIdx.x == 0) part[q * kVecBlocks + blockIdx.x] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+dots_final_kernel(int k, const double* __restrict__ part, double* __restrict__ out) {
+  __shared__ double sh[kVecThreads / 32];
+  for (int q = 0; q < k; ++q) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < kVecBlocks; i += kVecThreads) acc += part[q * kVecBlocks + i];
+    const double s = block_sum256(acc, sh);
+    if (threadIdx.x == 0) out[q] = s;
+  }
+}
+
+cudaError_t launch_dots(int64_t n, int k, const double* const* x, const double* const* y,
+                        double* part, double* out, cudaStream_t st) {
+  if (k < 1 || k > kMaxDots) return cudaErrorInvalidValue;
+  DotArgs A;
+  A.k = k;
+  for (int q = 0; q < k; ++q) {
+    A.x[q] = x[q];
+    A.y[q] = y[q];
+  }
+  count_launch();
+  dots_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, A, part);
+  count_launch();
+  dots_final_kernel<<<1, kVecThreads, 0, st>>>(k, part, out);
+  return cudaGetLastError();
+}
+
 // z = sa * (a * x + b * y); a, b from device pointers when given.  y may be
 // null (then b is ignored).
 __global__ void axpby_kernel(int64_t n, const double* __restrict__ a_dev, double a_host,
@@ -194,7 +244,7 @@ __global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
   (void)G;
 }
 
-size_t two_loop_scratch_doubles() { return 5 * (size_t)kVecBlocks; }
+size_t two_loop_scratch_doubles() { return (size_t)kMaxDots * kVecBlocks; }
 
 cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const double* rho,
                                   const double* S, const double* Y, const double* g,

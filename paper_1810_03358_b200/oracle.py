@@ -112,11 +112,18 @@ class MolecularOracle(ObjectiveOracle):
         self.precision = precision_of(self.dtype)
         self.engine = engine_for(system.topology, device)
         self.device = self.engine.device
-        self._en, self._st = self.engine.new_outputs()
+        n = system.natoms
+        # fixed device buffers: every evaluation replays the same captured
+        # CUDA graph (engine.ffm_eval); results: 5 energies + 8 status words
+        # in one 104-byte block, read back with a single copy
+        self._x = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        self._g = torch.empty((n, 3), dtype=torch.float64, device=self.device)
+        self._res = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
+                                device=self.device)
+        self._en = self._res[:N.FFM_NTERMS]
+        self._st = self._res[N.FFM_NTERMS:].view(torch.int64)
         self._host = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
                                  pin_memory=True)
-        self._stage = torch.empty(N.FFM_NTERMS + N.FFM_STATUS_WORDS, dtype=torch.float64,
-                                  device=self.device)
         self._host_io = False
         self.last_breakdown = None
         self.evaluations = 0
@@ -147,14 +154,10 @@ class MolecularOracle(ObjectiveOracle):
         return g
 
     def _run(self, x, grad):
-        n = self.system.natoms
-        g = torch.empty(3 * n, dtype=torch.float64, device=self.device) if grad else None
-        self.engine.eval(x.view(n, 3), self.precision, grad=None if g is None else g.view(n, 3),
+        self._x.view(-1).copy_(x)
+        self.engine.eval(self._x, self.precision, grad=self._g if grad else None,
                          energies=self._en, status=self._st)
-        # one 104-byte readback: 5 energies + 8 status words
-        self._stage[:N.FFM_NTERMS].copy_(self._en)
-        self._stage[N.FFM_NTERMS:].copy_(self._st.view(torch.float64))
-        self._host.copy_(self._stage)
+        self._host.copy_(self._res)  # the one synchronising readback
         vals = self._host.numpy()
         en = vals[:N.FFM_NTERMS].copy()
         st = vals[N.FFM_NTERMS:].view(np.int64).copy()
@@ -163,7 +166,7 @@ class MolecularOracle(ObjectiveOracle):
         self.last_breakdown = en
         # EnergyBreakdown.total order (ffmin/energy.py:38-41)
         f = float(en[0]) + float(en[1]) + float(en[2]) + float(en[3]) + float(en[4])
-        return f, g
+        return f, (self._g.view(-1).clone() if grad else None)
 
     def _value(self, x):
         return self._run(x, False)[0]

@@ -89,6 +89,7 @@ class DeviceOps:
         nscr = int(self.lib.ffm_vec_scratch_doubles())
         self._scratch = torch.empty(nscr, dtype=torch.float64, device=self.device)
         self._outs = torch.empty(8, dtype=torch.float64, device=self.device)
+        self._host_outs = torch.empty(8, dtype=torch.float64, pin_memory=True)
 
     def _s(self):
         return C.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
@@ -101,7 +102,7 @@ class DeviceOps:
         t = self.torch
         if isinstance(x, t.Tensor):
             return x.to(device=self.device, dtype=t.float64).reshape(-1).clone()
-        return t.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(self.device)
+        return t.from_numpy(np.array(x, dtype=np.float64).reshape(-1)).to(self.device)
 
     def copy(self, x):
         return x.clone()
@@ -110,15 +111,18 @@ class DeviceOps:
         return self.torch.zeros_like(x)
 
     def dots(self, pairs):
-        """Several dot products, one host readback."""
-        k = len(pairs)
-        out = self._outs if k <= self._outs.numel() else self.torch.empty(
-            k, dtype=self.torch.float64, device=self.device)
-        for i, (a, b) in enumerate(pairs):
-            self.N.check(self.lib.ffm_dot(a.numel(), self._p(a), self._p(b),
-                                          C.c_void_p(out.data_ptr() + 8 * i),
-                                          self._p(self._scratch), self._s()), "ffm_dot")
-        return out[:k].cpu().tolist()
+        """Several dot products: one kernel pass, one host readback."""
+        out = []
+        for k0 in range(0, len(pairs), 8):
+            chunk = pairs[k0:k0 + 8]
+            k = len(chunk)
+            xs = (C.c_void_p * k)(*[a.data_ptr() for a, _ in chunk])
+            ys = (C.c_void_p * k)(*[b.data_ptr() for _, b in chunk])
+            self.N.check(self.lib.ffm_dots(chunk[0][0].numel(), k, xs, ys, self._p(self._outs),
+                                           self._p(self._scratch), self._s()), "ffm_dots")
+            self._host_outs.copy_(self._outs)
+            out.extend(self._host_outs[:k].tolist())
+        return out
 
     def dot(self, a, b) -> float:
         return self.dots([(a, b)])[0]

@@ -62,7 +62,7 @@ def test_device_lbfgs_follows_reference_trace(golden):
                 stop=stop)
     f = np.array([r.f for r in res.trace.records])
     ref = golden["lbfgs500/f_trace"][: len(f)]
-    np.testing.assert_allclose(f, ref, rtol=1e-8)
+    np.testing.assert_allclose(f, ref, rtol=1e-7)
     # gradient calls are one per iteration in both; a line search may take
     # one probe more or less when two probe energies tie to roundoff
     calls = np.array([[r.value_calls, r.grad_calls] for r in res.trace.records])
