@@ -45,6 +45,7 @@ int upload(T** dst, const std::vector<T>& src) {
 struct Work {
   void* pos = nullptr;     // [batch][np] Vec4 (j side)
   void* ipos = nullptr;    // [batch][4][np/2] pairs (i side)
+  void* bbox = nullptr;    // [batch][np/32][6] block boxes (cutoff culling)
   int pos_batch = 0;
   void* ipart = nullptr;   // [nunits][3][S]
   void* jpart = nullptr;
@@ -144,7 +145,7 @@ void free_all(ffm_system* s) {
   if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
-    void* wp[] = {w.pos, w.ipos, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
+    void* wp[] = {w.pos, w.ipos, w.bbox, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
     for (void* p : wp)
       if (p) cudaFree(p);
   }
@@ -285,11 +286,11 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
     Work* w;
     void* p[8];
     Bump(ffm_system* s_, Work* w_) : s(s_), w(w_) {
-      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, nullptr};
+      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox};
       for (int i = 0; i < 8; ++i) p[i] = q[i];
     }
     ~Bump() {
-      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, nullptr};
+      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox};
       for (int i = 0; i < 8; ++i)
         if (q[i] != p[i]) {
           drop_graphs(s);
@@ -303,10 +304,14 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   if (w.pos_batch < batch) {
     if (w.pos) cudaFree(w.pos);
     if (w.ipos) cudaFree(w.ipos);
-    w.pos = w.ipos = nullptr;
+    if (w.bbox) cudaFree(w.bbox);
+    w.pos = w.ipos = w.bbox = nullptr;
     const size_t bytes = (size_t)batch * p.np * 4 * tsz;
     if (cudaMalloc(&w.pos, bytes) != cudaSuccess || cudaMalloc(&w.ipos, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for packed coordinates");
+    if (p.has_cutoff &&
+        cudaMalloc(&w.bbox, (size_t)batch * (p.np / kJB) * 6 * tsz) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for block boxes");
     w.pos_batch = batch;
     FFM_CUDA(launch_pad(p.n, p.np, batch, f64, w.pos, w.ipos, 0));
     FFM_CUDA(cudaDeviceSynchronize());
@@ -640,9 +645,11 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
                        status_d, st));
   const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
+  if (do_nb && s->plan.has_cutoff)
+    FFM_CUDA(launch_bbox(s->plan.n, s->plan.np, 1, f64, w.pos, w.bbox, st));
   if (do_nb)
-    FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.ipart, w.jpart, w.epart,
-                       1, st));
+    FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.bbox, w.ipart, w.jpart,
+                       w.epart, 1, st));
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
   FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
   if (grad && s->plan.n > 0)
@@ -762,8 +769,9 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   const void* ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
   FFM_CUDA(launch_pack(s->plan.n, s->plan.np, B, f64, coords_d, s->d_qt, w.pos, w.ipos,
                        status_d, st));
-  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, w.ipos, ilj, nullptr, nullptr, w.epart,
-                     B, st));
+  if (s->plan.has_cutoff) FFM_CUDA(launch_bbox(s->plan.n, s->plan.np, B, f64, w.pos, w.bbox, st));
+  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, w.ipos, ilj, w.bbox, nullptr, nullptr,
+                     w.epart, B, st));
   TermPlanDev tp = s->tp;
   if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
   FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));

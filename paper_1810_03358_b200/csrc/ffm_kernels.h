@@ -15,9 +15,12 @@ size_t nb_smem_bytes(int S, bool fp64, bool grad);
 
 // all-pairs sweep over every super-unit; batch > 1 only without GRAD.
 // pos/lj: j-side records; ipos/ilj: the same data in the i-side pair layout
+// bbox: per 32-atom block bounding boxes (cutoff culling), null without cutoff
 cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
-                      const void* lj, const void* ipos, const void* ilj, void* ipart,
-                      void* jpart, double* epart, int batch, cudaStream_t st);
+                      const void* lj, const void* ipos, const void* ilj, const void* bbox,
+                      void* ipart, void* jpart, double* epart, int batch, cudaStream_t st);
+cudaError_t launch_bbox(int n, int np, int batch, bool fp64, const void* pos, void* bbox,
+                        cudaStream_t st);
 
 // coords (fp64, [batch][n][3]) -> padded pos / ipos records of the chosen
 // precision; also resets the status words of every batch entry.

@@ -54,6 +54,107 @@ __device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restric
   return {d.x, d.y};
 }
 
+// ------------------------------------------------ cutoff culling helpers
+// boxes: [lo x, lo y, lo z, hi x, hi y, hi z] per 32-atom j-block; empty
+// blocks (only padding atoms) hold +inf / -inf and never interact
+template <typename T>
+__device__ __forceinline__ T box_dist2(const T (&a)[6], const T (&b)[6]) {
+  T d2 = T(0);
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    const T gap = fmax(fmax(a[c] - b[3 + c], b[c] - a[3 + c]), T(0));
+    d2 += gap * gap;
+  }
+  return d2 != d2 ? T(1e30) : d2;  // empty boxes give inf - inf = NaN
+}
+
+template <typename T>
+__device__ __forceinline__ void box_union_seq(const T* __restrict__ bbox, int first, int count,
+                                              T (&out)[6]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    out[c] = T(INFINITY);
+    out[3 + c] = T(-INFINITY);
+  }
+  for (int b = 0; b < count; ++b) {
+    const T* q = bbox + (size_t)(first + b) * 6;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      out[c] = fmin(out[c], q[c]);
+      out[3 + c] = fmax(out[3 + c], q[3 + c]);
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void box_union_warp(const T* __restrict__ bbox, int first, int count,
+                                               int lane, T (&out)[6]) {
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    out[c] = T(INFINITY);
+    out[3 + c] = T(-INFINITY);
+  }
+  for (int b = lane; b < count; b += 32) {
+    const T* q = bbox + (size_t)(first + b) * 6;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      out[c] = fmin(out[c], q[c]);
+      out[3 + c] = fmax(out[3 + c], q[3 + c]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      out[c] = fmin(out[c], __shfl_xor_sync(0xffffffffu, out[c], o));
+      out[3 + c] = fmax(out[3 + c], __shfl_xor_sync(0xffffffffu, out[3 + c], o));
+    }
+}
+
+template <typename T>
+__global__ void bbox_kernel(int n, int np, int batch, const typename Vec4T<T>::type* __restrict__ pos,
+                            T* __restrict__ bbox) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nbox = np / kJB;
+  if (w >= (int64_t)batch * nbox) return;
+  const int64_t b = w / nbox;
+  const int blk = (int)(w - b * nbox);
+  const int a = blk * kJB + lane;
+  const auto p = pos[b * np + a];
+  const bool real = a < n;
+  T lo[3] = {real ? p.x : T(INFINITY), real ? p.y : T(INFINITY), real ? p.z : T(INFINITY)};
+  T hi[3] = {real ? p.x : T(-INFINITY), real ? p.y : T(-INFINITY), real ? p.z : T(-INFINITY)};
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    for (int o = 16; o > 0; o >>= 1) {
+      lo[c] = fmin(lo[c], __shfl_xor_sync(0xffffffffu, lo[c], o));
+      hi[c] = fmax(hi[c], __shfl_xor_sync(0xffffffffu, hi[c], o));
+    }
+  if (lane == 0) {
+    T* q = bbox + (size_t)w * 6;
+    q[0] = lo[0];
+    q[1] = lo[1];
+    q[2] = lo[2];
+    q[3] = hi[0];
+    q[4] = hi[1];
+    q[5] = hi[2];
+  }
+}
+
+cudaError_t launch_bbox(int n, int np, int batch, bool fp64, const void* pos, void* bbox,
+                        cudaStream_t st) {
+  const int64_t threads = (int64_t)batch * (np / kJB) * 32;
+  const int blocks = (int)((threads + 255) / 256);
+  count_launch();
+  if (fp64)
+    bbox_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<const double4*>(pos),
+                                                static_cast<double*>(bbox));
+  else
+    bbox_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<const float4*>(pos),
+                                               static_cast<float*>(bbox));
+  return cudaGetLastError();
+}
+
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
 // j-block, so step t of lane l reads entry l + t (atom (l + t) mod 32) with
 // an immediate offset.  MASKED tiles carry per-lane activity bitmasks
@@ -252,8 +353,8 @@ template <typename T, bool GRAD, bool CUTOFF>
 __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? FFM_MINB : 1)
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
-                const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,
-                double* __restrict__ epart) {
+                const T* __restrict__ ilj, const T* __restrict__ bbox,
+                T* __restrict__ ipart, T* __restrict__ jpart, double* __restrict__ epart) {
   using P = Pk<T>;
   using V = typename P::V;
   using V4 = typename Vec4T<T>::type;
@@ -275,6 +376,35 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   const int i0 = rc.x * S, j0 = rc.y * S;
   const bool diag = rc.x == rc.y;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nbox = plan.np / kJB;
+  if (CUTOFF) {
+    // cutoff culling, unit level: if the bounding boxes of the row and
+    // column blocks are farther apart than the cutoff no pair interacts;
+    // the unit's partials are zeroed (the gather reads every unit)
+    bbox += (size_t)bidx * nbox * 6;
+    __shared__ int cull;
+    if (warp == 0) {
+      T r[6], c[6];
+      box_union_warp<T>(bbox, i0 / kJB, S / kJB, lane, r);
+      box_union_warp<T>(bbox, j0 / kJB, S / kJB, lane, c);
+      if (lane == 0) cull = box_dist2<T>(r, c) > T(plan.cull2);
+    }
+    __syncthreads();
+    if (cull) {
+      if (GRAD)
+        for (int x = tid; x < 3 * S; x += kThreads) {
+          ipart[(size_t)u * 3 * S + x] = T(0);
+          jpart[(size_t)u * 3 * S + x] = T(0);
+        }
+      if (tid == 0) {
+        double* e = epart + ((size_t)bidx * plan.nunits + u) * 3;
+        e[0] = 0.0;
+        e[1] = 0.0;
+        e[2] = 1e30;
+      }
+      return;
+    }
+  }
 
   for (int e = tid; e < 2 * S; e += kThreads) {
     const int a = j0 + (e >> 6) * kJB + (e & 31);
@@ -314,10 +444,17 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
     V ec2 = P::zero(), ev2 = P::zero();
     const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];
+    T ibox[6];
+    if (CUTOFF) box_union_seq<T>(bbox, ib / kJB, kIB / kJB, ibox);
 
     for (int m = warp; m < njb; m += kWarps) {
       const int jb = j0 + m * kJB;
       if (diag && jb + kJB <= ib) continue;  // whole tile has j < i
+      if (CUTOFF) {  // tile-level culling
+        T jbox[6];
+        box_union_seq<T>(bbox, jb / kJB, 1, jbox);
+        if (box_dist2<T>(ibox, jbox) > T(plan.cull2)) continue;
+      }
       bool masked = diag && jb < ib + kIB;   // straddles the diagonal
       uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
       if (masked) {
@@ -397,8 +534,9 @@ size_t nb_smem_bytes(int S, bool fp64, bool grad) {
 
 template <typename T, bool GRAD, bool CUTOFF>
 static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const void* lj,
-                               const void* ipos, const void* ilj, void* ipart, void* jpart,
-                               double* epart, int batch, cudaStream_t st) {
+                               const void* ipos, const void* ilj, const void* bbox,
+                               void* ipart, void* jpart, double* epart, int batch,
+                               cudaStream_t st) {
   const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD);
   auto k = nb_units_kernel<T, GRAD, CUTOFF>;
   // opt in once, for the largest super-unit (not a stream operation, so it
@@ -417,16 +555,17 @@ static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const voi
   count_launch(), k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
                                   static_cast<const typename Vec2T<T>::type*>(lj),
                                   static_cast<const T*>(ipos), static_cast<const T*>(ilj),
-                                  static_cast<T*>(ipart), static_cast<T*>(jpart), epart);
+                                  static_cast<const T*>(bbox), static_cast<T*>(ipart),
+                                  static_cast<T*>(jpart), epart);
   return cudaGetLastError();
 }
 
 cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,
-                      const void* lj, const void* ipos, const void* ilj, void* ipart,
-                      void* jpart, double* epart, int batch, cudaStream_t st) {
+                      const void* lj, const void* ipos, const void* ilj, const void* bbox,
+                      void* ipart, void* jpart, double* epart, int batch, cudaStream_t st) {
   const bool cut = plan.has_cutoff != 0;
 #define FFM_NB(T, G, C) \
-  return launch_nb_t<T, G, C>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, batch, st)
+  return launch_nb_t<T, G, C>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart, epart, batch, st)
   if (fp64) {
     if (grad) { if (cut) FFM_NB(double, true, true); else FFM_NB(double, true, false); }
     else { if (cut) FFM_NB(double, false, true); else FFM_NB(double, false, false); }

@@ -25,6 +25,7 @@ struct NbPlanDev {
   const uint32_t* spt_mask;  // [nspt][128] bit jj set: pair (i, jb+jj) special
   int has_cutoff;
   double cut2;
+  double cull2;  // (cutoff + margin)^2: boxes farther apart than this never interact
 };
 
 // Bonded terms + scaled (1-4) pairs, all evaluated in FP64.

@@ -283,3 +283,23 @@ def test_kernel_backend_farfield_functions(golden):
         assert bad == b2 == -1
         assert dec == pytest.approx(parts[0], rel=1e-10, abs=1e-10)
         assert dev == pytest.approx(parts[1], rel=1e-10, abs=1e-10)
+
+
+@pytest.mark.parametrize("cutoff", [7.0, 12.0])
+def test_cutoff_culling_matches_oracle(cutoff):
+    """With a cutoff, super-units and tiles whose bounding boxes are farther
+    apart than the cutoff are skipped; the result must equal the oracle's
+    (which evaluates every pair and drops r > cutoff, kernels.py:303)."""
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(30000, seed=5, cutoff=cutoff)
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    assert err is None
+    gmax = np.max(np.abs(g_ref))
+    for dt, et, gt in ((np.float64, 1e-10, 1e-10), (np.float32, 1e-5, 1e-4)):
+        bd, g = energy_and_gradient(s, dt)
+        got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        assert _rel(got, e_ref) <= et
+        assert np.max(np.abs(g - g_ref)) <= gt * gmax
