@@ -394,6 +394,11 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   p.unit_list = nullptr;
   p.nlaunch = p.nunits;
   p.cut2 = cutoff > 0.0 ? cutoff * cutoff : 0.0;
+  {  // culling margin: the boxes are built in the kernel precision, so pad
+     // the cutoff by a relative and an absolute slack before comparing
+    const double cm = cutoff > 0.0 ? cutoff * (1.0 + 1e-5) + 1e-4 : 0.0;
+    p.cull2 = cm * cm;
+  }
   int rc;
 #define FFM_TRY(x)     \
   do {                 \
