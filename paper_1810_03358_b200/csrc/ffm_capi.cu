@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -161,9 +162,16 @@ void drop_graphs(ffm_system* s) {
 // CTAs per SM slot at 4 CTAs/SM), so the hardware block scheduler balances
 // the triangle; never below 256.
 int choose_S(int64_t n) {
-  for (int S : {1024, 512, 256}) {
+  if (const char* f = getenv("FFM_FORCE_S")) {  // tuning aid; njb = S / 32 must fit 32 bits
+    const int v = atoi(f);
+    if (v >= 256 && v <= 1024 && v % 256 == 0) return v;
+  }
+  // largest super-unit that still gives ~6 waves of units on 148 SMs x 2
+  // CTAs: bigger units amortise the per-sub-block reductions, more units
+  // shorten the tail (measured on B200, 5k..100k atoms, tools/time_nb.py)
+  for (int S : {1024, 768, 512, 256}) {
     const int64_t nb = (n + S - 1) / S;
-    if (nb * (nb + 1) / 2 >= 2048) return S;
+    if (nb * (nb + 1) / 2 >= 1700) return S;
   }
   return 256;
 }

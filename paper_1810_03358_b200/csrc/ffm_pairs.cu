@@ -183,6 +183,9 @@ __device__ __forceinline__ void warp_tile(
 #ifndef FFM_SCHED
 #define FFM_SCHED 1
 #endif
+#ifndef FFM_VFMA
+#define FFM_VFMA 0
+#endif
 #if FFM_SCHED == 1
     // phase-separated: both pairs' geometry first, the four MUFU.RSQ issued
     // back to back, coefficient products while they are in flight
@@ -225,13 +228,21 @@ __device__ __forceinline__ void warp_tile(
       const V i2 = P::mul(ri[pp], ri[pp]);
       const V i4 = P::mul(i2, i2);
       const V i6 = P::mul(i4, i2);
+#if FFM_VFMA
+      const V v = P::fma(A[pp], i6, nB[pp]);  // A / r^6 - B
+#else
       const V u = P::mul(A[pp], i6);
       const V v = P::add(u, nB[pp]);
+#endif
       ev2 = P::fma(v, i6, ev2);
       const V ecp = P::mul(Q[pp], ri[pp]);
       ec2 = P::add(ec2, ecp);
       if (GRAD) {
+#if FFM_VFMA
+        const V pw = P::fma(A[pp], i6, v);    // 2 A / r^6 - B
+#else
         const V pw = P::add(u, v);
+#endif
         const V k = P::mul(pw, i6);
         const V w = P::fma(k, P::bc(T(6)), ecp);
         const V g = P::mul(w, i2);
@@ -286,14 +297,13 @@ __device__ __forceinline__ void warp_tile(
       const V i2 = P::mul(ri, ri);
       const V i4 = P::mul(i2, i2);
       const V i6 = P::mul(i4, i2);
-      const V u = P::mul(A, i6);     // A / r^6
-      const V v = P::add(u, nB);     // A / r^6 - B
+      const V v = P::fma(A, i6, nB); // A / r^6 - B
       ev2 = P::fma(v, i6, ev2);      // A / r^12 - B / r^6
       const V ecp = P::mul(Q, ri);   // C q_i q_j / r
       ec2 = P::add(ec2, ecp);
       if (GRAD) {
         // g = -(dE/dr)/r = (C q q / r + 12 A / r^12 - 6 B / r^6) / r^2
-        const V pw = P::add(u, v);   // 2 A / r^6 - B
+        const V pw = P::fma(A, i6, v); // 2 A / r^6 - B
         const V k = P::mul(pw, i6);
         const V w = P::fma(k, P::bc(T(6)), ecp);
         const V g = P::mul(w, i2);
@@ -444,6 +454,15 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
     V ec2 = P::zero(), ev2 = P::zero();
     const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];
+    // which j-blocks of this unit carry special pairs for these rows: one
+    // bit per j-block (njb <= 32), so the tile loop tests a bit instead of
+    // scanning the row's special-tile list
+    uint32_t spbits = 0;
+    for (int e = e_beg + lane; e < e_end; e += 32) {
+      const int d = plan.spt_m[e] - j0 / kJB;
+      if (d >= 0 && d < njb) spbits |= 1u << d;
+    }
+    spbits = __reduce_or_sync(0xffffffffu, spbits);
     T ibox[6];
     if (CUTOFF) box_union_seq<T>(bbox, ib / kJB, kIB / kJB, ibox);
 
@@ -465,12 +484,14 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
         }
       }
       const int mg = jb / kJB;
-      for (int e = e_beg; e < e_end; ++e) {
-        if (plan.spt_m[e] == mg) {
-          masked = true;
+      if ((spbits >> m) & 1u) {
+        for (int e = e_beg; e < e_end; ++e) {
+          if (plan.spt_m[e] == mg) {
+            masked = true;
 #pragma unroll
-          for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)e * kIB + 32 * p + lane];
-          break;
+            for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)e * kIB + 32 * p + lane];
+            break;
+          }
         }
       }
       T* jc = jacc + m * kJB;

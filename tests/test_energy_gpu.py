@@ -317,3 +317,26 @@ def test_cutoff_culling_matches_oracle(cutoff):
         m = keep if dt is np.float32 else np.ones(s.natoms, bool)
         dg = np.abs(np.reshape(g, (-1, 3)) - np.reshape(g_ref, (-1, 3)))
         assert np.max(dg[m]) <= gt * gmax
+
+
+@pytest.mark.parametrize("S", [256, 512, 768, 1024])
+def test_every_super_unit_size(S, monkeypatch):
+    """The unit size is picked from {256, 512, 768, 1024} by system size;
+    force each one (FFM_FORCE_S, read at plan creation) on one system, with
+    special pairs and a ragged last block, and compare with the oracle."""
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    monkeypatch.setenv("FFM_FORCE_S", str(S))
+    s = make_globule_system(2900, seed=11)
+    assert DeviceSystem(s.topology).info["S"] == S
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    assert err is None
+    gmax = np.max(np.abs(g_ref))
+    for dt, et, gt in ((np.float64, 1e-10, 1e-10), (np.float32, 1e-5, 1e-4)):
+        bd, g = energy_and_gradient(s, dt)
+        got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        assert _rel(got, e_ref) <= et
+        assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
