@@ -339,7 +339,10 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
     const size_t bytes = (size_t)batch * p.nunits * 3 * sizeof(double);
     if (cudaMalloc(&w.epart, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for energy partials");
-    FFM_CUDA(cudaMemset(w.epart, 0, bytes));
+    // units another rank owns: no energy, no close contact (min r^2 = 1e30)
+    std::vector<double> init((size_t)batch * p.nunits * 3, 0.0);
+    for (size_t k = 2; k < init.size(); k += 3) init[k] = 1e30;
+    FFM_CUDA(cudaMemcpy(w.epart, init.data(), bytes, cudaMemcpyHostToDevice));
     w.e_batch = batch;
   }
   if (w.te_batch < batch) {

@@ -246,6 +246,7 @@ def test_row_shards_sum_to_the_full_evaluation(world):
         g = torch.empty_like(c)
         e, st = eng.eval(c, N.FFM_F64, grad=g)
         assert int(st[0]) == -1
+        assert int(st[5]) == 0  # no spurious close-contact flag from other ranks' slots
         if rank != 0:
             assert float(e[0]) == float(e[1]) == float(e[2]) == 0.0  # bonded on rank 0 only
         g_sum += g
