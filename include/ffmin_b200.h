@@ -182,6 +182,53 @@ int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const doubl
                        const double* S_d, const double* Y_d, const double* g_d, double* d_d,
                        double* scratch_d, void* stream);
 
+/* ---- graph-resident L-BFGS (ffmin/optimizers/lbfgs.py:93-128) ----
+ *
+ * The whole iteration -- direction (two-loop recursion), the line search
+ * (ls_par / ls_h with the LineSearcher warm start and retry,
+ * ffmin/linesearch.py, ffmin/optimizers/common.py), the gradient at the new
+ * point, the curvature-guarded memory update and the convergence test -- runs
+ * as one CUDA graph with conditional nodes; no value crosses to the host
+ * between iterations.  The host launches chunks of iterations and reads the
+ * trace records after each chunk.  Single-rank systems only. */
+typedef struct ffm_lbfgs ffm_lbfgs_t;
+
+typedef struct {
+  int32_t m;                   /* memory depth, 1..32 */
+  int32_t ls_kind;             /* 0 = ls_h, 1 = ls_par */
+  int32_t K;                   /* ls_par refinement budget, 2..22 */
+  int32_t use_gradient_start;  /* ls_par seed */
+  int32_t stop_on_linesearch_failure;
+  int32_t chunk;               /* iterations per ffm_lbfgs_run launch, >= 1 */
+  int64_t max_iterations;      /* -1: unbounded */
+  int64_t max_oracle_calls;    /* -1: unbounded (value + gradient calls) */
+  double threshold;            /* stop when |g| <= threshold */
+  double h0, eps_h, k_plus, k_minus, trust;  /* line-search configuration */
+} ffm_lbfgs_config;
+
+int ffm_lbfgs_create(ffm_system_t* sys, int precision, const ffm_lbfgs_config* cfg,
+                     ffm_lbfgs_t** out);
+/* start point: x_d, g_d device (3n) float64; f, |g| as computed by the
+ * caller; warm_h = the line searcher's current warm-start step */
+int ffm_lbfgs_start(ffm_lbfgs_t* run, const double* x_d, const double* g_d, double f,
+                    double gnorm, double warm_h, void* stream);
+/* one chunk of up to cfg.chunk iterations (asynchronous) */
+int ffm_lbfgs_run(ffm_lbfgs_t* run, void* stream);
+/* synchronise and read the run state.  ints[8] = (iterations, status
+ * 0 none / 1 converged / 2 iteration budget / 3 line-search failure /
+ * 4 oracle budget, done, error 0 none / 1 evaluation / 2 divergence,
+ * error came from a gradient evaluation, value calls, gradient calls,
+ * memory pairs); dbls[4] = (f, |g|, warm-start step, ns since the chunk
+ * started); rec_h[cap][7] receives the chunk's trace records (iteration, f,
+ * |g|, step, value calls, gradient calls, ns since the chunk started),
+ * *nrec their number; err_status_h[8] the status words of a failed
+ * evaluation. */
+int ffm_lbfgs_poll(ffm_lbfgs_t* run, int64_t* ints, double* dbls, double* rec_h, int64_t cap,
+                   int64_t* nrec, int64_t* err_status_h);
+/* copy the current iterate and gradient out (device pointers, 3n) */
+int ffm_lbfgs_result(ffm_lbfgs_t* run, double* x_d, double* g_d, void* stream);
+int ffm_lbfgs_destroy(ffm_lbfgs_t* run);
+
 #ifdef __cplusplus
 }
 #endif

@@ -58,7 +58,29 @@ SIGNATURES = {
     "ffm_dots": (_I, [_I64, _I, _P, _P, _P, _P, _P]),
     "ffm_axpby": (_I, [_I64, _P, _D, _D, _P, _P, _D, _P, _P, _P]),
     "ffm_lbfgs_two_loop": (_I, [_I64, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "ffm_lbfgs_create": (_I, [_P, _I, _P, C.POINTER(_P)]),
+    "ffm_lbfgs_start": (_I, [_P, _P, _P, _D, _D, _D, _P]),
+    "ffm_lbfgs_run": (_I, [_P, _P]),
+    "ffm_lbfgs_poll": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
+    "ffm_lbfgs_result": (_I, [_P, _P, _P, _P]),
+    "ffm_lbfgs_destroy": (_I, [_P]),
 }
+
+
+class LbfgsConfig(C.Structure):
+    """ffm_lbfgs_config (include/ffmin_b200.h)."""
+
+    _fields_ = [("m", C.c_int32), ("ls_kind", C.c_int32), ("K", C.c_int32),
+                ("use_gradient_start", C.c_int32), ("stop_on_linesearch_failure", C.c_int32),
+                ("chunk", C.c_int32), ("max_iterations", C.c_int64),
+                ("max_oracle_calls", C.c_int64), ("threshold", C.c_double),
+                ("h0", C.c_double), ("eps_h", C.c_double), ("k_plus", C.c_double),
+                ("k_minus", C.c_double), ("trust", C.c_double)]
+
+
+LBFGS_STATUS = {0: None, 1: "converged", 2: "iteration_budget", 3: "linesearch_failure",
+                4: "oracle_budget"}
+LBFGS_REC_WIDTH = 7
 
 _lock = threading.Lock()
 _lib = None

@@ -12,6 +12,7 @@
 
 #include "../../include/ffmin_b200.h"
 #include "ffm_kernels.h"
+#include "ffm_min.cuh"
 
 using namespace ffm;
 
@@ -873,6 +874,358 @@ int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const doubl
     return fail(FFM_EINVAL, "bad two-loop arguments");
   FFM_CUDA(launch_lbfgs_two_loop(n, count, order_h, rho_h, S_d, Y_d, g_d, d_d, scratch_d,
                                  static_cast<cudaStream_t>(stream)));
+  return FFM_OK;
+}
+
+
+// ------------------------------------------------- graph-resident L-BFGS
+}  // extern "C"
+
+struct ffm_lbfgs {
+  ffm_system* sys = nullptr;
+  int prec = 0;
+  MinConfig cfg{};
+  int64_t n = 0;  // 3 * atoms
+  MinState* S = nullptr;
+  double* rec = nullptr;
+  double* buf = nullptr;  // x, g, x_new, g_new, x_trial, d, r, s_tmp, y_tmp, ring S, ring Y
+  double *x, *g, *xn, *gnew, *xt, *d, *r, *st, *yt, *ring_s, *ring_y;
+  double* scratch = nullptr;
+  double* en = nullptr;      // energies of the last evaluation
+  int64_t* stw = nullptr;    // its status words
+  cudaStream_t cap[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaGraphExec_t exec = nullptr;
+  long long gen = -1;
+  std::vector<double> rec_h;
+};
+
+namespace {
+
+// append a conditional node to the capture running on `st`; its body graph
+// is filled by a nested capture on another stream
+int add_conditional(cudaStream_t st, cudaGraphConditionalHandle h,
+                    cudaGraphConditionalNodeType type, cudaGraph_t* body) {
+  cudaStreamCaptureStatus cs;
+  cudaGraph_t g = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  FFM_CUDA(cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &nd));
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaGraphNode_t node;
+  FFM_CUDA(cudaGraphAddNode(&node, g, deps, nd, &p));
+  FFM_CUDA(cudaStreamUpdateCaptureDependencies(st, &node, 1, cudaStreamSetCaptureDependencies));
+  *body = p.conditional.phGraph_out[0];
+  return FFM_OK;
+}
+
+#define FFM_TRYR(x)  \
+  do {               \
+    int rc_ = (x);   \
+    if (rc_) return rc_; \
+  } while (0)
+
+// bodies of the iteration graph (see ffm_min.cuh); each runs inside a
+// capture on stream st
+int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls) {
+  MinState* S = L->S;
+  FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, &S->count, S->idx_nf, S->rho_nf, &S->gn, L->ring_s,
+                                     L->ring_y, L->g, L->d, L->scratch, st));
+  const double* xs[1] = {L->d};
+  FFM_CUDA(launch_dots(L->n, 1, xs, xs, L->scratch, &S->dd, st));
+  FFM_CUDA(launch_min_dir(S, hls, st));
+  return FFM_OK;
+}
+
+int cap_trial(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hloop) {
+  MinState* S = L->S;
+  // phi(h) = f(x + h r): lincomb(1.0, x, h, r)
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->h_trial, 0.0, L->r, L->xt, st));
+  FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY, L->xt, nullptr, L->en, L->stw, st));
+  FFM_CUDA(launch_min_ls_step(S, L->en, L->stw, hloop, st));
+  return FFM_OK;
+}
+
+int cap_accept(ffm_lbfgs* L, cudaStream_t st) {
+  MinState* S = L->S;
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->res_h, 0.0, L->r, L->xn, st));
+  FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->gnew, L->en, L->stw,
+                      st));
+  const double* gs[1] = {L->gnew};
+  FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
+  FFM_CUDA(launch_min_acc_check(S, L->stw, st));
+  // s = x_new - x, y = g_new - g (LbfgsMemory._axpy_into)
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->xn, nullptr, -1.0, L->x, L->st, st));
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->gnew, nullptr, -1.0, L->g, L->yt, st));
+  const double* xa[3] = {L->st, L->st, L->yt};
+  const double* ya[3] = {L->yt, L->st, L->yt};
+  FFM_CUDA(launch_dots(L->n, 3, xa, ya, L->scratch, &S->sy, st));
+  FFM_CUDA(launch_min_commit(S, st));
+  FFM_CUDA(launch_min_store(S, L->n, L->st, L->yt, L->ring_s, L->ring_y, L->xn, L->gnew, L->x,
+                            L->g, st));
+  FFM_CUDA(launch_min_iter_end(S, L->rec, st));
+  return FFM_OK;
+}
+
+int lbfgs_build(ffm_lbfgs* L) {
+  ffm_system* s = L->sys;
+  if (L->exec) {
+    cudaGraphExecDestroy(L->exec);
+    L->exec = nullptr;
+  }
+  FFM_TRYR(ensure_work(s, L->prec, 1, true));
+  // first use of each kernel variant outside any capture (function
+  // attributes are set on first launch)
+  FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, L->cap[0]));
+  FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->gnew, L->en, L->stw, L->cap[0]));
+  FFM_CUDA(cudaStreamSynchronize(L->cap[0]));
+  MinState* S = L->S;
+  const long long before = g_launch_count.load();
+  cudaGraph_t top = nullptr;
+  FFM_CUDA(cudaGraphCreate(&top, 0));
+  auto fail_graph = [&](int rc) {
+    g_launch_count.fetch_sub(g_launch_count.load() - before);
+    for (cudaStream_t c : L->cap) {
+      cudaStreamCaptureStatus cs;
+      if (cudaStreamIsCapturing(c, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+        cudaGraph_t t = nullptr;
+        cudaStreamEndCapture(c, &t);
+        if (t && t != top) cudaGraphDestroy(t);
+      }
+    }
+    cudaGraphDestroy(top);
+    return rc;
+  };
+#define FFM_G(x)                     \
+  do {                               \
+    int rc_ = (x);                   \
+    if (rc_) return fail_graph(rc_); \
+  } while (0)
+#define FFM_GC(x)                                                                        \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      return fail_graph(fail(FFM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_))); \
+  } while (0)
+  cudaGraphConditionalHandle hout, hdir, hls, hacc, hloop;
+  FFM_GC(cudaGraphConditionalHandleCreate(&hout, top, 1, cudaGraphCondAssignDefault));
+  cudaStream_t c0 = L->cap[0], c1 = L->cap[1], c2 = L->cap[2], c3 = L->cap[3];
+  cudaGraph_t tmp = nullptr;
+  // top: launch_begin -> WHILE(hout) { iteration }
+  FFM_GC(cudaStreamBeginCaptureToGraph(c0, top, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  FFM_GC(launch_min_launch_begin(S, c0));
+  cudaGraph_t body = nullptr;
+  FFM_G(add_conditional(c0, hout, cudaGraphCondTypeWhile, &body));
+  FFM_GC(cudaGraphConditionalHandleCreate(&hdir, body, 0, 0));
+  FFM_GC(cudaGraphConditionalHandleCreate(&hls, body, 0, 0));
+  FFM_GC(cudaGraphConditionalHandleCreate(&hacc, body, 0, 0));
+  {  // iteration
+    FFM_GC(cudaStreamBeginCaptureToGraph(c1, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    FFM_GC(launch_min_it_begin(S, hdir, hls, hacc, c1));
+    cudaGraph_t bdir = nullptr, bls = nullptr, bacc = nullptr, bloop = nullptr;
+    FFM_G(add_conditional(c1, hdir, cudaGraphCondTypeIf, &bdir));
+    FFM_GC(cudaStreamBeginCaptureToGraph(c2, bdir, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    FFM_G(cap_direction(L, c2, hls));
+    FFM_GC(cudaStreamEndCapture(c2, &tmp));
+    FFM_G(add_conditional(c1, hls, cudaGraphCondTypeIf, &bls));
+    {  // line search
+      FFM_GC(cudaGraphConditionalHandleCreate(&hloop, bls, 0, 0));
+      FFM_GC(cudaStreamBeginCaptureToGraph(c2, bls, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
+      const double* gs[1] = {L->g};
+      const double* rs[1] = {L->r};
+      FFM_GC(launch_dots(L->n, 1, gs, rs, L->scratch, &S->slope, c2));
+      FFM_GC(launch_min_ls_init(S, hloop, c2));
+      FFM_G(add_conditional(c2, hloop, cudaGraphCondTypeWhile, &bloop));
+      FFM_GC(cudaStreamBeginCaptureToGraph(c3, bloop, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+      FFM_G(cap_trial(L, c3, hloop));
+      FFM_GC(cudaStreamEndCapture(c3, &tmp));
+      FFM_GC(launch_min_ls_post(S, L->rec, hacc, c2));
+      FFM_GC(cudaStreamEndCapture(c2, &tmp));
+    }
+    FFM_G(add_conditional(c1, hacc, cudaGraphCondTypeIf, &bacc));
+    FFM_GC(cudaStreamBeginCaptureToGraph(c2, bacc, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    FFM_G(cap_accept(L, c2));
+    FFM_GC(cudaStreamEndCapture(c2, &tmp));
+    FFM_GC(launch_min_it_end(S, hout, c1));
+    FFM_GC(cudaStreamEndCapture(c1, &tmp));
+  }
+  FFM_GC(cudaStreamEndCapture(c0, &tmp));
+#undef FFM_G
+#undef FFM_GC
+  g_launch_count.fetch_sub(g_launch_count.load() - before);
+  cudaError_t e = cudaGraphInstantiate(&L->exec, top, 0);
+  cudaGraphDestroy(top);
+  if (e != cudaSuccess) {
+    L->exec = nullptr;
+    return fail(FFM_ECUDA, std::string("lbfgs graph instantiate: ") + cudaGetErrorString(e));
+  }
+  L->gen = s->gen;
+  return FFM_OK;
+}
+
+void lbfgs_free(ffm_lbfgs* L) {
+  if (L->exec) cudaGraphExecDestroy(L->exec);
+  for (void* p : {(void*)L->S, (void*)L->rec, (void*)L->buf, (void*)L->scratch, (void*)L->en,
+                  (void*)L->stw})
+    if (p) cudaFree(p);
+  for (cudaStream_t c : L->cap)
+    if (c) cudaStreamDestroy(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg,
+                     ffm_lbfgs_t** out) {
+  if (!s || !cfg || !out) return fail(FFM_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
+  if (s->nranks != 1) return fail(FFM_EINVAL, "graph-resident L-BFGS needs an unsharded system");
+  if (cfg->m < 1 || cfg->m > kMaxLbfgsPairs) return fail(FFM_EINVAL, "memory depth m out of range");
+  if (cfg->ls_kind != 0 && cfg->ls_kind != 1) return fail(FFM_EINVAL, "bad line-search kind");
+  if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
+    return fail(FFM_EINVAL, "ls_par K out of range");
+  if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
+  DeviceGuard guard(s->device);
+  auto* L = new ffm_lbfgs();
+  L->sys = s;
+  L->prec = precision;
+  MinConfig& c = L->cfg;
+  c.m = cfg->m;
+  c.ls_kind = cfg->ls_kind;
+  c.K = cfg->K;
+  c.use_gs = cfg->use_gradient_start;
+  c.stop_on_ls_failure = cfg->stop_on_linesearch_failure;
+  c.chunk = cfg->chunk;
+  c.max_iter = cfg->max_iterations;
+  c.max_calls = cfg->max_oracle_calls;
+  c.thr = cfg->threshold;
+  c.h0 = cfg->h0;
+  c.eps_h = cfg->eps_h;
+  c.k_plus = cfg->k_plus;
+  c.k_minus = cfg->k_minus;
+  c.trust = cfg->trust;
+  L->n = 3 * (int64_t)std::max(1, s->plan.n);
+  const int64_t n = L->n;
+  const size_t nbuf = (size_t)n * (9 + 2 * (c.m + 1));
+  bool ok = cudaMalloc(&L->S, sizeof(MinState)) == cudaSuccess &&
+            cudaMalloc(&L->rec, (size_t)(c.chunk + 1) * kMinRecWidth * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&L->buf, nbuf * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&L->scratch, two_loop_scratch_doubles() * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&L->en, FFM_NTERMS * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&L->stw, FFM_STATUS_WORDS * sizeof(int64_t)) == cudaSuccess;
+  if (!ok) {
+    lbfgs_free(L);
+    delete L;
+    return fail(FFM_ENOMEM, "cudaMalloc failed for the L-BFGS run");
+  }
+  double* p = L->buf;
+  for (double** v : {&L->x, &L->g, &L->xn, &L->gnew, &L->xt, &L->d, &L->r, &L->st, &L->yt}) {
+    *v = p;
+    p += n;
+  }
+  L->ring_s = p;
+  L->ring_y = p + (size_t)n * (c.m + 1);
+  cudaMemset(L->buf, 0, nbuf * sizeof(double));
+  for (cudaStream_t& cs : L->cap)
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
+      lbfgs_free(L);
+      delete L;
+      return fail(FFM_ECUDA, "stream creation failed");
+    }
+  L->rec_h.resize((size_t)(c.chunk + 1) * kMinRecWidth);
+  *out = L;
+  return FFM_OK;
+}
+
+int ffm_lbfgs_start(ffm_lbfgs_t* L, const double* x_d, const double* g_d, double f, double gnorm,
+                    double warm_h, void* stream) {
+  if (!L || !x_d || !g_d) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(L->sys->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t nb = (size_t)3 * L->sys->plan.n * sizeof(double);
+  FFM_CUDA(cudaMemcpyAsync(L->x, x_d, nb, cudaMemcpyDeviceToDevice, st));
+  FFM_CUDA(cudaMemcpyAsync(L->g, g_d, nb, cudaMemcpyDeviceToDevice, st));
+  MinState h;
+  std::memset(&h, 0, sizeof(h));
+  h.c = L->cfg;
+  h.f = f;
+  h.gn = gnorm;
+  h.warm = warm_h;
+  h.count = 0;
+  h.nfree = L->cfg.m + 1;
+  for (int q = 0; q <= L->cfg.m; ++q) h.freel[q] = q;
+  h.store_slot = -1;
+  FFM_CUDA(cudaMemcpyAsync(L->S, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  FFM_CUDA(cudaStreamSynchronize(st));  // h lives on this stack frame
+  return FFM_OK;
+}
+
+int ffm_lbfgs_run(ffm_lbfgs_t* L, void* stream) {
+  if (!L) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(L->sys->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!L->exec || L->gen != L->sys->gen) {
+    // (re)build after the system's workspace moved; x/g already hold the
+    // iterate, the warm-up evaluations only touch scratch outputs
+    FFM_CUDA(cudaStreamSynchronize(st));
+    FFM_TRYR(lbfgs_build(L));
+  }
+  FFM_CUDA(cudaGraphLaunch(L->exec, st));
+  count_launch();
+  return FFM_OK;
+}
+
+int ffm_lbfgs_poll(ffm_lbfgs_t* L, int64_t* ints, double* dbls, double* rec_h, int64_t cap,
+                   int64_t* nrec, int64_t* err_status_h) {
+  if (!L || !ints || !dbls || !nrec) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(L->sys->device);
+  MinState h;
+  FFM_CUDA(cudaDeviceSynchronize());
+  FFM_CUDA(cudaMemcpy(&h, L->S, sizeof(h), cudaMemcpyDeviceToHost));
+  ints[0] = h.k;
+  ints[1] = h.status;
+  ints[2] = h.done;
+  ints[3] = h.err;
+  ints[4] = h.err_grad;
+  ints[5] = h.vcalls;
+  ints[6] = h.gcalls;
+  ints[7] = h.count;
+  dbls[0] = h.f;
+  dbls[1] = h.gn;
+  dbls[2] = h.warm;
+  dbls[3] = 0.0;
+  const int64_t k = std::min<int64_t>(h.nrec, cap);
+  if (k > 0 && rec_h)
+    FFM_CUDA(cudaMemcpy(rec_h, L->rec, (size_t)k * kMinRecWidth * sizeof(double),
+                        cudaMemcpyDeviceToHost));
+  *nrec = h.nrec;
+  if (err_status_h)
+    for (int q = 0; q < 8; ++q) err_status_h[q] = h.err_st[q];
+  return FFM_OK;
+}
+
+int ffm_lbfgs_result(ffm_lbfgs_t* L, double* x_d, double* g_d, void* stream) {
+  if (!L) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(L->sys->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t nb = (size_t)3 * L->sys->plan.n * sizeof(double);
+  if (x_d) FFM_CUDA(cudaMemcpyAsync(x_d, L->x, nb, cudaMemcpyDeviceToDevice, st));
+  if (g_d) FFM_CUDA(cudaMemcpyAsync(g_d, L->g, nb, cudaMemcpyDeviceToDevice, st));
+  return FFM_OK;
+}
+
+int ffm_lbfgs_destroy(ffm_lbfgs_t* L) {
+  if (!L) return FFM_OK;
+  DeviceGuard guard(L->sys->device);
+  cudaDeviceSynchronize();
+  lbfgs_free(L);
+  delete L;
   return FFM_OK;
 }
 

@@ -91,5 +91,30 @@ size_t two_loop_scratch_doubles();
 cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const double* rho,
                                   const double* S, const double* Y, const double* g,
                                   double* q, double* scratch, cudaStream_t st);
+// the same with count / slots / rho / |g| read from device memory
+cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* idx,
+                                      const double* rho, const double* gn, const double* S,
+                                      const double* Y, const double* g, double* q,
+                                      double* scratch, cudaStream_t st);
+
+// ---- device-resident L-BFGS controllers (ffm_minimize.cu, state in ffm_min.cuh) ----
+struct MinState;
+cudaError_t launch_min_launch_begin(MinState* S, cudaStream_t st);
+cudaError_t launch_min_it_begin(MinState* S, cudaGraphConditionalHandle hdir,
+                                cudaGraphConditionalHandle hls, cudaGraphConditionalHandle hacc,
+                                cudaStream_t st);
+cudaError_t launch_min_dir(MinState* S, cudaGraphConditionalHandle hls, cudaStream_t st);
+cudaError_t launch_min_ls_init(MinState* S, cudaGraphConditionalHandle hloop, cudaStream_t st);
+cudaError_t launch_min_ls_step(MinState* S, const double* en, const int64_t* stw,
+                               cudaGraphConditionalHandle hloop, cudaStream_t st);
+cudaError_t launch_min_ls_post(MinState* S, double* rec, cudaGraphConditionalHandle hacc,
+                               cudaStream_t st);
+cudaError_t launch_min_acc_check(MinState* S, const int64_t* stw, cudaStream_t st);
+cudaError_t launch_min_commit(MinState* S, cudaStream_t st);
+cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,
+                             double* ring_s, double* ring_y, const double* x_new,
+                             const double* g_new, double* x, double* g, cudaStream_t st);
+cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st);
+cudaError_t launch_min_it_end(MinState* S, cudaGraphConditionalHandle hout, cudaStream_t st);
 
 }  // namespace ffm

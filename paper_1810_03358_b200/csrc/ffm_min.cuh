@@ -1,0 +1,69 @@
+// ffm_min.cuh -- state of a device-resident L-BFGS run (ffm_lbfgs_*).
+//
+// The reference drives L-BFGS from Python: every line-search probe, every
+// curvature dot product and every convergence test is a host decision
+// (ffmin/optimizers/lbfgs.py:93-128, ffmin/linesearch.py, ffmin/optimizers/
+// common.py).  Here the whole iteration runs as one CUDA graph with
+// conditional nodes: single-thread controller kernels replay the reference's
+// scalar logic on this struct (same IEEE double operations in the same
+// order, compiled without FMA contraction), so no value leaves the device
+// between iterations.  The host polls it once per chunk of iterations.
+#pragma once
+#include "ffm_kernels.h"
+
+namespace ffm {
+
+constexpr int kLsMaxPoints = 24;  // ls_par keeps <= K + 2 points per attempt
+
+struct MinConfig {
+  int m;                  // memory depth
+  int ls_kind;            // 0 = ls_h, 1 = ls_par
+  int K;                  // ls_par refinement budget
+  int use_gs;             // ls_par: seed with the directional derivative
+  int stop_on_ls_failure;
+  int chunk;              // iterations per graph launch
+  long long max_iter;     // -1: no bound
+  long long max_calls;    // -1: no bound (value + gradient calls)
+  double thr;             // gradient-norm threshold
+  double h0, eps_h, k_plus, k_minus, trust;
+};
+
+// run status codes (host maps them to the reference's strings)
+enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
+             kMinOracleBudget = 4 };
+// error kinds
+enum : int { kMinErrNone = 0, kMinErrEval = 1, kMinErrDiverged = 2 };
+
+constexpr int kMinRecWidth = 7;  // k, f, |g|, step, value calls, grad calls, t (ns)
+
+struct MinState {
+  MinConfig c;
+  // run
+  long long k, vcalls, gcalls, nrec, iters_launch;
+  int status, done, pause, cleared, err, err_grad;
+  long long err_st[8];
+  double f, gn;
+  unsigned long long t_launch;
+  // direction and the dot products the controllers consume
+  double dd, dn, inv_dn, slope, gg, sy, ss, yy;
+  // L-BFGS memory: ring slots of the m most recent pairs, oldest first,
+  // and the free slots (LbfgsMemory._free); newest-first copies feed the
+  // two-loop kernel
+  int count, nfree, store_slot, pad0;
+  int order[kMaxLbfgsPairs + 1];
+  int freel[kMaxLbfgsPairs + 1];
+  double rho[kMaxLbfgsPairs];
+  int idx_nf[kMaxLbfgsPairs];
+  double rho_nf[kMaxLbfgsPairs];
+  // line search (LineSearcher warm start + one attempt's state)
+  double warm;
+  int attempt, stage, nref, np;
+  double a_h0, lo, hi, f0;
+  double ph[kLsMaxPoints], pf[kLsMaxPoints];
+  double h_trial;
+  double h_keep, f_keep;  // ls_h: first accepted probe
+  int found, pad1;
+  double res_h, res_f;
+};
+
+}  // namespace ffm

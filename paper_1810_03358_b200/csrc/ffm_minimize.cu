@@ -1,0 +1,448 @@
+// ffm_minimize.cu -- controller kernels of the graph-resident L-BFGS.
+//
+// Each controller is a single-thread kernel that advances the scalar part of
+// the reference's L-BFGS iteration on MinState (ffm_min.cuh) and steers the
+// CUDA graph through conditional handles; the vector work (two-loop
+// recursion, dot products, axpby, energy/gradient evaluations) stays in the
+// engine's own kernels.  The scalar logic restates, operation for operation:
+//   ffmin/optimizers/lbfgs.py:93-128   iteration, memory clear-and-retry
+//   ffmin/optimizers/lbfgs.py:20-50    curvature guard, ring of m pairs
+//   ffmin/linesearch.py (ls_h, ls_par) one-dimensional searches
+//   ffmin/optimizers/common.py         LineSearcher warm start and retry,
+//                                      budget checks, trace records
+// This file is compiled with -fmad=false: every product and sum rounds
+// separately, as in the reference's Python float arithmetic.
+#include <cfloat>
+#include "ffm_min.cuh"
+
+namespace ffm {
+
+namespace {
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// raise_status (energy.py): energy-only evaluations report coincident
+// nonbonded pairs, angles and dihedrals; gradient evaluations also bonds
+__device__ bool bad_status(const int64_t* stw, bool grad) {
+  return stw[kStNbBadI] >= 0 || stw[kStAngle] >= 0 || stw[kStDihedral] >= 0 ||
+         (grad && stw[kStBond] >= 0);
+}
+
+__device__ void set_err(MinState* S, int kind, const int64_t* stw, bool grad) {
+  S->err = kind;
+  S->err_grad = grad ? 1 : 0;
+  if (stw)
+    for (int q = 0; q < 8; ++q) S->err_st[q] = stw[q];
+  S->done = 1;
+}
+
+__device__ void record(MinState* S, double* rec, double step) {
+  double* r = rec + S->nrec * kMinRecWidth;
+  r[0] = (double)S->k;
+  r[1] = S->f;
+  r[2] = S->gn;
+  r[3] = step;
+  r[4] = (double)S->vcalls;
+  r[5] = (double)S->gcalls;
+  r[6] = (double)(globaltimer() - S->t_launch);
+  S->nrec++;
+}
+
+__device__ void memory_clear(MinState* S) {
+  S->count = 0;
+  S->nfree = S->c.m + 1;
+  for (int q = 0; q <= S->c.m; ++q) S->freel[q] = q;
+}
+
+// --------------------------------------------------------- line searches
+__device__ __forceinline__ bool rank_less(double fa, double ha, double fb, double hb) {
+  // Python tuple order of (f, |h|)
+  return fa < fb || (fa == fb && fabs(ha) < fabs(hb));
+}
+
+// _accept_vertex (linesearch.py): finite, clamped to [lo, hi], not a
+// duplicate of a sampled abscissa
+__device__ bool accept_vertex(const MinState* S, double& v) {
+  if (!isfinite(v)) return false;
+  if (S->lo > v) v = S->lo;  // max(v, lo)
+  if (S->hi < v) v = S->hi;  // min(v, hi)
+  const double av = fabs(v);
+  const double scale = av > 1.0 ? av : 1.0;
+  for (int q = 0; q < S->np; ++q) {
+    const double ah = fabs(S->ph[q]);
+    const double m = ah > scale ? ah : scale;
+    if (fabs(v - S->ph[q]) <= 1e-13 * m) return false;
+  }
+  return true;
+}
+
+__device__ void ls_start(MinState* S, double h0) {
+  const MinConfig& c = S->c;
+  S->a_h0 = h0;
+  S->np = 0;
+  S->nref = 0;
+  S->found = 0;
+  if (c.ls_kind == 1) {
+    S->hi = c.trust * h0;
+    S->lo = c.use_gs ? 0.0 : -S->hi;
+    S->ph[0] = 0.0;
+    S->pf[0] = S->f0;
+    S->np = 1;
+    if (c.use_gs) {
+      S->stage = 10;
+      S->h_trial = h0;
+    } else {
+      S->stage = 20;
+      S->h_trial = -0.5 * h0;
+    }
+  } else {
+    S->stage = 1;
+    S->h_trial = h0;
+  }
+}
+
+__device__ void ls_finish(MinState* S, bool found, double h, double f) {
+  S->found = found ? 1 : 0;
+  S->res_h = found ? h : 0.0;
+  S->res_f = found ? f : S->f0;
+}
+
+// ls_par: the remaining refinement steps (at most K - 1)
+__device__ bool ls_par_refine(MinState* S) {
+  if (S->nref >= S->c.K - 1 || S->np < 3) return false;
+  // sorted(pts, key=(f, |h|))[:3] -- a stable selection of the three best
+  int b[3] = {-1, -1, -1};
+  for (int q = 0; q < S->np; ++q) {
+    int pos = 3;
+    for (int t = 2; t >= 0; --t)
+      if (b[t] < 0 || rank_less(S->pf[q], S->ph[q], S->pf[b[t]], S->ph[b[t]])) pos = t;
+    if (pos < 3) {
+      for (int t = 2; t > pos; --t) b[t] = b[t - 1];
+      b[pos] = q;
+    }
+  }
+  const double x0 = S->ph[b[0]], x1 = S->ph[b[1]], x2 = S->ph[b[2]];
+  const double f0 = S->pf[b[0]], f1 = S->pf[b[1]], f2 = S->pf[b[2]];
+  if (x0 == x1 || x0 == x2 || x1 == x2) return false;
+  // fit_parabola: divided differences
+  const double s01 = (f1 - f0) / (x1 - x0);
+  const double s12 = (f2 - f1) / (x2 - x1);
+  const double curv = (s12 - s01) / (x2 - x0);
+  double mx = fabs(f0);
+  if (fabs(f1) > mx) mx = fabs(f1);
+  if (fabs(f2) > mx) mx = fabs(f2);
+  const bool degenerate = fabs(curv) < 1e-12 * mx;
+  if (curv <= 0.0 || degenerate) return false;
+  double v = 0.5 * (x0 + x1) - s01 / (2.0 * curv);
+  if (!accept_vertex(S, v)) return false;
+  S->nref++;
+  S->h_trial = v;
+  return true;
+}
+
+__device__ void ls_par_finish(MinState* S) {
+  int bi = 0;  // min(pts, key=rank): the first minimal point
+  for (int q = 1; q < S->np; ++q)
+    if (rank_less(S->pf[q], S->ph[q], S->pf[bi], S->ph[bi])) bi = q;
+  const double hb = S->ph[bi], fb = S->pf[bi];
+  ls_finish(S, hb != 0.0 && fb < S->f0, hb, fb);
+}
+
+// consume phi(h_trial) = f; true while the attempt wants another probe
+__device__ bool ls_on_value(MinState* S, double f) {
+  const MinConfig& c = S->c;
+  if (c.ls_kind == 1) {
+    S->ph[S->np] = S->h_trial;
+    S->pf[S->np] = f;
+    S->np++;
+    switch (S->stage) {
+      case 10: {  // seeded by the slope at 0 and phi(h0)
+        const double h0 = S->a_h0, f0 = S->f0, f1 = f;
+        const double curv = (f1 - f0 - S->slope * h0) / (h0 * h0);
+        const double mx = fabs(f0) > fabs(f1) ? fabs(f0) : fabs(f1);
+        if (curv <= 0.0 || fabs(curv) < 1e-12 * mx) break;  // ok = False
+        double v = -S->slope / (2.0 * curv);
+        if (!accept_vertex(S, v)) break;
+        S->stage = 11;
+        S->h_trial = v;
+        return true;
+      }
+      case 20:
+        S->stage = 21;
+        S->h_trial = 0.5 * S->a_h0;
+        return true;
+      default:  // 11, 21: initial points complete; 30: a refinement probe
+        S->stage = 30;
+        if (ls_par_refine(S)) return true;
+        break;
+    }
+    ls_par_finish(S);
+    return false;
+  }
+  // ls_h
+  switch (S->stage) {
+    case 1:
+      if (f < S->f0) {
+        S->h_keep = S->h_trial;
+        S->f_keep = f;
+        S->stage = 2;
+        S->h_trial = c.k_plus * S->h_trial;
+        return true;
+      }
+      S->stage = 3;
+      S->h_trial = c.k_minus * S->a_h0;
+      return true;
+    case 2:
+      if (f < S->f_keep) ls_finish(S, true, S->h_trial, f);
+      else ls_finish(S, true, S->h_keep, S->f_keep);
+      return false;
+    default: {  // 3: contraction
+      if (f < S->f0) {
+        ls_finish(S, true, S->h_trial, f);
+        return false;
+      }
+      const double h = c.k_minus * S->h_trial;
+      if (h <= c.eps_h) {
+        ls_finish(S, false, 0.0, S->f0);
+        return false;
+      }
+      S->h_trial = h;
+      return true;
+    }
+  }
+}
+
+// ------------------------------------------------------------ kernels
+__global__ void min_launch_begin_kernel(MinState* S) {
+  S->iters_launch = 0;
+  S->pause = 0;
+  S->nrec = 0;
+  S->t_launch = globaltimer();
+}
+
+__global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir,
+                                    cudaGraphConditionalHandle hls,
+                                    cudaGraphConditionalHandle hacc) {
+  cudaGraphSetConditional(hls, 0);
+  cudaGraphSetConditional(hacc, 0);
+  unsigned go = 0;
+  const MinConfig& c = S->c;
+  if (!S->done) {
+    // Run.budget_status order: iterations, (wall time: host, per chunk), calls
+    if (c.max_iter >= 0 && S->k >= c.max_iter) {
+      S->status = kMinIterBudget;
+      S->done = 1;
+    } else if (c.max_calls >= 0 && S->vcalls + S->gcalls >= c.max_calls) {
+      S->status = kMinOracleBudget;
+      S->done = 1;
+    } else if (S->iters_launch >= c.chunk) {
+      S->pause = 1;
+    } else {
+      S->iters_launch++;
+      go = 1;
+    }
+  }
+  cudaGraphSetConditional(hdir, go);
+}
+
+// after d (two-loop or antigradient) and <d, d>
+__global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
+  const double dn = sqrt(S->dd);
+  S->dn = dn;
+  if (dn == 0.0) {
+    S->status = kMinConverged;
+    S->done = 1;
+    cudaGraphSetConditional(hls, 0);
+    return;
+  }
+  S->inv_dn = 1.0 / dn;  // ops.div(d, dn) = lincomb(1 / dn, d)
+  cudaGraphSetConditional(hls, 1);
+}
+
+// after r = d / |d| and slope = <g, r>: LineSearcher.search, first attempt
+__global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop) {
+  S->f0 = S->f;
+  S->attempt = 0;
+  ls_start(S, S->warm);
+  cudaGraphSetConditional(hloop, 1);
+}
+
+__global__ void min_ls_step_kernel(MinState* S, const double* en, const int64_t* stw,
+                                   cudaGraphConditionalHandle hloop) {
+  S->vcalls++;
+  if (bad_status(stw, false)) {
+    set_err(S, kMinErrEval, stw, false);
+    cudaGraphSetConditional(hloop, 0);
+    return;
+  }
+  const double f = en[0] + en[1] + en[2] + en[3] + en[4];  // EnergyBreakdown.total order
+  bool more = ls_on_value(S, f);
+  if (!more) {
+    // LineSearcher: one retry from the configured h0 after a warm-started miss
+    if (!S->found && S->attempt == 0 && S->warm != S->c.h0) {
+      S->attempt = 1;
+      ls_start(S, S->c.h0);
+      more = true;
+    } else {
+      S->warm = S->found ? fabs(S->res_h) : S->c.h0;
+    }
+  }
+  cudaGraphSetConditional(hloop, more ? 1u : 0u);
+}
+
+// lbfgs.py: what a line-search result does to the iteration
+__global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditionalHandle hacc) {
+  unsigned acc = 0;
+  if (!S->err) {
+    if (!S->found) {
+      if (S->count > 0 && !S->cleared) {
+        memory_clear(S);  // stale metric: drop it, retry along the antigradient
+        S->cleared = 1;
+      } else if (S->c.stop_on_ls_failure) {
+        S->status = kMinLsFailure;
+        S->done = 1;
+      } else {
+        S->k++;
+        record(S, rec, 0.0);
+        S->cleared = 0;
+      }
+    } else {
+      S->cleared = 0;
+      acc = 1;
+    }
+  }
+  cudaGraphSetConditional(hacc, acc);
+}
+
+// after the gradient at x_new and <g_new, g_new>
+__global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
+  S->gcalls++;
+  if (bad_status(stw, true)) {
+    set_err(S, kMinErrEval, stw, true);
+    return;
+  }
+  if (!isfinite(S->res_f) || !isfinite(S->gg)) set_err(S, kMinErrDiverged, nullptr, true);
+}
+
+// after <s,y>, <s,s>, <y,y>: LbfgsMemory._commit
+__global__ void min_commit_kernel(MinState* S) {
+  S->store_slot = -1;
+  if (S->err) return;
+  const double sy = S->sy, ss = S->ss, yy = S->yy;
+  if (!(sy > 1e-12 * sqrt(ss) * sqrt(yy))) return;  // curvature guard
+  const int m = S->c.m;
+  const int slot = S->freel[0];
+  for (int q = 1; q < S->nfree; ++q) S->freel[q - 1] = S->freel[q];
+  S->nfree--;
+  if (S->count == m) {  // evict the oldest pair, its slot becomes free
+    S->freel[S->nfree++] = S->order[0];
+    for (int q = 1; q < m; ++q) {
+      S->order[q - 1] = S->order[q];
+      S->rho[q - 1] = S->rho[q];
+    }
+    S->count--;
+  }
+  S->order[S->count] = slot;
+  S->rho[S->count] = 1.0 / sy;
+  S->count++;
+  for (int q = 0; q < S->count; ++q) {  // newest first for the two-loop kernel
+    S->idx_nf[q] = S->order[S->count - 1 - q];
+    S->rho_nf[q] = S->rho[S->count - 1 - q];
+  }
+  S->store_slot = slot;
+}
+
+__global__ void min_store_kernel(const MinState* S, int64_t n, const double* __restrict__ s_tmp,
+                                 const double* __restrict__ y_tmp, double* __restrict__ ring_s,
+                                 double* __restrict__ ring_y, const double* __restrict__ x_new,
+                                 const double* __restrict__ g_new, double* __restrict__ x,
+                                 double* __restrict__ g) {
+  if (S->err) return;
+  const int slot = S->store_slot;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (slot >= 0) {
+      ring_s[(int64_t)slot * n + i] = s_tmp[i];
+      ring_y[(int64_t)slot * n + i] = y_tmp[i];
+    }
+    x[i] = x_new[i];
+    g[i] = g_new[i];
+  }
+}
+
+__global__ void min_iter_end_kernel(MinState* S, double* rec) {
+  if (S->err) return;
+  S->f = S->res_f;
+  S->gn = sqrt(S->gg);
+  S->k++;
+  record(S, rec, S->res_h);
+  if (S->gn <= S->c.thr) {
+    S->status = kMinConverged;
+    S->done = 1;
+  }
+}
+
+__global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) {
+  cudaGraphSetConditional(hout, (!S->done && !S->pause) ? 1u : 0u);
+}
+
+}  // namespace
+
+#define FFM_ONE(kern, ...)                   \
+  do {                                       \
+    count_launch();                          \
+    kern<<<1, 1, 0, st>>>(__VA_ARGS__);      \
+    return cudaGetLastError();               \
+  } while (0)
+
+cudaError_t launch_min_launch_begin(MinState* S, cudaStream_t st) {
+  FFM_ONE(min_launch_begin_kernel, S);
+}
+cudaError_t launch_min_it_begin(MinState* S, cudaGraphConditionalHandle hdir,
+                                cudaGraphConditionalHandle hls, cudaGraphConditionalHandle hacc,
+                                cudaStream_t st) {
+  FFM_ONE(min_it_begin_kernel, S, hdir, hls, hacc);
+}
+cudaError_t launch_min_dir(MinState* S, cudaGraphConditionalHandle hls, cudaStream_t st) {
+  FFM_ONE(min_dir_kernel, S, hls);
+}
+cudaError_t launch_min_ls_init(MinState* S, cudaGraphConditionalHandle hloop, cudaStream_t st) {
+  FFM_ONE(min_ls_init_kernel, S, hloop);
+}
+cudaError_t launch_min_ls_step(MinState* S, const double* en, const int64_t* stw,
+                               cudaGraphConditionalHandle hloop, cudaStream_t st) {
+  FFM_ONE(min_ls_step_kernel, S, en, stw, hloop);
+}
+cudaError_t launch_min_ls_post(MinState* S, double* rec, cudaGraphConditionalHandle hacc,
+                               cudaStream_t st) {
+  FFM_ONE(min_ls_post_kernel, S, rec, hacc);
+}
+cudaError_t launch_min_acc_check(MinState* S, const int64_t* stw, cudaStream_t st) {
+  FFM_ONE(min_acc_check_kernel, S, stw);
+}
+cudaError_t launch_min_commit(MinState* S, cudaStream_t st) { FFM_ONE(min_commit_kernel, S); }
+cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {
+  FFM_ONE(min_iter_end_kernel, S, rec);
+}
+cudaError_t launch_min_it_end(MinState* S, cudaGraphConditionalHandle hout, cudaStream_t st) {
+  FFM_ONE(min_it_end_kernel, S, hout);
+}
+#undef FFM_ONE
+
+cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,
+                             double* ring_s, double* ring_y, const double* x_new,
+                             const double* g_new, double* x, double* g, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  count_launch();
+  min_store_kernel<<<(int)blocks, 256, 0, st>>>(S, n, s_tmp, y_tmp, ring_s, ring_y, x_new, g_new,
+                                                x, g);
+  return cudaGetLastError();
+}
+
+}  // namespace ffm

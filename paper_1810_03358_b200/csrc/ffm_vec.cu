@@ -156,7 +156,7 @@ __device__ __forceinline__ double grid_sum(const double* part) {
   return s;
 }
 
-__global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
+__device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kVecThreads / 32];
   __shared__ double bc;
@@ -244,7 +244,70 @@ __global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
   (void)G;
 }
 
+__global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) { two_loop_body(A); }
+
+// Device-driven variant for the graph-resident L-BFGS (ffm_min.cuh): the
+// pair count, ring slots (newest first) and rho come from device memory.
+// count = 0 gives the normalised antigradient of lbfgs_direction
+// (ffmin/optimizers/lbfgs.py:53-58): d = (1 / |g|) (-g), or -g when |g| = 0.
+struct TwoLoopDevArgs {
+  int64_t n;
+  const int* count;
+  const int* idx;
+  const double* rho;
+  const double* gn;
+  const double* S;
+  const double* Y;
+  const double* g;
+  double* q;
+  double* part;
+};
+
+__global__ void __launch_bounds__(kVecThreads) two_loop_dev_kernel(TwoLoopDevArgs D) {
+  const int count = *D.count;
+  if (count == 0) {
+    const double gn = *D.gn;
+    const double inv = 1.0 / gn;
+    for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < D.n;
+         i += (int64_t)gridDim.x * kVecThreads) {
+      const double v = -D.g[i];
+      D.q[i] = gn == 0.0 ? v : inv * v;
+    }
+    return;
+  }
+  TwoLoopArgs A;
+  A.n = D.n;
+  A.count = count;
+  for (int k = 0; k < count; ++k) {
+    A.idx[k] = D.idx[k];
+    A.rho[k] = D.rho[k];
+  }
+  A.S = D.S;
+  A.Y = D.Y;
+  A.g = D.g;
+  A.q = D.q;
+  A.part = D.part;
+  two_loop_body(A);
+}
+
 size_t two_loop_scratch_doubles() { return (size_t)kMaxDots * kVecBlocks; }
+
+// co-resident grid of the two-loop kernels: both variants use the same size
+// so their reductions combine partials in the same order
+static int two_loop_grid(int64_t n) {
+  int dev = 0, sms = 0, per_sm = 0, per_sm2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, two_loop_kernel, kVecThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, two_loop_dev_kernel, kVecThreads, 0);
+  if (per_sm2 < per_sm) per_sm = per_sm2;
+  int blocks = sms * (per_sm < 2 ? per_sm : 2);
+  const int64_t need = (n + kVecThreads - 1) / kVecThreads;
+  if (blocks > need) blocks = (int)need;
+  if (blocks > kVecBlocks) blocks = kVecBlocks;
+  if (blocks < 1) blocks = 1;
+  return blocks;
+}
 
 cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const double* rho,
                                   const double* S, const double* Y, const double* g,
@@ -262,18 +325,21 @@ cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const do
   a.g = g;
   a.q = q;
   a.part = scratch;
-  int dev = 0, sms = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, two_loop_kernel, kVecThreads, 0);
-  int blocks = sms * (per_sm < 2 ? per_sm : 2);
-  const int64_t need = (n + kVecThreads - 1) / kVecThreads;
-  if (blocks > need) blocks = (int)need;
-  if (blocks > kVecBlocks) blocks = kVecBlocks;
-  if (blocks < 1) blocks = 1;
   void* args[] = {&a};
   count_launch();
-  return cudaLaunchCooperativeKernel((void*)two_loop_kernel, blocks, kVecThreads, args, 0, st);
+  return cudaLaunchCooperativeKernel((void*)two_loop_kernel, two_loop_grid(n), kVecThreads,
+                                     args, 0, st);
+}
+
+cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* idx,
+                                      const double* rho, const double* gn, const double* S,
+                                      const double* Y, const double* g, double* q,
+                                      double* scratch, cudaStream_t st) {
+  TwoLoopDevArgs d{n, count, idx, rho, gn, S, Y, g, q, scratch};
+  void* args[] = {&d};
+  count_launch();
+  return cudaLaunchCooperativeKernel((void*)two_loop_dev_kernel, two_loop_grid(n), kVecThreads,
+                                     args, 0, st);
 }
 
 }  // namespace ffm

@@ -134,3 +134,61 @@ def test_every_driver_on_device_tracks_reference(golden, name):
     k = len(ref) if name in FIXED_STEP else 11
     np.testing.assert_allclose(f[:k], ref[:k], rtol=1e-7)
     assert res.status == str(golden[f"drv30/{name}/status"])
+
+
+def _run_lbfgs(s, host_loop, monkeypatch, kind, m, stop, dtype=np.float64, **ls):
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import lbfgs, make_linesearch
+
+    if host_loop:
+        monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+    else:
+        monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+    o = MolecularOracle(s, dtype=dtype)
+    res = lbfgs(o, s.coords.ravel(), m=m, linesearch=make_linesearch(kind, **ls), stop=stop)
+    return res, o
+
+
+@pytest.mark.parametrize("case", [
+    ("conv60", "par", 5, {}), ("conv200", "par", 3, {}), ("conv200", "h", 5, {}),
+    ("lbfgs500", "par", 3, {"use_gradient_start": False}), ("globule", "par", 5, {}),
+    ("globule32", "par", 5, {})])
+def test_graph_lbfgs_equals_host_driven_loop(golden, monkeypatch, case):
+    """The graph-resident iteration (conditional CUDA graph, csrc/
+    ffm_minimize.cu) makes the same decisions with the same arithmetic as
+    the host-driven loop: identical trace records, iterate and status."""
+    from paper_1810_03358_b200.optimizers import StopCriteria
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    name, kind, m, ls = case
+    dtype = np.float32 if name == "globule32" else np.float64
+    if name.startswith("globule"):
+        s = make_globule_system(1500, seed=3)
+        stop = StopCriteria(max_iterations=60, gradient_norm_rtol=1e-4)
+    else:
+        s = golden_system(golden, name)
+        stop = StopCriteria(max_iterations=400, gradient_norm_tol=1e-6, gradient_norm_rtol=0.0)
+    a, oa = _run_lbfgs(s, True, monkeypatch, kind, m, stop, dtype, **ls)
+    b, ob = _run_lbfgs(s, False, monkeypatch, kind, m, stop, dtype, **ls)
+    ra = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in b.trace.records]
+    assert len(ra) == len(rb)
+    assert ra == rb
+    assert a.status == b.status and a.f == b.f and a.grad_norm == b.grad_norm
+    assert np.array_equal(a.x, b.x)
+    assert (oa.value_calls, oa.grad_calls) == (ob.value_calls, ob.grad_calls)
+
+
+def test_graph_lbfgs_budgets(golden, monkeypatch):
+    """Iteration and oracle-call budgets stop the graph run where the host
+    loop stops."""
+    from paper_1810_03358_b200.optimizers import StopCriteria
+
+    s = golden_system(golden, "conv200")
+    for stop in (StopCriteria(max_iterations=7, gradient_norm_rtol=0.0),
+                 StopCriteria(max_iterations=None, max_oracle_calls=41, gradient_norm_rtol=0.0)):
+        a, _ = _run_lbfgs(s, True, monkeypatch, "par", 5, stop)
+        b, _ = _run_lbfgs(s, False, monkeypatch, "par", 5, stop)
+        assert a.status == b.status and a.iterations == b.iterations and a.f == b.f
