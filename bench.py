@@ -414,6 +414,55 @@ def run_extras(rank, world, local):
         eng.close()
         # configs[0]: L-BFGS time-to-converge against the reference run
         out["lbfgs_converge"] = lbfgs_converge()
+        # configs[2]: optimiser comparison on a 10k-atom globule
+        out["optimizer_comparison_10k"] = optimizer_comparison(10000, iters=100)
+        # configs[4]: L-BFGS iterations on the 100k-atom system (1 GPU)
+        out["lbfgs_100k"] = optimizer_comparison(100000, iters=10, methods=("lbfgs",),
+                                                 dtype=np.float32)
+    return out
+
+
+def optimizer_comparison(natoms, iters, methods=("sd", "fgm", "cg", "lbfgs", "wiggle"),
+                         dtype=np.float64):
+    """Every minimiser from the same perturbed start with the same iteration
+    budget: final energy, calls and wall time (device-resident iterates)."""
+    import torch
+
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import StopCriteria, cg, fgm, lbfgs, make_linesearch
+    from paper_1810_03358_b200.optimizers import steepest_descent
+    from paper_1810_03358_b200.optimizers.wiggle import WiggleConfig, atom_wiggle
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(natoms, seed=1)
+    out = {"natoms": natoms, "iterations_budget": iters,
+           "precision": "f32" if dtype == np.float32 else "f64"}
+    for name in methods:
+        stop = StopCriteria(max_iterations=iters, gradient_norm_rtol=1e-6)
+        o = MolecularOracle(s, dtype=dtype)
+        ls = make_linesearch("par")
+        run = {"sd": lambda: steepest_descent(o, s.coords.ravel(), ls, stop),
+               "fgm": lambda: fgm(o, s.coords.ravel(), ls, stop),
+               "cg": lambda: cg(o, s.coords.ravel(), "prp+", ls, stop),
+               "lbfgs": lambda: lbfgs(o, s.coords.ravel(), m=5, linesearch=ls, stop=stop)}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if name == "wiggle":
+            # gradient-free: one probe batch per atom move; 20 moves per atom
+            # budget unit is scaled so the call count is comparable
+            res = atom_wiggle(s, WiggleConfig(seed=0),
+                              StopCriteria(max_iterations=iters * 20, gradient_norm_rtol=0.0))
+            calls = res.trace.records[-1].value_calls
+            gcalls = 0
+        else:
+            res = run[name]()
+            calls, gcalls = o.value_calls, o.grad_calls
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"f": float(res.f), "iterations": int(res.iterations), "status": res.status,
+                     "value_calls": int(calls), "grad_calls": int(gcalls), "seconds": dt,
+                     "ms_per_iteration": dt / max(1, res.iterations) * 1e3}
+    out["f_start"] = float(MolecularOracle(s, dtype=dtype).value(s.coords.ravel()))
     return out
 
 
