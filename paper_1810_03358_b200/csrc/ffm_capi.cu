@@ -34,6 +34,12 @@ int fail(int code, const std::string& msg) {
       return fail(FFM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));  \
   } while (0)
 
+#define FFM_TRYR(x)    \
+  do {                 \
+    int rc_ = (x);     \
+    if (rc_) return rc_; \
+  } while (0)
+
 template <typename T>
 int upload(T** dst, const std::vector<T>& src) {
   *dst = nullptr;
@@ -103,6 +109,12 @@ struct ffm_system {
   // row sharding (ffm_system_set_shard): units u with u % nranks == rank
   int rank = 0, nranks = 1;
   int* d_unit_list = nullptr;
+  // small-system tile mode (NbPlanDev::ntiles > 0)
+  int2* d_tiles = nullptr;
+  int* d_tile_list = nullptr;
+  int* d_trow_ptr = nullptr;  // [np/128 + 1] tiles of each i-sub-block (contiguous)
+  int* d_tcol_ptr = nullptr;  // [np/32 + 1] tiles of each j-block ...
+  int* d_tcol_idx = nullptr;  // ... listed here, by i-sub-block
   // host copies needed to rebuild the term plan
   std::vector<std::pair<int, int>> scaled;  // (i, j)
   std::vector<double> scaled_s;
@@ -138,7 +150,8 @@ void free_all(ffm_system* s) {
                   s->d_sc_s, s->d_bond_idx, s->d_bond_K, s->d_bond_r0, s->d_ang_idx,
                   s->d_ang_K, s->d_ang_t0, s->d_dih_idx, s->d_dih_V, s->d_slot_ptr,
                   s->d_slot_idx, s->d_aterm_ptr, s->d_aterm_idx, s->h_coords_d, s->h_grad_d,
-                  s->h_en_d, s->h_st_d, s->d_unit_list};
+                  s->h_en_d, s->h_st_d, s->d_unit_list, s->d_tiles, s->d_tile_list,
+                  s->d_trow_ptr, s->d_tcol_ptr, s->d_tcol_idx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
@@ -287,6 +300,50 @@ int build_terms(ffm_system* s, int64_t nbond, const int64_t* bidx, const double*
   return FFM_OK;
 }
 
+// energy-partial slots of the pair sweep: one per tile or per super-unit
+int nb_slots(const NbPlanDev& p) { return p.ntiles ? p.ntiles : p.nunits; }
+
+// small systems sweep tiles instead of super-units when the units would
+// not fill the GPU (fewer than 2 per SM)
+bool use_tiles(const NbPlanDev& p, int device) {
+  if (const char* f = getenv("FFM_FORCE_TILES")) return atoi(f) != 0;  // tuning / tests
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return p.nunits < 2 * sms;
+}
+
+int build_tiles(ffm_system* s) {
+  NbPlanDev& p = s->plan;
+  const int nkk = p.np / kIB, nmg = p.np / kJB;
+  std::vector<int2> tiles;
+  std::vector<int> rptr(nkk + 1, 0);
+  std::vector<std::vector<int>> col(nmg);
+  for (int kk = 0; kk < nkk; ++kk) {
+    for (int mg = 4 * kk; mg < nmg; ++mg) {
+      if (kk * kIB >= p.n || mg * kJB >= p.n) continue;  // padding only
+      col[mg].push_back((int)tiles.size());
+      tiles.push_back(make_int2(kk, mg));
+    }
+    rptr[kk + 1] = (int)tiles.size();
+  }
+  std::vector<int> cptr(nmg + 1, 0), cidx;
+  for (int mg = 0; mg < nmg; ++mg) {
+    cptr[mg + 1] = cptr[mg] + (int)col[mg].size();
+    cidx.insert(cidx.end(), col[mg].begin(), col[mg].end());
+  }
+  if (cidx.empty()) cidx.push_back(0);
+  if (tiles.empty()) tiles.push_back(make_int2(0, 0));  // n = 0: never launched
+  FFM_TRYR(upload(&s->d_tiles, tiles));
+  FFM_TRYR(upload(&s->d_trow_ptr, rptr));
+  FFM_TRYR(upload(&s->d_tcol_ptr, cptr));
+  FFM_TRYR(upload(&s->d_tcol_idx, cidx));
+  p.tiles = s->d_tiles;
+  p.tile_list = nullptr;
+  p.ntiles = (int)tiles.size();
+  p.nlaunch = p.n > 0 ? p.ntiles : 0;
+  return FFM_OK;
+}
+
 // allocate / grow the workspace of one precision
 int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   Work& w = s->w[prec];
@@ -328,20 +385,23 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   // partial slots of units another rank owns are never written: they must
   // read as zero in the gather and the energy reduction
   if (grad && !w.ipart) {
-    const size_t bytes = (size_t)p.nunits * 3 * p.S * tsz;
-    if (cudaMalloc(&w.ipart, bytes) != cudaSuccess || cudaMalloc(&w.jpart, bytes) != cudaSuccess)
+    const size_t ib = p.ntiles ? (size_t)p.ntiles * 3 * kIB * tsz : (size_t)p.nunits * 3 * p.S * tsz;
+    const size_t jb = p.ntiles ? (size_t)p.ntiles * 3 * kJB * tsz : ib;
+    if (cudaMalloc(&w.ipart, ib) != cudaSuccess || cudaMalloc(&w.jpart, jb) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for gradient partials");
-    FFM_CUDA(cudaMemset(w.ipart, 0, bytes));
-    FFM_CUDA(cudaMemset(w.jpart, 0, bytes));
+    FFM_CUDA(cudaMemset(w.ipart, 0, ib));
+    FFM_CUDA(cudaMemset(w.jpart, 0, jb));
+    // the caller's stream may not be ordered after the legacy stream
+    FFM_CUDA(cudaDeviceSynchronize());
   }
   if (w.e_batch < batch) {
     if (w.epart) cudaFree(w.epart);
     w.epart = nullptr;
-    const size_t bytes = (size_t)batch * p.nunits * 3 * sizeof(double);
+    const size_t bytes = (size_t)batch * nb_slots(p) * 3 * sizeof(double);
     if (cudaMalloc(&w.epart, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for energy partials");
     // units another rank owns: no energy, no close contact (min r^2 = 1e30)
-    std::vector<double> init((size_t)batch * p.nunits * 3, 0.0);
+    std::vector<double> init((size_t)batch * nb_slots(p) * 3, 0.0);
     for (size_t k = 2; k < init.size(); k += 3) init[k] = 1e30;
     FFM_CUDA(cudaMemcpy(w.epart, init.data(), bytes, cudaMemcpyHostToDevice));
     w.e_batch = batch;
@@ -546,6 +606,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_unit_rc, urc));
   FFM_TRY(upload(&s->d_unit_index, uidx));
   p.unit_rc = s->d_unit_rc;
+  if (n > 0 && use_tiles(p, device)) FFM_TRY(build_tiles(s));
   p.spt_ptr = s->d_spt_ptr;
   p.spt_m = s->d_spt_m;
   p.spt_mask = s->d_spt_mask;
@@ -595,7 +656,21 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
   s->d_unit_list = nullptr;
   s->rank = rank;
   s->nranks = nranks;
-  if (nranks == 1) {
+  if (s->d_tile_list) cudaFree(s->d_tile_list);
+  s->d_tile_list = nullptr;
+  if (s->plan.ntiles > 0) {  // tile mode: tiles dealt round-robin
+    s->plan.tile_list = nullptr;
+    s->plan.nlaunch = s->plan.n > 0 ? s->plan.ntiles : 0;
+    if (nranks > 1) {
+      std::vector<int> mine;
+      for (int t = rank; t < s->plan.ntiles; t += nranks) mine.push_back(t);
+      if (mine.empty()) mine.push_back(0), s->plan.nlaunch = 0;
+      else s->plan.nlaunch = (int)mine.size();
+      int rc = upload(&s->d_tile_list, mine);
+      if (rc) return rc;
+      s->plan.tile_list = s->d_tile_list;
+    }
+  } else if (nranks == 1) {
     s->plan.unit_list = nullptr;
     s->plan.nlaunch = s->plan.nunits;
   } else {
@@ -670,10 +745,12 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
   FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
   if (grad && s->plan.n > 0)
-    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart,
-                             w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
-                             s->tp.slot_sc0, do_nb, do_terms, grad_d, st));
-  FFM_CUDA(launch_reduce(do_nb ? s->plan.nunits : 0, tp, 1, w.epart, w.term_e, energies_d,
+    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index,
+                             s->plan.ntiles ? s->d_trow_ptr : nullptr, s->d_tcol_ptr,
+                             s->d_tcol_idx, w.ipart, w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
+                             s->tp.slot_sc0, do_nb, do_terms && s->rank == 0,
+                             do_nb && s->rank == 0, grad_d, st));
+  FFM_CUDA(launch_reduce(do_nb ? nb_slots(s->plan) : 0, tp, 1, w.epart, w.term_e, energies_d,
                          status_d, st));
   FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
                          s->d_sp_j, s->d_sp_s, status_d, st));
@@ -792,7 +869,7 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   TermPlanDev tp = s->tp;
   if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
   FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
-  FFM_CUDA(launch_reduce(s->plan.nunits, tp, B, w.epart, w.term_e, energies_d, status_d, st));
+  FFM_CUDA(launch_reduce(nb_slots(s->plan), tp, B, w.epart, w.term_e, energies_d, status_d, st));
   FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                          s->d_sp_s, status_d, st));
   return FFM_OK;
@@ -922,11 +999,6 @@ int add_conditional(cudaStream_t st, cudaGraphConditionalHandle h,
   return FFM_OK;
 }
 
-#define FFM_TRYR(x)  \
-  do {               \
-    int rc_ = (x);   \
-    if (rc_) return rc_; \
-  } while (0)
 
 // bodies of the iteration graph (see ffm_min.cuh); each runs inside a
 // capture on stream st
@@ -1132,6 +1204,7 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   L->ring_s = p;
   L->ring_y = p + (size_t)n * (c.m + 1);
   cudaMemset(L->buf, 0, nbuf * sizeof(double));
+  cudaDeviceSynchronize();  // before any use on the caller's (maybe non-blocking) stream
   for (cudaStream_t& cs : L->cap)
     if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) {
       lbfgs_free(L);

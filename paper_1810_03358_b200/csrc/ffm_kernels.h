@@ -42,12 +42,15 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
                          double* term_part, double* term_f, int64_t* status, cudaStream_t st);
 
 // gradient[a] = sum of nonbonded partials + incident term slots, fixed order
-// use_nb: add the pair partials and the scaled-pair slots; use_terms: add
-// the bonded slots (slots below slot_sc0)
+// use_nb: add the pair partials; use_terms: add the bonded slots (below
+// slot_sc0); use_sc: add the scaled-pair slots.  Term and scaled slots are
+// written by rank 0 only: other ranks of a sharded system must not read them
 cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
+                            const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
                             const void* ipart, const void* jpart, const int* slot_ptr,
                             const int* slot_idx, const double* term_f, int slot_sc0,
-                            bool use_nb, bool use_terms, double* grad, cudaStream_t st);
+                            bool use_nb, bool use_terms, bool use_sc, double* grad,
+                            cudaStream_t st);
 
 // energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
 // coincidences for the finder

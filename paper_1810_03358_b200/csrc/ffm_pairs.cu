@@ -546,6 +546,136 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   }
 }
 
+// ------------------------------------------------------- small systems
+// One warp per 128 x 32 tile (i-sub-block kk, global j-block mg >= 4 kk),
+// four warps per CTA: a system of a few thousand atoms has a handful of
+// super-units, which would leave most SMs idle and run each unit's tiles
+// back to back on one SM; here every tile of the triangle runs at once.
+// Partials per tile: i-rows [tile][3][128], j-columns [tile][3][32],
+// energies [batch][tile][3]; the gather sums them in a fixed order.
+constexpr int kTileWarps = 4;
+
+template <typename T, bool GRAD, bool CUTOFF>
+__global__ void __launch_bounds__(kTileWarps * 32)
+nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
+                const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
+                const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,
+                double* __restrict__ epart) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  using V4 = typename Vec4T<T>::type;
+  using V2 = typename Vec2T<T>::type;
+  __shared__ V4 sj[kTileWarps][2 * kJB];
+  __shared__ V2 sl[kTileWarps][2 * kJB];
+  __shared__ T jacc[kTileWarps][3 * kJB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int slot = blockIdx.x * kTileWarps + warp;
+  if (slot >= plan.nlaunch) return;  // warp-uniform; no block barriers below
+  const int t = plan.tile_list ? plan.tile_list[slot] : slot;
+  const int2 tk = plan.tiles[t];
+  const int kk = tk.x, mg = tk.y;
+  const int ib = kk * kIB, jb = mg * kJB;
+  const int bidx = blockIdx.y;
+  pos += (size_t)bidx * plan.np;
+  ipos += (size_t)bidx * 4 * plan.np;
+  const int64_t half = plan.np >> 1;
+  {
+    V4 p = pos[jb + lane];
+    p.x = -p.x;
+    p.y = -p.y;
+    p.z = -p.z;
+    sj[warp][lane] = p;
+    sj[warp][lane + 32] = p;
+    V2 l = lj[jb + lane];
+    l.y = -l.y;
+    sl[warp][lane] = l;
+    sl[warp][lane + 32] = l;
+    if (GRAD) jacc[warp][lane] = jacc[warp][32 + lane] = jacc[warp][64 + lane] = T(0);
+  }
+  __syncwarp();
+  V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp) {
+    const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
+    xi[pp] = ld_pair<T>(ipos, r);
+    yi[pp] = ld_pair<T>(ipos, half + r);
+    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+    ai[pp] = ld_pair<T>(ilj, r);
+    bi[pp] = ld_pair<T>(ilj, half + r);
+  }
+  V F[2][3];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
+  V ec2 = P::zero(), ev2 = P::zero();
+  T minr2 = T(1e30);
+  bool masked = jb < ib + kIB;  // straddles the diagonal
+  uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
+  if (masked) {
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      const int d = ib + lane + 32 * p - jb;  // pair active iff jj > d
+      mk[p] = d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
+    }
+  }
+  for (int e = plan.spt_ptr[kk]; e < plan.spt_ptr[kk + 1]; ++e) {
+    if (plan.spt_m[e] == mg) {
+      masked = true;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)e * kIB + 32 * p + lane];
+      break;
+    }
+  }
+  const T cut2 = T(plan.cut2);
+  if (masked)
+    warp_tile<T, GRAD, CUTOFF, true>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F, ec2,
+                                     ev2, jacc[warp], kJB, mk, cut2, minr2);
+  else
+    warp_tile<T, GRAD, CUTOFF, false>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F, ec2,
+                                      ev2, jacc[warp], kJB, mk, cut2, minr2);
+  double ec = double(P::lo(ec2)) + double(P::hi(ec2));
+  double ev = double(P::lo(ev2)) + double(P::hi(ev2));
+  double mr = double(minr2);
+  for (int o = 16; o > 0; o >>= 1) {
+    ec += __shfl_xor_sync(0xffffffffu, ec, o);
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+    mr = fmin(mr, __shfl_xor_sync(0xffffffffu, mr, o));
+  }
+  if (lane == 0) {
+    double* e = epart + ((size_t)bidx * plan.ntiles + t) * 3;
+    e[0] = ec;
+    e[1] = ev;
+    e[2] = mr;
+  }
+  if (GRAD) {
+    T* ip = ipart + (size_t)t * 3 * kIB;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {  // F = -gradient
+        ip[c * kIB + lane + 64 * pp] = -P::lo(F[pp][c]);
+        ip[c * kIB + lane + 64 * pp + 32] = -P::hi(F[pp][c]);
+      }
+    __syncwarp();
+    T* jp = jpart + (size_t)t * 3 * kJB;
+    for (int c = 0; c < 3; ++c) jp[c * kJB + lane] = jacc[warp][c * kJB + lane];
+  }
+}
+
+template <typename T, bool GRAD, bool CUTOFF>
+static cudaError_t launch_tiles_t(const NbPlanDev& plan, const void* pos, const void* lj,
+                                  const void* ipos, const void* ilj, void* ipart, void* jpart,
+                                  double* epart, int batch, cudaStream_t st) {
+  if (plan.nlaunch == 0) return cudaSuccess;
+  dim3 grid((plan.nlaunch + kTileWarps - 1) / kTileWarps, batch);
+  count_launch();
+  nb_tiles_kernel<T, GRAD, CUTOFF><<<grid, kTileWarps * 32, 0, st>>>(
+      plan, static_cast<const typename Vec4T<T>::type*>(pos),
+      static_cast<const typename Vec2T<T>::type*>(lj), static_cast<const T*>(ipos),
+      static_cast<const T*>(ilj), static_cast<T*>(ipart), static_cast<T*>(jpart), epart);
+  return cudaGetLastError();
+}
+
 size_t nb_smem_bytes(int S, bool fp64, bool grad) {
   const size_t t = fp64 ? 8 : 4;
   size_t b = (size_t)2 * S * (4 * t + 2 * t);
@@ -585,6 +715,18 @@ cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* p
                       const void* lj, const void* ipos, const void* ilj, const void* bbox,
                       void* ipart, void* jpart, double* epart, int batch, cudaStream_t st) {
   const bool cut = plan.has_cutoff != 0;
+  if (plan.ntiles > 0) {  // small system: tile-parallel sweep
+#define FFM_NT(T, G, C) \
+  return launch_tiles_t<T, G, C>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, batch, st)
+    if (fp64) {
+      if (grad) { if (cut) FFM_NT(double, true, true); else FFM_NT(double, true, false); }
+      else { if (cut) FFM_NT(double, false, true); else FFM_NT(double, false, false); }
+    } else {
+      if (grad) { if (cut) FFM_NT(float, true, true); else FFM_NT(float, true, false); }
+      else { if (cut) FFM_NT(float, false, true); else FFM_NT(float, false, false); }
+    }
+#undef FFM_NT
+  }
 #define FFM_NB(T, G, C) \
   return launch_nb_t<T, G, C>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart, epart, batch, st)
   if (fp64) {

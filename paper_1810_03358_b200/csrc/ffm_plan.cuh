@@ -26,6 +26,11 @@ struct NbPlanDev {
   int has_cutoff;
   double cut2;
   double cull2;  // (cutoff + margin)^2: boxes farther apart than this never interact
+  // small systems (ntiles > 0): the sweep runs one warp per 128 x 32 tile
+  // instead of per super-unit (nb_tiles_kernel); nlaunch then counts tiles
+  int ntiles;
+  const int2* tiles;         // [ntiles] (i-sub-block, global j-block), row-major
+  const int* tile_list;      // tiles this launch evaluates (row sharding), or null = all
 };
 
 // Bonded terms + scaled (1-4) pairs, all evaluated in FP64.

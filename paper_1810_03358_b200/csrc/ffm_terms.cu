@@ -351,18 +351,27 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
 // ---------------------------------------------------------- gradient gather
 template <typename T>
 __global__ void assemble_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
+                                const int* __restrict__ trow_ptr,
+                                const int* __restrict__ tcol_ptr,
+                                const int* __restrict__ tcol_idx,
                                 const T* __restrict__ ipart, const T* __restrict__ jpart,
                                 const int* __restrict__ slot_ptr,
                                 const int* __restrict__ slot_idx,
                                 const double* __restrict__ term_f, int slot_sc0, bool use_nb,
-                                bool use_terms, double* __restrict__ grad) {
+                                bool use_terms, bool use_sc, double* __restrict__ grad) {
   // one thread per (atom, component): 3 n threads, coalesced along atoms
   const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= 3 * (int64_t)n) return;
   const int c = (int)(x / n), a = (int)(x - (int64_t)c * n);
   const int b = a / S, off = a - b * S;
   double g = 0.0;
-  if (use_nb) {
+  if (use_nb && trow_ptr) {  // tile mode (nb_tiles_kernel)
+    const int kk = a / kIB, row = a - kk * kIB, mg = a / kJB, l = a - mg * kJB;
+    for (int t = trow_ptr[kk]; t < trow_ptr[kk + 1]; ++t)
+      g += (double)ipart[((size_t)t * 3 + c) * kIB + row];
+    for (int e = tcol_ptr[mg]; e < tcol_ptr[mg + 1]; ++e)
+      g += (double)jpart[((size_t)tcol_idx[e] * 3 + c) * kJB + l];
+  } else if (use_nb) {
     const size_t co = (size_t)c * S + off;
 #pragma unroll 4
     for (int cc = b; cc < nb; ++cc)  // i-side: units (b, cc)
@@ -373,27 +382,29 @@ __global__ void assemble_kernel(int n, int S, int nb, const int* __restrict__ un
   }
   for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
     const int k = slot_idx[s];
-    if (k < slot_sc0 ? !use_terms : !use_nb) continue;
+    if (k < slot_sc0 ? !use_terms : !use_sc) continue;
     g += term_f[3 * (size_t)k + c];
   }
   grad[3 * (size_t)a + c] = g;
 }
 
 cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
+                            const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
                             const void* ipart, const void* jpart, const int* slot_ptr,
                             const int* slot_idx, const double* term_f, int slot_sc0,
-                            bool use_nb, bool use_terms, double* grad, cudaStream_t st) {
+                            bool use_nb, bool use_terms, bool use_sc, double* grad,
+                            cudaStream_t st) {
   const int blocks = (int)((3 * (int64_t)n + 127) / 128);
   if (fp64)
     count_launch(), assemble_kernel<double><<<blocks, 128, 0, st>>>(
-        n, S, nb, unit_index, static_cast<const double*>(ipart),
+        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, static_cast<const double*>(ipart),
         static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, grad);
+        use_terms, use_sc, grad);
   else
     count_launch(), assemble_kernel<float><<<blocks, 128, 0, st>>>(
-        n, S, nb, unit_index, static_cast<const float*>(ipart),
+        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, static_cast<const float*>(ipart),
         static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, grad);
+        use_terms, use_sc, grad);
   return cudaGetLastError();
 }
 

@@ -330,6 +330,7 @@ def test_every_super_unit_size(S, monkeypatch):
     from paper_1810_03358_b200.synth import make_globule_system
 
     monkeypatch.setenv("FFM_FORCE_S", str(S))
+    monkeypatch.setenv("FFM_FORCE_TILES", "0")  # super-unit sweep even at this size
     s = make_globule_system(2900, seed=11)
     assert DeviceSystem(s.topology).info["S"] == S
     A = O.Arrays.from_system(s)
@@ -341,3 +342,49 @@ def test_every_super_unit_size(S, monkeypatch):
         got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
         assert _rel(got, e_ref) <= et
         assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
+
+
+@pytest.mark.parametrize("n,cutoff", [(37, None), (300, None), (1000, 9.0), (4100, None)])
+def test_tile_sweep_matches_oracle_and_unit_sweep(n, cutoff, monkeypatch):
+    """Small systems sweep one warp per 128 x 32 tile (nb_tiles_kernel):
+    same energies / gradients as the oracle and as the super-unit sweep,
+    ragged last blocks, cutoff, and row-sharded partial sums."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(n, seed=7, cutoff=cutoff)
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    assert err is None
+    gmax = np.max(np.abs(g_ref))
+    c = torch.from_numpy(s.coords.copy()).cuda()
+    out = {}
+    for tiles in ("1", "0"):
+        monkeypatch.setenv("FFM_FORCE_TILES", tiles)
+        eng = DeviceSystem(s.topology)
+        for prec, et, gt in ((N.FFM_F64, 1e-10, 1e-10), (N.FFM_F32, 1e-5, 1e-4)):
+            g = torch.empty_like(c)
+            e, st = eng.eval(c, prec, grad=g)
+            e = e.cpu().numpy()
+            assert int(st[0]) == -1
+            assert _rel(e, e_ref) <= et
+            assert np.max(np.abs(g.cpu().numpy().ravel() - g_ref.ravel())) <= gt * gmax
+            out[(tiles, prec)] = (e, g.cpu().numpy())
+        eng.close()
+    # row shards of the tile sweep sum to the full evaluation
+    monkeypatch.setenv("FFM_FORCE_TILES", "1")
+    e_sum, g_sum = 0.0, 0.0
+    for rank in range(3):
+        eng = DeviceSystem(s.topology)
+        N.check(eng.lib.ffm_system_set_shard(eng.handle, rank, 3), "set_shard")
+        g = torch.empty_like(c)
+        e, st = eng.eval(c, N.FFM_F64, grad=g)
+        assert int(st[5]) == 0
+        e_sum = e_sum + e.cpu().numpy()
+        g_sum = g_sum + g.cpu().numpy()
+        eng.close()
+    np.testing.assert_allclose(e_sum, out[("1", N.FFM_F64)][0], rtol=1e-12, atol=1e-9)
+    assert np.max(np.abs(g_sum - out[("1", N.FFM_F64)][1])) <= 1e-11 * gmax
