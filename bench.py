@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "pair-interactions/sec (energy+grad)"
 NATOMS = 100_000
 FLOP_PER_PAIR = 38  # 27 FP32 ops (10 of them FMA -> +10) + 1 rsqrt, DESIGN.md
-FMA_SLOTS_PER_PAIR = 26  # FP32 lane-ops on the FMA pipe per pair: 12 FFMA2 + 10 FMUL2 + 4 FADD2 per packed pair-of-pairs (SASS)
+FMA_SLOTS_PER_PAIR = 26  # FP32 lane-ops on the FMA pipe per pair (SASS: 11.5 FFMA2 + 10 FMUL2 + 4.5 FADD2 per 2 pairs)
 
 
 def parse():
