@@ -22,10 +22,17 @@
 
 namespace ffm {
 
+#ifndef FFM_MINB64
+#define FFM_MINB64 2  // FP64: two CTAs per SM (<= 128 registers)
+#endif
 #ifndef FFM_UNROLL
 #define FFM_UNROLL 32
 #endif
+#ifndef FFM_UNROLL64
+#define FFM_UNROLL64 0  // 0: 4 with gradient, 8 energy-only (measured best)
+#endif
 constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
+constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/SM)
 
 template <typename T>
 __device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
@@ -155,31 +162,40 @@ cudaError_t launch_bbox(int n, int np, int batch, bool fp64, const void* pos, vo
   return cudaGetLastError();
 }
 
+// i-atom pairs held per pass: FP32 keeps both packed pairs (4 i-atoms per
+// lane) live; FP64 sweeps them one after the other so the kernel fits 128
+// registers and two CTAs per SM
+template <typename T> struct PairsPerPass { static constexpr int value = 2; };
+template <> struct PairsPerPass<double> { static constexpr int value = 1; };
+
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
 // j-block, so step t of lane l reads entry l + t (atom (l + t) mod 32) with
 // an immediate offset.  MASKED tiles carry per-lane activity bitmasks
 // (diagonal i < j condition and/or special pairs); inactive pairs are
 // neutralised (r2 -> 1, coefficients -> 0) so they contribute exactly zero.
-template <typename T, bool GRAD, bool CUTOFF, bool MASKED>
+template <typename T, bool GRAD, bool CUTOFF, bool MASKED, int NP, bool DOUBLED = true>
 __device__ __forceinline__ void warp_tile(
     const typename Vec4T<T>::type* __restrict__ J,
     const typename Vec2T<T>::type* __restrict__ L, int lane,
-    const typename Pk<T>::V (&xi)[2], const typename Pk<T>::V (&yi)[2],
-    const typename Pk<T>::V (&zi)[2], const typename Pk<T>::V (&qi)[2],
-    const typename Pk<T>::V (&ai)[2], const typename Pk<T>::V (&bi)[2],
-    typename Pk<T>::V (&F)[2][3], typename Pk<T>::V& ec2,
+    const typename Pk<T>::V (&xi)[NP], const typename Pk<T>::V (&yi)[NP],
+    const typename Pk<T>::V (&zi)[NP], const typename Pk<T>::V (&qi)[NP],
+    const typename Pk<T>::V (&ai)[NP], const typename Pk<T>::V (&bi)[NP],
+    typename Pk<T>::V (&F)[NP][3], typename Pk<T>::V& ec2,
     typename Pk<T>::V& ev2, T* __restrict__ jacc, int jacc_stride,
-    const uint32_t (&mk)[4], T cut2, T& minr2) {
+    const uint32_t (&mk)[2 * NP], T cut2, T& minr2) {
   using P = Pk<T>;
   using V = typename P::V;
   V gx = P::zero(), gy = P::zero(), gz = P::zero();
   const int src = (lane + 1) & 31;
-  J += lane;
-  L += lane;
-#pragma unroll kStepUnroll
+  if (DOUBLED) {  // j-block stored twice: entry lane + t is an immediate offset
+    J += lane;
+    L += lane;
+  }
+#pragma unroll(sizeof(T) == 8 ? (kStepUnroll64 ? kStepUnroll64 : (GRAD ? 4 : 8)) : kStepUnroll)
   for (int t = 0; t < 32; ++t) {
-    const auto pj = J[t];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
-    const auto lj = L[t];  // (a, -b)
+    const int jt = DOUBLED ? t : ((lane + t) & 31);
+    const auto pj = J[jt];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
+    const auto lj = L[jt];  // (a, -b)
 #ifndef FFM_SCHED
 #define FFM_SCHED 1
 #endif
@@ -189,9 +205,9 @@ __device__ __forceinline__ void warp_tile(
 #if FFM_SCHED == 1
     // phase-separated: both pairs' geometry first, the four MUFU.RSQ issued
     // back to back, coefficient products while they are in flight
-    V dx[2], dy[2], dz[2], r2[2], A[2], nB[2], Q[2], ri[2];
+    V dx[NP], dy[NP], dz[NP], r2[NP], A[NP], nB[NP], Q[NP], ri[NP];
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < NP; ++pp) {
       dx[pp] = P::add(xi[pp], P::bc(pj.x));
       dy[pp] = P::add(yi[pp], P::bc(pj.y));
       dz[pp] = P::add(zi[pp], P::bc(pj.z));
@@ -200,7 +216,7 @@ __device__ __forceinline__ void warp_tile(
       r2[pp] = P::fma(dz[pp], dz[pp], r2[pp]);
     }
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < NP; ++pp) {
       A[pp] = P::mul(ai[pp], P::bc(lj.x));
       nB[pp] = P::mul(bi[pp], P::bc(lj.y));
       Q[pp] = P::mul(qi[pp], P::bc(pj.w));
@@ -224,7 +240,7 @@ __device__ __forceinline__ void warp_tile(
       ri[pp] = P::rsqrt(r2[pp]);
     }
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < NP; ++pp) {
       const V i2 = P::mul(ri[pp], ri[pp]);
       const V i4 = P::mul(i2, i2);
       const V i6 = P::mul(i4, i2);
@@ -262,7 +278,7 @@ __device__ __forceinline__ void warp_tile(
     }
 #else
 #pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
+    for (int pp = 0; pp < NP; ++pp) {
       V dx = P::add(xi[pp], P::bc(pj.x));
       V dy = P::add(yi[pp], P::bc(pj.y));
       V dz = P::add(zi[pp], P::bc(pj.z));
@@ -360,7 +376,7 @@ __device__ __forceinline__ double block_min(double v, double* red) {
 #define FFM_MINB 2
 #endif
 template <typename T, bool GRAD, bool CUTOFF>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? FFM_MINB : 1)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? FFM_MINB : FFM_MINB64)
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, const T* __restrict__ bbox,
@@ -373,8 +389,12 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   __shared__ double red[kWarps];
   const int S = plan.S;
   V4* sj = reinterpret_cast<V4*>(smem_raw);   // [2S]: each j-block stored twice
-  V2* sl = reinterpret_cast<V2*>(sj + 2 * S);  // [2S]
-  T* jacc = reinterpret_cast<T*>(sl + 2 * S);  // [3][S]      (GRAD)
+  // FP32 stores each j-block twice (immediate-offset addressing in the hot
+  // loop); FP64, bound by its pipe, stores it once so two CTAs fit an SM
+  constexpr bool kDbl = sizeof(T) == 4;
+  constexpr int kRep = kDbl ? 2 : 1;
+  V2* sl = reinterpret_cast<V2*>(sj + kRep * S);  // [kRep S]
+  T* jacc = reinterpret_cast<T*>(sl + kRep * S);  // [3][S]      (GRAD)
   T* ired = jacc + 3 * S;                      // [kWarps][3][kIB] (GRAD)
 
   const int u = plan.unit_list ? plan.unit_list[blockIdx.x] : blockIdx.x;
@@ -416,8 +436,8 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     }
   }
 
-  for (int e = tid; e < 2 * S; e += kThreads) {
-    const int a = j0 + (e >> 6) * kJB + (e & 31);
+  for (int e = tid; e < kRep * S; e += kThreads) {
+    const int a = kDbl ? j0 + (e >> 6) * kJB + (e & 31) : j0 + e;
     V4 p = pos[a];
     p.x = -p.x;
     p.y = -p.y;
@@ -435,24 +455,10 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   T minr2 = T(1e30);
   const T cut2 = T(plan.cut2);
   const int nsub = S / kIB, njb = S / kJB;
+  constexpr int NP = PairsPerPass<T>::value;
   for (int ks = 0; ks < nsub; ++ks) {
     const int ib = i0 + ks * kIB;
     const int kk = ib / kIB;
-    V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) {
-      const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
-      xi[pp] = ld_pair<T>(ipos, r);
-      yi[pp] = ld_pair<T>(ipos, half + r);
-      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
-      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
-      ai[pp] = ld_pair<T>(ilj, r);
-      bi[pp] = ld_pair<T>(ilj, half + r);
-    }
-    V F[2][3];
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
-    V ec2 = P::zero(), ev2 = P::zero();
     const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];
     // which j-blocks of this unit carry special pairs for these rows: one
     // bit per j-block (njb <= 32), so the tile loop tests a bit instead of
@@ -465,7 +471,23 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     spbits = __reduce_or_sync(0xffffffffu, spbits);
     T ibox[6];
     if (CUTOFF) box_union_seq<T>(bbox, ib / kJB, kIB / kJB, ibox);
-
+    T* my = ired + warp * 3 * kIB;
+    for (int p0 = 0; p0 < 2; p0 += NP) {
+    V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const int64_t r = (int64_t)kk * 64 + (p0 + pp) * 32 + lane;
+      xi[pp] = ld_pair<T>(ipos, r);
+      yi[pp] = ld_pair<T>(ipos, half + r);
+      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+      ai[pp] = ld_pair<T>(ilj, r);
+      bi[pp] = ld_pair<T>(ilj, half + r);
+    }
+    V F[NP][3];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
+    V ec2 = P::zero(), ev2 = P::zero();
     for (int m = warp; m < njb; m += kWarps) {
       const int jb = j0 + m * kJB;
       if (diag && jb + kJB <= ib) continue;  // whole tile has j < i
@@ -494,31 +516,36 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
           }
         }
       }
+      uint32_t mkp[2 * NP];
+#pragma unroll
+      for (int q = 0; q < 2 * NP; ++q) mkp[q] = mk[2 * p0 + q];
       T* jc = jacc + m * kJB;
-      const V4* J = sj + m * 2 * kJB;
-      const V2* L = sl + m * 2 * kJB;
+      const V4* J = sj + m * kRep * kJB;
+      const V2* L = sl + m * kRep * kJB;
       if (masked)
-        warp_tile<T, GRAD, CUTOFF, true>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jc,
-                                         S, mk, cut2, minr2);
+        warp_tile<T, GRAD, CUTOFF, true, NP, kDbl>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2,
+                                                   ev2, jc, S, mkp, cut2, minr2);
       else
-        warp_tile<T, GRAD, CUTOFF, false>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jc,
-                                          S, mk, cut2, minr2);
+        warp_tile<T, GRAD, CUTOFF, false, NP, kDbl>(J, L, lane, xi, yi, zi, qi, ai, bi, F, ec2,
+                                                    ev2, jc, S, mkp, cut2, minr2);
       Ec += double(P::lo(ec2)) + double(P::hi(ec2));
       Ev += double(P::lo(ev2)) + double(P::hi(ev2));
       ec2 = P::zero();
       ev2 = P::zero();
     }
     if (GRAD) {
-      // cross-warp reduction of the i-rows of this sub-block (fixed order)
-      T* my = ired + warp * 3 * kIB;
 #pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
+      for (int pp = 0; pp < NP; ++pp) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          my[c * kIB + lane + 64 * pp] = P::lo(F[pp][c]);
-          my[c * kIB + lane + 64 * pp + 32] = P::hi(F[pp][c]);
+          my[c * kIB + lane + 64 * (p0 + pp)] = P::lo(F[pp][c]);
+          my[c * kIB + lane + 64 * (p0 + pp) + 32] = P::hi(F[pp][c]);
         }
       }
+    }
+    }  // p0
+    if (GRAD) {
+      // cross-warp reduction of the i-rows of this sub-block (fixed order)
       __syncthreads();
       for (int x = tid; x < 3 * kIB; x += kThreads) {
         const int c = x / kIB, a = x - c * kIB;
@@ -593,22 +620,7 @@ nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     if (GRAD) jacc[warp][lane] = jacc[warp][32 + lane] = jacc[warp][64 + lane] = T(0);
   }
   __syncwarp();
-  V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
-#pragma unroll
-  for (int pp = 0; pp < 2; ++pp) {
-    const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
-    xi[pp] = ld_pair<T>(ipos, r);
-    yi[pp] = ld_pair<T>(ipos, half + r);
-    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
-    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
-    ai[pp] = ld_pair<T>(ilj, r);
-    bi[pp] = ld_pair<T>(ilj, half + r);
-  }
-  V F[2][3];
-#pragma unroll
-  for (int pp = 0; pp < 2; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
-  V ec2 = P::zero(), ev2 = P::zero();
-  T minr2 = T(1e30);
+  constexpr int NP = PairsPerPass<T>::value;
   bool masked = jb < ib + kIB;  // straddles the diagonal
   uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
   if (masked) {
@@ -627,14 +639,46 @@ nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     }
   }
   const T cut2 = T(plan.cut2);
-  if (masked)
-    warp_tile<T, GRAD, CUTOFF, true>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F, ec2,
-                                     ev2, jacc[warp], kJB, mk, cut2, minr2);
-  else
-    warp_tile<T, GRAD, CUTOFF, false>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F, ec2,
-                                      ev2, jacc[warp], kJB, mk, cut2, minr2);
-  double ec = double(P::lo(ec2)) + double(P::hi(ec2));
-  double ev = double(P::lo(ev2)) + double(P::hi(ev2));
+  T minr2 = T(1e30);
+  double ec = 0.0, ev = 0.0;
+  for (int p0 = 0; p0 < 2; p0 += NP) {
+    V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const int64_t r = (int64_t)kk * 64 + (p0 + pp) * 32 + lane;
+      xi[pp] = ld_pair<T>(ipos, r);
+      yi[pp] = ld_pair<T>(ipos, half + r);
+      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+      ai[pp] = ld_pair<T>(ilj, r);
+      bi[pp] = ld_pair<T>(ilj, half + r);
+    }
+    V F[NP][3];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
+    V ec2 = P::zero(), ev2 = P::zero();
+    uint32_t mkp[2 * NP];
+#pragma unroll
+    for (int q = 0; q < 2 * NP; ++q) mkp[q] = mk[2 * p0 + q];
+    if (masked)
+      warp_tile<T, GRAD, CUTOFF, true, NP>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F,
+                                           ec2, ev2, jacc[warp], kJB, mkp, cut2, minr2);
+    else
+      warp_tile<T, GRAD, CUTOFF, false, NP>(sj[warp], sl[warp], lane, xi, yi, zi, qi, ai, bi, F,
+                                            ec2, ev2, jacc[warp], kJB, mkp, cut2, minr2);
+    ec += double(P::lo(ec2)) + double(P::hi(ec2));
+    ev += double(P::lo(ev2)) + double(P::hi(ev2));
+    if (GRAD) {
+      T* ip = ipart + (size_t)t * 3 * kIB;
+#pragma unroll
+      for (int pp = 0; pp < NP; ++pp)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {  // F = -gradient
+          ip[c * kIB + lane + 64 * (p0 + pp)] = -P::lo(F[pp][c]);
+          ip[c * kIB + lane + 64 * (p0 + pp) + 32] = -P::hi(F[pp][c]);
+        }
+    }
+  }
   double mr = double(minr2);
   for (int o = 16; o > 0; o >>= 1) {
     ec += __shfl_xor_sync(0xffffffffu, ec, o);
@@ -648,14 +692,6 @@ nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     e[2] = mr;
   }
   if (GRAD) {
-    T* ip = ipart + (size_t)t * 3 * kIB;
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {  // F = -gradient
-        ip[c * kIB + lane + 64 * pp] = -P::lo(F[pp][c]);
-        ip[c * kIB + lane + 64 * pp + 32] = -P::hi(F[pp][c]);
-      }
     __syncwarp();
     T* jp = jpart + (size_t)t * 3 * kJB;
     for (int c = 0; c < 3; ++c) jp[c * kJB + lane] = jacc[warp][c * kJB + lane];
@@ -678,7 +714,7 @@ static cudaError_t launch_tiles_t(const NbPlanDev& plan, const void* pos, const 
 
 size_t nb_smem_bytes(int S, bool fp64, bool grad) {
   const size_t t = fp64 ? 8 : 4;
-  size_t b = (size_t)2 * S * (4 * t + 2 * t);
+  size_t b = (size_t)(fp64 ? 1 : 2) * S * (4 * t + 2 * t);  // j-block copies, see nb_units_kernel
   if (grad) b += (size_t)3 * S * t + (size_t)kWarps * 3 * kIB * t;
   return b;
 }

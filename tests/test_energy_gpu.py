@@ -388,3 +388,28 @@ def test_tile_sweep_matches_oracle_and_unit_sweep(n, cutoff, monkeypatch):
         eng.close()
     np.testing.assert_allclose(e_sum, out[("1", N.FFM_F64)][0], rtol=1e-12, atol=1e-9)
     assert np.max(np.abs(g_sum - out[("1", N.FFM_F64)][1])) <= 1e-11 * gmax
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 32, 33, 128, 129])
+def test_tiny_and_block_edge_systems(n):
+    """Atom counts at and around the 32-atom block and 128-row sub-block
+    edges (and a single atom): energies and gradients equal the oracle's."""
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.model import MolecularSystem
+
+    rng = np.random.default_rng(n)
+    side = int(np.ceil(max(1, n) ** (1 / 3)))
+    grid = np.stack(np.meshgrid(*[np.arange(side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    coords = 3.2 * grid[rng.permutation(len(grid))[:n]] + rng.uniform(-0.4, 0.4, size=(n, 3))
+    s = MolecularSystem.from_arrays(rng.uniform(-0.5, 0.5, n), rng.uniform(2.5, 3.5, n),
+                                    rng.uniform(0.05, 0.2, n), coords)
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=1)
+    if err is not None:
+        pytest.skip("random cloud has a coincident pair")
+    gmax = max(np.max(np.abs(g_ref)), 1e-300)
+    for dt, et, gt in ((np.float64, 1e-10, 1e-10), (np.float32, 1e-5, 1e-4)):
+        bd, g = energy_and_gradient(s, dt)
+        got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        assert np.max(np.abs(got - e_ref)) <= et * max(1.0, np.max(np.abs(e_ref)))
+        assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
