@@ -8,8 +8,8 @@ call) of a 100,000-atom synthetic protein-like system (BASELINE.json metric
 "pair-interactions/sec (energy+grad) at N=10k/100k"), FP32 pair arithmetic
 with FP64 accumulation; the FP64 mode is measured alongside.  value = pair
 interactions (N(N-1)/2 per step) per second, whole job, inputs resident in
-HBM; e2e = the same through the public host API (energy_and_gradient on
-pinned NumPy coordinates, copies inside the timed region).
+HBM; e2e = the same through the public host API (MolecularOracle.
+value_and_gradient on a pinned NumPy vector, copies inside the timed region).
 
 N > 1 (torchrun): the pair triangle is row-sharded over the ranks
 (paper_1810_03358_b200.parallel), gradients/energies all-reduced over
@@ -39,7 +39,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "pair-interactions/sec (energy+grad)"
 NATOMS = 100_000
 FLOP_PER_PAIR = 38  # 27 FP32 ops (10 of them FMA -> +10) + 1 rsqrt, DESIGN.md
-FMA_SLOTS_PER_PAIR = 26  # FP32 lane-ops on the FMA pipe per pair (SASS: 11.5 FFMA2 + 10 FMUL2 + 4.5 FADD2 per 2 pairs)
+FMA_SLOTS_PER_PAIR = 24  # FP32 lane-ops on the FMA pipe per pair (SASS: 2 x 12 packed FFMA2/FMUL2/FADD2 per 2 pairs; r^-2 on MUFU)
 
 
 def parse():
@@ -77,60 +77,71 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: an NVML polling thread (2 ms period; the timed region is only
+    ~50 ms, too short for nvidia-smi's 100 ms loop).  Falls back to one
+    nvidia-smi query when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.002):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._nv = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml as nv
+
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self._t = threading.Thread(target=self._poll, daemon=True)
+            self._t.start()
         except Exception:
-            self.proc = None
+            self._nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _poll(self):
+        nv = self._nv
+        masks = [(name, getattr(nv, attr, 0)) for name, attr in self.REASONS]
+        while not self._stop.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self.reasons.update(name for name, m in masks if m and (r & m))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join(1.0)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() in ("active", "1"):
-                    reasons.add(nm)
-        if not sm:
+        if not self.sm:
+            return self._smi_once()
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml 2 ms"}
+
+    def _smi_once(self):
+        try:
+            out = subprocess.run(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm",
+                 "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10)
+            sm, mx = (float(x) for x in out.stdout.strip().split(","))
+            return {"sm_mhz": sm, "sm_max_mhz": mx, "reasons": ["unsampled"], "samples": 1,
+                    "source": "nvidia-smi after the timed region"}
+        except Exception:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
 
 
 # ------------------------------------------------------------- reference arm
@@ -235,7 +246,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def time_device(prec, steps, warmup):
+    def time_device(prec, steps, warmup, clk=None):
         for k in range(warmup):
             eng.eval(steps_coords[k % 4], prec, grad=grad, energies=en, status=st)
         barrier()
@@ -243,6 +254,8 @@ def main():
               for _ in range(steps)]
         nb_ms = []
         l0 = lib.ffm_launch_count()
+        if clk is not None:
+            clk.__enter__()  # sample clocks during the timed steps only
         for k in range(steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             ev[k][0].record()
@@ -253,6 +266,8 @@ def main():
             N.check(lib.ffm_system_nb_ms(handle, ms.ctypes.data), "nb_ms")
             nb_ms.append(float(ms[0]))
         barrier()
+        if clk is not None:
+            clk.__exit__(None, None, None)
         launches = lib.ffm_launch_count() - l0
         step_ms = [a.elapsed_time(b) for a, b in ev]
         tot = float(np.sum(step_ms))
@@ -265,29 +280,33 @@ def main():
         assert int(st[0]) == -1, "coincident atoms in the benchmark system"
         return tot / steps, nbm, launches
 
-    with ClockSampler(local) as clk:
-        ms32, nb32, launches = time_device(N.FFM_F32, args.steps, args.warmup)
+    clk = ClockSampler(local)
+    ms32, nb32, launches = time_device(N.FFM_F32, args.steps, args.warmup, clk)
     clocks = clk.summary()
     ms64, nb64, _ = time_device(N.FFM_F64, max(3, args.steps // 2), 2)
     value = pairs / (ms32 * 1e-3)
 
-    # ---- e2e through the public API, host buffers (pinned), FP32 mode
-    pinned = torch.empty((n, 3), dtype=torch.float64).pin_memory()
+    # ---- e2e through the public API, host buffers (pinned), FP32 mode: the
+    # objective oracle every minimiser calls (value_and_gradient on a NumPy
+    # vector -> (float, NumPy float64 gradient)), copies inside the timed region
+    pinned = torch.empty(3 * n, dtype=torch.float64).pin_memory()
     if sharded:
         from paper_1810_03358_b200.parallel import ShardedMolecularOracle
 
         orc = ShardedMolecularOracle(s, np.float32, device=local)
+    else:
+        from paper_1810_03358_b200.oracle import MolecularOracle
+
+        orc = MolecularOracle(s, np.float32, device=local)
     e2e_times = []
     for k in range(args.warmup + args.steps):
-        pinned.numpy()[:] = steps_coords[k % 4].cpu().numpy()
+        pinned.numpy()[:] = steps_coords[k % 4].cpu().numpy().reshape(-1)
         host = pinned.numpy()
         barrier()
         t0 = time.perf_counter()
-        if sharded:
-            f, g = orc.value_and_gradient(host.reshape(-1))
-        else:
-            bd, g = energy_and_gradient(s.with_coords(host), np.float32)
+        f, g = orc.value_and_gradient(host)
         t1 = time.perf_counter()
+        assert isinstance(g, np.ndarray) and g.shape == (3 * n,)
         if k >= args.warmup:
             e2e_times.append(t1 - t0)
     e2e_s = float(np.mean(e2e_times))
@@ -317,8 +336,8 @@ def main():
         "value_f64": pairs / (ms64 * 1e-3), "ms_per_step_f64": ms64,
         "e2e": {"value": pairs / e2e_s, "unit": "pairs/s", "h2d_bytes_per_step": n * 3 * 8,
                 "d2h_bytes_per_step": n * 3 * 8 + 5 * 8 + 8 * 8,
-                "api": "paper_1810_03358_b200.energy.energy_and_gradient(system, np.float32)"
-                       if not sharded else "parallel.ShardedMolecularOracle.value_and_gradient"},
+                "api": "oracle.MolecularOracle(system, np.float32).value_and_gradient(x)"
+                       if not sharded else "parallel.ShardedMolecularOracle.value_and_gradient(x)"},
         "roofline": {"bound": "fp32-fma-pipe", "kernel": "nb_units_kernel<float,GRAD>",
                      "achieved": achieved / 1e12, "peak": flop_peak / 1e12, "unit": "TFLOP/s",
                      "frac": achieved / flop_peak, "traffic": nb_traffic(n),

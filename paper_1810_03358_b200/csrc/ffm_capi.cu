@@ -503,7 +503,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   if (cudaMalloc(&s->d_ilj32, (size_t)p.np * 2 * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&s->d_ilj64, (size_t)p.np * 2 * sizeof(double)) != cudaSuccess)
     FFM_TRY(fail(FFM_ENOMEM, "cudaMalloc failed for LJ records"));
-  if (launch_ilj(p.np, false, s->d_lj32, s->d_ilj32, 0) != cudaSuccess ||
+  if (launch_ilj(p.np, false, s->d_lj64, s->d_ilj32, 0) != cudaSuccess ||
       launch_ilj(p.np, true, s->d_lj64, s->d_ilj64, 0) != cudaSuccess ||
       cudaDeviceSynchronize() != cudaSuccess)
     FFM_TRY(fail(FFM_ECUDA, "building the LJ pair records failed"));

@@ -17,6 +17,14 @@ constexpr double kCoulomb = 1389.38757;
 constexpr double kRmin = 1e-12;
 constexpr double kDegenerateEps = 1e-12;
 
+// FP32 i-side LJ records (ilj) carry a factor 6: the FP32 pair kernel then
+// forms 6A/r^6 and 6B directly, so the gradient needs no separate scaling
+// multiply (12 A/r^12 - 6 B/r^6 = (6A/r^6 + 6(A/r^6 - B))/r^6), and the vdW
+// energy sum is divided by 6 once per super-unit.  FP64 keeps scale 1 (its
+// register-bound schedule measured faster with the explicit multiply).
+template <typename T> struct LjIScale { static constexpr double value = 6.0; };
+template <> struct LjIScale<double> { static constexpr double value = 1.0; };
+
 // Pair-kernel tiling:
 //   a warp tile is 128 i-atoms (4 per lane, two packed pairs) x 32 j-atoms;
 //   a CTA is 8 warps and owns one super-unit of S x S atoms.
@@ -72,6 +80,15 @@ template <> struct Pk<float> {
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(b));
     return make(ra, rb);
   }
+  // r^-2: MUFU.RCP per lane (the XU pipe has slack; the FMA pipe is the bound)
+  static __device__ __forceinline__ V rcp_or_sq(V r2, V /*ri*/) {
+    float a, b;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r2));
+    float ra, rb;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(a));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rb) : "f"(b));
+    return make(ra, rb);
+  }
   static __device__ __forceinline__ V zero() { return 0ull; }
 };
 
@@ -99,6 +116,8 @@ template <> struct Pk<double> {
     return ::fma(0.5 * y, e, y);
   }
   static __device__ __forceinline__ V rsqrt(V v) { return {rsqrt1(v.x), rsqrt1(v.y)}; }
+  // FP64 keeps r^-2 = (r^-1)^2 (no full-precision MUFU reciprocal)
+  static __device__ __forceinline__ V rcp_or_sq(V /*r2*/, V ri) { return mul(ri, ri); }
   static __device__ __forceinline__ void fma_pair(V g, V d, V& a, V& b) {
     a = fma(g, d, a);
     b = fma(g, d, b);

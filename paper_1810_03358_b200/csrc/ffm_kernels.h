@@ -33,7 +33,8 @@ cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipo
                        cudaStream_t st);
 
 // LJ (a, b) records -> i-side pair layout (once per system)
-cudaError_t launch_ilj(int np, bool fp64, const void* lj, void* ilj, cudaStream_t st);
+// ilj from the FP64 (a, b) records, scaled by LjIScale<T>
+cudaError_t launch_ilj(int np, bool fp64, const void* lj64, void* ilj, cudaStream_t st);
 
 // bonded + scaled-pair terms in FP64; writes per-block energy partials
 // term_part[batch][term_blocks(tp)][5] and slot forces

@@ -33,6 +33,9 @@ namespace ffm {
 #endif
 constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
 constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/SM)
+#ifndef FFM_RCP
+#define FFM_RCP 1  // FP32 r^-2 from MUFU.RCP instead of an FMA-pipe multiply
+#endif
 
 template <typename T>
 __device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
@@ -196,16 +199,9 @@ __device__ __forceinline__ void warp_tile(
     const int jt = DOUBLED ? t : ((lane + t) & 31);
     const auto pj = J[jt];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
     const auto lj = L[jt];  // (a, -b)
-#ifndef FFM_SCHED
-#define FFM_SCHED 1
-#endif
-#ifndef FFM_VFMA
-#define FFM_VFMA 0
-#endif
-#if FFM_SCHED == 1
-    // phase-separated: both pairs' geometry first, the four MUFU.RSQ issued
-    // back to back, coefficient products while they are in flight
-    V dx[NP], dy[NP], dz[NP], r2[NP], A[NP], nB[NP], Q[NP], ri[NP];
+    // phase-separated: both pairs' geometry first, the MUFU ops issued back
+    // to back, coefficient products while they are in flight
+    V dx[NP], dy[NP], dz[NP], r2[NP], A[NP], nB[NP], Q[NP], ri[NP], i2[NP];
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) {
       dx[pp] = P::add(xi[pp], P::bc(pj.x));
@@ -217,8 +213,8 @@ __device__ __forceinline__ void warp_tile(
     }
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) {
-      A[pp] = P::mul(ai[pp], P::bc(lj.x));
-      nB[pp] = P::mul(bi[pp], P::bc(lj.y));
+      A[pp] = P::mul(ai[pp], P::bc(lj.x));   // s A  (the i side carries s = LjIScale<T>)
+      nB[pp] = P::mul(bi[pp], P::bc(lj.y));  // -s B
       Q[pp] = P::mul(qi[pp], P::bc(pj.w));
       if (MASKED) {
         const int jj = (lane + t) & 31;
@@ -238,30 +234,35 @@ __device__ __forceinline__ void warp_tile(
         Q[pp] = P::make(c0 ? P::lo(Q[pp]) : T(0), c1 ? P::hi(Q[pp]) : T(0));
       }
       ri[pp] = P::rsqrt(r2[pp]);
+      // FP32: r^-2 from MUFU.RCP (the FMA pipe is the bound, XU has slack)
+      // (FP64 squares r^-1 in the consumer loop below)
+      constexpr bool f32 = sizeof(T) == 4;
+      if (f32 && (FFM_RCP == 1 || (FFM_RCP == 2 && pp == 0))) i2[pp] = P::rcp_or_sq(r2[pp], ri[pp]);
     }
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) {
-      const V i2 = P::mul(ri[pp], ri[pp]);
-      const V i4 = P::mul(i2, i2);
-      const V i6 = P::mul(i4, i2);
-#if FFM_VFMA
-      const V v = P::fma(A[pp], i6, nB[pp]);  // A / r^6 - B
-#else
-      const V u = P::mul(A[pp], i6);
-      const V v = P::add(u, nB[pp]);
-#endif
-      ev2 = P::fma(v, i6, ev2);
-      const V ecp = P::mul(Q[pp], ri[pp]);
+      constexpr bool f32 = sizeof(T) == 4;
+      if (!f32 || FFM_RCP == 0 || (FFM_RCP == 2 && pp != 0)) i2[pp] = P::mul(ri[pp], ri[pp]);
+      if (f32 && FFM_RCP == 3) i2[pp] = P::rcp_or_sq(r2[pp], ri[pp]);
+      const V i4 = P::mul(i2[pp], i2[pp]);
+      const V i6 = P::mul(i4, i2[pp]);
+      const V u = P::mul(A[pp], i6);       // s A / r^6
+      const V v = P::add(u, nB[pp]);       // s (A / r^6 - B)
+      ev2 = P::fma(v, i6, ev2);            // s (A / r^12 - B / r^6)
+      const V ecp = P::mul(Q[pp], ri[pp]); // C q_i q_j / r
       ec2 = P::add(ec2, ecp);
       if (GRAD) {
-#if FFM_VFMA
-        const V pw = P::fma(A[pp], i6, v);    // 2 A / r^6 - B
-#else
-        const V pw = P::add(u, v);
-#endif
-        const V k = P::mul(pw, i6);
-        const V w = P::fma(k, P::bc(T(6)), ecp);
-        const V g = P::mul(w, i2);
+        // g = -(dE/dr)/r = (C q q / r + 12 A / r^12 - 6 B / r^6) / r^2
+        const V pw = P::add(u, v);         // s (2 A / r^6 - B)
+        V w;
+        if constexpr (sizeof(T) == 4) {
+          w = P::fma(pw, i6, ecp);         // s = 6: no separate scaling multiply
+        } else {                           // FP64 (s = 1): measured faster this way
+          const V k = P::mul(pw, i6);
+          w = P::fma(k, P::bc(T(6)), ecp);
+        }
+        const V g = P::mul(w, i2[pp]);
+        // F_i = -grad_i = g (x_i - x_j);  grad_j += g (x_i - x_j)
 #if defined(FFM_PAIRFMA) && FFM_PAIRFMA
         P::fma_pair(g, dx[pp], F[pp][0], gx);
         P::fma_pair(g, dy[pp], F[pp][1], gy);
@@ -276,63 +277,6 @@ __device__ __forceinline__ void warp_tile(
 #endif
       }
     }
-#else
-#pragma unroll
-    for (int pp = 0; pp < NP; ++pp) {
-      V dx = P::add(xi[pp], P::bc(pj.x));
-      V dy = P::add(yi[pp], P::bc(pj.y));
-      V dz = P::add(zi[pp], P::bc(pj.z));
-      V r2 = P::mul(dx, dx);
-      r2 = P::fma(dy, dy, r2);
-      r2 = P::fma(dz, dz, r2);
-      V A = P::mul(ai[pp], P::bc(lj.x));
-      V nB = P::mul(bi[pp], P::bc(lj.y));
-      V Q = P::mul(qi[pp], P::bc(pj.w));
-      if (MASKED) {
-        const int jj = (lane + t) & 31;
-        const bool a0 = (mk[2 * pp] >> jj) & 1u;
-        const bool a1 = (mk[2 * pp + 1] >> jj) & 1u;
-        r2 = P::make(a0 ? P::lo(r2) : T(1), a1 ? P::hi(r2) : T(1));
-        A = P::make(a0 ? P::lo(A) : T(0), a1 ? P::hi(A) : T(0));
-        nB = P::make(a0 ? P::lo(nB) : T(0), a1 ? P::hi(nB) : T(0));
-        Q = P::make(a0 ? P::lo(Q) : T(0), a1 ? P::hi(Q) : T(0));
-      }
-      if constexpr (sizeof(T) == 8) {
-        // FP64 mode tracks the closest pair exactly (coincidence check of
-        // ffmin/kernels.py:330-332 happens before the cutoff test)
-        minr2 = fmin(minr2, fmin(P::lo(r2), P::hi(r2)));
-      }
-      if (CUTOFF) {
-        const bool c0 = P::lo(r2) <= cut2;
-        const bool c1 = P::hi(r2) <= cut2;
-        A = P::make(c0 ? P::lo(A) : T(0), c1 ? P::hi(A) : T(0));
-        nB = P::make(c0 ? P::lo(nB) : T(0), c1 ? P::hi(nB) : T(0));
-        Q = P::make(c0 ? P::lo(Q) : T(0), c1 ? P::hi(Q) : T(0));
-      }
-      const V ri = P::rsqrt(r2);
-      const V i2 = P::mul(ri, ri);
-      const V i4 = P::mul(i2, i2);
-      const V i6 = P::mul(i4, i2);
-      const V v = P::fma(A, i6, nB); // A / r^6 - B
-      ev2 = P::fma(v, i6, ev2);      // A / r^12 - B / r^6
-      const V ecp = P::mul(Q, ri);   // C q_i q_j / r
-      ec2 = P::add(ec2, ecp);
-      if (GRAD) {
-        // g = -(dE/dr)/r = (C q q / r + 12 A / r^12 - 6 B / r^6) / r^2
-        const V pw = P::fma(A, i6, v); // 2 A / r^6 - B
-        const V k = P::mul(pw, i6);
-        const V w = P::fma(k, P::bc(T(6)), ecp);
-        const V g = P::mul(w, i2);
-        // F_i = -grad_i = g (x_i - x_j);  grad_j += g (x_i - x_j)
-        F[pp][0] = P::fma(g, dx, F[pp][0]);
-        F[pp][1] = P::fma(g, dy, F[pp][1]);
-        F[pp][2] = P::fma(g, dz, F[pp][2]);
-        gx = P::fma(g, dx, gx);
-        gy = P::fma(g, dy, gy);
-        gz = P::fma(g, dz, gz);
-      }
-    }
-#endif
     if (GRAD) {  // the j column moves one lane down with its atom
       gx = shfl_rot<T>(gx, src);
       gy = shfl_rot<T>(gy, src);
@@ -563,7 +507,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     for (int x = tid; x < 3 * S; x += kThreads) jpart[(size_t)u * 3 * S + x] = jacc[x];
   }
   const double ec = block_sum<T>(Ec, red);
-  const double ev = block_sum<T>(Ev, red);
+  const double ev = block_sum<T>(Ev, red) / LjIScale<T>::value;
   const double mr = block_min(double(minr2), red);
   if (tid == 0) {
     double* e = epart + ((size_t)bidx * plan.nunits + u) * 3;
@@ -688,7 +632,7 @@ nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   if (lane == 0) {
     double* e = epart + ((size_t)bidx * plan.ntiles + t) * 3;
     e[0] = ec;
-    e[1] = ev;
+    e[1] = ev / LjIScale<T>::value;
     e[2] = mr;
   }
   if (GRAD) {

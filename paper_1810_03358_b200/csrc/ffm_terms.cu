@@ -104,24 +104,23 @@ cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipo
   return cudaGetLastError();
 }
 
-// LJ (a, b) in the i-side pair layout, built once per system
+// LJ (a, b) in the i-side pair layout, built once per system from the FP64
+// records and scaled by LjIScale<T> (see ffm_common.cuh)
 template <typename T>
-__global__ void ilj_kernel(int np, const typename Vec2T<T>::type* __restrict__ lj,
-                           T* __restrict__ ilj) {
+__global__ void ilj_kernel(int np, const double2* __restrict__ lj64, T* __restrict__ ilj) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= np) return;
-  ilj[ipos_index(a, np, 0)] = lj[a].x;
-  ilj[ipos_index(a, np, 1)] = lj[a].y;
+  ilj[ipos_index(a, np, 0)] = T(LjIScale<T>::value * lj64[a].x);
+  ilj[ipos_index(a, np, 1)] = T(LjIScale<T>::value * lj64[a].y);
 }
 
-cudaError_t launch_ilj(int np, bool fp64, const void* lj, void* ilj, cudaStream_t st) {
+cudaError_t launch_ilj(int np, bool fp64, const void* lj64, void* ilj, cudaStream_t st) {
   const int blocks = (np + 255) / 256;
+  const double2* src = static_cast<const double2*>(lj64);
   if (fp64)
-    count_launch(), ilj_kernel<double><<<blocks, 256, 0, st>>>(np, static_cast<const double2*>(lj),
-                                               static_cast<double*>(ilj));
+    count_launch(), ilj_kernel<double><<<blocks, 256, 0, st>>>(np, src, static_cast<double*>(ilj));
   else
-    count_launch(), ilj_kernel<float><<<blocks, 256, 0, st>>>(np, static_cast<const float2*>(lj),
-                                              static_cast<float*>(ilj));
+    count_launch(), ilj_kernel<float><<<blocks, 256, 0, st>>>(np, src, static_cast<float*>(ilj));
   return cudaGetLastError();
 }
 
