@@ -48,6 +48,8 @@ extern "C" {
 #define FFM_TIME_NB 16  /* record CUDA events around the pair sweep          */
 #define FFM_NO_GRAPH 32 /* issue the kernels directly instead of replaying a
                          * captured CUDA graph of the same call              */
+#define FFM_NO_FUSE 64  /* small systems: run the kernel chain instead of the
+                         * one-launch fused evaluation (same bits; tests)    */
 
 /* status words (int64[8] per evaluation) */
 #define FFM_ST_NB_BAD_I 0   /* first coincident nonbonded pair, -1 clean */
@@ -100,6 +102,12 @@ int ffm_system_nb_ms(ffm_system_t* sys, float* ms_h);
 
 /* Number of kernels this library has launched in the process. */
 long long ffm_launch_count(void);
+
+/* Tuning aid: the fused small-system evaluation (FFM_NO_FUSE clears it)
+ * writes 6 globaltimer stamps per CTA into clock_d ([grid][6] uint64, or
+ * NULL to stop) at its phase boundaries; grids_h[4] receives the
+ * cooperative grid sizes [precision][grad] chosen so far (0 = not yet). */
+int ffm_debug_phase_clock(ffm_system_t* sys, void* clock_d, int* grids_h);
 
 /* info[0..7] = n, padded n, super-unit S, blocks, units, special tiles,
  * scaled pairs, device */

@@ -18,7 +18,8 @@ CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "libffmin_b200.so"
 INCLUDE = PKG.parent / "include"
-SOURCES = ("ffm_pairs.cu", "ffm_terms.cu", "ffm_vec.cu", "ffm_minimize.cu", "ffm_capi.cu")
+SOURCES = ("ffm_pairs.cu", "ffm_terms.cu", "ffm_small.cu", "ffm_vec.cu", "ffm_minimize.cu",
+           "ffm_capi.cu")
 NVCC_FLAGS = (
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
@@ -27,7 +28,8 @@ NVCC_FLAGS = (
 # per-file extras: the bonded terms are evaluated without FMA contraction so
 # that degeneracy thresholds (ffmin/kernels.py:130-140) see the same roundoff
 # as the reference's CPU arithmetic
-EXTRA = {"ffm_terms.cu": ("-fmad=false",), "ffm_minimize.cu": ("-fmad=false",)}
+EXTRA = {"ffm_terms.cu": ("-fmad=false",), "ffm_small.cu": ("-fmad=false",),
+         "ffm_minimize.cu": ("-fmad=false",)}
 
 
 def nvcc_path() -> str:

@@ -27,6 +27,7 @@ FFM_NO_NB = 4
 FFM_NO_TERMS = 8
 FFM_TIME_NB = 16
 FFM_NO_GRAPH = 32
+FFM_NO_FUSE = 64
 FFM_NTERMS = 5
 FFM_STATUS_WORDS = 8
 ST_NB_BAD_I, ST_NB_BAD_J, ST_BOND, ST_ANGLE, ST_DIHEDRAL = 0, 1, 2, 3, 4
@@ -47,6 +48,7 @@ SIGNATURES = {
     "ffm_system_info": (_I, [_P, _P]),
     "ffm_system_nb_ms": (_I, [_P, _P]),
     "ffm_launch_count": (C.c_longlong, []),
+    "ffm_debug_phase_clock": (_I, [_P, _P, _P]),
     "ffm_eval": (_I, [_P, _I, _I, _P, _P, _P, _P, _P]),
     "ffm_eval_host": (_I, [_P, _I, _I, _P, _P, _P, _P]),
     "ffm_eval_batch": (_I, [_P, _I, _I64, _P, _P, _P, _P]),

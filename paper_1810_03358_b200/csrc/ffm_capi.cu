@@ -108,6 +108,9 @@ struct ffm_system {
   int* d_aterm_idx = nullptr;
   // row sharding (ffm_system_set_shard): units u with u % nranks == rank
   int rank = 0, nranks = 1;
+  // fused small-system evaluation: cooperative grid per [precision][grad], 0 = not sized yet
+  int small_grid[2][2] = {{0, 0}, {0, 0}};
+  unsigned long long* phase_clock = nullptr;  // ffm_debug_phase_clock (tuning aid)
   int* d_unit_list = nullptr;
   // small-system tile mode (NbPlanDev::ntiles > 0)
   int2* d_tiles = nullptr;
@@ -697,6 +700,14 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
   return FFM_OK;
 }
 
+int ffm_debug_phase_clock(ffm_system_t* s, void* clock_d, int* grids) {
+  if (!s || !grids) return fail(FFM_EINVAL, "NULL argument");
+  s->phase_clock = static_cast<unsigned long long*>(clock_d);
+  for (int p = 0; p < 2; ++p)
+    for (int g = 0; g < 2; ++g) grids[2 * p + g] = s->small_grid[p][g];
+  return FFM_OK;
+}
+
 int ffm_system_nb_ms(ffm_system_t* s, float* ms) {
   if (!s || !ms) return fail(FFM_EINVAL, "NULL argument");
   if (!s->timed) return fail(FFM_EINVAL, "last evaluation was not timed (FFM_TIME_NB)");
@@ -733,9 +744,46 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
   TermPlanDev tp = s->tp;  // the term types this call evaluates
   if (!do_terms || s->rank != 0) tp.nbond = tp.nangle = tp.ndih = 0;  // O(N) terms: rank 0
   if (!do_nb || s->rank != 0) tp.nscaled = 0;
+  const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
+  // small system evaluated whole: one cooperative launch (ffm_small.cu)
+  if (s->plan.ntiles > 0 && s->plan.n > 0 && s->nranks == 1 && do_nb && do_terms && !time_nb &&
+      !(flags & FFM_NO_FUSE)) {
+    int& grid = s->small_grid[precision][grad ? 1 : 0];
+    SmallEvalArgs a;
+    a.plan = s->plan;
+    a.tp = tp;
+    a.nterm_blocks = term_blocks(tp);
+    a.coords = coords_d;
+    a.qt = s->d_qt;
+    a.pos = w.pos;
+    a.ipos = w.ipos;
+    a.lj = lj;
+    a.ilj = ilj;
+    a.ipart = w.ipart;
+    a.jpart = w.jpart;
+    a.epart = w.epart;
+    a.term_part = w.term_e;
+    a.term_f = w.term_f;
+    a.trow_ptr = s->d_trow_ptr;
+    a.tcol_ptr = s->d_tcol_ptr;
+    a.tcol_idx = s->d_tcol_idx;
+    a.slot_ptr = s->d_slot_ptr;
+    a.slot_idx = s->d_slot_idx;
+    a.sp_ptr = s->d_sp_ptr;
+    a.sp_j = s->d_sp_j;
+    a.sp_s = s->d_sp_s;
+    a.grad = grad_d;
+    a.energies = energies_d;
+    a.status = status_d;
+    a.phase_clock = s->phase_clock;
+    if (grid == 0) grid = small_eval_grid(a, f64, grad, s->device);
+    if (grid > 0) {
+      FFM_CUDA(launch_small_eval(a, f64, grad, grid, st));
+      return FFM_OK;
+    }
+  }
   FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
                        status_d, st));
-  const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
   if (do_nb && s->plan.has_cutoff)
     FFM_CUDA(launch_bbox(s->plan.n, s->plan.np, 1, f64, w.pos, w.bbox, st));

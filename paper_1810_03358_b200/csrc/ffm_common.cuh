@@ -97,23 +97,29 @@ struct D2 {
 };
 
 template <> struct Pk<double> {
+  // explicitly rounded operations: no contraction under any -fmad setting,
+  // so every translation unit evaluates a pair to the same bits
   using V = D2;
   static __device__ __forceinline__ V make(double a, double b) { return {a, b}; }
   static __device__ __forceinline__ V bc(double a) { return {a, a}; }
   static __device__ __forceinline__ double lo(V v) { return v.x; }
   static __device__ __forceinline__ double hi(V v) { return v.y; }
-  static __device__ __forceinline__ V add(V a, V b) { return {a.x + b.x, a.y + b.y}; }
-  static __device__ __forceinline__ V mul(V a, V b) { return {a.x * b.x, a.y * b.y}; }
+  static __device__ __forceinline__ V add(V a, V b) {
+    return {__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)};
+  }
+  static __device__ __forceinline__ V mul(V a, V b) {
+    return {__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)};
+  }
   static __device__ __forceinline__ V fma(V a, V b, V c) {
-    return {::fma(a.x, b.x, c.x), ::fma(a.y, b.y, c.y)};
+    return {__fma_rn(a.x, b.x, c.x), __fma_rn(a.y, b.y, c.y)};
   }
   // MUFU.RSQ64H seed + one Newton step: relative error ~1e-14
   static __device__ __forceinline__ double rsqrt1(double x) {
     double y;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double h = x * y;
-    double e = ::fma(-h, y, 1.0);
-    return ::fma(0.5 * y, e, y);
+    const double h = __dmul_rn(x, y);
+    const double e = __fma_rn(-h, y, 1.0);
+    return __fma_rn(__dmul_rn(0.5, y), e, y);
   }
   static __device__ __forceinline__ V rsqrt(V v) { return {rsqrt1(v.x), rsqrt1(v.y)}; }
   // FP64 keeps r^-2 = (r^-1)^2 (no full-precision MUFU reciprocal)

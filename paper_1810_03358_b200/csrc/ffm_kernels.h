@@ -81,6 +81,43 @@ cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const i
                             double* e0_coef, uint8_t* near_mask, int64_t* bad,
                             cudaStream_t st);
 
+// ---- fused small-system evaluation (ffm_small.cu) ----
+// One cooperative launch = pack + term blocks + pair tiles + gather +
+// reduction (+ finder when flagged) for a tile-mode system evaluated whole
+// (batch 1, unsharded, all terms), same bits as the kernel chain.
+struct SmallEvalArgs {
+  NbPlanDev plan;
+  TermPlanDev tp;
+  int nterm_blocks;
+  const double* coords;
+  const double* qt;
+  void* pos;
+  void* ipos;
+  const void* lj;
+  const void* ilj;
+  void* ipart;
+  void* jpart;
+  double* epart;
+  double* term_part;
+  double* term_f;
+  const int* trow_ptr;
+  const int* tcol_ptr;
+  const int* tcol_idx;
+  const int* slot_ptr;
+  const int* slot_idx;
+  const int* sp_ptr;
+  const int* sp_j;
+  const double* sp_s;
+  double* grad;
+  double* energies;
+  int64_t* status;
+  unsigned long long* phase_clock;  // null, or [grid][6] timestamps (tuning aid)
+};
+// grid size (co-resident CTAs, at most what the work needs); 0 on error
+int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device);
+cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int grid,
+                              cudaStream_t st);
+
 // ---- vector algebra (ffm_vec.cu) ----
 int vec_reduce_blocks();
 cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,

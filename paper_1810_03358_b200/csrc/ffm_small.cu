@@ -1,0 +1,151 @@
+// ffm_small.cu -- one-launch evaluation of a small system (tile mode).
+//
+// A system of up to a few thousand atoms costs ~2-20 us of pair work, less
+// than the launch chain around it (pack, pair tiles, bonded terms, gather,
+// reduction, finder: seven dependent kernels, ~40 us per evaluation inside
+// an L-BFGS line search).  This cooperative kernel runs the same per-item
+// bodies (ffm_device.cuh, ffm_tile.cuh) in phases separated by grid-wide
+// barriers, so it produces the same bits as the kernel chain:
+//
+//   P0  pack coordinates into the pair records, reset the status words
+//   P1  bonded / scaled-pair term blocks (CTA items) and 128 x 32 pair tiles
+//       (warp items)
+//   P2  gradient gather (thread items); energy reduction (CTA 0); every CTA
+//       decides from the same data whether a coincidence is possible
+//   P3  only then: the exact first-coincident-pair finder, and the status
+//       conventions (CTA 0)
+//
+// Compiled with -fmad=false like ffm_terms.cu (the bonded terms need it; the
+// pair tile arithmetic is explicit and flag-independent).
+#include <algorithm>
+
+#include <cooperative_groups.h>
+
+#include "ffm_device.cuh"
+#include "ffm_kernels.h"
+#include "ffm_tile.cuh"
+
+namespace ffm {
+
+namespace cg = cooperative_groups;
+
+constexpr int kSmallThreads = 128;  // = kTermThreads = kRedThreads = 4 tile warps
+static_assert(kSmallThreads == kTermThreads && kSmallThreads == kRedThreads, "block shape");
+
+template <typename T, bool GRAD, bool CUTOFF>
+__global__ void __launch_bounds__(kSmallThreads)
+small_eval_kernel(SmallEvalArgs a) {
+  using V4 = typename Vec4T<T>::type;
+  using V2 = typename Vec2T<T>::type;
+  __shared__ V4 sj[4][2 * kJB];
+  __shared__ V2 sl[4][2 * kJB];
+  __shared__ T jacc[4][3 * kJB];
+  __shared__ double sh[5][kTermThreads / 32];
+  __shared__ double red[32];
+  cg::grid_group grid = cg::this_grid();
+  const NbPlanDev& plan = a.plan;
+  const int n = plan.n, warp = threadIdx.x >> 5;
+  const int64_t gt = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
+  const int64_t gs = (int64_t)gridDim.x * kSmallThreads;
+  V4* pos = static_cast<V4*>(a.pos);
+  T* ipos = static_cast<T*>(a.ipos);
+  T* ipart = static_cast<T*>(a.ipart);
+  T* jpart = static_cast<T*>(a.jpart);
+  // optional phase clock (tools/time_small_phases.py): [CTA][6] globaltimer stamps
+  unsigned long long* clk = a.phase_clock ? a.phase_clock + 6 * blockIdx.x : nullptr;
+  auto stamp = [&](int k) {
+    if (clk && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      clk[k] = t;
+    }
+  };
+  stamp(0);
+
+  // P0
+  for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs)
+    pack_item<T>(k, n, plan.np, 1, a.coords, a.qt, pos, ipos, a.status);
+  grid.sync();
+  stamp(1);
+
+  // P1: term blocks first (block-synchronous), then the warp-independent tiles
+  for (int vb = blockIdx.x; vb < a.nterm_blocks; vb += gridDim.x)
+    term_block(a.tp, GRAD, a.coords, a.term_part, a.term_f, a.status, 0, vb, a.nterm_blocks, sh);
+  for (int slot = blockIdx.x * 4 + warp; slot < plan.nlaunch; slot += gridDim.x * 4)
+    tile_warp<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
+                               static_cast<const T*>(a.ilj), ipart, jpart, a.epart, slot, 0,
+                               sj[warp], sl[warp], jacc[warp]);
+  __syncthreads();
+  stamp(2);
+  grid.sync();
+  stamp(3);
+
+  // P2: the finder decision, made identically by every CTA: a coincident
+  // pair shows as a non-finite tile partial (FP32) or a closest-pair r^2
+  // below RMIN^2 (FP64), or was flagged by the scaled-pair terms
+  int suspect = a.status[kStNbSuspect] != 0;
+  for (int t = threadIdx.x; t < plan.ntiles && !suspect; t += kSmallThreads) {
+    const double* e = a.epart + 3 * (size_t)t;
+    if (!isfinite(e[0]) || !isfinite(e[1]) || e[2] < kRmin * kRmin) suspect = 1;
+  }
+  suspect = __syncthreads_or(suspect);
+  if (GRAD)
+    for (int64_t x = gt; x < 3 * (int64_t)n; x += gs)
+      assemble_item<T>(x, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr, a.tcol_idx,
+                       ipart, jpart, a.slot_ptr, a.slot_idx, a.term_f, a.tp.slot_sc0, true, true,
+                       true, a.grad);
+  if (blockIdx.x == 0)
+    reduce_entry(plan.ntiles, a.nterm_blocks, a.epart, a.term_part, a.energies, a.status, 0, red,
+                 false);
+  __syncthreads();
+  stamp(4);
+  if (suspect) {  // P3 (uniform across the grid)
+    grid.sync();
+    for (int64_t i = gt; i < n; i += gs)
+      finder_row<T>((int)i, n, pos, a.sp_ptr, a.sp_j, a.sp_s, a.status);
+    grid.sync();
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.status[kStNbSuspect] = 1;  // as the chain leaves it
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) finalize_entry(n, a.status);
+  stamp(5);
+}
+
+template <typename T, bool GRAD, bool CUTOFF>
+static void* small_kernel_ptr() {
+  return reinterpret_cast<void*>(&small_eval_kernel<T, GRAD, CUTOFF>);
+}
+
+static void* small_kernel(bool fp64, bool grad, bool cut) {
+  if (fp64) {
+    if (grad) return cut ? small_kernel_ptr<double, true, true>() : small_kernel_ptr<double, true, false>();
+    return cut ? small_kernel_ptr<double, false, true>() : small_kernel_ptr<double, false, false>();
+  }
+  if (grad) return cut ? small_kernel_ptr<float, true, true>() : small_kernel_ptr<float, true, false>();
+  return cut ? small_kernel_ptr<float, false, true>() : small_kernel_ptr<float, false, false>();
+}
+
+int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device) {
+  const bool cut = a.plan.has_cutoff != 0;
+  int sms = 0, per_sm = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel(fp64, grad, cut),
+                                                    kSmallThreads, 0) != cudaSuccess)
+    return 0;
+  int64_t want = 1;
+  want = std::max<int64_t>(want, (a.plan.nlaunch + 3) / 4);
+  want = std::max<int64_t>(want, a.nterm_blocks);
+  want = std::max<int64_t>(want, (3 * (int64_t)a.plan.n + kSmallThreads - 1) / kSmallThreads);
+  return (int)std::min<int64_t>(want, (int64_t)sms * per_sm);
+}
+
+cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int grid,
+                              cudaStream_t st) {
+  if (grid < 1) return cudaErrorInvalidConfiguration;
+  SmallEvalArgs args = a;
+  void* params[] = {&args};
+  count_launch();
+  return cudaLaunchCooperativeKernel(small_kernel(fp64, grad, a.plan.has_cutoff != 0),
+                                     dim3(grid), dim3(kSmallThreads), params, 0, st);
+}
+
+}  // namespace ffm

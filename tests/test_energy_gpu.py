@@ -413,3 +413,44 @@ def test_tiny_and_block_edge_systems(n):
         got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
         assert np.max(np.abs(got - e_ref)) <= et * max(1.0, np.max(np.abs(e_ref)))
         assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
+
+
+@pytest.mark.parametrize("name", ["chain10", "cloud24", "cloud24c7", "chain200", "chain12cut",
+                                  "globule1500", "coincident", "collinear", "explicit8"])
+def test_fused_small_evaluation_equals_kernel_chain(golden, name):
+    """Small (tile-mode) systems evaluate in one cooperative launch
+    (ffm_small.cu) running the same per-item bodies as the kernel chain:
+    energies, gradient and status words must be bit-identical, in both
+    precisions, with and without the gradient, error cases included."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import engine_for
+
+    s = golden_system(golden, name)
+    eng = engine_for(s.topology)
+    c = torch.from_numpy(np.ascontiguousarray(s.coords)).cuda()
+    lib = N.load()
+    for prec in (N.FFM_F64, N.FFM_F32):
+        for grad in (False, True):
+            base = N.FFM_ENERGY | (N.FFM_GRAD if grad else 0) | N.FFM_NO_GRAPH
+            en, st = eng.new_outputs()
+            for extra in (0, N.FFM_NO_FUSE):  # first call sizes the workspace
+                eng.eval(c, prec, grad=torch.empty_like(c) if grad else None, energies=en,
+                         status=st, flags=base | extra)
+            out = []
+            for extra in (0, N.FFM_NO_FUSE):
+                g = torch.full_like(c, np.nan) if grad else None
+                en, st = eng.new_outputs()
+                torch.cuda.synchronize()
+                l0 = lib.ffm_launch_count()
+                eng.eval(c, prec, grad=g, energies=en, status=st, flags=base | extra)
+                torch.cuda.synchronize()
+                out.append((lib.ffm_launch_count() - l0, en.cpu().numpy(), st.cpu().numpy(),
+                            None if g is None else g.cpu().numpy()))
+            (l_f, e_f, s_f, g_f), (l_c, e_c, s_c, g_c) = out
+            assert l_f == 1 and l_c >= 4, (l_f, l_c)
+            assert np.array_equal(e_f, e_c, equal_nan=True), (prec, grad, e_f, e_c)
+            assert np.array_equal(s_f, s_c), (prec, grad, s_f, s_c)
+            if grad:
+                assert np.array_equal(g_f, g_c, equal_nan=True)

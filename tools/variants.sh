@@ -7,9 +7,9 @@ L=paper_1810_03358_b200/_lib
 C=paper_1810_03358_b200/csrc
 mkdir -p $L/variants $L/obj
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC"
-for src in ffm_terms ffm_vec ffm_minimize ffm_capi; do
-  extra=""; { [ $src = ffm_terms ] || [ $src = ffm_minimize ]; } && extra="-fmad=false"
-  [ $L/obj/$src.o -nt $C/$src.cu ] || nvcc $F $extra -c -o $L/obj/$src.o $C/$src.cu &
+for src in ffm_terms ffm_small ffm_vec ffm_minimize ffm_capi; do
+  extra=""; { [ $src = ffm_terms ] || [ $src = ffm_small ] || [ $src = ffm_minimize ]; } && extra="-fmad=false"
+  nvcc $F $extra -c -o $L/obj/$src.o $C/$src.cu &
 done
 wait
 while [ $# -ge 2 ]; do
@@ -18,6 +18,6 @@ while [ $# -ge 2 ]; do
      | grep -A2 "Compiling entry function '_ZN3ffm15nb_units_kernelIfLb1ELb0" \
      | grep -oE "Used [0-9]+ registers|[0-9]+ bytes spill stores" | tr '\n' ' '; echo " <- $name ($flags)"
    nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $L/variants/lib_$name.so \
-     $L/obj/pairs_$name.o $L/obj/ffm_terms.o $L/obj/ffm_vec.o $L/obj/ffm_minimize.o $L/obj/ffm_capi.o) &
+     $L/obj/pairs_$name.o $L/obj/ffm_terms.o $L/obj/ffm_small.o $L/obj/ffm_vec.o $L/obj/ffm_minimize.o $L/obj/ffm_capi.o) &
 done
 wait
