@@ -134,6 +134,9 @@ struct ffm_system {
   std::vector<GraphEntry> graphs;
   long long gen = 0;
   cudaStream_t cap_stream = nullptr;
+  // the O(N) term kernel runs on a forked branch beside the pair sweep
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // FFM_TIME_NB: events around the pair sweep of the last evaluation
   cudaEvent_t ev_nb0 = nullptr, ev_nb1 = nullptr;
   bool timed = false;
@@ -160,6 +163,9 @@ void free_all(ffm_system* s) {
   for (auto& g : s->graphs) cudaGraphExecDestroy(g.exec);
   s->graphs.clear();
   if (s->cap_stream) cudaStreamDestroy(s->cap_stream);
+  if (s->side) cudaStreamDestroy(s->side);
+  if (s->ev_fork) cudaEventDestroy(s->ev_fork);
+  if (s->ev_join) cudaEventDestroy(s->ev_join);
   if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
@@ -784,6 +790,20 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
   }
   FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
                        status_d, st));
+  // fork: the term kernel (bonded terms, scaled pairs) beside the sweep; it
+  // fills the sweep's last partial wave instead of running after it
+  const bool fork = term_blocks(tp) > 0 && do_nb && s->plan.n > 0;
+  if (fork) {
+    if (!s->side) {
+      FFM_CUDA(cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking));
+      FFM_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+      FFM_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
+    }
+    FFM_CUDA(cudaEventRecord(s->ev_fork, st));
+    FFM_CUDA(cudaStreamWaitEvent(s->side, s->ev_fork, 0));
+    FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, s->side));
+    FFM_CUDA(cudaEventRecord(s->ev_join, s->side));
+  }
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb0, st));
   if (do_nb && s->plan.has_cutoff)
     FFM_CUDA(launch_bbox(s->plan.n, s->plan.np, 1, f64, w.pos, w.bbox, st));
@@ -791,7 +811,21 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
     FFM_CUDA(launch_nb(s->plan, f64, grad, w.pos, lj, w.ipos, ilj, w.bbox, w.ipart, w.jpart,
                        w.epart, 1, st));
   if (time_nb) FFM_CUDA(cudaEventRecord(s->ev_nb1, st));
-  FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
+  if (fork)
+    FFM_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+  else
+    FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
+  if (grad && s->plan.n > 0 && s->plan.ntiles == 0 && do_nb) {
+    // super-unit mode: gather + energy reduction in one launch
+    FFM_CUDA(launch_assemble_reduce(
+        s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart, w.jpart,
+        s->d_slot_ptr, s->d_slot_idx, w.term_f, s->tp.slot_sc0, do_nb,
+        do_terms && s->rank == 0, do_nb && s->rank == 0, grad_d, nb_slots(s->plan), tp,
+        w.epart, w.term_e, energies_d, status_d, st));
+    FFM_CUDA(launch_finder(s->plan.n, s->plan.np, 1, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
+                           s->d_sp_s, status_d, st));
+    return FFM_OK;
+  }
   if (grad && s->plan.n > 0)
     FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index,
                              s->plan.ntiles ? s->d_trow_ptr : nullptr, s->d_tcol_ptr,
@@ -799,7 +833,7 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
                              s->tp.slot_sc0, do_nb, do_terms && s->rank == 0,
                              do_nb && s->rank == 0, grad_d, st));
   FFM_CUDA(launch_reduce(do_nb ? nb_slots(s->plan) : 0, tp, 1, w.epart, w.term_e, energies_d,
-                         status_d, st));
+                         status_d, s->plan.n, st));
   FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
                          s->d_sp_j, s->d_sp_s, status_d, st));
   return FFM_OK;
@@ -917,7 +951,8 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   TermPlanDev tp = s->tp;
   if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
   FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
-  FFM_CUDA(launch_reduce(nb_slots(s->plan), tp, B, w.epart, w.term_e, energies_d, status_d, st));
+  FFM_CUDA(launch_reduce(nb_slots(s->plan), tp, B, w.epart, w.term_e, energies_d, status_d,
+                         s->plan.n, st));
   FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                          s->d_sp_s, status_d, st));
   return FFM_OK;

@@ -327,6 +327,16 @@ __device__ __forceinline__ void assemble_item(int64_t x, int n, int S, int nb,
   grad[3 * (size_t)a + c] = g;
 }
 
+// status sentinels -> the reference's conventions (-1 = clean)
+__device__ __forceinline__ void finalize_entry(int n, int64_t* s) {
+  if (s[kStNbKey] != kSentinel) {
+    s[kStNbBadI] = s[kStNbKey] / n;
+    s[kStNbBadJ] = s[kStNbKey] % n;
+  }
+  for (int k = kStBond; k <= kStDihedral; ++k)
+    if (s[k] == kSentinel) s[k] = -1;
+}
+
 // ---------------------------------------------------------- energy reduction
 // one block of kRedThreads per batch entry; every partial summed in a fixed
 // order (strided per thread, then a warp/block tree)
@@ -365,7 +375,7 @@ __device__ __forceinline__ void reduce_entry(int nunits, int nterm_blocks,
                                              const double* __restrict__ term_part,
                                              double* __restrict__ energies,
                                              int64_t* __restrict__ status, int b, double* sh,
-                                             bool flag_suspect = true) {
+                                             bool flag_suspect = true, int finalize_n = -1) {
   epart += (size_t)b * nunits * 3;
   term_part += (size_t)b * nterm_blocks * 5;
   double ec = 0.0, ev = 0.0, mr = DBL_MAX, es = 0.0, eb = 0.0, et = 0.0;
@@ -398,6 +408,10 @@ __device__ __forceinline__ void reduce_entry(int nunits, int nterm_blocks,
     int64_t* s = status + (size_t)b * kStWords;
     if (flag_suspect && (!isfinite(ec) || !isfinite(ev) || mr < kRmin * kRmin))
       s[kStNbSuspect] = 1;
+    // finalize_n >= 0: a clean entry (nothing for the finder, including
+    // suspects flagged by the scaled-pair terms) is finalised here, so the
+    // finder kernel exits at once and no separate finalize launch is needed
+    if (finalize_n >= 0 && s[kStNbSuspect] == 0) finalize_entry(finalize_n, s);
   }
 }
 
@@ -426,14 +440,5 @@ __device__ __forceinline__ void finder_row(int i, int n, const typename Vec4T<T>
   }
 }
 
-// status sentinels -> the reference's conventions (-1 = clean)
-__device__ __forceinline__ void finalize_entry(int n, int64_t* s) {
-  if (s[kStNbKey] != kSentinel) {
-    s[kStNbBadI] = s[kStNbKey] / n;
-    s[kStNbBadJ] = s[kStNbKey] % n;
-  }
-  for (int k = kStBond; k <= kStDihedral; ++k)
-    if (s[k] == kSentinel) s[k] = -1;
-}
 
 }  // namespace ffm

@@ -55,12 +55,23 @@ cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_ind
 
 // energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
 // coincidences for the finder
+// (clean entries are finalised here: sentinels -> -1; n = atoms)
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
-                          const double* term_part, double* energies, int64_t* status,
+                          const double* term_part, double* energies, int64_t* status, int n,
                           cudaStream_t st);
 
+// super-unit mode, batch 1: the gradient gather and the energy reduction
+// in one launch (gather split over 8 warps per 32 atoms, fixed order)
+cudaError_t launch_assemble_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
+                                   const void* ipart, const void* jpart, const int* slot_ptr,
+                                   const int* slot_idx, const double* term_f, int slot_sc0,
+                                   bool use_nb, bool use_terms, bool use_sc, double* grad,
+                                   int nslots, const TermPlanDev& tp, const double* epart,
+                                   const double* term_part, double* energies,
+                                   int64_t* status, cudaStream_t st);
+
 // exact first coincident pair (reference loop order), only when flagged;
-// then converts the status sentinels to -1.
+// the last block then converts the status sentinels to -1.
 cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
                           const int* sp_ptr, const int* sp_j, const double* sp_s,
                           int64_t* status, cudaStream_t st);

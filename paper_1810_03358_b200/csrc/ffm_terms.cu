@@ -142,21 +142,107 @@ cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_ind
   return cudaGetLastError();
 }
 
+// Super-unit mode: one block of kAsmWarps warps per 32 consecutive atoms (a
+// 32-atom group never straddles a super-block).  An atom of super-block b
+// has nb + 1 partial entries: the i-rows of units (b, b..nb-1), then the
+// j-columns of units (0..b, b); warp w sums entries w, w + kAsmWarps, ...
+// for all three components (coalesced 128-byte rows), and the kAsmWarps
+// sums plus the atom's term slots are added in a fixed order.  The grid's
+// extra last block reduces the energies (reduce_entry), so one launch does
+// what the gather and reduce kernels did; the order is fixed, so results
+// are bit-identical run to run.
+constexpr int kAsmWarps = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(kAsmWarps * 32)
+assemble_units_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
+                      const T* __restrict__ ipart, const T* __restrict__ jpart,
+                      const int* __restrict__ slot_ptr, const int* __restrict__ slot_idx,
+                      const double* __restrict__ term_f, int slot_sc0, bool use_nb,
+                      bool use_terms, bool use_sc, double* __restrict__ grad, int nslots,
+                      int nterm_blocks, const double* __restrict__ epart,
+                      const double* __restrict__ term_part, double* __restrict__ energies,
+                      int64_t* __restrict__ status) {
+  __shared__ double part[kAsmWarps][3][32];
+  const int ngroups = (n + 31) >> 5;
+  if ((int)blockIdx.x == ngroups) {
+    reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
+                 true, n);
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a0 = blockIdx.x << 5;
+  const int b = a0 / S, off = a0 - b * S + lane;  // partial rows are padded to S
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+  if (use_nb) {
+    const int ni = nb - b;
+    for (int k = warp; k <= nb; k += kAsmWarps) {
+      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
+                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
+      g0 += (double)p[off];
+      g1 += (double)p[S + off];
+      g2 += (double)p[2 * S + off];
+    }
+  }
+  part[warp][0][lane] = g0;
+  part[warp][1][lane] = g1;
+  part[warp][2][lane] = g2;
+  __syncthreads();
+  if (threadIdx.x < 96) {
+    // thread t writes grad[3 a0 + t]: coalesced
+    const int l = threadIdx.x / 3, c = threadIdx.x - 3 * l, a = a0 + l;
+    if (a < n) {
+      double g = 0.0;
+#pragma unroll
+      for (int w = 0; w < kAsmWarps; ++w) g += part[w][c][l];
+      for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
+        const int k = slot_idx[s];
+        if (k < slot_sc0 ? !use_terms : !use_sc) continue;
+        g += term_f[3 * (size_t)k + c];
+      }
+      grad[3 * (size_t)a + c] = g;
+    }
+  }
+}
+
+cudaError_t launch_assemble_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
+                                   const void* ipart, const void* jpart, const int* slot_ptr,
+                                   const int* slot_idx, const double* term_f, int slot_sc0,
+                                   bool use_nb, bool use_terms, bool use_sc, double* grad,
+                                   int nslots, const TermPlanDev& tp, const double* epart,
+                                   const double* term_part, double* energies,
+                                   int64_t* status, cudaStream_t st) {
+  const int blocks = (n + 31) / 32 + 1;
+  count_launch();
+  if (fp64)
+    assemble_units_kernel<double><<<blocks, kAsmWarps * 32, 0, st>>>(
+        n, S, nb, unit_index, static_cast<const double*>(ipart),
+        static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
+        use_terms, use_sc, grad, nslots, term_blocks(tp), epart, term_part, energies, status);
+  else
+    assemble_units_kernel<float><<<blocks, kAsmWarps * 32, 0, st>>>(
+        n, S, nb, unit_index, static_cast<const float*>(ipart),
+        static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
+        use_terms, use_sc, grad, nslots, term_blocks(tp), epart, term_part, energies, status);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------- energy reduction
 __global__ void __launch_bounds__(kRedThreads)
 reduce_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
               const double* __restrict__ term_part, double* __restrict__ energies,
-              int64_t* __restrict__ status) {
+              int64_t* __restrict__ status, int n) {
   __shared__ double sh[32];
-  reduce_entry(nunits, nterm_blocks, epart, term_part, energies, status, blockIdx.x, sh);
+  reduce_entry(nunits, nterm_blocks, epart, term_part, energies, status, blockIdx.x, sh, true,
+               n);
 }
 
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
-                          const double* term_part, double* energies, int64_t* status,
+                          const double* term_part, double* energies, int64_t* status, int n,
                           cudaStream_t st) {
   count_launch();
   reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, term_blocks(tp), epart, term_part,
-                                                energies, status);
+                                                energies, status, n);
   return cudaGetLastError();
 }
 
@@ -167,30 +253,35 @@ __global__ void finder_kernel(int n, int np, const typename Vec4T<T>::type* __re
                               const double* __restrict__ sp_s, int64_t* __restrict__ status) {
   const int b = blockIdx.y;
   int64_t* s = status + (size_t)b * kStWords;
-  if (s[kStNbSuspect] == 0) return;
+  // clean entries were finalised by the reduction (reduce_entry)
+  if (*(volatile int64_t*)(s + kStNbSuspect) == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  finder_row<T>(i, n, pos + (size_t)b * np, sp_ptr, sp_j, sp_s, s);
-}
-
-__global__ void finalize_kernel(int n, int batch, int64_t* __restrict__ status) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
-  finalize_entry(n, status + (size_t)b * kStWords);
+  if (i < n) finder_row<T>(i, n, pos + (size_t)b * np, sp_ptr, sp_j, sp_s, s);
+  // the entry's last finder block converts the sentinels (status word 7
+  // counts finished blocks; reset for the next evaluation)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(s + 7);
+    if (atomicAdd(cnt, 1ull) == gridDim.x - 1) {
+      __threadfence();
+      finalize_entry(n, s);
+      *cnt = 0;
+    }
+  }
 }
 
 cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
                           const int* sp_ptr, const int* sp_j, const double* sp_s,
                           int64_t* status, cudaStream_t st) {
   dim3 grid((n + 127) / 128, batch);
-  if (n == 0) {
-  } else if (fp64)
+  if (n == 0) return cudaSuccess;  // nothing to find; the reduction finalised
+  if (fp64)
     count_launch(), finder_kernel<double><<<grid, 128, 0, st>>>(n, np, static_cast<const double4*>(pos),
                                                 sp_ptr, sp_j, sp_s, status);
   else
     count_launch(), finder_kernel<float><<<grid, 128, 0, st>>>(n, np, static_cast<const float4*>(pos), sp_ptr,
                                                sp_j, sp_s, status);
-  count_launch(); finalize_kernel<<<(batch + 127) / 128, 128, 0, st>>>(n, batch, status);
   return cudaGetLastError();
 }
 
