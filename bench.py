@@ -498,7 +498,7 @@ def lbfgs_converge():
 
     G = np.load(ROOT / "tests" / "golden" / "golden_v1.npz")
     out = {}
-    for name in ("conv60", "conv200"):
+    for name in ("lbfgs500", "conv60", "conv200"):
         cut = float(G[f"{name}/cutoff"])
         s = MolecularSystem.from_arrays(
             G[f"{name}/q"], G[f"{name}/sigma"], G[f"{name}/epsilon"], G[f"{name}/coords"],
@@ -506,13 +506,23 @@ def lbfgs_converge():
             G[f"{name}/ang_idx"], G[f"{name}/ang_K"], G[f"{name}/ang_t0"], G[f"{name}/dih_idx"],
             G[f"{name}/dih_V"], excluded=G[f"{name}/excluded"], scaled14=G[f"{name}/scaled14"],
             s14=float(G[f"{name}/s14"]), cutoff=None if cut <= 0 else cut)
-        ref_f, _, ref_it, tol = G[f"{name}/final"]
-        stop = StopCriteria(max_iterations=50000, gradient_norm_tol=tol, gradient_norm_rtol=0.0)
-        lbfgs(MolecularOracle(s), s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+        if name == "lbfgs500":
+            # configs[0]: the reference's bounded 500-atom chain run (m = 3,
+            # 300 iterations or |g| <= 1e-3), make_golden.py
+            ref_f, _, ref_it = G[f"{name}/final"]
+            m = 3
+            stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3,
+                                gradient_norm_rtol=0.0)
+        else:
+            ref_f, _, ref_it, tol = G[f"{name}/final"]
+            m = 5
+            stop = StopCriteria(max_iterations=50000, gradient_norm_tol=tol,
+                                gradient_norm_rtol=0.0)
+        lbfgs(MolecularOracle(s), s.coords.ravel(), m=m, linesearch=make_linesearch("par"),
               stop=StopCriteria(max_iterations=3, gradient_norm_rtol=0.0))  # warm-up
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        res = lbfgs(MolecularOracle(s), s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+        res = lbfgs(MolecularOracle(s), s.coords.ravel(), m=m, linesearch=make_linesearch("par"),
                     stop=stop)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0

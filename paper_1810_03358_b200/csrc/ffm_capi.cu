@@ -312,13 +312,17 @@ int build_terms(ffm_system* s, int64_t nbond, const int64_t* bidx, const double*
 // energy-partial slots of the pair sweep: one per tile or per super-unit
 int nb_slots(const NbPlanDev& p) { return p.ntiles ? p.ntiles : p.nunits; }
 
-// small systems sweep tiles instead of super-units when the units would
-// not fill the GPU (fewer than 2 per SM)
+// small systems sweep tiles (one CTA per 128 x 32 tile, ffm_tile.cuh)
+// instead of super-units: below ~150 units (about 4300 atoms at S = 256)
+// the units leave SMs idle and the one-launch tile evaluation is faster;
+// above it the tile gather (a row of up to np/32 tile partials per atom)
+// costs more than it saves.  Measured (tools/mid_sweep.py, tiles vs units,
+// FP32 / FP64 energy+gradient, us): 2000 atoms 21.2 / 24.8 vs 28.9 / 43.2;
+// 4000 atoms 37.1 / 55.0 vs 37.3 / 69.8; 5000 atoms 47.4 / 74.2 vs 37.7 / 70.0
 bool use_tiles(const NbPlanDev& p, int device) {
   if (const char* f = getenv("FFM_FORCE_TILES")) return atoi(f) != 0;  // tuning / tests
-  int sms = 148;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  return p.nunits < 2 * sms;
+  (void)device;
+  return p.nunits < 150;
 }
 
 int build_tiles(ffm_system* s) {
@@ -815,23 +819,18 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
     FFM_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
   else
     FFM_CUDA(launch_terms(tp, grad, 1, coords_d, w.term_e, w.term_f, status_d, st));
-  if (grad && s->plan.n > 0 && s->plan.ntiles == 0 && do_nb) {
-    // super-unit mode: gather + energy reduction in one launch
-    FFM_CUDA(launch_assemble_reduce(
-        s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index, w.ipart, w.jpart,
-        s->d_slot_ptr, s->d_slot_idx, w.term_f, s->tp.slot_sc0, do_nb,
-        do_terms && s->rank == 0, do_nb && s->rank == 0, grad_d, nb_slots(s->plan), tp,
-        w.epart, w.term_e, energies_d, status_d, st));
+  if (grad && s->plan.n > 0) {
+    // gather + energy reduction in one launch
+    FFM_CUDA(launch_gather_reduce(
+        s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index,
+        s->plan.ntiles ? s->d_trow_ptr : nullptr, s->d_tcol_ptr, s->d_tcol_idx, w.ipart,
+        w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f, s->tp.slot_sc0, do_nb,
+        do_terms && s->rank == 0, do_nb && s->rank == 0, grad_d,
+        do_nb ? nb_slots(s->plan) : 0, tp, w.epart, w.term_e, energies_d, status_d, st));
     FFM_CUDA(launch_finder(s->plan.n, s->plan.np, 1, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                            s->d_sp_s, status_d, st));
     return FFM_OK;
   }
-  if (grad && s->plan.n > 0)
-    FFM_CUDA(launch_assemble(s->plan.n, s->plan.S, s->plan.nb, f64, s->d_unit_index,
-                             s->plan.ntiles ? s->d_trow_ptr : nullptr, s->d_tcol_ptr,
-                             s->d_tcol_idx, w.ipart, w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f,
-                             s->tp.slot_sc0, do_nb, do_terms && s->rank == 0,
-                             do_nb && s->rank == 0, grad_d, st));
   FFM_CUDA(launch_reduce(do_nb ? nb_slots(s->plan) : 0, tp, 1, w.epart, w.term_e, energies_d,
                          status_d, s->plan.n, st));
   FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,

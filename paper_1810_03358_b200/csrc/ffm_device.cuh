@@ -286,45 +286,74 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
 }
 
 // ---------------------------------------------------------- gradient gather
-// item x = c * n + a: component c of atom a (coalesced along atoms); the
-// pair partials then the incident term slots, in a fixed order
-template <typename T>
-__device__ __forceinline__ void assemble_item(int64_t x, int n, int S, int nb,
-                                              const int* __restrict__ unit_index,
-                                              const int* __restrict__ trow_ptr,
-                                              const int* __restrict__ tcol_ptr,
-                                              const int* __restrict__ tcol_idx,
-                                              const T* __restrict__ ipart,
-                                              const T* __restrict__ jpart,
-                                              const int* __restrict__ slot_ptr,
-                                              const int* __restrict__ slot_idx,
-                                              const double* __restrict__ term_f, int slot_sc0,
-                                              bool use_nb, bool use_terms, bool use_sc,
-                                              double* __restrict__ grad) {
-  const int c = (int)(x / n), a = (int)(x - (int64_t)c * n);
-  const int b = a / S, off = a - b * S;
-  double g = 0.0;
-  if (use_nb && trow_ptr) {  // tile mode (nb_tiles_kernel)
-    const int kk = a / kIB, row = a - kk * kIB, mg = a / kJB, l = a - mg * kJB;
-    for (int t = trow_ptr[kk]; t < trow_ptr[kk + 1]; ++t)
-      g += (double)ipart[((size_t)t * 3 + c) * kIB + row];
-    for (int e = tcol_ptr[mg]; e < tcol_ptr[mg + 1]; ++e)
-      g += (double)jpart[((size_t)tcol_idx[e] * 3 + c) * kJB + l];
-  } else if (use_nb) {
-    const size_t co = (size_t)c * S + off;
-#pragma unroll 4
-    for (int cc = b; cc < nb; ++cc)  // i-side: units (b, cc)
-      g += (double)ipart[(size_t)unit_index[b * nb + cc] * 3 * S + co];
-#pragma unroll 4
-    for (int r = 0; r <= b; ++r)  // j-side: units (r, b)
-      g += (double)jpart[(size_t)unit_index[r * nb + b] * 3 * S + co];
+// The gather of one 32-atom group (atoms 32 g .. 32 g + 31; a group never
+// straddles a super-block or a tile row) by the NW warps of a block
+// (block-uniform call, contains __syncthreads).  The group's partial
+// entries -- super-unit mode: the i-rows of units (b, b..nb-1) then the
+// j-columns of units (0..b, b); tile mode: the i-rows of the tiles of its
+// sub-block row, then the j-columns of the tiles of its j-block -- are dealt
+// to the warps (entry k to warp k mod NW, 128-byte coalesced rows, all
+// three components); the NW warp sums and the atom's term slots are then
+// added in a fixed order.  part: NW x 3 x 32 doubles of shared memory.
+template <typename T, int NW>
+__device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
+                                             const int* __restrict__ unit_index,
+                                             const int* __restrict__ trow_ptr,
+                                             const int* __restrict__ tcol_ptr,
+                                             const int* __restrict__ tcol_idx,
+                                             const T* __restrict__ ipart,
+                                             const T* __restrict__ jpart,
+                                             const int* __restrict__ slot_ptr,
+                                             const int* __restrict__ slot_idx,
+                                             const double* __restrict__ term_f, int slot_sc0,
+                                             bool use_nb, bool use_terms, bool use_sc,
+                                             double* __restrict__ grad, double (*part)[3][32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a0 = g << 5;
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+  if (use_nb && trow_ptr) {  // tile mode: [tile][3][128] rows, [tile][3][32] columns
+    const int kk = a0 / kIB, mg = a0 / kJB, row = a0 - kk * kIB + lane;
+    const int r0 = trow_ptr[kk], nr = trow_ptr[kk + 1] - r0;
+    const int c0 = tcol_ptr[mg], nt = nr + tcol_ptr[mg + 1] - c0;
+    for (int k = warp; k < nt; k += NW) {
+      const bool isrow = k < nr;
+      const int st = isrow ? kIB : kJB;
+      const T* p = isrow ? ipart + (size_t)(r0 + k) * 3 * kIB + row
+                         : jpart + (size_t)tcol_idx[c0 + k - nr] * 3 * kJB + lane;
+      g0 += (double)p[0];
+      g1 += (double)p[st];
+      g2 += (double)p[2 * st];
+    }
+  } else if (use_nb) {  // super-unit mode: [unit][3][S] rows and columns
+    const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
+    for (int k = warp; k <= nb; k += NW) {
+      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
+                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
+      g0 += (double)p[off];
+      g1 += (double)p[S + off];
+      g2 += (double)p[2 * S + off];
+    }
   }
-  for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
-    const int k = slot_idx[s];
-    if (k < slot_sc0 ? !use_terms : !use_sc) continue;
-    g += term_f[3 * (size_t)k + c];
+  part[warp][0][lane] = g0;
+  part[warp][1][lane] = g1;
+  part[warp][2][lane] = g2;
+  __syncthreads();
+  for (int x = threadIdx.x; x < 96; x += NW * 32) {
+    // thread x writes grad[3 a0 + x]: coalesced
+    const int l = x / 3, c = x - 3 * l, a = a0 + l;
+    if (a < n) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v += part[w][c][l];
+      for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
+        const int k = slot_idx[s];
+        if (k < slot_sc0 ? !use_terms : !use_sc) continue;
+        v += term_f[3 * (size_t)k + c];
+      }
+      grad[3 * (size_t)a + c] = v;
+    }
   }
-  grad[3 * (size_t)a + c] = g;
+  __syncthreads();  // part is reused by the block's next group
 }
 
 // status sentinels -> the reference's conventions (-1 = clean)

@@ -42,17 +42,6 @@ int term_blocks(const TermPlanDev& tp);
 cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const double* coords,
                          double* term_part, double* term_f, int64_t* status, cudaStream_t st);
 
-// gradient[a] = sum of nonbonded partials + incident term slots, fixed order
-// use_nb: add the pair partials; use_terms: add the bonded slots (below
-// slot_sc0); use_sc: add the scaled-pair slots.  Term and scaled slots are
-// written by rank 0 only: other ranks of a sharded system must not read them
-cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
-                            const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
-                            const void* ipart, const void* jpart, const int* slot_ptr,
-                            const int* slot_idx, const double* term_f, int slot_sc0,
-                            bool use_nb, bool use_terms, bool use_sc, double* grad,
-                            cudaStream_t st);
-
 // energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
 // coincidences for the finder
 // (clean entries are finalised here: sentinels -> -1; n = atoms)
@@ -60,15 +49,19 @@ cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const do
                           const double* term_part, double* energies, int64_t* status, int n,
                           cudaStream_t st);
 
-// super-unit mode, batch 1: the gradient gather and the energy reduction
-// in one launch (gather split over 8 warps per 32 atoms, fixed order)
-cudaError_t launch_assemble_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
-                                   const void* ipart, const void* jpart, const int* slot_ptr,
-                                   const int* slot_idx, const double* term_f, int slot_sc0,
-                                   bool use_nb, bool use_terms, bool use_sc, double* grad,
-                                   int nslots, const TermPlanDev& tp, const double* epart,
-                                   const double* term_part, double* energies,
-                                   int64_t* status, cudaStream_t st);
+// batch 1: the gradient gather (gather_group, ffm_device.cuh: tile mode
+// when trow_ptr is set, else super-unit mode) and the energy reduction in
+// one launch
+constexpr int kGatherWarpsUnits = 8;
+constexpr int kGatherWarpsTiles = 4;
+cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
+                                 const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
+                                 const void* ipart, const void* jpart, const int* slot_ptr,
+                                 const int* slot_idx, const double* term_f, int slot_sc0,
+                                 bool use_nb, bool use_terms, bool use_sc, double* grad,
+                                 int nslots, const TermPlanDev& tp, const double* epart,
+                                 const double* term_part, double* energies, int64_t* status,
+                                 cudaStream_t st);
 
 // exact first coincident pair (reference loop order), only when flagged;
 // the last block then converts the status sentinels to -1.

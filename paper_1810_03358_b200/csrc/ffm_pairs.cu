@@ -350,22 +350,15 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   }
 }
 
-constexpr int kTileWarps = 4;
-
 template <typename T, bool GRAD, bool CUTOFF>
 __global__ void __launch_bounds__(kTileWarps * 32)
 nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,
                 double* __restrict__ epart) {
-  __shared__ typename Vec4T<T>::type sj[kTileWarps][2 * kJB];
-  __shared__ typename Vec2T<T>::type sl[kTileWarps][2 * kJB];
-  __shared__ T jacc[kTileWarps][3 * kJB];
-  const int warp = threadIdx.x >> 5;
-  const int slot = blockIdx.x * kTileWarps + warp;
-  if (slot >= plan.nlaunch) return;  // warp-uniform; no block barriers below
-  tile_warp<T, GRAD, CUTOFF>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, slot, blockIdx.y,
-                             sj[warp], sl[warp], jacc[warp]);
+  __shared__ TileSmem<T> sm;
+  tile_cta<T, GRAD, CUTOFF>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, blockIdx.x, blockIdx.y,
+                            sm);
 }
 
 template <typename T, bool GRAD, bool CUTOFF>
@@ -373,7 +366,7 @@ static cudaError_t launch_tiles_t(const NbPlanDev& plan, const void* pos, const 
                                   const void* ipos, const void* ilj, void* ipart, void* jpart,
                                   double* epart, int batch, cudaStream_t st) {
   if (plan.nlaunch == 0) return cudaSuccess;
-  dim3 grid((plan.nlaunch + kTileWarps - 1) / kTileWarps, batch);
+  dim3 grid(plan.nlaunch, batch);  // one CTA per tile
   count_launch();
   nb_tiles_kernel<T, GRAD, CUTOFF><<<grid, kTileWarps * 32, 0, st>>>(
       plan, static_cast<const typename Vec4T<T>::type*>(pos),

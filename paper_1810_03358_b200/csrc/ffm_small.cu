@@ -37,14 +37,13 @@ __global__ void __launch_bounds__(kSmallThreads)
 small_eval_kernel(SmallEvalArgs a) {
   using V4 = typename Vec4T<T>::type;
   using V2 = typename Vec2T<T>::type;
-  __shared__ V4 sj[4][2 * kJB];
-  __shared__ V2 sl[4][2 * kJB];
-  __shared__ T jacc[4][3 * kJB];
+  __shared__ TileSmem<T> tsm;
+  __shared__ double gpart[kGatherWarpsTiles][3][32];
   __shared__ double sh[5][kTermThreads / 32];
   __shared__ double red[32];
   cg::grid_group grid = cg::this_grid();
   const NbPlanDev& plan = a.plan;
-  const int n = plan.n, warp = threadIdx.x >> 5;
+  const int n = plan.n;
   const int64_t gt = (int64_t)blockIdx.x * kSmallThreads + threadIdx.x;
   const int64_t gs = (int64_t)gridDim.x * kSmallThreads;
   V4* pos = static_cast<V4*>(a.pos);
@@ -68,13 +67,18 @@ small_eval_kernel(SmallEvalArgs a) {
   grid.sync();
   stamp(1);
 
-  // P1: term blocks first (block-synchronous), then the warp-independent tiles
-  for (int vb = blockIdx.x; vb < a.nterm_blocks; vb += gridDim.x)
-    term_block(a.tp, GRAD, a.coords, a.term_part, a.term_f, a.status, 0, vb, a.nterm_blocks, sh);
-  for (int slot = blockIdx.x * 4 + warp; slot < plan.nlaunch; slot += gridDim.x * 4)
-    tile_warp<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
-                               static_cast<const T*>(a.ilj), ipart, jpart, a.epart, slot, 0,
-                               sj[warp], sl[warp], jacc[warp]);
+  // P1: CTA items -- the pair tiles (one CTA each, the longer items, first)
+  // and the bonded / scaled-pair term blocks, dealt round-robin so a CTA
+  // with a tile does not also run a term block when the grid covers both
+  const int nitems = plan.nlaunch + a.nterm_blocks;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    if (it < plan.nlaunch)
+      tile_cta<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
+                                static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it, 0, tsm);
+    else
+      term_block(a.tp, GRAD, a.coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
+                 a.nterm_blocks, sh);
+  }
   __syncthreads();
   stamp(2);
   grid.sync();
@@ -89,12 +93,13 @@ small_eval_kernel(SmallEvalArgs a) {
     if (!isfinite(e[0]) || !isfinite(e[1]) || e[2] < kRmin * kRmin) suspect = 1;
   }
   suspect = __syncthreads_or(suspect);
-  if (GRAD)
-    for (int64_t x = gt; x < 3 * (int64_t)n; x += gs)
-      assemble_item<T>(x, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr, a.tcol_idx,
-                       ipart, jpart, a.slot_ptr, a.slot_idx, a.term_f, a.tp.slot_sc0, true, true,
-                       true, a.grad);
-  if (blockIdx.x == 0)
+  if (GRAD)  // 32-atom groups, the same 4-warp split as the chain's gather
+    for (int g = blockIdx.x; g < ((n + 31) >> 5); g += gridDim.x)
+      gather_group<T, kGatherWarpsTiles>(g, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr,
+                                         a.tcol_idx, ipart, jpart, a.slot_ptr, a.slot_idx,
+                                         a.term_f, a.tp.slot_sc0, true, true, true, a.grad,
+                                         gpart);
+  if (blockIdx.x == gridDim.x - 1)  // the gather groups fill the first CTAs
     reduce_entry(plan.ntiles, a.nterm_blocks, a.epart, a.term_part, a.energies, a.status, 0, red,
                  false);
   __syncthreads();
@@ -132,8 +137,7 @@ int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device) {
                                                     kSmallThreads, 0) != cudaSuccess)
     return 0;
   int64_t want = 1;
-  want = std::max<int64_t>(want, (a.plan.nlaunch + 3) / 4);
-  want = std::max<int64_t>(want, a.nterm_blocks);
+  want = std::max<int64_t>(want, (int64_t)a.plan.nlaunch + a.nterm_blocks);
   want = std::max<int64_t>(want, (3 * (int64_t)a.plan.n + kSmallThreads - 1) / kSmallThreads);
   return (int)std::min<int64_t>(want, (int64_t)sms * per_sm);
 }

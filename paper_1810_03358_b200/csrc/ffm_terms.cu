@@ -105,126 +105,74 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
 }
 
 // ---------------------------------------------------------- gradient gather
-template <typename T>
-__global__ void assemble_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
-                                const int* __restrict__ trow_ptr,
-                                const int* __restrict__ tcol_ptr,
-                                const int* __restrict__ tcol_idx,
-                                const T* __restrict__ ipart, const T* __restrict__ jpart,
-                                const int* __restrict__ slot_ptr,
-                                const int* __restrict__ slot_idx,
-                                const double* __restrict__ term_f, int slot_sc0, bool use_nb,
-                                bool use_terms, bool use_sc, double* __restrict__ grad) {
-  // one thread per (atom, component): 3 n threads, coalesced along atoms
-  const int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= 3 * (int64_t)n) return;
-  assemble_item<T>(x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
-                   slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc, grad);
-}
-
-cudaError_t launch_assemble(int n, int S, int nb, bool fp64, const int* unit_index,
-                            const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
-                            const void* ipart, const void* jpart, const int* slot_ptr,
-                            const int* slot_idx, const double* term_f, int slot_sc0,
-                            bool use_nb, bool use_terms, bool use_sc, double* grad,
-                            cudaStream_t st) {
-  const int blocks = (int)((3 * (int64_t)n + 127) / 128);
-  if (fp64)
-    count_launch(), assemble_kernel<double><<<blocks, 128, 0, st>>>(
-        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, static_cast<const double*>(ipart),
-        static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, use_sc, grad);
-  else
-    count_launch(), assemble_kernel<float><<<blocks, 128, 0, st>>>(
-        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, static_cast<const float*>(ipart),
-        static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, use_sc, grad);
-  return cudaGetLastError();
-}
-
-// Super-unit mode: one block of kAsmWarps warps per 32 consecutive atoms (a
-// 32-atom group never straddles a super-block).  An atom of super-block b
-// has nb + 1 partial entries: the i-rows of units (b, b..nb-1), then the
-// j-columns of units (0..b, b); warp w sums entries w, w + kAsmWarps, ...
-// for all three components (coalesced 128-byte rows), and the kAsmWarps
-// sums plus the atom's term slots are added in a fixed order.  The grid's
-// extra last block reduces the energies (reduce_entry), so one launch does
-// what the gather and reduce kernels did; the order is fixed, so results
-// are bit-identical run to run.
-constexpr int kAsmWarps = 8;
-
-template <typename T>
-__global__ void __launch_bounds__(kAsmWarps * 32)
-assemble_units_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
-                      const T* __restrict__ ipart, const T* __restrict__ jpart,
-                      const int* __restrict__ slot_ptr, const int* __restrict__ slot_idx,
-                      const double* __restrict__ term_f, int slot_sc0, bool use_nb,
-                      bool use_terms, bool use_sc, double* __restrict__ grad, int nslots,
-                      int nterm_blocks, const double* __restrict__ epart,
-                      const double* __restrict__ term_part, double* __restrict__ energies,
-                      int64_t* __restrict__ status) {
-  __shared__ double part[kAsmWarps][3][32];
-  const int ngroups = (n + 31) >> 5;
-  if ((int)blockIdx.x == ngroups) {
+// Gather + energy reduction in one launch: block g < ngroups gathers atom
+// group g (gather_group: NW warps, fixed order), the extra last block
+// reduces the energies (reduce_entry), so results are bit-identical run to
+// run.  Super-unit mode uses 8 warps per group, tile mode 4 (the same split
+// as the fused small-system kernel, so both produce the same bits).
+template <typename T, int NW>
+__global__ void __launch_bounds__(NW * 32)
+gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
+                     const int* __restrict__ trow_ptr, const int* __restrict__ tcol_ptr,
+                     const int* __restrict__ tcol_idx, const T* __restrict__ ipart,
+                     const T* __restrict__ jpart, const int* __restrict__ slot_ptr,
+                     const int* __restrict__ slot_idx, const double* __restrict__ term_f,
+                     int slot_sc0, bool use_nb, bool use_terms, bool use_sc,
+                     double* __restrict__ grad, int nslots, int nterm_blocks,
+                     const double* __restrict__ epart, const double* __restrict__ term_part,
+                     double* __restrict__ energies, int64_t* __restrict__ status) {
+  __shared__ double part[NW][3][32];
+  if ((int)blockIdx.x == (n + 31) >> 5) {
     reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
                  true, n);
     return;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int a0 = blockIdx.x << 5;
-  const int b = a0 / S, off = a0 - b * S + lane;  // partial rows are padded to S
-  double g0 = 0.0, g1 = 0.0, g2 = 0.0;
-  if (use_nb) {
-    const int ni = nb - b;
-    for (int k = warp; k <= nb; k += kAsmWarps) {
-      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
-                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
-      g0 += (double)p[off];
-      g1 += (double)p[S + off];
-      g2 += (double)p[2 * S + off];
-    }
-  }
-  part[warp][0][lane] = g0;
-  part[warp][1][lane] = g1;
-  part[warp][2][lane] = g2;
-  __syncthreads();
-  if (threadIdx.x < 96) {
-    // thread t writes grad[3 a0 + t]: coalesced
-    const int l = threadIdx.x / 3, c = threadIdx.x - 3 * l, a = a0 + l;
-    if (a < n) {
-      double g = 0.0;
-#pragma unroll
-      for (int w = 0; w < kAsmWarps; ++w) g += part[w][c][l];
-      for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
-        const int k = slot_idx[s];
-        if (k < slot_sc0 ? !use_terms : !use_sc) continue;
-        g += term_f[3 * (size_t)k + c];
-      }
-      grad[3 * (size_t)a + c] = g;
-    }
-  }
+  gather_group<T, NW>(blockIdx.x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart,
+                      jpart, slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
+                      grad, part);
 }
 
-cudaError_t launch_assemble_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
-                                   const void* ipart, const void* jpart, const int* slot_ptr,
-                                   const int* slot_idx, const double* term_f, int slot_sc0,
-                                   bool use_nb, bool use_terms, bool use_sc, double* grad,
-                                   int nslots, const TermPlanDev& tp, const double* epart,
-                                   const double* term_part, double* energies,
-                                   int64_t* status, cudaStream_t st) {
+template <typename T>
+static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, const int* trow_ptr,
+                               const int* tcol_ptr, const int* tcol_idx, const void* ipart,
+                               const void* jpart, const int* slot_ptr, const int* slot_idx,
+                               const double* term_f, int slot_sc0, bool use_nb, bool use_terms,
+                               bool use_sc, double* grad, int nslots, int nterm_blocks,
+                               const double* epart, const double* term_part, double* energies,
+                               int64_t* status, cudaStream_t st) {
   const int blocks = (n + 31) / 32 + 1;
+  const T* ip = static_cast<const T*>(ipart);
+  const T* jp = static_cast<const T*>(jpart);
   count_launch();
-  if (fp64)
-    assemble_units_kernel<double><<<blocks, kAsmWarps * 32, 0, st>>>(
-        n, S, nb, unit_index, static_cast<const double*>(ipart),
-        static_cast<const double*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, use_sc, grad, nslots, term_blocks(tp), epart, term_part, energies, status);
+  if (trow_ptr)
+    gather_reduce_kernel<T, kGatherWarpsTiles><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
+        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
+        slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
+        energies, status);
   else
-    assemble_units_kernel<float><<<blocks, kAsmWarps * 32, 0, st>>>(
-        n, S, nb, unit_index, static_cast<const float*>(ipart),
-        static_cast<const float*>(jpart), slot_ptr, slot_idx, term_f, slot_sc0, use_nb,
-        use_terms, use_sc, grad, nslots, term_blocks(tp), epart, term_part, energies, status);
+    gather_reduce_kernel<T, kGatherWarpsUnits><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
+        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
+        slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
+        energies, status);
   return cudaGetLastError();
+}
+
+cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* unit_index,
+                                 const int* trow_ptr, const int* tcol_ptr, const int* tcol_idx,
+                                 const void* ipart, const void* jpart, const int* slot_ptr,
+                                 const int* slot_idx, const double* term_f, int slot_sc0,
+                                 bool use_nb, bool use_terms, bool use_sc, double* grad,
+                                 int nslots, const TermPlanDev& tp, const double* epart,
+                                 const double* term_part, double* energies, int64_t* status,
+                                 cudaStream_t st) {
+  if (fp64)
+    return launch_gr_t<double>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
+                               slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
+                               grad, nslots, term_blocks(tp), epart, term_part, energies, status,
+                               st);
+  return launch_gr_t<float>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
+                            slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc, grad,
+                            nslots, term_blocks(tp), epart, term_part, energies, status, st);
 }
 
 // ---------------------------------------------------------- energy reduction

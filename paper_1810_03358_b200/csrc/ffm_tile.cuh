@@ -18,7 +18,14 @@ namespace ffm {
 #ifndef FFM_UNROLL64
 #define FFM_UNROLL64 0  // 0: 4 with gradient, 8 energy-only (measured best)
 #endif
+#ifndef FFM_UNROLL_SMALL
+#define FFM_UNROLL_SMALL 4
+#endif
 constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
+// tile-mode / fused small-system sweeps: a few warps run each tile once, so
+// a cold instruction cache, not the FMA pipe, bounds them; a short loop body
+// (a few KB instead of ~25 KB fully unrolled) is faster there
+constexpr int kStepUnrollSmall = FFM_UNROLL_SMALL;
 constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/SM)
 #ifndef FFM_F64FORM
 #define FFM_F64FORM 2  // FP64 energy/gradient algebra variant (see warp_tile; 2 measured best)
@@ -65,7 +72,13 @@ template <> struct PairsPerPass<double> { static constexpr int value = 1; };
 // an immediate offset.  MASKED tiles carry per-lane activity bitmasks
 // (diagonal i < j condition and/or special pairs); inactive pairs are
 // neutralised (r2 -> 1, coefficients -> 0) so they contribute exactly zero.
-template <typename T, bool GRAD, bool CUTOFF, bool MASKED, int NP, bool DOUBLED = true>
+//
+// NSTEP < 32 evaluates only steps t0 .. t0 + NSTEP - 1 of the rotation (the
+// small-system CTA tile splits one tile over four warps); the j-gradient
+// column then ends in lane (j - t0 - NSTEP) mod 32 and is added to
+// jacc[(lane + t0 + NSTEP) mod 32].
+template <typename T, bool GRAD, bool CUTOFF, bool MASKED, int NP, bool DOUBLED = true,
+          int UNR = 0, int NSTEP = 32>
 __device__ __forceinline__ void warp_tile(
     const typename Vec4T<T>::type* __restrict__ J,
     const typename Vec2T<T>::type* __restrict__ L, int lane,
@@ -74,18 +87,19 @@ __device__ __forceinline__ void warp_tile(
     const typename Pk<T>::V (&ai)[NP], const typename Pk<T>::V (&bi)[NP],
     typename Pk<T>::V (&F)[NP][3], typename Pk<T>::V& ec2,
     typename Pk<T>::V& ev2, T* __restrict__ jacc, int jacc_stride,
-    const uint32_t (&mk)[2 * NP], T cut2, T& minr2) {
+    const uint32_t (&mk)[2 * NP], T cut2, T& minr2, int t0 = 0) {
   using P = Pk<T>;
   using V = typename P::V;
   V gx = P::zero(), gy = P::zero(), gz = P::zero();
   const int src = (lane + 1) & 31;
   if (DOUBLED) {  // j-block stored twice: entry lane + t is an immediate offset
-    J += lane;
-    L += lane;
+    J += lane + t0;
+    L += lane + t0;
   }
-#pragma unroll(sizeof(T) == 8 ? (kStepUnroll64 ? kStepUnroll64 : (GRAD ? 4 : 8)) : kStepUnroll)
-  for (int t = 0; t < 32; ++t) {
-    const int jt = DOUBLED ? t : ((lane + t) & 31);
+#pragma unroll(UNR ? UNR : sizeof(T) == 8 ? (kStepUnroll64 ? kStepUnroll64 : (GRAD ? 4 : 8)) : kStepUnroll)
+  for (int ts = 0; ts < NSTEP; ++ts) {
+    const int t = t0 + ts;
+    const int jt = DOUBLED ? ts : ((lane + t) & 31);
     const auto pj = J[jt];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
     const auto lj = L[jt];  // (a, -b)
     // phase-separated: both pairs' geometry first, the MUFU ops issued back
@@ -184,60 +198,73 @@ __device__ __forceinline__ void warp_tile(
   }
   if (GRAD) {
     // after 32 rotations lane l holds the column of j = l again
-    jacc[lane] += P::lo(gx) + P::hi(gx);
-    jacc[jacc_stride + lane] += P::lo(gy) + P::hi(gy);
-    jacc[2 * jacc_stride + lane] += P::lo(gz) + P::hi(gz);
+    const int jl = NSTEP == 32 ? lane : ((lane + t0 + NSTEP) & 31);
+    jacc[jl] += P::lo(gx) + P::hi(gx);
+    jacc[jacc_stride + jl] += P::lo(gy) + P::hi(gy);
+    jacc[2 * jacc_stride + jl] += P::lo(gz) + P::hi(gz);
   }
 }
 
 
 // ------------------------------------------------------- small systems
-// One warp per 128 x 32 tile (i-sub-block kk, global j-block mg >= 4 kk): a
-// system of a few thousand atoms has a handful of super-units, which would
-// leave most SMs idle and run each unit's tiles back to back on one SM; in
-// tile mode every tile of the triangle runs at once.  Partials per tile:
-// i-rows [tile][3][128], j-columns [tile][3][32], energies
-// [batch][tile][3]; the gather sums them in a fixed order.
-//
-// tile_warp evaluates launch slot `slot` of batch entry bidx with one warp;
-// sj / sl / jacc are that warp's private shared-memory staging (2 x 32 j
-// records, 2 x 32 LJ records, 3 x 32 column accumulators).
+// One CTA of kTileWarps warps per 128 x 32 tile (i-sub-block kk, global
+// j-block mg >= 4 kk).  A system of a few thousand atoms has a handful of
+// super-units (most SMs idle) and, even in tiles, so few that each runs
+// alone on its SM sub-partition: the tile's 32 rotation steps are then a
+// latency chain.  Splitting them over the CTA's warps (warp q evaluates
+// steps 8q .. 8q + 7 of the same tile) cuts that chain four-fold.  Warp
+// partials (i-rows, j-columns, energies) are combined in a fixed order, so
+// results are bit-identical run to run.  Partials per tile: i-rows
+// [tile][3][128], j-columns [tile][3][32], energies [batch][tile][3]; the
+// gather sums them in a fixed order.
+constexpr int kTileWarps = 4;
+constexpr int kTileSteps = 32 / kTileWarps;
+
+template <typename T>
+struct TileSmem {
+  typename Vec4T<T>::type sj[2 * kJB];
+  typename Vec2T<T>::type sl[2 * kJB];
+  T jacc[kTileWarps][3 * kJB];
+  T fred[kTileWarps][3 * kIB];
+  double ered[kTileWarps][3];
+};
+
+// tile_cta evaluates launch slot `slot` of batch entry bidx with the whole
+// CTA (kTileWarps warps; block-uniform call, contains __syncthreads)
 template <typename T, bool GRAD, bool CUTOFF>
-__device__ __forceinline__ void tile_warp(const NbPlanDev& plan,
-                                          const typename Vec4T<T>::type* __restrict__ pos,
-                                          const typename Vec2T<T>::type* __restrict__ lj,
-                                          const T* __restrict__ ipos, const T* __restrict__ ilj,
-                                          T* __restrict__ ipart, T* __restrict__ jpart,
-                                          double* __restrict__ epart, int slot, int bidx,
-                                          typename Vec4T<T>::type* sj,
-                                          typename Vec2T<T>::type* sl, T* jacc) {
+__device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
+                                         const typename Vec4T<T>::type* __restrict__ pos,
+                                         const typename Vec2T<T>::type* __restrict__ lj,
+                                         const T* __restrict__ ipos, const T* __restrict__ ilj,
+                                         T* __restrict__ ipart, T* __restrict__ jpart,
+                                         double* __restrict__ epart, int slot, int bidx,
+                                         TileSmem<T>& sm) {
   using P = Pk<T>;
   using V = typename P::V;
   using V4 = typename Vec4T<T>::type;
   using V2 = typename Vec2T<T>::type;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
   const int t = plan.tile_list ? plan.tile_list[slot] : slot;
-  __syncwarp();  // a warp running several tiles: the previous tile is done with sj / sl
+  __syncthreads();  // a CTA running several tiles: the previous one is done with sm
   const int2 tk = plan.tiles[t];
   const int kk = tk.x, mg = tk.y;
   const int ib = kk * kIB, jb = mg * kJB;
   pos += (size_t)bidx * plan.np;
   ipos += (size_t)bidx * 4 * plan.np;
   const int64_t half = plan.np >> 1;
-  {
+  if (q == 0) {
     V4 p = pos[jb + lane];
     p.x = -p.x;
     p.y = -p.y;
     p.z = -p.z;
-    sj[lane] = p;
-    sj[lane + 32] = p;
+    sm.sj[lane] = p;
+    sm.sj[lane + 32] = p;
+  } else if (q == 1) {
     V2 l = lj[jb + lane];
     l.y = -l.y;
-    sl[lane] = l;
-    sl[lane + 32] = l;
-    if (GRAD) jacc[lane] = jacc[32 + lane] = jacc[64 + lane] = T(0);
+    sm.sl[lane] = l;
+    sm.sl[lane + 32] = l;
   }
-  __syncwarp();
   constexpr int NP = PairsPerPass<T>::value;
   bool masked = jb < ib + kIB;  // straddles the diagonal
   uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
@@ -248,17 +275,30 @@ __device__ __forceinline__ void tile_warp(const NbPlanDev& plan,
       mk[p] = d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
     }
   }
-  for (int e = plan.spt_ptr[kk]; e < plan.spt_ptr[kk + 1]; ++e) {
-    if (plan.spt_m[e] == mg) {
-      masked = true;
+  // this tile's special-pair mask, if any: the row's special-tile list is
+  // searched 32 entries per step by the whole warp (one round of loads, not
+  // a chain of dependent ones -- a lone tile is latency-bound)
+  {
+    const int e_end = plan.spt_ptr[kk + 1];
+    for (int e0 = plan.spt_ptr[kk]; e0 < e_end; e0 += 32) {
+      const int e = e0 + lane;
+      const uint32_t hit = __ballot_sync(0xffffffffu, e < e_end && plan.spt_m[e] == mg);
+      if (hit) {
+        const int ef = e0 + __ffs(hit) - 1;
+        masked = true;
 #pragma unroll
-      for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)e * kIB + 32 * p + lane];
-      break;
+        for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)ef * kIB + 32 * p + lane];
+        break;
+      }
     }
   }
   const T cut2 = T(plan.cut2);
   T minr2 = T(1e30);
   double ec = 0.0, ev = 0.0;
+  T* jacc = sm.jacc[q];
+  if (GRAD) jacc[lane] = jacc[32 + lane] = jacc[64 + lane] = T(0);
+  __syncthreads();  // sj / sl staged
+  const int t0 = q * kTileSteps;
   for (int p0 = 0; p0 < 2; p0 += NP) {
     V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
 #pragma unroll
@@ -277,23 +317,24 @@ __device__ __forceinline__ void tile_warp(const NbPlanDev& plan,
     V ec2 = P::zero(), ev2 = P::zero();
     uint32_t mkp[2 * NP];
 #pragma unroll
-    for (int q = 0; q < 2 * NP; ++q) mkp[q] = mk[2 * p0 + q];
+    for (int x = 0; x < 2 * NP; ++x) mkp[x] = mk[2 * p0 + x];
     if (masked)
-      warp_tile<T, GRAD, CUTOFF, true, NP>(sj, sl, lane, xi, yi, zi, qi, ai, bi, F,
-                                           ec2, ev2, jacc, kJB, mkp, cut2, minr2);
+      warp_tile<T, GRAD, CUTOFF, true, NP, true, kTileSteps, kTileSteps>(
+          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mkp, cut2, minr2,
+          t0);
     else
-      warp_tile<T, GRAD, CUTOFF, false, NP>(sj, sl, lane, xi, yi, zi, qi, ai, bi, F,
-                                            ec2, ev2, jacc, kJB, mkp, cut2, minr2);
+      warp_tile<T, GRAD, CUTOFF, false, NP, true, kTileSteps, kTileSteps>(
+          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mkp, cut2, minr2,
+          t0);
     ec += double(P::lo(ec2)) + double(P::hi(ec2));
     ev += double(P::lo(ev2)) + double(P::hi(ev2));
     if (GRAD) {
-      T* ip = ipart + (size_t)t * 3 * kIB;
 #pragma unroll
       for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {  // F = -gradient
-          ip[c * kIB + lane + 64 * (p0 + pp)] = -P::lo(F[pp][c]);
-          ip[c * kIB + lane + 64 * (p0 + pp) + 32] = -P::hi(F[pp][c]);
+        for (int c = 0; c < 3; ++c) {
+          sm.fred[q][c * kIB + lane + 64 * (p0 + pp)] = P::lo(F[pp][c]);
+          sm.fred[q][c * kIB + lane + 64 * (p0 + pp) + 32] = P::hi(F[pp][c]);
         }
     }
   }
@@ -304,15 +345,41 @@ __device__ __forceinline__ void tile_warp(const NbPlanDev& plan,
     mr = fmin(mr, __shfl_xor_sync(0xffffffffu, mr, o));
   }
   if (lane == 0) {
+    sm.ered[q][0] = ec;
+    sm.ered[q][1] = ev;
+    sm.ered[q][2] = mr;
+  }
+  __syncthreads();
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    double e0 = 0.0, e1 = 0.0, e2 = sm.ered[0][2];
+#pragma unroll
+    for (int w = 0; w < kTileWarps; ++w) {
+      e0 += sm.ered[w][0];
+      e1 += sm.ered[w][1];
+      e2 = fmin(e2, sm.ered[w][2]);
+    }
     double* e = epart + ((size_t)bidx * plan.ntiles + t) * 3;
-    e[0] = ec;
-    e[1] = ev / LjIScale<T>::value;
-    e[2] = mr;
+    e[0] = e0;
+    e[1] = e1 / LjIScale<T>::value;
+    e[2] = e2;
   }
   if (GRAD) {
-    __syncwarp();
+    // F = -gradient; warp partials summed in warp order
+    T* ip = ipart + (size_t)t * 3 * kIB;
+    for (int x = tid; x < 3 * kIB; x += kTileWarps * 32) {
+      T f = sm.fred[0][x];
+#pragma unroll
+      for (int w = 1; w < kTileWarps; ++w) f += sm.fred[w][x];
+      ip[x] = -f;
+    }
     T* jp = jpart + (size_t)t * 3 * kJB;
-    for (int c = 0; c < 3; ++c) jp[c * kJB + lane] = jacc[c * kJB + lane];
+    if (tid < 3 * kJB) {
+      T g = sm.jacc[0][tid];
+#pragma unroll
+      for (int w = 1; w < kTileWarps; ++w) g += sm.jacc[w][tid];
+      jp[tid] = g;
+    }
   }
 }
 

@@ -13,7 +13,10 @@ from paper_1810_03358_b200.engine import DeviceSystem
 from paper_1810_03358_b200.synth import make_globule_system
 
 sizes = [int(a) for a in sys.argv[1:]] or [3000, 5000, 10000, 20000, 30000]
+only = os.environ.get("VARIANTS")
+PREC = N.FFM_F64 if os.environ.get("PREC") == "f64" else N.FFM_F32
 variants = [("auto", {}), ("S256", {"FFM_FORCE_S": "256", "FFM_FORCE_TILES": "0"}),
+            ("tiles256", {"FFM_FORCE_S": "256", "FFM_FORCE_TILES": "1"}),
             ("S512", {"FFM_FORCE_S": "512", "FFM_FORCE_TILES": "0"}),
             ("tiles", {"FFM_FORCE_TILES": "1"})]
 for n in sizes:
@@ -21,6 +24,8 @@ for n in sizes:
     c = torch.from_numpy(s.coords.copy()).cuda()
     g = torch.empty_like(c)
     for name, env in variants:
+        if only and name not in only.split(","):
+            continue
         for k in ("FFM_FORCE_S", "FFM_FORCE_TILES"):
             os.environ.pop(k, None)
         os.environ.update(env)
@@ -29,19 +34,19 @@ for n in sizes:
         fl = N.FFM_ENERGY | N.FFM_GRAD
         nb = []
         for k in range(8):
-            eng.eval(c, N.FFM_F32, grad=g, energies=en, status=st, flags=fl | N.FFM_TIME_NB)
+            eng.eval(c, PREC, grad=g, energies=en, status=st, flags=fl | N.FFM_TIME_NB)
             v = np.zeros(1, np.float32)
             N.check(eng.lib.ffm_system_nb_ms(eng.handle, v.ctypes.data), "nb_ms")
             if k >= 3:
                 nb.append(float(v[0]))
         for _ in range(3):
-            eng.eval(c, N.FFM_F32, grad=g, energies=en, status=st, flags=fl)
+            eng.eval(c, PREC, grad=g, energies=en, status=st, flags=fl)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 50
         e0.record()
         for _ in range(reps):
-            eng.eval(c, N.FFM_F32, grad=g, energies=en, status=st, flags=fl)
+            eng.eval(c, PREC, grad=g, energies=en, status=st, flags=fl)
         e1.record()
         torch.cuda.synchronize()
         tot = e0.elapsed_time(e1) / reps
