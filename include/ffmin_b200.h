@@ -212,6 +212,16 @@ typedef struct {
   int64_t max_oracle_calls;    /* -1: unbounded (value + gradient calls) */
   double threshold;            /* stop when |g| <= threshold */
   double h0, eps_h, k_plus, k_minus, trust;  /* line-search configuration */
+  /* the search-direction method run by the same graph (appended fields):
+   * 0 = L-BFGS (ffmin/optimizers/lbfgs.py:93-128), 1 = nonlinear conjugate
+   * gradients (ffmin/optimizers/cg.py:95-152; cg_kind 0..6 = fr, prp, prp+,
+   * hs, cd, ls, dy; restart every restart_period iterations), 2 = steepest
+   * descent (ffmin/optimizers/gradient.py, Eq. (4)).  m is ignored (but must
+   * be in range) for methods 1 and 2. */
+  int32_t method;
+  int32_t cg_kind;
+  int32_t restart_period;
+  int32_t reserved;
 } ffm_lbfgs_config;
 
 int ffm_lbfgs_create(ffm_system_t* sys, int precision, const ffm_lbfgs_config* cfg,

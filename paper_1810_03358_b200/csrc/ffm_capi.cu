@@ -1086,11 +1086,16 @@ int add_conditional(cudaStream_t st, cudaGraphConditionalHandle h,
 // capture on stream st
 int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls) {
   MinState* S = L->S;
-  FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, &S->count, S->idx_nf, S->rho_nf, &S->gn, L->ring_s,
-                                     L->ring_y, L->g, L->d, L->scratch, st));
-  const double* xs[1] = {L->d};
-  FFM_CUDA(launch_dots(L->n, 1, xs, xs, L->scratch, &S->dd, st));
+  const int method = L->cfg.method;
+  if (method == kMethodLbfgs)
+    FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, &S->count, S->idx_nf, S->rho_nf, &S->gn,
+                                       L->ring_s, L->ring_y, L->g, L->d, L->scratch, st));
+  if (method != kMethodSd) {  // L-BFGS: d = two-loop direction; CG: d = p
+    const double* xs[1] = {L->d};
+    FFM_CUDA(launch_dots(L->n, 1, xs, xs, L->scratch, &S->dd, st));
+  }
   FFM_CUDA(launch_min_dir(S, hls, st));
+  if (method == kMethodCg) FFM_CUDA(launch_select_neg(S, L->n, L->g, L->d, st));
   return FFM_OK;
 }
 
@@ -1111,6 +1116,25 @@ int cap_accept(ffm_lbfgs* L, cudaStream_t st) {
   const double* gs[1] = {L->gnew};
   FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
   FFM_CUDA(launch_min_acc_check(S, L->stw, st));
+  if (L->cfg.method == kMethodCg) {
+    // y = g+ - g; beta from five dot products; p+ in place; descent test
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->gnew, nullptr, -1.0, L->g, L->yt, st));
+    const double* xa[5] = {L->gnew, L->gnew, L->g, L->d, L->d};
+    const double* ya[5] = {L->gnew, L->yt, L->g, L->yt, L->g};
+    FFM_CUDA(launch_dots(L->n, 5, xa, ya, L->scratch, S->cgd, st));
+    FFM_CUDA(launch_min_cg_beta(S, st));
+    FFM_CUDA(launch_cg_update(S, L->n, L->gnew, L->d, st));
+    const double* pa[1] = {L->d};
+    FFM_CUDA(launch_dots(L->n, 1, pa, gs, L->scratch, &S->pg, st));
+    FFM_CUDA(launch_min_cg_check(S, st));
+    FFM_CUDA(launch_select_neg(S, L->n, L->gnew, L->d, st));
+  }
+  if (L->cfg.method != kMethodLbfgs) {  // no memory: x <- x+, g <- g+ (store_slot -1)
+    FFM_CUDA(launch_min_store(S, L->n, L->st, L->yt, L->ring_s, L->ring_y, L->xn, L->gnew,
+                              L->x, L->g, st));
+    FFM_CUDA(launch_min_iter_end(S, L->rec, st));
+    return FFM_OK;
+  }
   // s = x_new - x, y = g_new - g (LbfgsMemory._axpy_into)
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->xn, nullptr, -1.0, L->x, L->st, st));
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->gnew, nullptr, -1.0, L->g, L->yt, st));
@@ -1188,7 +1212,10 @@ int lbfgs_build(ffm_lbfgs* L) {
     {  // line search
       FFM_GC(cudaGraphConditionalHandleCreate(&hloop, bls, 0, 0));
       FFM_GC(cudaStreamBeginCaptureToGraph(c2, bls, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
+      if (L->cfg.method == kMethodSd)  // r = (1 / |g|) (-g)
+        FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, -1.0, L->g, nullptr, 0.0, nullptr, L->r, c2));
+      else
+        FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
       const double* gs[1] = {L->g};
       const double* rs[1] = {L->r};
       FFM_GC(launch_dots(L->n, 1, gs, rs, L->scratch, &S->slope, c2));
@@ -1198,6 +1225,7 @@ int lbfgs_build(ffm_lbfgs* L) {
       FFM_G(cap_trial(L, c3, hloop));
       FFM_GC(cudaStreamEndCapture(c3, &tmp));
       FFM_GC(launch_min_ls_post(S, L->rec, hacc, c2));
+      if (L->cfg.method == kMethodCg) FFM_GC(launch_select_neg(S, L->n, L->g, L->d, c2));
       FFM_GC(cudaStreamEndCapture(c2, &tmp));
     }
     FFM_G(add_conditional(c1, hacc, cudaGraphCondTypeIf, &bacc));
@@ -1245,6 +1273,9 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
     return fail(FFM_EINVAL, "ls_par K out of range");
   if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
+  if (cfg->method < kMethodLbfgs || cfg->method > kMethodSd) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method == kMethodCg && (cfg->cg_kind < 0 || cfg->cg_kind > 6 || cfg->restart_period < 1))
+    return fail(FFM_EINVAL, "bad CG variant");
   DeviceGuard guard(s->device);
   auto* L = new ffm_lbfgs();
   L->sys = s;
@@ -1264,6 +1295,9 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   c.k_plus = cfg->k_plus;
   c.k_minus = cfg->k_minus;
   c.trust = cfg->trust;
+  c.method = cfg->method;
+  c.cg_kind = cfg->cg_kind;
+  c.restart_period = cfg->restart_period;
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
   const int64_t n = L->n;
   const size_t nbuf = (size_t)n * (9 + 2 * (c.m + 1));
@@ -1316,6 +1350,9 @@ int ffm_lbfgs_start(ffm_lbfgs_t* L, const double* x_d, const double* g_d, double
   h.nfree = L->cfg.m + 1;
   for (int q = 0; q <= L->cfg.m; ++q) h.freel[q] = q;
   h.store_slot = -1;
+  if (L->cfg.method == kMethodCg)  // p = lincomb(-1, g) (ffmin/optimizers/cg.py:101)
+    FFM_CUDA(launch_axpby(L->n, nullptr, -1.0, 1.0, L->g, nullptr,
+                          0.0, nullptr, L->d, st));
   FFM_CUDA(cudaMemcpyAsync(L->S, &h, sizeof(h), cudaMemcpyHostToDevice, st));
   FFM_CUDA(cudaStreamSynchronize(st));  // h lives on this stack frame
   return FFM_OK;

@@ -156,6 +156,13 @@ cudaError_t launch_min_ls_post(MinState* S, double* rec, cudaGraphConditionalHan
                                cudaStream_t st);
 cudaError_t launch_min_acc_check(MinState* S, const int64_t* stw, cudaStream_t st);
 cudaError_t launch_min_commit(MinState* S, cudaStream_t st);
+// nonlinear CG: beta from S->cgd, p+ in place, descent check, p <- -src when S->cg_reset
+cudaError_t launch_min_cg_beta(MinState* S, cudaStream_t st);
+cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double* p,
+                             cudaStream_t st);
+cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st);
+cudaError_t launch_select_neg(MinState* S, int64_t n, const double* src, double* dst,
+                              cudaStream_t st);
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,
                              double* ring_s, double* ring_y, const double* x_new,
                              const double* g_new, double* x, double* g, cudaStream_t st);

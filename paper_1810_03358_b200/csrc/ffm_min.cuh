@@ -26,7 +26,13 @@ struct MinConfig {
   long long max_calls;    // -1: no bound (value + gradient calls)
   double thr;             // gradient-norm threshold
   double h0, eps_h, k_plus, k_minus, trust;
+  int method;          // kMethodLbfgs / kMethodCg / kMethodSd
+  int cg_kind;         // 0..6: fr, prp, prp+, hs, cd, ls, dy
+  int restart_period;  // CG: restart p <- -g every restart_period iterations
+  int pad;
 };
+
+enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2 };
 
 // run status codes (host maps them to the reference's strings)
 enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
@@ -64,6 +70,10 @@ struct MinState {
   double h_keep, f_keep;  // ls_h: first accepted probe
   int found, pad1;
   double res_h, res_f;
+  // CG (ffmin/optimizers/cg.py): the running direction p lives in the
+  // direction buffer; cgd = <g+,g+>, <g+,y>, <g,g>, <p,y>, <p,g>; pg = <p+,g+>
+  int since_restart, failures, cg_reset, cg_else;
+  double beta, cgd[5], pg;
 };
 
 }  // namespace ffm

@@ -251,6 +251,28 @@ __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir
 
 // after d (two-loop or antigradient) and <d, d>
 __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
+  if (S->c.method == kMethodSd) {
+    // r = div(lincomb(-1, g), |g|)  (ffmin/optimizers/gradient.py, Eq. (4))
+    S->dn = S->gn;
+    S->inv_dn = 1.0 / S->gn;
+    cudaGraphSetConditional(hls, 1);
+    return;
+  }
+  if (S->c.method == kMethodCg) {
+    // pn = |p|; a zero p restarts along the antigradient with pn = |g|
+    // (ffmin/optimizers/cg.py:107-110)
+    double pn = sqrt(S->dd);
+    S->cg_reset = 0;
+    if (pn == 0.0) {
+      S->cg_reset = 1;  // p <- -g (select_neg_kernel)
+      pn = S->gn;
+      S->since_restart = 0;
+    }
+    S->dn = pn;
+    S->inv_dn = 1.0 / pn;
+    cudaGraphSetConditional(hls, 1);
+    return;
+  }
   const double dn = sqrt(S->dd);
   S->dn = dn;
   if (dn == 0.0) {
@@ -297,6 +319,32 @@ __global__ void min_ls_step_kernel(MinState* S, const double* en, const int64_t*
 // lbfgs.py: what a line-search result does to the iteration
 __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditionalHandle hacc) {
   unsigned acc = 0;
+  if (!S->err && S->c.method == kMethodCg) {
+    // ffmin/optimizers/cg.py:112-124: a second consecutive failure ends the
+    // run (or records an idle iteration); every failure restarts p <- -g
+    S->cg_reset = 0;
+    if (!S->found) {
+      S->failures++;
+      if (S->failures >= 2) {
+        if (S->c.stop_on_ls_failure) {
+          S->status = kMinLsFailure;
+          S->done = 1;
+          cudaGraphSetConditional(hacc, 0);
+          return;
+        }
+        S->k++;
+        record(S, rec, 0.0);
+        S->failures = 0;
+      }
+      S->cg_reset = 1;
+      S->since_restart = 0;
+    } else {
+      S->failures = 0;
+      acc = 1;
+    }
+    cudaGraphSetConditional(hacc, acc);
+    return;
+  }
   if (!S->err) {
     if (!S->found) {
       if (S->count > 0 && !S->cleared) {
@@ -374,6 +422,70 @@ __global__ void min_store_kernel(const MinState* S, int64_t n, const double* __r
   }
 }
 
+// ---- nonlinear CG (ffmin/optimizers/cg.py:125-145), after the five dot
+// products <g+,g+>, <g+,y>, <g,g>, <p,y>, <p,g> (y = g+ - g)
+__device__ double cg_beta_of(int kind, const double* d) {
+  const double gg_new = d[0], gy = d[1], gg_old = d[2], py = d[3], pg = d[4];
+  double num, den;
+  switch (kind) {
+    case 0: num = gg_new; den = gg_old; break;                // fr
+    case 1: num = gy; den = gg_old; break;                    // prp
+    case 2: num = (0.0 > gy) ? 0.0 : gy; den = gg_old; break;  // prp+: max(gy, 0.0)
+    case 3: num = gy; den = py; break;                        // hs
+    case 4: num = gg_new; den = -pg; break;                   // cd
+    case 5: num = gy; den = -pg; break;                       // ls
+    default: num = gg_new; den = py; break;                   // dy
+  }
+  return den == 0.0 ? (double)NAN : num / den;
+}
+
+__global__ void min_cg_beta_kernel(MinState* S) {
+  if (S->err) return;
+  S->since_restart++;
+  if (S->since_restart >= S->c.restart_period) {
+    S->cg_else = 0;  // periodic restart: p+ = -g+
+    S->since_restart = 0;
+    S->beta = 0.0;
+  } else {
+    S->cg_else = 1;
+    S->beta = cg_beta_of(S->c.cg_kind, S->cgd);
+  }
+}
+
+// p+ = lincomb(-1, g+, beta, p) for a finite beta, else lincomb(-1, g+);
+// in place (each element reads its old p first)
+__global__ void cg_update_kernel(const MinState* S, int64_t n, const double* __restrict__ g_new,
+                                 double* __restrict__ p) {
+  if (S->err) return;
+  const double beta = S->beta;
+  const bool use_beta = S->cg_else && isfinite(beta);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = -1.0 * g_new[i];
+    p[i] = use_beta ? fma(beta, p[i], v) : v;
+  }
+}
+
+// descent test dot(p+, -g+) <= 0 (= -<p+, g+>, the negation is exact) or a
+// non-finite beta: restart p+ = -g+
+__global__ void min_cg_check_kernel(MinState* S) {
+  S->cg_reset = 0;
+  if (S->err || !S->cg_else) return;
+  if (!isfinite(S->beta) || -S->pg <= 0.0) {
+    S->cg_reset = 1;
+    S->since_restart = 0;
+  }
+}
+
+// dst = lincomb(-1, src) when *flag (device-decided restarts)
+__global__ void select_neg_kernel(const int* flag, const int* err, int64_t n,
+                                  const double* __restrict__ src, double* __restrict__ dst) {
+  if (!*flag || *err) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = -1.0 * src[i];
+}
+
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
@@ -425,6 +537,8 @@ cudaError_t launch_min_acc_check(MinState* S, const int64_t* stw, cudaStream_t s
   FFM_ONE(min_acc_check_kernel, S, stw);
 }
 cudaError_t launch_min_commit(MinState* S, cudaStream_t st) { FFM_ONE(min_commit_kernel, S); }
+cudaError_t launch_min_cg_beta(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_beta_kernel, S); }
+cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_check_kernel, S); }
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(min_iter_end_kernel, S, rec);
 }
@@ -432,6 +546,26 @@ cudaError_t launch_min_it_end(MinState* S, cudaGraphConditionalHandle hout, cuda
   FFM_ONE(min_it_end_kernel, S, hout);
 }
 #undef FFM_ONE
+
+static int vec_blocks(int64_t n) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  return blocks < 1 ? 1 : (int)blocks;
+}
+
+cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double* p,
+                             cudaStream_t st) {
+  count_launch();
+  cg_update_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, g_new, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_select_neg(MinState* S, int64_t n, const double* src, double* dst,
+                              cudaStream_t st) {
+  count_launch();
+  select_neg_kernel<<<vec_blocks(n), 256, 0, st>>>(&S->cg_reset, &S->err, n, src, dst);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,
                              double* ring_s, double* ring_y, const double* x_new,

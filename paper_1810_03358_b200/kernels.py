@@ -220,7 +220,7 @@ def farfield_build(coords, q, scale, atom, cutoff):
     eng = _engine((q, scale), lambda: _topology(n, q, None, np.zeros(n), scale, -1.0), n)
     import torch
 
-    c = torch.from_numpy(_f64coords(coords)).to(eng.device)
+    c = torch.from_numpy(np.array(_f64coords(coords))).to(eng.device)
     e, m, b = eng.farfield(c, int(atom), float(cutoff))
     e = e.cpu().numpy()
     return float(e[0]), float(e[1]), float(e[2]), float(e[3]), m.cpu().numpy(), int(b.item())

@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import math
 
+from . import graph
 from .common import (
     CONVERGED,
     DIVERGENCE_FACTOR,
@@ -56,6 +57,9 @@ def steepest_descent(oracle, x0, linesearch, stop=None) -> OptimizeResult:
     run, ops, x, f, g, gn = start(oracle, x0, stop,
                                   {"method": "sd", "linesearch": linesearch.describe()})
     status = CONVERGED if gn <= run.threshold else None
+    if status is None and graph.eligible(oracle, ops, linesearch):
+        # the whole iteration on the device (optimizers/graph.py)
+        return graph.run_graph(run, oracle, x, f, g, gn, linesearch, graph.SD)
     k = 0
     while status is None:
         status = run.budget_status(k)

@@ -135,7 +135,7 @@ class MolecularOracle(ObjectiveOracle):
 
     def initial_point(self):
         """x0 of the wrapped system as a device vector."""
-        return torch.from_numpy(np.ascontiguousarray(self.system.coords).reshape(-1)).to(
+        return torch.from_numpy(np.array(self.system.coords, dtype=np.float64).reshape(-1)).to(
             self.device)
 
     def _coerce(self, x):

@@ -192,3 +192,60 @@ def test_graph_lbfgs_budgets(golden, monkeypatch):
         a, _ = _run_lbfgs(s, True, monkeypatch, "par", 5, stop)
         b, _ = _run_lbfgs(s, False, monkeypatch, "par", 5, stop)
         assert a.status == b.status and a.iterations == b.iterations and a.f == b.f
+
+
+def _run_method(s, host_loop, monkeypatch, method, stop, dtype=np.float64, kind="par", **kw):
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import cg, make_linesearch, steepest_descent
+
+    if host_loop:
+        monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+    else:
+        monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+    o = MolecularOracle(s, dtype=dtype)
+    ls = make_linesearch(kind)
+    if method == "sd":
+        res = steepest_descent(o, s.coords.ravel(), ls, stop)
+    else:
+        from paper_1810_03358_b200.optimizers.cg import CgVariant
+
+        res = cg(o, s.coords.ravel(), CgVariant(kind=method, **kw), ls, stop)
+    return res, o
+
+
+@pytest.mark.parametrize("case", [
+    ("sd", "conv60", "par", {}), ("sd", "conv200", "h", {}),
+    ("fr", "conv200", "par", {}), ("prp", "conv200", "par", {}), ("prp+", "conv200", "h", {}),
+    ("hs", "conv60", "par", {}), ("cd", "conv60", "par", {}), ("ls", "conv200", "par", {}),
+    ("dy", "conv200", "par", {}), ("prp+", "conv200", "par", {"restart_period": 7}),
+    ("prp+", "globule", "par", {}), ("fr", "globule32", "par", {}),
+    ("sd", "globule32", "par", {})])
+def test_graph_cg_sd_equal_host_driven_loop(golden, monkeypatch, case):
+    """Nonlinear CG (all seven betas, periodic and descent restarts, the
+    two-failure rule) and steepest descent run as the same conditional CUDA
+    graph as L-BFGS: identical trace records, iterate, status and call
+    counts to the host-driven loop."""
+    from paper_1810_03358_b200.optimizers import StopCriteria
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    method, name, kind, kw = case
+    dtype = np.float32 if name == "globule32" else np.float64
+    if name.startswith("globule"):
+        s = make_globule_system(1500, seed=3)
+        stop = StopCriteria(max_iterations=60, gradient_norm_rtol=1e-4)
+    else:
+        s = golden_system(golden, name)
+        stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-6, gradient_norm_rtol=0.0,
+                            stop_on_linesearch_failure=(name != "conv60"))
+    a, oa = _run_method(s, True, monkeypatch, method, stop, dtype, kind, **kw)
+    b, ob = _run_method(s, False, monkeypatch, method, stop, dtype, kind, **kw)
+    assert "_graph_runs" not in oa.__dict__ and "_graph_runs" in ob.__dict__  # paths taken
+    ra = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in b.trace.records]
+    assert len(ra) == len(rb)
+    assert ra == rb
+    assert a.status == b.status and a.f == b.f and a.grad_norm == b.grad_norm
+    assert np.array_equal(a.x, b.x)
+    assert (oa.value_calls, oa.grad_calls) == (ob.value_calls, ob.grad_calls)
