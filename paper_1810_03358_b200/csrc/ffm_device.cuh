@@ -315,6 +315,7 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
     const int kk = a0 / kIB, mg = a0 / kJB, row = a0 - kk * kIB + lane;
     const int r0 = trow_ptr[kk], nr = trow_ptr[kk + 1] - r0;
     const int c0 = tcol_ptr[mg], nt = nr + tcol_ptr[mg + 1] - c0;
+#pragma unroll 4
     for (int k = warp; k < nt; k += NW) {
       const bool isrow = k < nr;
       const int st = isrow ? kIB : kJB;
@@ -326,6 +327,7 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
     }
   } else if (use_nb) {  // super-unit mode: [unit][3][S] rows and columns
     const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
+#pragma unroll 4
     for (int k = warp; k <= nb; k += NW) {
       const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
                           : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;

@@ -147,6 +147,23 @@ __device__ __forceinline__ double block_min(double v, double* red) {
   return s;
 }
 
+#ifdef FFM_UNIT_STAMPS
+// tuning aid (variant builds only): globaltimer stamps of each CTA's phases
+__device__ unsigned long long* g_unit_clock = nullptr;
+#define FFM_STAMP(k)                                                              \
+  do {                                                                            \
+    if (g_unit_clock && threadIdx.x == 0 && blockIdx.y == 0) {                    \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                       \
+      g_unit_clock[(size_t)blockIdx.x * 16 + (k)] = t_;                           \
+    }                                                                             \
+  } while (0)
+#else
+#define FFM_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
+
 // grid = (nunits, batch).  ipart/jpart: [nunits][3][S] gradient partials
 // (GRAD only); epart: [batch][nunits][3] = (coulomb, vdw, min r^2).
 #ifndef FFM_MINB
@@ -174,6 +191,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   T* jacc = reinterpret_cast<T*>(sl + kRep * S);  // [3][S]      (GRAD)
   T* ired = jacc + 3 * S;                      // [kWarps][3][kIB] (GRAD)
 
+  FFM_STAMP(0);
   const int u = plan.unit_list ? plan.unit_list[blockIdx.x] : blockIdx.x;
   const int bidx = blockIdx.y;
   pos += (size_t)bidx * plan.np;
@@ -227,6 +245,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   if (GRAD)
     for (int a = tid; a < 3 * S; a += kThreads) jacc[a] = T(0);
   __syncthreads();
+  FFM_STAMP(1);
 
   double Ec = 0.0, Ev = 0.0;
   T minr2 = T(1e30);
@@ -309,6 +328,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
       Ev += double(P::lo(ev2)) + double(P::hi(ev2));
       ec2 = P::zero();
       ev2 = P::zero();
+      if (ks == 0 && m < 32) FFM_STAMP(10 + m / kWarps);
     }
     if (GRAD) {
 #pragma unroll
@@ -321,6 +341,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
       }
     }
     }  // p0
+    if (ks < 8) FFM_STAMP(2 + ks);
     if (GRAD) {
       // cross-warp reduction of the i-rows of this sub-block (fixed order)
       __syncthreads();
@@ -348,6 +369,14 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     e[1] = ev;
     e[2] = mr;
   }
+#ifdef FFM_UNIT_STAMPS
+  if (g_unit_clock && tid == 0 && blockIdx.y == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    g_unit_clock[(size_t)blockIdx.x * 16 + 15] = smid;
+  }
+#endif
+  FFM_STAMP(14);
 }
 
 template <typename T, bool GRAD, bool CUTOFF>
@@ -439,3 +468,9 @@ cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* p
 }
 
 }  // namespace ffm
+
+#ifdef FFM_UNIT_STAMPS
+extern "C" int ffm_debug_unit_clock(void* clock_d) {
+  return (int)cudaMemcpyToSymbol(ffm::g_unit_clock, &clock_d, sizeof(void*));
+}
+#endif

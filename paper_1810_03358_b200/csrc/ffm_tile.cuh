@@ -64,7 +64,10 @@ __device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restric
 // i-atom pairs held per pass: FP32 keeps both packed pairs (4 i-atoms per
 // lane) live; FP64 sweeps them one after the other so the kernel fits 128
 // registers and two CTAs per SM
-template <typename T> struct PairsPerPass { static constexpr int value = 2; };
+#ifndef FFM_NP32
+#define FFM_NP32 2
+#endif
+template <typename T> struct PairsPerPass { static constexpr int value = FFM_NP32; };
 template <> struct PairsPerPass<double> { static constexpr int value = 1; };
 
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the

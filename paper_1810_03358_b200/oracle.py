@@ -145,19 +145,31 @@ class MolecularOracle(ObjectiveOracle):
                 x = x.to(device=self.device, dtype=torch.float64)
             return x.reshape(-1).contiguous()
         self._host_io = True
-        return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64).reshape(-1)).to(
-            self.device)
+        x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1)
+        if x.shape[0] != self.n:
+            raise ValueError(f"x must have {self.n} entries, got {x.shape[0]}")
+        return x
 
     def _out(self, g):
-        if self._host_io:
-            return g.cpu().numpy()
-        return g
+        return g  # _run already produced the caller's kind of vector
 
     def _run(self, x, grad):
-        self._x.view(-1).copy_(x)
+        # host vectors: one H2D copy straight into the evaluation buffer and
+        # one D2H copy of the gradient into a fresh page-locked array (from
+        # torch's caching host allocator: DMA at full speed, no staging; the
+        # NumPy array owns it), the 104-byte result block alongside; one
+        # synchronisation for both
+        host = isinstance(x, np.ndarray)
+        self._x.view(-1).copy_(torch.from_numpy(x) if host else x)
         self.engine.eval(self._x, self.precision, grad=self._g if grad else None,
                          energies=self._en, status=self._st)
-        self._host.copy_(self._res)  # the one synchronising readback
+        self._host.copy_(self._res, non_blocking=True)
+        g_out = None
+        if grad and host:
+            gp = torch.empty(self.n, dtype=torch.float64, pin_memory=True)
+            gp.copy_(self._g.view(-1), non_blocking=True)
+            g_out = gp.numpy()
+        torch.cuda.current_stream(self.device).synchronize()
         vals = self._host.numpy()
         en = vals[:N.FFM_NTERMS].copy()
         st = vals[N.FFM_NTERMS:].view(np.int64).copy()
@@ -166,7 +178,9 @@ class MolecularOracle(ObjectiveOracle):
         self.last_breakdown = en
         # EnergyBreakdown.total order (ffmin/energy.py:38-41)
         f = float(en[0]) + float(en[1]) + float(en[2]) + float(en[3]) + float(en[4])
-        return f, (self._g.view(-1).clone() if grad else None)
+        if grad and not host:
+            g_out = self._g.view(-1).clone()
+        return f, g_out
 
     def _value(self, x):
         return self._run(x, False)[0]
