@@ -40,6 +40,8 @@ METRIC = "pair-interactions/sec (energy+grad)"
 NATOMS = 100_000
 FLOP_PER_PAIR = 38  # 27 FP32 ops (10 of them FMA -> +10) + 1 rsqrt, DESIGN.md
 FMA_SLOTS_PER_PAIR = 24  # FP32 lane-ops on the FMA pipe per pair (SASS: 2 x 12 packed FFMA2/FMUL2/FADD2 per 2 pairs; r^-2 on MUFU)
+FP64_OPS_PER_PAIR = 32  # FP64-pipe operations per pair (ncu: fp64 pipe 66.9% at 12.87 ms)
+DFMA_PEAK = 18.49e12  # measured DFMA/s (63.6 per clk per SM, profiles/r01_pipes_microbench.txt)
 
 
 def parse():
@@ -344,6 +346,11 @@ def main():
                      "flop_per_pair": FLOP_PER_PAIR, "fma_pipe_frac": fma_frac,
                      "nb_ms": nb32, "nb_ms_f64": nb64,
                      "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt"},
+        "roofline_f64": {"bound": "fp64-pipe", "kernel": "nb_units_kernel<double,GRAD>",
+                         "achieved": nb_pairs_per_rank * FP64_OPS_PER_PAIR / (nb64 * 1e-3) / 1e12,
+                         "peak": DFMA_PEAK / 1e12, "unit": "T fp64-pipe ops/s",
+                         "frac": nb_pairs_per_rank * FP64_OPS_PER_PAIR / (nb64 * 1e-3) / DFMA_PEAK,
+                         "ops_per_pair": FP64_OPS_PER_PAIR, "nb_ms": nb64},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

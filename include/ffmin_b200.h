@@ -216,8 +216,9 @@ typedef struct {
    * 0 = L-BFGS (ffmin/optimizers/lbfgs.py:93-128), 1 = nonlinear conjugate
    * gradients (ffmin/optimizers/cg.py:95-152; cg_kind 0..6 = fr, prp, prp+,
    * hs, cd, ls, dy; restart every restart_period iterations), 2 = steepest
-   * descent (ffmin/optimizers/gradient.py, Eq. (4)).  m is ignored (but must
-   * be in range) for methods 1 and 2. */
+   * descent (ffmin/optimizers/gradient.py, Eq. (4)), 3 = FGM with the theta
+   * schedule and best-point tracking (ffmin/optimizers/fgm.py, Algorithm 1).
+   * m is ignored (but must be in range) for methods 1..3. */
   int32_t method;
   int32_t cg_kind;
   int32_t restart_period;
@@ -236,15 +237,18 @@ int ffm_lbfgs_run(ffm_lbfgs_t* run, void* stream);
  * 0 none / 1 converged / 2 iteration budget / 3 line-search failure /
  * 4 oracle budget, done, error 0 none / 1 evaluation / 2 divergence,
  * error came from a gradient evaluation, value calls, gradient calls,
- * memory pairs); dbls[4] = (f, |g|, warm-start step, ns since the chunk
- * started); rec_h[cap][7] receives the chunk's trace records (iteration, f,
- * |g|, step, value calls, gradient calls, ns since the chunk started),
+ * memory pairs); dbls[4] = (f, |g|, warm-start step, best f so far);
+ * rec_h[cap][8] receives the chunk's trace records (iteration, f, |g|, step,
+ * value calls, gradient calls, ns since the chunk started, best f),
  * *nrec their number; err_status_h[8] the status words of a failed
  * evaluation. */
 int ffm_lbfgs_poll(ffm_lbfgs_t* run, int64_t* ints, double* dbls, double* rec_h, int64_t cap,
                    int64_t* nrec, int64_t* err_status_h);
 /* copy the current iterate and gradient out (device pointers, 3n) */
 int ffm_lbfgs_result(ffm_lbfgs_t* run, double* x_d, double* g_d, void* stream);
+/* copy the best point seen so far out (device pointer, 3n; FGM's result
+ * unless the run converged -- OptimizationRun.finish_best) */
+int ffm_lbfgs_best(ffm_lbfgs_t* run, double* x_d, void* stream);
 int ffm_lbfgs_destroy(ffm_lbfgs_t* run);
 
 #ifdef __cplusplus

@@ -65,6 +65,7 @@ SIGNATURES = {
     "ffm_lbfgs_run": (_I, [_P, _P]),
     "ffm_lbfgs_poll": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
     "ffm_lbfgs_result": (_I, [_P, _P, _P, _P]),
+    "ffm_lbfgs_best": (_I, [_P, _P, _P]),
     "ffm_lbfgs_destroy": (_I, [_P]),
 }
 
@@ -83,9 +84,9 @@ class LbfgsConfig(C.Structure):
 
 LBFGS_STATUS = {0: None, 1: "converged", 2: "iteration_budget", 3: "linesearch_failure",
                 4: "oracle_budget"}
-LBFGS_REC_WIDTH = 7
+LBFGS_REC_WIDTH = 8
 # ffm_lbfgs_config.method / cg_kind codes
-METHOD_LBFGS, METHOD_CG, METHOD_SD = 0, 1, 2
+METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM = 0, 1, 2, 3
 CG_KINDS = ("fr", "prp", "prp+", "hs", "cd", "ls", "dy")
 
 _lock = threading.Lock()

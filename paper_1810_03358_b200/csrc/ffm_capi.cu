@@ -1047,8 +1047,9 @@ struct ffm_lbfgs {
   int64_t n = 0;  // 3 * atoms
   MinState* S = nullptr;
   double* rec = nullptr;
-  double* buf = nullptr;  // x, g, x_new, g_new, x_trial, d, r, s_tmp, y_tmp, ring S, ring Y
-  double *x, *g, *xn, *gnew, *xt, *d, *r, *st, *yt, *ring_s, *ring_y;
+  double* buf = nullptr;  // x, g, x_new, g_new, x_trial, d, r, s_tmp, y_tmp, best, ring S, ring Y
+  // (FGM: xn = w, st = x_prev, yt = x - x_prev, xt = x+ after the search)
+  double *x, *g, *xn, *gnew, *xt, *d, *r, *st, *yt, *best, *ring_s, *ring_y;
   double* scratch = nullptr;
   double* en = nullptr;      // energies of the last evaluation
   int64_t* stw = nullptr;    // its status words
@@ -1101,15 +1102,47 @@ int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls)
 
 int cap_trial(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hloop) {
   MinState* S = L->S;
-  // phi(h) = f(x + h r): lincomb(1.0, x, h, r)
-  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->h_trial, 0.0, L->r, L->xt, st));
+  // phi(h) = f(x + h r): lincomb(1.0, x, h, r)  (FGM: from w)
+  const double* base = L->cfg.method == kMethodFgm ? L->xn : L->x;
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, base, &S->h_trial, 0.0, L->r, L->xt, st));
   FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY, L->xt, nullptr, L->en, L->stw, st));
   FFM_CUDA(launch_min_ls_step(S, L->en, L->stw, hloop, st));
   return FFM_OK;
 }
 
+// FGM head of an iteration (ffmin/optimizers/fgm.py): theta / beta, the
+// extrapolated point w, f and grad f at w (skipped at k = 0, where w = x),
+// <g_w, g_w> and the checks; c3 captures the conditional evaluation
+int cap_fgm_head(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdir,
+                 cudaGraphConditionalHandle hls) {
+  MinState* S = L->S;
+  cudaGraphConditionalHandle heval;
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&heval, bdir, 0, 0));
+  FFM_CUDA(launch_fgm_pre(S, heval, st));
+  // w = lincomb(1, x, beta, lincomb(1, x, -1, x_prev))
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, nullptr, -1.0, L->st, L->yt, st));
+  FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->beta, 0.0, L->yt, L->xn, st));
+  cudaGraph_t beval = nullptr, tmp = nullptr;
+  FFM_TRYR(add_conditional(st, heval, cudaGraphCondTypeIf, &beval));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, beval, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+  int rc = issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->g, L->en, L->stw, c3);
+  cudaError_t e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  const double* gs[1] = {L->g};
+  FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
+  FFM_CUDA(launch_fgm_post_eval(S, L->en, L->stw, hls, st));
+  return FFM_OK;
+}
+
 int cap_accept(ffm_lbfgs* L, cudaStream_t st) {
   MinState* S = L->S;
+  if (L->cfg.method == kMethodFgm) {  // x+ = lincomb(1, w, h, r); no gradient at x+
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->xn, &S->res_h, 0.0, L->r, L->xt, st));
+    FFM_CUDA(launch_fgm_accept(S, L->rec, st));
+    return FFM_OK;
+  }
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->res_h, 0.0, L->r, L->xn, st));
   FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->gnew, L->en, L->stw,
                       st));
@@ -1206,13 +1239,16 @@ int lbfgs_build(ffm_lbfgs* L) {
     cudaGraph_t bdir = nullptr, bls = nullptr, bacc = nullptr, bloop = nullptr;
     FFM_G(add_conditional(c1, hdir, cudaGraphCondTypeIf, &bdir));
     FFM_GC(cudaStreamBeginCaptureToGraph(c2, bdir, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    FFM_G(cap_direction(L, c2, hls));
+    if (L->cfg.method == kMethodFgm)
+      FFM_G(cap_fgm_head(L, c2, c3, bdir, hls));
+    else
+      FFM_G(cap_direction(L, c2, hls));
     FFM_GC(cudaStreamEndCapture(c2, &tmp));
     FFM_G(add_conditional(c1, hls, cudaGraphCondTypeIf, &bls));
     {  // line search
       FFM_GC(cudaGraphConditionalHandleCreate(&hloop, bls, 0, 0));
       FFM_GC(cudaStreamBeginCaptureToGraph(c2, bls, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      if (L->cfg.method == kMethodSd)  // r = (1 / |g|) (-g)
+      if (L->cfg.method == kMethodSd || L->cfg.method == kMethodFgm)  // r = (1 / |g|) (-g)
         FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, -1.0, L->g, nullptr, 0.0, nullptr, L->r, c2));
       else
         FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
@@ -1232,6 +1268,8 @@ int lbfgs_build(ffm_lbfgs* L) {
     FFM_GC(cudaStreamBeginCaptureToGraph(c2, bacc, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     FFM_G(cap_accept(L, c2));
     FFM_GC(cudaStreamEndCapture(c2, &tmp));
+    if (L->cfg.method == kMethodFgm)
+      FFM_GC(launch_fgm_shift(S, L->n, L->x, L->st, L->xn, L->xt, L->best, c1));
     FFM_GC(launch_min_it_end(S, hout, c1));
     FFM_GC(cudaStreamEndCapture(c1, &tmp));
   }
@@ -1273,7 +1311,7 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
     return fail(FFM_EINVAL, "ls_par K out of range");
   if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
-  if (cfg->method < kMethodLbfgs || cfg->method > kMethodSd) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method < kMethodLbfgs || cfg->method > kMethodFgm) return fail(FFM_EINVAL, "bad method");
   if (cfg->method == kMethodCg && (cfg->cg_kind < 0 || cfg->cg_kind > 6 || cfg->restart_period < 1))
     return fail(FFM_EINVAL, "bad CG variant");
   DeviceGuard guard(s->device);
@@ -1300,7 +1338,7 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   c.restart_period = cfg->restart_period;
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
   const int64_t n = L->n;
-  const size_t nbuf = (size_t)n * (9 + 2 * (c.m + 1));
+  const size_t nbuf = (size_t)n * (10 + 2 * (c.m + 1));
   bool ok = cudaMalloc(&L->S, sizeof(MinState)) == cudaSuccess &&
             cudaMalloc(&L->rec, (size_t)(c.chunk + 1) * kMinRecWidth * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&L->buf, nbuf * sizeof(double)) == cudaSuccess &&
@@ -1313,7 +1351,8 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
     return fail(FFM_ENOMEM, "cudaMalloc failed for the L-BFGS run");
   }
   double* p = L->buf;
-  for (double** v : {&L->x, &L->g, &L->xn, &L->gnew, &L->xt, &L->d, &L->r, &L->st, &L->yt}) {
+  for (double** v : {&L->x, &L->g, &L->xn, &L->gnew, &L->xt, &L->d, &L->r, &L->st, &L->yt,
+                     &L->best}) {
     *v = p;
     p += n;
   }
@@ -1350,6 +1389,11 @@ int ffm_lbfgs_start(ffm_lbfgs_t* L, const double* x_d, const double* g_d, double
   h.nfree = L->cfg.m + 1;
   for (int q = 0; q <= L->cfg.m; ++q) h.freel[q] = q;
   h.store_slot = -1;
+  h.best_f = f;  // OptimizationRun.update_best(x0, f0)
+  h.theta_prev = h.theta = 1.0;
+  FFM_CUDA(cudaMemcpyAsync(L->best, x_d, nb, cudaMemcpyDeviceToDevice, st));
+  if (L->cfg.method == kMethodFgm)  // x_prev = copy(x0)
+    FFM_CUDA(cudaMemcpyAsync(L->st, x_d, nb, cudaMemcpyDeviceToDevice, st));
   if (L->cfg.method == kMethodCg)  // p = lincomb(-1, g) (ffmin/optimizers/cg.py:101)
     FFM_CUDA(launch_axpby(L->n, nullptr, -1.0, 1.0, L->g, nullptr,
                           0.0, nullptr, L->d, st));
@@ -1391,7 +1435,7 @@ int ffm_lbfgs_poll(ffm_lbfgs_t* L, int64_t* ints, double* dbls, double* rec_h, i
   dbls[0] = h.f;
   dbls[1] = h.gn;
   dbls[2] = h.warm;
-  dbls[3] = 0.0;
+  dbls[3] = h.best_f;
   const int64_t k = std::min<int64_t>(h.nrec, cap);
   if (k > 0 && rec_h)
     FFM_CUDA(cudaMemcpy(rec_h, L->rec, (size_t)k * kMinRecWidth * sizeof(double),
@@ -1409,6 +1453,15 @@ int ffm_lbfgs_result(ffm_lbfgs_t* L, double* x_d, double* g_d, void* stream) {
   const size_t nb = (size_t)3 * L->sys->plan.n * sizeof(double);
   if (x_d) FFM_CUDA(cudaMemcpyAsync(x_d, L->x, nb, cudaMemcpyDeviceToDevice, st));
   if (g_d) FFM_CUDA(cudaMemcpyAsync(g_d, L->g, nb, cudaMemcpyDeviceToDevice, st));
+  return FFM_OK;
+}
+
+int ffm_lbfgs_best(ffm_lbfgs_t* L, double* x_d, void* stream) {
+  if (!L || !x_d) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(L->sys->device);
+  const size_t nb = (size_t)3 * L->sys->plan.n * sizeof(double);
+  FFM_CUDA(cudaMemcpyAsync(x_d, L->best, nb, cudaMemcpyDeviceToDevice,
+                           static_cast<cudaStream_t>(stream)));
   return FFM_OK;
 }
 

@@ -163,6 +163,14 @@ cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double
 cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st);
 cudaError_t launch_select_neg(MinState* S, int64_t n, const double* src, double* dst,
                               cudaStream_t st);
+// FGM: theta / beta (heval = evaluate at w when k > 0), checks and |g_w| after
+// the evaluation, the accepted step, and the end-of-iteration vector shift
+cudaError_t launch_fgm_pre(MinState* S, cudaGraphConditionalHandle heval, cudaStream_t st);
+cudaError_t launch_fgm_post_eval(MinState* S, const double* en, const int64_t* stw,
+                                 cudaGraphConditionalHandle hls, cudaStream_t st);
+cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st);
+cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
+                             const double* x_new, double* best, cudaStream_t st);
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,
                              double* ring_s, double* ring_y, const double* x_new,
                              const double* g_new, double* x, double* g, cudaStream_t st);

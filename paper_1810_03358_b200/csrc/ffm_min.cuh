@@ -32,7 +32,7 @@ struct MinConfig {
   int pad;
 };
 
-enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2 };
+enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3 };
 
 // run status codes (host maps them to the reference's strings)
 enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
@@ -40,7 +40,7 @@ enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure 
 // error kinds
 enum : int { kMinErrNone = 0, kMinErrEval = 1, kMinErrDiverged = 2 };
 
-constexpr int kMinRecWidth = 7;  // k, f, |g|, step, value calls, grad calls, t (ns)
+constexpr int kMinRecWidth = 8;  // k, f, |g|, step, value calls, grad calls, t (ns), best f
 
 struct MinState {
   MinConfig c;
@@ -74,6 +74,12 @@ struct MinState {
   // direction buffer; cgd = <g+,g+>, <g+,y>, <g,g>, <p,y>, <p,g>; pg = <p+,g+>
   int since_restart, failures, cg_reset, cg_else;
   double beta, cgd[5], pg;
+  // best point so far (OptimizationRun.update_best) and FGM (ffmin/
+  // optimizers/fgm.py): theta schedule, f at the extrapolated point w, the
+  // end-of-iteration vector shift (1: x_prev <- x, x <- w; 2: x <- x+) and
+  // which vector becomes the best point (1: w, 2: x+)
+  double best_f, theta_prev, theta, fw;
+  int fgm_mode, best_src;
 };
 
 }  // namespace ffm

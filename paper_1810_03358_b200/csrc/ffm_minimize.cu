@@ -49,6 +49,7 @@ __device__ void record(MinState* S, double* rec, double step) {
   r[4] = (double)S->vcalls;
   r[5] = (double)S->gcalls;
   r[6] = (double)(globaltimer() - S->t_launch);
+  r[7] = S->best_f;
   S->nrec++;
 }
 
@@ -287,7 +288,7 @@ __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
 
 // after r = d / |d| and slope = <g, r>: LineSearcher.search, first attempt
 __global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop) {
-  S->f0 = S->f;
+  S->f0 = S->c.method == kMethodFgm ? S->fw : S->f;  // FGM searches from w
   S->attempt = 0;
   ls_start(S, S->warm);
   cudaGraphSetConditional(hloop, 1);
@@ -319,6 +320,28 @@ __global__ void min_ls_step_kernel(MinState* S, const double* en, const int64_t*
 // lbfgs.py: what a line-search result does to the iteration
 __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditionalHandle hacc) {
   unsigned acc = 0;
+  if (!S->err && S->c.method == kMethodFgm) {
+    // ffmin/optimizers/fgm.py: a failed search stops the run, or records an
+    // idle iteration and moves x to w
+    if (!S->found) {
+      if (S->c.stop_on_ls_failure) {
+        S->status = kMinLsFailure;
+        S->done = 1;
+      } else {
+        S->k++;
+        const double f = S->f;
+        S->f = S->fw;  // record(k, f_w, gn, 0.0)
+        record(S, rec, 0.0);
+        S->f = f;
+        S->fgm_mode = 1;
+        S->theta_prev = S->theta;
+      }
+    } else {
+      acc = 1;
+    }
+    cudaGraphSetConditional(hacc, acc);
+    return;
+  }
   if (!S->err && S->c.method == kMethodCg) {
     // ffmin/optimizers/cg.py:112-124: a second consecutive failure ends the
     // run (or records an idle iteration); every failure restarts p <- -g
@@ -486,11 +509,89 @@ __global__ void select_neg_kernel(const int* flag, const int* err, int64_t n,
     dst[i] = -1.0 * src[i];
 }
 
+// ---- FGM (ffmin/optimizers/fgm.py, Algorithm 1)
+// theta_k and beta_k from theta_{k-1}; the caller then forms
+// w = lincomb(1, x, beta, lincomb(1, x, -1, x_prev))
+__global__ void fgm_pre_kernel(MinState* S, cudaGraphConditionalHandle heval) {
+  const double tp = S->theta_prev;
+  const double theta = 0.5 * tp * (sqrt(tp * tp + 4.0) - tp);
+  S->theta = theta;
+  S->beta = tp * (1.0 - tp) / (tp * tp + theta);
+  S->fgm_mode = 0;
+  S->best_src = 0;
+  cudaGraphSetConditional(heval, S->k > 0 ? 1u : 0u);  // k == 0: f_w, g_w = f, g
+}
+
+// after f(w), grad f(w) (k > 0) and <g_w, g_w>: finiteness, best point,
+// |g_w| and the convergence test, then the search direction scale
+__global__ void fgm_post_eval_kernel(MinState* S, const double* en, const int64_t* stw,
+                                     cudaGraphConditionalHandle hls) {
+  cudaGraphSetConditional(hls, 0);
+  if (S->k > 0) {
+    S->vcalls++;
+    S->gcalls++;
+    if (bad_status(stw, true)) {
+      set_err(S, kMinErrEval, stw, true);
+      return;
+    }
+    S->fw = en[0] + en[1] + en[2] + en[3] + en[4];
+  } else {
+    S->fw = S->f;
+  }
+  if (!isfinite(S->fw) || !isfinite(S->gg)) {
+    set_err(S, kMinErrDiverged, nullptr, true);
+    return;
+  }
+  if (S->fw < S->best_f) {
+    S->best_f = S->fw;
+    S->best_src = 1;
+  }
+  S->gn = sqrt(S->gg);
+  if (S->gn <= S->c.thr) {
+    S->status = kMinConverged;
+    S->done = 1;
+    return;
+  }
+  S->dn = S->gn;
+  S->inv_dn = 1.0 / S->gn;  // r = div(lincomb(-1, g_w), |g_w|)
+  cudaGraphSetConditional(hls, 1);
+}
+
+__global__ void fgm_accept_kernel(MinState* S, double* rec) {
+  S->f = S->res_f;
+  S->theta_prev = S->theta;
+  S->k++;
+  if (S->f < S->best_f) {
+    S->best_f = S->f;
+    S->best_src = 2;
+  }
+  record(S, rec, S->res_h);
+  S->fgm_mode = 2;
+}
+
+// end of an FGM iteration: best point copy, then x_prev <- x, x <- w or x+
+__global__ void fgm_shift_kernel(const MinState* S, int64_t n, double* __restrict__ x,
+                                 double* __restrict__ x_prev, const double* __restrict__ w,
+                                 const double* __restrict__ x_new, double* __restrict__ best) {
+  if (S->err) return;
+  const int mode = S->fgm_mode, bs = S->best_src;
+  if (mode == 0 && bs == 0) return;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (bs) best[i] = bs == 1 ? w[i] : x_new[i];
+    if (mode) {
+      x_prev[i] = x[i];
+      x[i] = mode == 1 ? w[i] : x_new[i];
+    }
+  }
+}
+
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
   S->gn = sqrt(S->gg);
   S->k++;
+  if (S->f < S->best_f) S->best_f = S->f;
   record(S, rec, S->res_h);
   if (S->gn <= S->c.thr) {
     S->status = kMinConverged;
@@ -499,6 +600,8 @@ __global__ void min_iter_end_kernel(MinState* S, double* rec) {
 }
 
 __global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) {
+  S->fgm_mode = 0;  // consumed by fgm_shift_kernel
+  S->best_src = 0;
   cudaGraphSetConditional(hout, (!S->done && !S->pause) ? 1u : 0u);
 }
 
@@ -538,6 +641,16 @@ cudaError_t launch_min_acc_check(MinState* S, const int64_t* stw, cudaStream_t s
 }
 cudaError_t launch_min_commit(MinState* S, cudaStream_t st) { FFM_ONE(min_commit_kernel, S); }
 cudaError_t launch_min_cg_beta(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_beta_kernel, S); }
+cudaError_t launch_fgm_pre(MinState* S, cudaGraphConditionalHandle heval, cudaStream_t st) {
+  FFM_ONE(fgm_pre_kernel, S, heval);
+}
+cudaError_t launch_fgm_post_eval(MinState* S, const double* en, const int64_t* stw,
+                                 cudaGraphConditionalHandle hls, cudaStream_t st) {
+  FFM_ONE(fgm_post_eval_kernel, S, en, stw, hls);
+}
+cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st) {
+  FFM_ONE(fgm_accept_kernel, S, rec);
+}
 cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_check_kernel, S); }
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(min_iter_end_kernel, S, rec);
@@ -557,6 +670,13 @@ cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double
                              cudaStream_t st) {
   count_launch();
   cg_update_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, g_new, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
+                             const double* x_new, double* best, cudaStream_t st) {
+  count_launch();
+  fgm_shift_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, x, x_prev, w, x_new, best);
   return cudaGetLastError();
 }
 

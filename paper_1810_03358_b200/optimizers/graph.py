@@ -1,10 +1,10 @@
-"""Graph-resident drivers: L-BFGS, nonlinear CG and steepest descent with
+"""Graph-resident drivers: L-BFGS, nonlinear CG, steepest descent and FGM with
 the whole iteration on the device (include/ffmin_b200.h ffm_lbfgs_*,
 csrc/ffm_minimize.cu).
 
 The reference decides every line-search probe, curvature / beta dot product
 and convergence test in Python (ffmin/optimizers/lbfgs.py:93-128,
-cg.py:95-152, gradient.py; linesearch.py).  Here one CUDA graph with
+cg.py:95-152, gradient.py, fgm.py; linesearch.py).  Here one CUDA graph with
 conditional nodes runs up to GRAPH_CHUNK iterations per launch: single-thread
 controller kernels replay the drivers' scalar logic in IEEE double, vectors
 go through the same kernels as the host-driven loop, so the traces are
@@ -19,7 +19,7 @@ import os
 
 import numpy as np
 
-LBFGS, CG, SD = 0, 1, 2
+LBFGS, CG, SD, FGM = 0, 1, 2, 3
 GRAPH_CHUNK = 32  # iterations per graph launch between host polls
 
 
@@ -113,7 +113,7 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
             run.trace.append(TraceRecord(
                 iteration=int(r[0]), f=float(r[1]), grad_norm=float(r[2]), step=float(r[3]),
                 value_calls=calls0[0] + int(r[4]), grad_calls=calls0[1] + int(r[5]),
-                wall_seconds=t_launch + float(r[6]) * 1e-9, best_f=float(r[1])))
+                wall_seconds=t_launch + float(r[6]) * 1e-9, best_f=float(r[7])))
         oracle.value_calls = calls0[0] + int(ints[5])
         oracle.grad_calls = calls0[1] + int(ints[6])
         if ints[3] == 1:
@@ -133,6 +133,10 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
     N.check(lib.ffm_lbfgs_result(h, C.c_void_p(x_out.data_ptr()), C.c_void_p(g_out.data_ptr()),
                                  stream), "ffm_lbfgs_result")
     f_out, gn_out = float(dbls[0]), float(dbls[1])
-    # every accepted step strictly lowers f: the iterate is the best point
-    run.best_f, run.best_x = f_out, x_out
+    if method == FGM:  # the extrapolated points can be the best ones
+        best = torch.empty_like(x)
+        N.check(lib.ffm_lbfgs_best(h, C.c_void_p(best.data_ptr()), stream), "ffm_lbfgs_best")
+        run.best_f, run.best_x = float(dbls[3]), best
+    else:  # every accepted step strictly lowers f: the iterate is the best point
+        run.best_f, run.best_x = f_out, x_out
     return run.finish_best(status, x_out, f_out, gn_out)

@@ -196,7 +196,7 @@ def test_graph_lbfgs_budgets(golden, monkeypatch):
 
 def _run_method(s, host_loop, monkeypatch, method, stop, dtype=np.float64, kind="par", **kw):
     from paper_1810_03358_b200.oracle import MolecularOracle
-    from paper_1810_03358_b200.optimizers import cg, make_linesearch, steepest_descent
+    from paper_1810_03358_b200.optimizers import cg, fgm, make_linesearch, steepest_descent
 
     if host_loop:
         monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
@@ -206,6 +206,8 @@ def _run_method(s, host_loop, monkeypatch, method, stop, dtype=np.float64, kind=
     ls = make_linesearch(kind)
     if method == "sd":
         res = steepest_descent(o, s.coords.ravel(), ls, stop)
+    elif method == "fgm":
+        res = fgm(o, s.coords.ravel(), ls, stop)
     else:
         from paper_1810_03358_b200.optimizers.cg import CgVariant
 
@@ -219,12 +221,14 @@ def _run_method(s, host_loop, monkeypatch, method, stop, dtype=np.float64, kind=
     ("hs", "conv60", "par", {}), ("cd", "conv60", "par", {}), ("ls", "conv200", "par", {}),
     ("dy", "conv200", "par", {}), ("prp+", "conv200", "par", {"restart_period": 7}),
     ("prp+", "globule", "par", {}), ("fr", "globule32", "par", {}),
-    ("sd", "globule32", "par", {})])
+    ("sd", "globule32", "par", {}), ("fgm", "conv200", "par", {}), ("fgm", "conv60", "h", {}),
+    ("fgm", "conv60", "par", {}), ("fgm", "globule", "par", {}), ("fgm", "globule32", "h", {})])
 def test_graph_cg_sd_equal_host_driven_loop(golden, monkeypatch, case):
     """Nonlinear CG (all seven betas, periodic and descent restarts, the
-    two-failure rule) and steepest descent run as the same conditional CUDA
-    graph as L-BFGS: identical trace records, iterate, status and call
-    counts to the host-driven loop."""
+    two-failure rule), steepest descent and FGM (theta schedule, search from
+    the extrapolated point, best-point tracking) run as the same conditional
+    CUDA graph as L-BFGS: identical trace records (best f included),
+    iterate, status and call counts to the host-driven loop."""
     from paper_1810_03358_b200.optimizers import StopCriteria
     from paper_1810_03358_b200.synth import make_globule_system
 
