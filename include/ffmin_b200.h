@@ -218,11 +218,20 @@ typedef struct {
    * hs, cd, ls, dy; restart every restart_period iterations), 2 = steepest
    * descent (ffmin/optimizers/gradient.py, Eq. (4)), 3 = FGM with the theta
    * schedule and best-point tracking (ffmin/optimizers/fgm.py, Algorithm 1).
-   * m is ignored (but must be in range) for methods 1..3. */
+   * m is ignored (but must be in range) for methods 1..4. */
   int32_t method;
   int32_t cg_kind;
   int32_t restart_period;
   int32_t reserved;
+  /* method 4 = fixed-step family (ffmin/optimizers/gradient.py): momentum_kind
+   * 0 = gradient descent x+ = x - step g (Eq. (2)), 1 = heavy ball with
+   * constant momentum (Eq. (9)), 2 = Nesterov with (k-1)/(k+2) and the
+   * gradient at the extrapolated point (Eq. (10)), 3 = the strongly convex
+   * Nesterov scheme with constant momentum (Eq. (11)); no line search. */
+  double fixed_step;
+  double momentum;
+  int32_t momentum_kind;
+  int32_t reserved2;
 } ffm_lbfgs_config;
 
 int ffm_lbfgs_create(ffm_system_t* sys, int precision, const ffm_lbfgs_config* cfg,

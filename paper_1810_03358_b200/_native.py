@@ -79,14 +79,16 @@ class LbfgsConfig(C.Structure):
                 ("max_oracle_calls", C.c_int64), ("threshold", C.c_double),
                 ("h0", C.c_double), ("eps_h", C.c_double), ("k_plus", C.c_double),
                 ("k_minus", C.c_double), ("trust", C.c_double), ("method", C.c_int32),
-                ("cg_kind", C.c_int32), ("restart_period", C.c_int32), ("reserved", C.c_int32)]
+                ("cg_kind", C.c_int32), ("restart_period", C.c_int32), ("reserved", C.c_int32),
+                ("fixed_step", C.c_double), ("momentum", C.c_double),
+                ("momentum_kind", C.c_int32), ("reserved2", C.c_int32)]
 
 
 LBFGS_STATUS = {0: None, 1: "converged", 2: "iteration_budget", 3: "linesearch_failure",
                 4: "oracle_budget"}
 LBFGS_REC_WIDTH = 8
 # ffm_lbfgs_config.method / cg_kind codes
-METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM = 0, 1, 2, 3
+METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM, METHOD_FIXED = 0, 1, 2, 3, 4
 CG_KINDS = ("fr", "prp", "prp+", "hs", "cd", "ls", "dy")
 
 _lock = threading.Lock()

@@ -516,10 +516,14 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   if (cudaMalloc(&s->d_ilj32, (size_t)p.np * 2 * sizeof(float)) != cudaSuccess ||
       cudaMalloc(&s->d_ilj64, (size_t)p.np * 2 * sizeof(double)) != cudaSuccess)
     FFM_TRY(fail(FFM_ENOMEM, "cudaMalloc failed for LJ records"));
-  if (launch_ilj(p.np, false, s->d_lj64, s->d_ilj32, 0) != cudaSuccess ||
-      launch_ilj(p.np, true, s->d_lj64, s->d_ilj64, 0) != cudaSuccess ||
-      cudaDeviceSynchronize() != cudaSuccess)
-    FFM_TRY(fail(FFM_ECUDA, "building the LJ pair records failed"));
+  {
+    cudaError_t e = launch_ilj(p.np, false, s->d_lj64, s->d_ilj32, 0);
+    if (e == cudaSuccess) e = launch_ilj(p.np, true, s->d_lj64, s->d_ilj64, 0);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess)
+      FFM_TRY(fail(FFM_ECUDA, std::string("building the LJ pair records failed: ") +
+                                  cudaGetErrorString(e)));
+  }
   FFM_TRY(upload(&s->d_q, qv));
   FFM_TRY(upload(&s->d_sigma, sg));
   FFM_TRY(upload(&s->d_eps, ep));
@@ -1042,6 +1046,7 @@ int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const doubl
 
 struct ffm_lbfgs {
   ffm_system* sys = nullptr;
+  int device = 0;  // kept apart from sys: destroy must not touch a freed system
   int prec = 0;
   MinConfig cfg{};
   int64_t n = 0;  // 3 * atoms
@@ -1133,6 +1138,49 @@ int cap_fgm_head(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdi
   const double* gs[1] = {L->g};
   FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
   FFM_CUDA(launch_fgm_post_eval(S, L->en, L->stw, hls, st));
+  return FFM_OK;
+}
+
+// fixed-step family (ffmin/optimizers/gradient.py): the whole iteration,
+// no line search; c3 captures the conditional gradient at w (Nesterov)
+int cap_fixed(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdir) {
+  MinState* S = L->S;
+  const int kind = L->cfg.momentum_kind;
+  const double step = L->cfg.fixed_step;
+  // the conditional gradient at w exists only for the Nesterov schemes (a
+  // handle without its conditional node fails graph instantiation)
+  cudaGraphConditionalHandle heval{};
+  if (kind >= 2) FFM_CUDA(cudaGraphConditionalHandleCreate(&heval, bdir, 0, 0));
+  FFM_CUDA(launch_mom_pre(S, heval, kind >= 2 ? 1 : 0, st));
+  double* x_new = L->xn;
+  if (kind == 0) {  // x - step g
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, nullptr, -step, L->g, L->xn, st));
+  } else if (kind == 1) {  // lincomb(1, lincomb(1, x, -step, g), m, lincomb(1, x, -1, x_prev))
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, nullptr, -step, L->g, L->yt, st));
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, nullptr, -1.0, L->st, L->d, st));
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->yt, &S->beta, 0.0, L->d, L->xn, st));
+  } else {  // w = lincomb(1, x, m, x - x_prev); g_w (k > 0); x+ = lincomb(1, w, -step, g_w)
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, nullptr, -1.0, L->st, L->d, st));
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->beta, 0.0, L->d, L->xn, st));
+    cudaGraph_t beval = nullptr, tmp = nullptr;
+    FFM_TRYR(add_conditional(st, heval, cudaGraphCondTypeIf, &beval));
+    FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, beval, nullptr, nullptr, 0,
+                                           cudaStreamCaptureModeRelaxed));
+    int rc = issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->g, L->en, L->stw, c3);
+    if (!rc && launch_mom_wcheck(S, L->stw, c3) != cudaSuccess) rc = fail(FFM_ECUDA, "mom_wcheck");
+    cudaError_t e = cudaStreamEndCapture(c3, &tmp);
+    if (rc) return rc;
+    FFM_CUDA(e);
+    FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->xn, nullptr, -step, L->g, L->xt, st));
+    x_new = L->xt;
+  }
+  FFM_CUDA(launch_fgm_shift(S, L->n, L->x, L->st, L->xn, x_new, L->best, st));
+  const bool wform = kind >= 2;
+  FFM_TRYR(issue_eval(L->sys, L->prec, wform ? FFM_ENERGY : (FFM_ENERGY | FFM_GRAD), L->x,
+                      wform ? nullptr : L->g, L->en, L->stw, st));
+  const double* gs[1] = {L->g};
+  FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
+  FFM_CUDA(launch_mom_post(S, L->en, L->stw, L->rec, st));
   return FFM_OK;
 }
 
@@ -1241,6 +1289,8 @@ int lbfgs_build(ffm_lbfgs* L) {
     FFM_GC(cudaStreamBeginCaptureToGraph(c2, bdir, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
     if (L->cfg.method == kMethodFgm)
       FFM_G(cap_fgm_head(L, c2, c3, bdir, hls));
+    else if (L->cfg.method == kMethodFixed)
+      FFM_G(cap_fixed(L, c2, c3, bdir));
     else
       FFM_G(cap_direction(L, c2, hls));
     FFM_GC(cudaStreamEndCapture(c2, &tmp));
@@ -1311,12 +1361,16 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
     return fail(FFM_EINVAL, "ls_par K out of range");
   if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
-  if (cfg->method < kMethodLbfgs || cfg->method > kMethodFgm) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method < kMethodLbfgs || cfg->method > kMethodFixed) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method == kMethodFixed &&
+      (cfg->momentum_kind < 0 || cfg->momentum_kind > 3 || !(cfg->fixed_step > 0.0)))
+    return fail(FFM_EINVAL, "bad fixed-step configuration");
   if (cfg->method == kMethodCg && (cfg->cg_kind < 0 || cfg->cg_kind > 6 || cfg->restart_period < 1))
     return fail(FFM_EINVAL, "bad CG variant");
   DeviceGuard guard(s->device);
   auto* L = new ffm_lbfgs();
   L->sys = s;
+  L->device = s->device;
   L->prec = precision;
   MinConfig& c = L->cfg;
   c.m = cfg->m;
@@ -1336,6 +1390,9 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   c.method = cfg->method;
   c.cg_kind = cfg->cg_kind;
   c.restart_period = cfg->restart_period;
+  c.momentum_kind = cfg->momentum_kind;
+  c.fixed_step = cfg->fixed_step;
+  c.momentum = cfg->momentum;
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
   const int64_t n = L->n;
   const size_t nbuf = (size_t)n * (10 + 2 * (c.m + 1));
@@ -1390,9 +1447,10 @@ int ffm_lbfgs_start(ffm_lbfgs_t* L, const double* x_d, const double* g_d, double
   for (int q = 0; q <= L->cfg.m; ++q) h.freel[q] = q;
   h.store_slot = -1;
   h.best_f = f;  // OptimizationRun.update_best(x0, f0)
+  h.f_init = f;
   h.theta_prev = h.theta = 1.0;
   FFM_CUDA(cudaMemcpyAsync(L->best, x_d, nb, cudaMemcpyDeviceToDevice, st));
-  if (L->cfg.method == kMethodFgm)  // x_prev = copy(x0)
+  if (L->cfg.method == kMethodFgm || L->cfg.method == kMethodFixed)  // x_prev = copy(x0)
     FFM_CUDA(cudaMemcpyAsync(L->st, x_d, nb, cudaMemcpyDeviceToDevice, st));
   if (L->cfg.method == kMethodCg)  // p = lincomb(-1, g) (ffmin/optimizers/cg.py:101)
     FFM_CUDA(launch_axpby(L->n, nullptr, -1.0, 1.0, L->g, nullptr,
@@ -1467,7 +1525,9 @@ int ffm_lbfgs_best(ffm_lbfgs_t* L, double* x_d, void* stream) {
 
 int ffm_lbfgs_destroy(ffm_lbfgs_t* L) {
   if (!L) return FFM_OK;
-  DeviceGuard guard(L->sys->device);
+  // (its system may already be gone: garbage collection of a reference
+  // cycle finalises in any order; L->sys is not dereferenced here)
+  DeviceGuard guard(L->device);
   cudaDeviceSynchronize();
   lbfgs_free(L);
   delete L;

@@ -169,6 +169,13 @@ cudaError_t launch_fgm_pre(MinState* S, cudaGraphConditionalHandle heval, cudaSt
 cudaError_t launch_fgm_post_eval(MinState* S, const double* en, const int64_t* stw,
                                  cudaGraphConditionalHandle hls, cudaStream_t st);
 cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st);
+// fixed-step family: momentum coefficient (heval = gradient at w), the
+// check after grad f(w), and the bookkeeping after the evaluation at x+
+cudaError_t launch_mom_pre(MinState* S, cudaGraphConditionalHandle heval, int has_eval,
+                           cudaStream_t st);
+cudaError_t launch_mom_wcheck(MinState* S, const int64_t* stw, cudaStream_t st);
+cudaError_t launch_mom_post(MinState* S, const double* en, const int64_t* stw, double* rec,
+                            cudaStream_t st);
 cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
                              const double* x_new, double* best, cudaStream_t st);
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,

@@ -26,13 +26,14 @@ struct MinConfig {
   long long max_calls;    // -1: no bound (value + gradient calls)
   double thr;             // gradient-norm threshold
   double h0, eps_h, k_plus, k_minus, trust;
-  int method;          // kMethodLbfgs / kMethodCg / kMethodSd
+  int method;          // kMethodLbfgs / kMethodCg / kMethodSd / kMethodFgm / kMethodFixed
   int cg_kind;         // 0..6: fr, prp, prp+, hs, cd, ls, dy
   int restart_period;  // CG: restart p <- -g every restart_period iterations
-  int pad;
+  int momentum_kind;   // fixed-step family: 0 GD, 1 heavy ball, 2 NAG, 3 NAG-SC
+  double fixed_step, momentum;
 };
 
-enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3 };
+enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3, kMethodFixed = 4 };
 
 // run status codes (host maps them to the reference's strings)
 enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
@@ -80,6 +81,7 @@ struct MinState {
   // which vector becomes the best point (1: w, 2: x+)
   double best_f, theta_prev, theta, fw;
   int fgm_mode, best_src;
+  double f_init;  // f(x0): the fixed-step divergence test
 };
 
 }  // namespace ffm

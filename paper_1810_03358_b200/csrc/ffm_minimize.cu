@@ -586,6 +586,53 @@ __global__ void fgm_shift_kernel(const MinState* S, int64_t n, double* __restric
   }
 }
 
+// ---- fixed-step family (ffmin/optimizers/gradient.py): GD, heavy ball,
+// Nesterov (NAG, NAG-SC).  coef(k) and whether the gradient at w is needed
+__global__ void mom_pre_kernel(MinState* S, cudaGraphConditionalHandle heval, int has_eval) {
+  const int kind = S->c.momentum_kind;
+  const double k = (double)S->k;
+  S->beta = kind == 2 ? (k - 1.0) / (k + 2.0) : S->c.momentum;
+  S->fgm_mode = 2;  // x_prev <- x, x <- x+ (fgm_shift_kernel)
+  S->best_src = 0;
+  if (has_eval) cudaGraphSetConditional(heval, (kind >= 2 && S->k > 0) ? 1u : 0u);
+}
+
+// after grad f(w) (Nesterov schemes, k > 0): oracle.gradient(w)
+__global__ void mom_wcheck_kernel(MinState* S, const int64_t* stw) {
+  S->gcalls++;
+  if (bad_status(stw, true)) set_err(S, kMinErrEval, stw, true);
+}
+
+// after f (and grad f) at x+ and <g, g>: call counts, error / divergence
+// tests, record, convergence
+__global__ void mom_post_kernel(MinState* S, const double* en, const int64_t* stw, double* rec) {
+  if (S->err) return;
+  const int kind = S->c.momentum_kind;
+  const bool wform = kind >= 2;
+  S->vcalls++;
+  if (!wform) S->gcalls++;  // value_and_gradient(x+)
+  if (bad_status(stw, !wform)) {
+    set_err(S, kMinErrEval, stw, !wform);
+    return;
+  }
+  const double f = en[0] + en[1] + en[2] + en[3] + en[4];
+  const double af0 = fabs(S->f_init);
+  const bool diverged = !isfinite(f) || (kind > 0 && f > 1e3 * (af0 > 1.0 ? af0 : 1.0));
+  S->f = f;
+  if (diverged || !isfinite(S->gg)) {
+    set_err(S, kMinErrDiverged, nullptr, true);
+    return;
+  }
+  S->gn = sqrt(S->gg);
+  S->k++;
+  if (f < S->best_f) S->best_f = f;
+  record(S, rec, S->c.fixed_step);
+  if (S->gn <= S->c.thr) {
+    S->status = kMinConverged;
+    S->done = 1;
+  }
+}
+
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
@@ -650,6 +697,17 @@ cudaError_t launch_fgm_post_eval(MinState* S, const double* en, const int64_t* s
 }
 cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(fgm_accept_kernel, S, rec);
+}
+cudaError_t launch_mom_pre(MinState* S, cudaGraphConditionalHandle heval, int has_eval,
+                           cudaStream_t st) {
+  FFM_ONE(mom_pre_kernel, S, heval, has_eval);
+}
+cudaError_t launch_mom_wcheck(MinState* S, const int64_t* stw, cudaStream_t st) {
+  FFM_ONE(mom_wcheck_kernel, S, stw);
+}
+cudaError_t launch_mom_post(MinState* S, const double* en, const int64_t* stw, double* rec,
+                            cudaStream_t st) {
+  FFM_ONE(mom_post_kernel, S, en, stw, rec);
 }
 cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_check_kernel, S); }
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {

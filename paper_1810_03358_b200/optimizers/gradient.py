@@ -35,6 +35,10 @@ def gradient_descent_fixed(oracle, x0, L, stop=None) -> OptimizeResult:
     run, ops, x, f, g, gn = start(oracle, x0, stop, {"method": "gd", "L": L})
     status = CONVERGED if gn <= run.threshold else None
     step = 1.0 / L
+    if status is None and graph.eligible_fixed(oracle, ops):
+        # the whole iteration on the device (optimizers/graph.py)
+        return graph.run_graph(run, oracle, x, f, g, gn, None, graph.FIXED, step=step,
+                               momentum_kind=graph.GD)
     k = 0
     while status is None:
         status = run.budget_status(k)
@@ -87,11 +91,17 @@ def steepest_descent(oracle, x0, linesearch, stop=None) -> OptimizeResult:
     return run.finish_best(status, x, f, gn)
 
 
-def _momentum_run(oracle, x0, stop, meta, step, coef, use_w_gradient):
+def _momentum_run(oracle, x0, stop, meta, step, coef, use_w_gradient, kind=None, m=0.0):
     """Shared loop of heavy ball (gradient at x) and the Nesterov schemes
-    (gradient at the extrapolated point w)."""
+    (gradient at the extrapolated point w).  kind / m: the graph path's
+    momentum_kind and constant momentum (optimizers/graph.py)."""
     run, ops, x, f, g, gn = start(oracle, x0, stop, meta)
     f0 = f
+    if gn > run.threshold and kind is not None and graph.eligible_fixed(oracle, ops):
+        # the whole iteration on the device
+        msg = run.trace.meta.pop("_diverge", None)
+        return graph.run_graph(run, oracle, x, f, g, gn, None, graph.FIXED, step=step,
+                               momentum=m, momentum_kind=kind, diverge_msg=msg)
     x_prev = ops.copy(x)
     status = CONVERGED if gn <= run.threshold else None
     k = 0
@@ -135,7 +145,8 @@ def heavy_ball(oracle, x0, alpha, beta, stop=None) -> OptimizeResult:
     meta = {"method": "hb", "alpha": alpha, "beta": beta,
             "_diverge": "heavy ball diverged at iteration {k}: f={f!r} (start f={f0!r}); "
                         "reduce alpha or beta"}
-    return _momentum_run(oracle, x0, stop, meta, alpha, lambda k: beta, False)
+    return _momentum_run(oracle, x0, stop, meta, alpha, lambda k: beta, False,
+                         graph.HEAVY_BALL, beta)
 
 
 def nesterov_momentum(oracle, x0, L, stop=None) -> OptimizeResult:
@@ -145,7 +156,8 @@ def nesterov_momentum(oracle, x0, L, stop=None) -> OptimizeResult:
         raise ValueError("L must be positive")
     meta = {"method": "nag", "L": L,
             "_diverge": "nesterov momentum diverged at iteration {k}: f={f!r}"}
-    return _momentum_run(oracle, x0, stop, meta, 1.0 / L, lambda k: (k - 1.0) / (k + 2.0), True)
+    return _momentum_run(oracle, x0, stop, meta, 1.0 / L, lambda k: (k - 1.0) / (k + 2.0), True,
+                         graph.NAG)
 
 
 def nesterov_strongly_convex(oracle, x0, L, mu, stop=None) -> OptimizeResult:
@@ -157,4 +169,4 @@ def nesterov_strongly_convex(oracle, x0, L, mu, stop=None) -> OptimizeResult:
     m = (math.sqrt(L) - math.sqrt(mu)) / (math.sqrt(L) + math.sqrt(mu))
     meta = {"method": "nag-sc", "L": L, "mu": mu,
             "_diverge": "strongly convex nesterov diverged at iteration {k}: f={f!r}"}
-    return _momentum_run(oracle, x0, stop, meta, 1.0 / L, lambda k: m, True)
+    return _momentum_run(oracle, x0, stop, meta, 1.0 / L, lambda k: m, True, graph.NAG_SC, m)

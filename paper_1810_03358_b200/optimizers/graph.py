@@ -19,19 +19,28 @@ import os
 
 import numpy as np
 
-LBFGS, CG, SD, FGM = 0, 1, 2, 3
+LBFGS, CG, SD, FGM, FIXED = 0, 1, 2, 3, 4
+# fixed-step family (method FIXED): momentum_kind
+GD, HEAVY_BALL, NAG, NAG_SC = 0, 1, 2, 3
 GRAPH_CHUNK = 32  # iterations per graph launch between host polls
+
+
+def eligible_fixed(oracle, ops) -> bool:
+    """The device molecular oracle (and FFMIN_B200_HOST_LOOP unset): the
+    fixed-step drivers run in the graph."""
+    from ..oracle import MolecularOracle
+
+    if os.environ.get("FFMIN_B200_HOST_LOOP"):
+        return False
+    return ops.space == "device" and type(oracle) is MolecularOracle
 
 
 def eligible(oracle, ops, linesearch, m: int = 1) -> bool:
     """The device molecular oracle with a built-in line searcher (and
     FFMIN_B200_HOST_LOOP unset): the graph path applies."""
-    from ..oracle import MolecularOracle
     from .common import LineSearcher
 
-    if os.environ.get("FFMIN_B200_HOST_LOOP"):
-        return False
-    if ops.space != "device" or type(oracle) is not MolecularOracle:
+    if not eligible_fixed(oracle, ops):
         return False
     if not isinstance(linesearch, LineSearcher) or not 1 <= m <= 32:
         return False
@@ -62,9 +71,12 @@ class _GraphRun:
 
 
 def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
-              restart_period=100):
+              restart_period=100, step=0.0, momentum=0.0, momentum_kind=GD,
+              diverge_msg=None):
     """Run the iterations of `method` on the device from (x, f, g, |g|) and
-    finish `run` like the host loop would."""
+    finish `run` like the host loop would.  linesearch is None for the
+    fixed-step family (method FIXED: step, momentum, momentum_kind;
+    diverge_msg formats its divergence error with k, f and f0)."""
     import torch
 
     from .. import _native as N
@@ -72,8 +84,14 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
     from .common import TIME_BUDGET, DivergenceError, TraceRecord
 
     stop = run.stop
-    c = linesearch.config
-    kind = 1 if linesearch.kind == "par" else 0
+    if linesearch is None:  # fixed-step family: the line-search fields are unused
+        from ..linesearch import LsParConfig
+
+        c, kind, warm = LsParConfig(), 1, 1.0
+    else:
+        c = linesearch.config
+        kind = 1 if linesearch.kind == "par" else 0
+        warm = float(linesearch.h)
     calls0 = (oracle.value_calls, oracle.grad_calls)
     chunk = 4 if stop.max_wall_time is not None else GRAPH_CHUNK
     cfg = N.LbfgsConfig(
@@ -87,7 +105,10 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         k_plus=0.0 if kind else c.k_plus, k_minus=0.0 if kind else c.k_minus,
         trust=c.trust if kind else 0.0, method=method,
         cg_kind=N.CG_KINDS.index(cg_kind) if method == CG else 0,
-        restart_period=int(restart_period) if method == CG else 1, reserved=0)
+        restart_period=int(restart_period) if method == CG else 1, reserved=0,
+        fixed_step=float(step) if method == FIXED else 0.0,
+        momentum=float(momentum) if method == FIXED else 0.0,
+        momentum_kind=int(momentum_kind) if method == FIXED else 0, reserved2=0)
     key = tuple(getattr(cfg, name) for name, _ in cfg._fields_)
     cache = oracle.__dict__.setdefault("_graph_runs", {})
     gr = cache.get(key)
@@ -96,7 +117,7 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
     lib, h = gr.lib, gr.handle
     stream = C.c_void_p(torch.cuda.current_stream(oracle.device).cuda_stream)
     N.check(lib.ffm_lbfgs_start(h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), f, gn,
-                                float(linesearch.h), stream), "ffm_lbfgs_start")
+                                warm, stream), "ffm_lbfgs_start")
     ints = np.zeros(8, np.int64)
     dbls = np.zeros(4)
     recs = np.zeros((gr.cap, N.LBFGS_REC_WIDTH))
@@ -119,6 +140,9 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         if ints[3] == 1:
             raise_status(oracle.system, errst, grad=bool(ints[4]))
         if ints[3] == 2:
+            if diverge_msg is not None:
+                raise DivergenceError(diverge_msg.format(k=int(ints[0]) + 1, f=float(dbls[0]),
+                                                         f0=f))
             raise DivergenceError(f"non-finite objective or gradient at iteration "
                                   f"{int(ints[0]) + 1}")
         if ints[2]:
@@ -127,7 +151,8 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         if stop.max_wall_time is not None and run.elapsed() >= stop.max_wall_time:
             status = TIME_BUDGET
             break
-    linesearch.h = float(dbls[2])
+    if linesearch is not None:
+        linesearch.h = float(dbls[2])
     x_out = torch.empty_like(x)
     g_out = torch.empty_like(g)
     N.check(lib.ffm_lbfgs_result(h, C.c_void_p(x_out.data_ptr()), C.c_void_p(g_out.data_ptr()),

@@ -253,3 +253,62 @@ def test_graph_cg_sd_equal_host_driven_loop(golden, monkeypatch, case):
     assert a.status == b.status and a.f == b.f and a.grad_norm == b.grad_norm
     assert np.array_equal(a.x, b.x)
     assert (oa.value_calls, oa.grad_calls) == (ob.value_calls, ob.grad_calls)
+
+
+@pytest.mark.parametrize("name", ["gd", "hb", "nag", "nagsc", "sd_h", "fgm", "lbfgs", "cg_prp+"])
+@pytest.mark.parametrize("system", ["drv30", "globule"])
+def test_graph_drivers_equal_host_loop_table(golden, monkeypatch, name, system):
+    """Every graph-resident driver of the golden driver table (fixed-step GD,
+    heavy ball, both Nesterov schemes, and the line-searched ones) against
+    the host-driven loop on the same oracle: identical records and iterate."""
+    from drivers_common import driver_runs
+
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = golden_system(golden, "drv30") if system == "drv30" else make_globule_system(1200, seed=5)
+    out = []
+    for host in (True, False):
+        if host:
+            monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+        else:
+            monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+        o = MolecularOracle(s)
+        res = driver_runs(s.coords.ravel())[name](o)
+        out.append((res, o))
+    (a, oa), (b, ob) = out
+    assert "_graph_runs" not in oa.__dict__ and "_graph_runs" in ob.__dict__
+    ra = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in b.trace.records]
+    assert ra == rb
+    assert a.status == b.status and a.f == b.f and a.grad_norm == b.grad_norm
+    assert np.array_equal(a.x, b.x)
+    assert a.trace.meta == b.trace.meta
+
+
+@pytest.mark.parametrize("driver", ["gd", "hb", "nag"])
+def test_graph_fixed_step_divergence_matches_host(golden, monkeypatch, driver):
+    """A step far too long diverges: the graph raises the host loop's
+    DivergenceError, message included."""
+    from paper_1810_03358_b200.optimizers import (
+        DivergenceError, StopCriteria, gradient_descent_fixed, heavy_ball, nesterov_momentum)
+    from paper_1810_03358_b200.oracle import MolecularOracle
+
+    s = golden_system(golden, "drv30")
+    stop = StopCriteria(max_iterations=200, gradient_norm_rtol=0.0)
+    run = {"gd": lambda o: gradient_descent_fixed(o, s.coords.ravel(), 0.5, stop),
+           "hb": lambda o: heavy_ball(o, s.coords.ravel(), 2.0, 0.9, stop),
+           "nag": lambda o: nesterov_momentum(o, s.coords.ravel(), 0.5, stop)}[driver]
+    msgs = []
+    for host in (True, False):
+        if host:
+            monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+        else:
+            monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+        o = MolecularOracle(s)
+        with pytest.raises(Exception) as ei:
+            run(o)
+        msgs.append((type(ei.value).__name__, str(ei.value), o.value_calls, o.grad_calls))
+    assert msgs[0] == msgs[1]
