@@ -218,7 +218,8 @@ typedef struct {
    * hs, cd, ls, dy; restart every restart_period iterations), 2 = steepest
    * descent (ffmin/optimizers/gradient.py, Eq. (4)), 3 = FGM with the theta
    * schedule and best-point tracking (ffmin/optimizers/fgm.py, Algorithm 1).
-   * m is ignored (but must be in range) for methods 1..4. */
+   * m is ignored (but must be in range) for methods 1..5 (5 = OFGM, see
+   * ffm_lbfgs_set_schedule). */
   int32_t method;
   int32_t cg_kind;
   int32_t restart_period;
@@ -244,7 +245,7 @@ int ffm_lbfgs_start(ffm_lbfgs_t* run, const double* x_d, const double* g_d, doub
 int ffm_lbfgs_run(ffm_lbfgs_t* run, void* stream);
 /* synchronise and read the run state.  ints[8] = (iterations, status
  * 0 none / 1 converged / 2 iteration budget / 3 line-search failure /
- * 4 oracle budget, done, error 0 none / 1 evaluation / 2 divergence,
+ * 4 oracle budget / 5 horizon complete, done, error 0 none / 1 evaluation / 2 divergence,
  * error came from a gradient evaluation, value calls, gradient calls,
  * memory pairs); dbls[4] = (f, |g|, warm-start step, best f so far);
  * rec_h[cap][8] receives the chunk's trace records (iteration, f, |g|, step,
@@ -255,6 +256,10 @@ int ffm_lbfgs_poll(ffm_lbfgs_t* run, int64_t* ints, double* dbls, double* rec_h,
                    int64_t* nrec, int64_t* err_status_h);
 /* copy the current iterate and gradient out (device pointers, 3n) */
 int ffm_lbfgs_result(ffm_lbfgs_t* run, double* x_d, double* g_d, void* stream);
+/* OFGM (method 5, ffmin/optimizers/fgm.py Eq. (12)): the schedule t[0..N]
+ * (len = N + 1, ofgm_schedule), before ffm_lbfgs_start; fixed_step = 1/L
+ * selects the fixed-step variant, 0 the line-searched one */
+int ffm_lbfgs_set_schedule(ffm_lbfgs_t* run, const double* t_h, int64_t len);
 /* copy the best point seen so far out (device pointer, 3n; FGM's result
  * unless the run converged -- OptimizationRun.finish_best) */
 int ffm_lbfgs_best(ffm_lbfgs_t* run, double* x_d, void* stream);

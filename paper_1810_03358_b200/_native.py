@@ -66,6 +66,7 @@ SIGNATURES = {
     "ffm_lbfgs_poll": (_I, [_P, _P, _P, _P, _I64, _P, _P]),
     "ffm_lbfgs_result": (_I, [_P, _P, _P, _P]),
     "ffm_lbfgs_best": (_I, [_P, _P, _P]),
+    "ffm_lbfgs_set_schedule": (_I, [_P, _P, _I64]),
     "ffm_lbfgs_destroy": (_I, [_P]),
 }
 
@@ -85,10 +86,10 @@ class LbfgsConfig(C.Structure):
 
 
 LBFGS_STATUS = {0: None, 1: "converged", 2: "iteration_budget", 3: "linesearch_failure",
-                4: "oracle_budget"}
+                4: "oracle_budget", 5: "horizon_complete"}
 LBFGS_REC_WIDTH = 8
 # ffm_lbfgs_config.method / cg_kind codes
-METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM, METHOD_FIXED = 0, 1, 2, 3, 4
+METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM, METHOD_FIXED, METHOD_OFGM = 0, 1, 2, 3, 4, 5
 CG_KINDS = ("fr", "prp", "prp+", "hs", "cd", "ls", "dy")
 
 _lock = threading.Lock()

@@ -1053,12 +1053,16 @@ struct ffm_lbfgs {
   MinState* S = nullptr;
   double* rec = nullptr;
   double* buf = nullptr;  // x, g, x_new, g_new, x_trial, d, r, s_tmp, y_tmp, best, ring S, ring Y
-  // (FGM: xn = w, st = x_prev, yt = x - x_prev, xt = x+ after the search)
+  // (FGM: xn = w, st = x_prev, yt = x - x_prev, xt = x+ after the search;
+  //  OFGM: xn = y, gnew = grad f(y), d = the aggregated direction)
   double *x, *g, *xn, *gnew, *xt, *d, *r, *st, *yt, *best, *ring_s, *ring_y;
   double* scratch = nullptr;
   double* en = nullptr;      // energies of the last evaluation
   int64_t* stw = nullptr;    // its status words
-  cudaStream_t cap[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaStream_t cap[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* gsum = nullptr;    // OFGM: running weighted gradient sum
+  double* anchor = nullptr;  // OFGM: x0
+  double* sched = nullptr;   // OFGM: t[0..N] (device)
   cudaGraphExec_t exec = nullptr;
   long long gen = -1;
   std::vector<double> rec_h;
@@ -1108,7 +1112,7 @@ int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls)
 int cap_trial(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hloop) {
   MinState* S = L->S;
   // phi(h) = f(x + h r): lincomb(1.0, x, h, r)  (FGM: from w)
-  const double* base = L->cfg.method == kMethodFgm ? L->xn : L->x;
+  const double* base = (L->cfg.method == kMethodFgm || L->cfg.method == kMethodOfgm) ? L->xn : L->x;
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, base, &S->h_trial, 0.0, L->r, L->xt, st));
   FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY, L->xt, nullptr, L->en, L->stw, st));
   FFM_CUDA(launch_min_ls_step(S, L->en, L->stw, hloop, st));
@@ -1181,6 +1185,100 @@ int cap_fixed(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdir) 
   const double* gs[1] = {L->g};
   FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
   FFM_CUDA(launch_mom_post(S, L->en, L->stw, L->rec, st));
+  return FFM_OK;
+}
+
+// OFGM (ffmin/optimizers/fgm.py, Eq. (12)): the whole iteration inside the
+// IF(go) body; c3 / c4 capture the nested bodies (x = y, or the search)
+int cap_ofgm(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaStream_t c4, cudaGraph_t bdir) {
+  MinState* S = L->S;
+  const int64_t n = L->n;
+  FFM_CUDA(launch_ofgm_pre(S, st));
+  // grad_sum = lincomb(1, grad_sum, t_k, g); d = lincomb(1 - 1/t, g, 2/t, grad_sum);
+  // y = lincomb(1 - 1/t, x, 1/t, anchor)
+  FFM_CUDA(launch_axpby(n, nullptr, 1.0, 1.0, L->gsum, &S->oc[0], 0.0, L->g, L->gsum, st));
+  FFM_CUDA(launch_axpby(n, &S->oc[1], 0.0, 1.0, L->g, &S->oc[2], 0.0, L->gsum, L->d, st));
+  FFM_CUDA(launch_axpby(n, &S->oc[1], 0.0, 1.0, L->x, &S->oc[3], 0.0, L->anchor, L->xn, st));
+  const double* gs[1] = {L->g};
+  if (L->cfg.fixed_step > 0.0) {  // x = lincomb(1, y, -(1/L), d); f, g = value_and_gradient(x)
+    FFM_CUDA(launch_axpby(n, nullptr, 1.0, 1.0, L->xn, nullptr, -L->cfg.fixed_step, L->d, L->x,
+                          st));
+    FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->g, L->en, L->stw, st));
+    FFM_CUDA(launch_dots(n, 1, gs, gs, L->scratch, &S->gg, st));
+    FFM_CUDA(launch_ofgm_post(S, L->en, L->stw, L->rec, 1, st));
+    return FFM_OK;
+  }
+  const double* ds[1] = {L->d};
+  FFM_CUDA(launch_dots(n, 1, ds, ds, L->scratch, &S->dd, st));
+  cudaGraphConditionalHandle hz, hnz, hloop;
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&hz, bdir, 0, 0));
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&hnz, bdir, 0, 0));
+  FFM_CUDA(launch_ofgm_dir(S, hz, hnz, st));
+  cudaGraph_t bz = nullptr, bnz = nullptr, bloop = nullptr, tmp = nullptr;
+  int rc = FFM_OK;
+  cudaError_t e;
+  // dn == 0: x = y, f = value(x)
+  FFM_TRYR(add_conditional(st, hz, cudaGraphCondTypeIf, &bz));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, bz, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  if (launch_ofgm_x(S, n, L->xn, L->r, L->x, 0, c3) != cudaSuccess) rc = fail(FFM_ECUDA, "ofgm_x");
+  if (!rc) rc = issue_eval(L->sys, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, c3);
+  if (!rc && launch_ofgm_value(S, L->en, L->stw, 1, c3) != cudaSuccess) rc = fail(FFM_ECUDA, "ofgm_value");
+  e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  // dn > 0: r = div(lincomb(-1, d), dn); f_y = value(y); [g_y = gradient(y)];
+  // search from y; x = lincomb(1, y, h, r) or y
+  FFM_TRYR(add_conditional(st, hnz, cudaGraphCondTypeIf, &bnz));
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&hloop, bnz, 0, 0));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, bnz, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  do {
+    if (launch_axpby(n, &S->inv_dn, 0.0, -1.0, L->d, nullptr, 0.0, nullptr, L->r, c3) != cudaSuccess) {
+      rc = fail(FFM_ECUDA, "axpby");
+      break;
+    }
+    if ((rc = issue_eval(L->sys, L->prec, FFM_ENERGY, L->xn, nullptr, L->en, L->stw, c3))) break;
+    if (launch_ofgm_value(S, L->en, L->stw, 0, c3) != cudaSuccess) {
+      rc = fail(FFM_ECUDA, "ofgm_value");
+      break;
+    }
+    if (L->cfg.ls_needs_grad) {
+      if ((rc = issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->gnew, L->en, L->stw,
+                           c3)))
+        break;
+      const double* gy[1] = {L->gnew};
+      const double* rs[1] = {L->r};
+      if (launch_ofgm_gcheck(S, L->stw, c3) != cudaSuccess ||
+          launch_dots(n, 1, gy, rs, L->scratch, &S->slope, c3) != cudaSuccess) {
+        rc = fail(FFM_ECUDA, "ofgm slope");
+        break;
+      }
+    }
+    if (launch_min_ls_init(S, hloop, c3) != cudaSuccess) {
+      rc = fail(FFM_ECUDA, "ls_init");
+      break;
+    }
+    if ((rc = add_conditional(c3, hloop, cudaGraphCondTypeWhile, &bloop))) break;
+    if (cudaStreamBeginCaptureToGraph(c4, bloop, nullptr, nullptr, 0,
+                                      cudaStreamCaptureModeRelaxed) != cudaSuccess) {
+      rc = fail(FFM_ECUDA, "capture");
+      break;
+    }
+    rc = cap_trial(L, c4, hloop);
+    e = cudaStreamEndCapture(c4, &tmp);
+    if (!rc && e != cudaSuccess) rc = fail(FFM_ECUDA, "capture end");
+    if (rc) break;
+    if (launch_ofgm_ls_post(S, c3) != cudaSuccess ||
+        launch_ofgm_x(S, n, L->xn, L->r, L->x, 1, c3) != cudaSuccess)
+      rc = fail(FFM_ECUDA, "ofgm_ls_post");
+  } while (false);
+  e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  // g = gradient(x)
+  FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->g, L->en, L->stw, st));
+  FFM_CUDA(launch_ofgm_gcheck(S, L->stw, st));
+  FFM_CUDA(launch_dots(n, 1, gs, gs, L->scratch, &S->gg, st));
+  FFM_CUDA(launch_ofgm_post(S, L->en, L->stw, L->rec, 0, st));
   return FFM_OK;
 }
 
@@ -1271,7 +1369,7 @@ int lbfgs_build(ffm_lbfgs* L) {
   } while (0)
   cudaGraphConditionalHandle hout, hdir, hls, hacc, hloop;
   FFM_GC(cudaGraphConditionalHandleCreate(&hout, top, 1, cudaGraphCondAssignDefault));
-  cudaStream_t c0 = L->cap[0], c1 = L->cap[1], c2 = L->cap[2], c3 = L->cap[3];
+  cudaStream_t c0 = L->cap[0], c1 = L->cap[1], c2 = L->cap[2], c3 = L->cap[3], c4 = L->cap[4];
   cudaGraph_t tmp = nullptr;
   // top: launch_begin -> WHILE(hout) { iteration }
   FFM_GC(cudaStreamBeginCaptureToGraph(c0, top, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
@@ -1291,6 +1389,8 @@ int lbfgs_build(ffm_lbfgs* L) {
       FFM_G(cap_fgm_head(L, c2, c3, bdir, hls));
     else if (L->cfg.method == kMethodFixed)
       FFM_G(cap_fixed(L, c2, c3, bdir));
+    else if (L->cfg.method == kMethodOfgm)
+      FFM_G(cap_ofgm(L, c2, c3, c4, bdir));
     else
       FFM_G(cap_direction(L, c2, hls));
     FFM_GC(cudaStreamEndCapture(c2, &tmp));
@@ -1340,7 +1440,7 @@ int lbfgs_build(ffm_lbfgs* L) {
 void lbfgs_free(ffm_lbfgs* L) {
   if (L->exec) cudaGraphExecDestroy(L->exec);
   for (void* p : {(void*)L->S, (void*)L->rec, (void*)L->buf, (void*)L->scratch, (void*)L->en,
-                  (void*)L->stw})
+                  (void*)L->stw, (void*)L->sched})
     if (p) cudaFree(p);
   for (cudaStream_t c : L->cap)
     if (c) cudaStreamDestroy(c);
@@ -1361,7 +1461,7 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
     return fail(FFM_EINVAL, "ls_par K out of range");
   if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
-  if (cfg->method < kMethodLbfgs || cfg->method > kMethodFixed) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method < kMethodLbfgs || cfg->method > kMethodOfgm) return fail(FFM_EINVAL, "bad method");
   if (cfg->method == kMethodFixed &&
       (cfg->momentum_kind < 0 || cfg->momentum_kind > 3 || !(cfg->fixed_step > 0.0)))
     return fail(FFM_EINVAL, "bad fixed-step configuration");
@@ -1393,9 +1493,12 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   c.momentum_kind = cfg->momentum_kind;
   c.fixed_step = cfg->fixed_step;
   c.momentum = cfg->momentum;
+  c.ls_needs_grad = cfg->ls_kind == 1 && cfg->use_gradient_start;
+  c.horizon = 0;
+  c.sched = nullptr;
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
   const int64_t n = L->n;
-  const size_t nbuf = (size_t)n * (10 + 2 * (c.m + 1));
+  const size_t nbuf = (size_t)n * (12 + 2 * (c.m + 1));
   bool ok = cudaMalloc(&L->S, sizeof(MinState)) == cudaSuccess &&
             cudaMalloc(&L->rec, (size_t)(c.chunk + 1) * kMinRecWidth * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&L->buf, nbuf * sizeof(double)) == cudaSuccess &&
@@ -1409,7 +1512,7 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   }
   double* p = L->buf;
   for (double** v : {&L->x, &L->g, &L->xn, &L->gnew, &L->xt, &L->d, &L->r, &L->st, &L->yt,
-                     &L->best}) {
+                     &L->best, &L->gsum, &L->anchor}) {
     *v = p;
     p += n;
   }
@@ -1450,6 +1553,11 @@ int ffm_lbfgs_start(ffm_lbfgs_t* L, const double* x_d, const double* g_d, double
   h.f_init = f;
   h.theta_prev = h.theta = 1.0;
   FFM_CUDA(cudaMemcpyAsync(L->best, x_d, nb, cudaMemcpyDeviceToDevice, st));
+  if (L->cfg.method == kMethodOfgm) {
+    if (!L->sched) return fail(FFM_EINVAL, "OFGM needs ffm_lbfgs_set_schedule before start");
+    FFM_CUDA(cudaMemcpyAsync(L->anchor, x_d, nb, cudaMemcpyDeviceToDevice, st));  // anchor = x0
+    FFM_CUDA(cudaMemsetAsync(L->gsum, 0, nb, st));                                // zeros_like
+  }
   if (L->cfg.method == kMethodFgm || L->cfg.method == kMethodFixed)  // x_prev = copy(x0)
     FFM_CUDA(cudaMemcpyAsync(L->st, x_d, nb, cudaMemcpyDeviceToDevice, st));
   if (L->cfg.method == kMethodCg)  // p = lincomb(-1, g) (ffmin/optimizers/cg.py:101)
@@ -1511,6 +1619,18 @@ int ffm_lbfgs_result(ffm_lbfgs_t* L, double* x_d, double* g_d, void* stream) {
   const size_t nb = (size_t)3 * L->sys->plan.n * sizeof(double);
   if (x_d) FFM_CUDA(cudaMemcpyAsync(x_d, L->x, nb, cudaMemcpyDeviceToDevice, st));
   if (g_d) FFM_CUDA(cudaMemcpyAsync(g_d, L->g, nb, cudaMemcpyDeviceToDevice, st));
+  return FFM_OK;
+}
+
+int ffm_lbfgs_set_schedule(ffm_lbfgs_t* L, const double* t_h, int64_t len) {
+  if (!L || !t_h || len < 2) return fail(FFM_EINVAL, "bad OFGM schedule");
+  DeviceGuard guard(L->device);
+  if (L->sched) cudaFree(L->sched);
+  L->sched = nullptr;
+  FFM_CUDA(cudaMalloc(&L->sched, (size_t)len * sizeof(double)));
+  FFM_CUDA(cudaMemcpy(L->sched, t_h, (size_t)len * sizeof(double), cudaMemcpyHostToDevice));
+  L->cfg.horizon = len - 1;
+  L->cfg.sched = L->sched;
   return FFM_OK;
 }
 

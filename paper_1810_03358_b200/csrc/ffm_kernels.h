@@ -176,6 +176,19 @@ cudaError_t launch_mom_pre(MinState* S, cudaGraphConditionalHandle heval, int ha
 cudaError_t launch_mom_wcheck(MinState* S, const int64_t* stw, cudaStream_t st);
 cudaError_t launch_mom_post(MinState* S, const double* en, const int64_t* stw, double* rec,
                             cudaStream_t st);
+// OFGM (Eq. (12)): schedule coefficients, the dn == 0 / search split, value
+// and gradient bookkeeping, the search result, x from y, end of iteration
+cudaError_t launch_ofgm_pre(MinState* S, cudaStream_t st);
+cudaError_t launch_ofgm_dir(MinState* S, cudaGraphConditionalHandle hz,
+                            cudaGraphConditionalHandle hnz, cudaStream_t st);
+cudaError_t launch_ofgm_value(MinState* S, const double* en, const int64_t* stw, int which,
+                              cudaStream_t st);
+cudaError_t launch_ofgm_gcheck(MinState* S, const int64_t* stw, cudaStream_t st);
+cudaError_t launch_ofgm_ls_post(MinState* S, cudaStream_t st);
+cudaError_t launch_ofgm_x(MinState* S, int64_t n, const double* y, const double* r, double* x,
+                          int from_ls, cudaStream_t st);
+cudaError_t launch_ofgm_post(MinState* S, const double* en, const int64_t* stw, double* rec,
+                             int from_en, cudaStream_t st);
 cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
                              const double* x_new, double* best, cudaStream_t st);
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,

@@ -31,13 +31,20 @@ struct MinConfig {
   int restart_period;  // CG: restart p <- -g every restart_period iterations
   int momentum_kind;   // fixed-step family: 0 GD, 1 heavy ball, 2 NAG, 3 NAG-SC
   double fixed_step, momentum;
+  // OFGM: horizon N and the schedule t[0..N] (device array, ffm_lbfgs_set_schedule);
+  // fixed_step > 0 selects the 1/L variant, else the line-searched one
+  long long horizon;
+  const double* sched;
+  int ls_needs_grad;   // the line search seeds from the slope (ls_par + gradient start)
+  int pad2;
 };
 
-enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3, kMethodFixed = 4 };
+enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3, kMethodFixed = 4,
+             kMethodOfgm = 5 };
 
 // run status codes (host maps them to the reference's strings)
 enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
-             kMinOracleBudget = 4 };
+             kMinOracleBudget = 4, kMinHorizon = 5 };
 // error kinds
 enum : int { kMinErrNone = 0, kMinErrEval = 1, kMinErrDiverged = 2 };
 
@@ -82,6 +89,8 @@ struct MinState {
   double best_f, theta_prev, theta, fw;
   int fgm_mode, best_src;
   double f_init;  // f(x0): the fixed-step divergence test
+  // OFGM: t_k, 1 - 1/t_{k+1}, 2/t_{k+1}, 1/t_{k+1}; the iteration's step
+  double oc[4], step;
 };
 
 }  // namespace ffm

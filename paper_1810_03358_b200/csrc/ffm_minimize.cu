@@ -234,7 +234,10 @@ __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir
   const MinConfig& c = S->c;
   if (!S->done) {
     // Run.budget_status order: iterations, (wall time: host, per chunk), calls
-    if (c.max_iter >= 0 && S->k >= c.max_iter) {
+    if (c.method == kMethodOfgm && S->k >= c.horizon) {  // fgm.py: checked first
+      S->status = kMinHorizon;
+      S->done = 1;
+    } else if (c.max_iter >= 0 && S->k >= c.max_iter) {
       S->status = kMinIterBudget;
       S->done = 1;
     } else if (c.max_calls >= 0 && S->vcalls + S->gcalls >= c.max_calls) {
@@ -288,7 +291,12 @@ __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
 
 // after r = d / |d| and slope = <g, r>: LineSearcher.search, first attempt
 __global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop) {
-  S->f0 = S->c.method == kMethodFgm ? S->fw : S->f;  // FGM searches from w
+  if (S->err) {  // an evaluation before the search failed (OFGM: value(y))
+    cudaGraphSetConditional(hloop, 0);
+    return;
+  }
+  // FGM searches from w, OFGM from y
+  S->f0 = (S->c.method == kMethodFgm || S->c.method == kMethodOfgm) ? S->fw : S->f;
   S->attempt = 0;
   ls_start(S, S->warm);
   cudaGraphSetConditional(hloop, 1);
@@ -633,6 +641,109 @@ __global__ void mom_post_kernel(MinState* S, const double* en, const int64_t* st
   }
 }
 
+// ---- OFGM (ffmin/optimizers/fgm.py, Eq. (12))
+// the schedule coefficients of iteration k (host arithmetic: 1.0 - 1.0 / t,
+// 2.0 / t, 1.0 / t)
+__global__ void ofgm_pre_kernel(MinState* S) {
+  const double tk = S->c.sched[S->k], tk1 = S->c.sched[S->k + 1];
+  S->oc[0] = tk;
+  S->oc[1] = 1.0 - 1.0 / tk1;
+  S->oc[2] = 2.0 / tk1;
+  S->oc[3] = 1.0 / tk1;
+  S->step = S->c.fixed_step;
+  S->fgm_mode = 0;
+  S->best_src = 0;
+}
+
+// line-searched variant, after <d, d>: dn == 0 takes x = y (hz), else the
+// search along -d / |d| from y (hnz)
+__global__ void ofgm_dir_kernel(MinState* S, cudaGraphConditionalHandle hz,
+                                cudaGraphConditionalHandle hnz) {
+  const double dn = sqrt(S->dd);
+  S->dn = dn;
+  if (dn == 0.0) {
+    S->step = 0.0;
+    cudaGraphSetConditional(hz, 1);
+    cudaGraphSetConditional(hnz, 0);
+  } else {
+    S->inv_dn = 1.0 / dn;
+    cudaGraphSetConditional(hz, 0);
+    cudaGraphSetConditional(hnz, 1);
+  }
+}
+
+// after an energy-only evaluation: value(y) (which = 0: f_y, seeds the
+// search) or value(x) with x = y (which = 1: f)
+__global__ void ofgm_value_kernel(MinState* S, const double* en, const int64_t* stw, int which) {
+  if (S->err) return;
+  S->vcalls++;
+  if (bad_status(stw, false)) {
+    set_err(S, kMinErrEval, stw, false);
+    return;
+  }
+  const double f = en[0] + en[1] + en[2] + en[3] + en[4];
+  if (which == 0) S->fw = f; else S->f = f;
+}
+
+// after a gradient evaluation (gradient(y) for the slope, gradient(x))
+__global__ void ofgm_gcheck_kernel(MinState* S, const int64_t* stw) {
+  if (S->err) return;
+  S->gcalls++;
+  if (bad_status(stw, true)) set_err(S, kMinErrEval, stw, true);
+}
+
+// the search result: x = lincomb(1, y, h, r) when found, else x = y with f_y
+__global__ void ofgm_ls_post_kernel(MinState* S) {
+  if (S->err) return;
+  if (S->found) {
+    S->step = S->res_h;
+    S->f = S->res_f;
+  } else {
+    S->step = 0.0;
+    S->f = S->fw;
+  }
+}
+
+__global__ void ofgm_x_kernel(const MinState* S, int64_t n, const double* __restrict__ y,
+                              const double* __restrict__ r, double* __restrict__ x, int from_ls) {
+  if (S->err) return;
+  const bool move = from_ls && S->found;
+  const double h = S->res_h;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = move ? fma(h, r[i], 1.0 * y[i]) : y[i];
+}
+
+// end of an OFGM iteration, after grad f(x) and <g, g> (from_en: the 1/L
+// variant's value_and_gradient(x) supplies f and both call counts)
+__global__ void ofgm_post_kernel(MinState* S, const double* en, const int64_t* stw, double* rec,
+                                 int from_en) {
+  if (S->err) return;
+  if (from_en) {
+    S->vcalls++;
+    S->gcalls++;
+    if (bad_status(stw, true)) {
+      set_err(S, kMinErrEval, stw, true);
+      return;
+    }
+    S->f = en[0] + en[1] + en[2] + en[3] + en[4];
+  }
+  const double f = S->f;
+  const double af0 = fabs(S->f_init);
+  if (!isfinite(f) || f > 1e3 * (af0 > 1.0 ? af0 : 1.0) || !isfinite(S->gg)) {
+    set_err(S, kMinErrDiverged, nullptr, true);
+    return;
+  }
+  S->gn = sqrt(S->gg);
+  S->k++;
+  if (f < S->best_f) S->best_f = f;
+  record(S, rec, S->step);
+  if (S->gn <= S->c.thr) {
+    S->status = kMinConverged;
+    S->done = 1;
+  }
+}
+
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
@@ -698,6 +809,23 @@ cudaError_t launch_fgm_post_eval(MinState* S, const double* en, const int64_t* s
 cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(fgm_accept_kernel, S, rec);
 }
+cudaError_t launch_ofgm_pre(MinState* S, cudaStream_t st) { FFM_ONE(ofgm_pre_kernel, S); }
+cudaError_t launch_ofgm_dir(MinState* S, cudaGraphConditionalHandle hz,
+                            cudaGraphConditionalHandle hnz, cudaStream_t st) {
+  FFM_ONE(ofgm_dir_kernel, S, hz, hnz);
+}
+cudaError_t launch_ofgm_value(MinState* S, const double* en, const int64_t* stw, int which,
+                              cudaStream_t st) {
+  FFM_ONE(ofgm_value_kernel, S, en, stw, which);
+}
+cudaError_t launch_ofgm_gcheck(MinState* S, const int64_t* stw, cudaStream_t st) {
+  FFM_ONE(ofgm_gcheck_kernel, S, stw);
+}
+cudaError_t launch_ofgm_ls_post(MinState* S, cudaStream_t st) { FFM_ONE(ofgm_ls_post_kernel, S); }
+cudaError_t launch_ofgm_post(MinState* S, const double* en, const int64_t* stw, double* rec,
+                             int from_en, cudaStream_t st) {
+  FFM_ONE(ofgm_post_kernel, S, en, stw, rec, from_en);
+}
 cudaError_t launch_mom_pre(MinState* S, cudaGraphConditionalHandle heval, int has_eval,
                            cudaStream_t st) {
   FFM_ONE(mom_pre_kernel, S, heval, has_eval);
@@ -728,6 +856,13 @@ cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double
                              cudaStream_t st) {
   count_launch();
   cg_update_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, g_new, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ofgm_x(MinState* S, int64_t n, const double* y, const double* r, double* x,
+                          int from_ls, cudaStream_t st) {
+  count_launch();
+  ofgm_x_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, y, r, x, from_ls);
   return cudaGetLastError();
 }
 

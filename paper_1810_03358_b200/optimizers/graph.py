@@ -19,7 +19,7 @@ import os
 
 import numpy as np
 
-LBFGS, CG, SD, FGM, FIXED = 0, 1, 2, 3, 4
+LBFGS, CG, SD, FGM, FIXED, OFGM = 0, 1, 2, 3, 4, 5
 # fixed-step family (method FIXED): momentum_kind
 GD, HEAVY_BALL, NAG, NAG_SC = 0, 1, 2, 3
 GRAPH_CHUNK = 32  # iterations per graph launch between host polls
@@ -72,11 +72,12 @@ class _GraphRun:
 
 def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
               restart_period=100, step=0.0, momentum=0.0, momentum_kind=GD,
-              diverge_msg=None):
+              diverge_msg=None, schedule=None):
     """Run the iterations of `method` on the device from (x, f, g, |g|) and
     finish `run` like the host loop would.  linesearch is None for the
     fixed-step family (method FIXED: step, momentum, momentum_kind;
-    diverge_msg formats its divergence error with k, f and f0)."""
+    diverge_msg formats its divergence error with k, f and f0) and for
+    OFGM with a fixed step (schedule = ofgm_schedule's t, step = 1/L)."""
     import torch
 
     from .. import _native as N
@@ -106,7 +107,7 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         trust=c.trust if kind else 0.0, method=method,
         cg_kind=N.CG_KINDS.index(cg_kind) if method == CG else 0,
         restart_period=int(restart_period) if method == CG else 1, reserved=0,
-        fixed_step=float(step) if method == FIXED else 0.0,
+        fixed_step=float(step) if method in (FIXED, OFGM) else 0.0,
         momentum=float(momentum) if method == FIXED else 0.0,
         momentum_kind=int(momentum_kind) if method == FIXED else 0, reserved2=0)
     key = tuple(getattr(cfg, name) for name, _ in cfg._fields_)
@@ -115,6 +116,9 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
     if gr is None:
         gr = cache[key] = _GraphRun(oracle.engine, oracle.precision, cfg)
     lib, h = gr.lib, gr.handle
+    if method == OFGM:
+        t = np.ascontiguousarray(schedule, dtype=np.float64)
+        N.check(lib.ffm_lbfgs_set_schedule(h, t.ctypes.data, len(t)), "ffm_lbfgs_set_schedule")
     stream = C.c_void_p(torch.cuda.current_stream(oracle.device).cuda_stream)
     N.check(lib.ffm_lbfgs_start(h, C.c_void_p(x.data_ptr()), C.c_void_p(g.data_ptr()), f, gn,
                                 warm, stream), "ffm_lbfgs_start")

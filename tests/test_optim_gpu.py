@@ -255,7 +255,8 @@ def test_graph_cg_sd_equal_host_driven_loop(golden, monkeypatch, case):
     assert (oa.value_calls, oa.grad_calls) == (ob.value_calls, ob.grad_calls)
 
 
-@pytest.mark.parametrize("name", ["gd", "hb", "nag", "nagsc", "sd_h", "fgm", "lbfgs", "cg_prp+"])
+@pytest.mark.parametrize("name", ["gd", "hb", "nag", "nagsc", "sd_h", "fgm", "lbfgs", "cg_prp+",
+                                  "ofgm_L", "ofgm_ls"])
 @pytest.mark.parametrize("system", ["drv30", "globule"])
 def test_graph_drivers_equal_host_loop_table(golden, monkeypatch, name, system):
     """Every graph-resident driver of the golden driver table (fixed-step GD,
@@ -312,3 +313,35 @@ def test_graph_fixed_step_divergence_matches_host(golden, monkeypatch, driver):
             run(o)
         msgs.append((type(ei.value).__name__, str(ei.value), o.value_calls, o.grad_calls))
     assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("ls", ["par", "par_nogs", "h"])
+def test_graph_ofgm_line_search_variants(golden, monkeypatch, ls):
+    """OFGM along -d from y with every line search (ls_par seeded by the
+    slope needs grad f(y): one more gradient call per iteration), a horizon
+    shorter than the budget: identical to the host loop, horizon status."""
+    from paper_1810_03358_b200.optimizers import StopCriteria, make_linesearch, ofgm
+    from paper_1810_03358_b200.oracle import MolecularOracle
+
+    s = golden_system(golden, "conv200")
+    out = []
+    for host in (True, False):
+        if host:
+            monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+        else:
+            monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+        o = MolecularOracle(s)
+        lsr = make_linesearch("h") if ls == "h" else make_linesearch(
+            "par", use_gradient_start=(ls == "par"))
+        res = ofgm(o, s.coords.ravel(), 25, linesearch=lsr,
+                   stop=StopCriteria(max_iterations=100, gradient_norm_rtol=0.0))
+        out.append((res, o))
+    (a, oa), (b, ob) = out
+    assert "_graph_runs" in ob.__dict__
+    ra = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in b.trace.records]
+    assert ra == rb
+    assert a.status == b.status == "horizon_complete"
+    assert a.f == b.f and np.array_equal(a.x, b.x)
