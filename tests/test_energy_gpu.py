@@ -76,6 +76,36 @@ def test_coincident_pair_error(golden, E):
             E.energy_and_gradient(s, dt)
 
 
+@pytest.mark.parametrize("mode", ["units", "tiles", "units_sharded"])
+def test_coincident_pair_found_in_every_sweep_mode(mode, monkeypatch):
+    """Two coincident atoms far apart in index in a 3000-atom system: the
+    super-unit chain (finder launched only when flagged, its last block
+    finalising), the tile-mode fused evaluation and a sharded plan all
+    report the reference's first bad pair, then evaluate cleanly again."""
+    from paper_1810_03358_b200.energy import EnergyEvaluationError, energy_and_gradient
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    monkeypatch.setenv("FFM_FORCE_TILES", "1" if mode == "tiles" else "0")
+    s = make_globule_system(3000, seed=4)
+    c = s.coords.copy()
+    c[2500] = c[117]  # far from each other in the chain: not an excluded pair
+    bad = s.with_coords(c)
+    A = O.Arrays.from_system(bad)
+    _, _, err = O.energy_and_gradient(A, c, True, threads=O.host_threads())
+    assert err is not None
+    if mode == "units_sharded":
+        from paper_1810_03358_b200 import _native as N
+        from paper_1810_03358_b200.engine import engine_for
+
+        eng = engine_for(bad.topology)
+        N.check(eng.lib.ffm_system_set_shard(eng.handle, 0, 1), "shard")
+    for dt in (np.float64, np.float32):
+        with pytest.raises(EnergyEvaluationError, match=r"nonbonded pair \(117,2500\)"):
+            energy_and_gradient(bad, dt)
+        bd, g = energy_and_gradient(s, dt)  # the status words reset
+        assert np.isfinite(bd.total) and np.all(np.isfinite(g))
+
+
 def test_degenerate_terms_raise_reference_messages(golden, E):
     s = golden_system(golden, "collinear")
     msgs = golden["collinear/messages"].tolist()
