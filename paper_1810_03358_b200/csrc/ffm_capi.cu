@@ -69,6 +69,11 @@ struct Work {
 struct ffm_system {
   int device = 0;
   NbPlanDev plan{};
+  // batched (multi-candidate, energy-only) sweeps: super-units as large as
+  // divide np -- with B geometries per launch the grid is large whatever the
+  // unit size, so larger units amortise their overheads (configs[3])
+  NbPlanDev bplan{};
+  int2* d_unit_rc_b = nullptr;
   TermPlanDev tp{};
   int nspt = 0;
   // device tables
@@ -150,7 +155,8 @@ struct ffm_system {
 namespace {
 
 void free_all(ffm_system* s) {
-  void* ptrs[] = {s->d_unit_rc, s->d_unit_index, s->d_spt_ptr, s->d_spt_m, s->d_spt_mask,
+  void* ptrs[] = {s->d_unit_rc, s->d_unit_rc_b, s->d_unit_index, s->d_spt_ptr, s->d_spt_m,
+                  s->d_spt_mask,
                   s->d_sp_ptr, s->d_sp_j, s->d_sp_s, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
                   s->d_qt, s->d_lj32, s->d_lj64, s->d_ilj32, s->d_ilj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
                   s->d_sc_s, s->d_bond_idx, s->d_bond_K, s->d_bond_r0, s->d_ang_idx,
@@ -410,11 +416,13 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   if (w.e_batch < batch) {
     if (w.epart) cudaFree(w.epart);
     w.epart = nullptr;
-    const size_t bytes = (size_t)batch * nb_slots(p) * 3 * sizeof(double);
+    // (the batch plan's units, too: batch > 1 sweeps use s->bplan)
+    const size_t slots = std::max<size_t>(nb_slots(p), (size_t)s->bplan.nunits);
+    const size_t bytes = (size_t)batch * slots * 3 * sizeof(double);
     if (cudaMalloc(&w.epart, bytes) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for energy partials");
     // units another rank owns: no energy, no close contact (min r^2 = 1e30)
-    std::vector<double> init((size_t)batch * nb_slots(p) * 3, 0.0);
+    std::vector<double> init((size_t)batch * slots * 3, 0.0);
     for (size_t k = 2; k < init.size(); k += 3) init[k] = 1e30;
     FFM_CUDA(cudaMemcpy(w.epart, init.data(), bytes, cudaMemcpyHostToDevice));
     w.e_batch = batch;
@@ -623,10 +631,32 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_unit_rc, urc));
   FFM_TRY(upload(&s->d_unit_index, uidx));
   p.unit_rc = s->d_unit_rc;
+  {  // the batch plan: the largest unit edge that divides np (units mode)
+    NbPlanDev& b = s->bplan;
+    b = p;
+    for (int Sb : {1024, 512, 256})
+      if (Sb >= p.S && p.np % Sb == 0) {
+        b.S = Sb;
+        break;
+      }
+    b.nb = p.np / b.S;
+    b.nunits = b.nb * (b.nb + 1) / 2;
+    b.nlaunch = n > 0 ? b.nunits : 0;
+    std::vector<int2> brc;
+    for (int r = 0; r < b.nb; ++r)
+      for (int c = r + 1; c < b.nb; ++c) brc.push_back(make_int2(r, c));
+    for (int r = 0; r < b.nb; ++r) brc.push_back(make_int2(r, r));
+    FFM_TRY(upload(&s->d_unit_rc_b, brc));
+    b.unit_rc = s->d_unit_rc_b;
+    b.unit_list = nullptr;
+    b.ntiles = 0;
+    b.tiles = nullptr;
+    b.tile_list = nullptr;
+  }
   if (n > 0 && use_tiles(p, device)) FFM_TRY(build_tiles(s));
-  p.spt_ptr = s->d_spt_ptr;
-  p.spt_m = s->d_spt_m;
-  p.spt_mask = s->d_spt_mask;
+  p.spt_ptr = s->bplan.spt_ptr = s->d_spt_ptr;
+  p.spt_m = s->bplan.spt_m = s->d_spt_m;
+  p.spt_mask = s->bplan.spt_mask = s->d_spt_mask;
 
   s->tp.has_cutoff = p.has_cutoff;
   s->tp.cutoff = cutoff > 0.0 ? cutoff : 0.0;
@@ -949,12 +979,15 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   FFM_CUDA(launch_pack(s->plan.n, s->plan.np, B, f64, coords_d, s->d_qt, w.pos, w.ipos,
                        status_d, st));
   if (s->plan.has_cutoff) FFM_CUDA(launch_bbox(s->plan.n, s->plan.np, B, f64, w.pos, w.bbox, st));
-  FFM_CUDA(launch_nb(s->plan, f64, false, w.pos, lj, w.ipos, ilj, w.bbox, nullptr, nullptr,
+  // unsharded systems sweep the batch with the batch plan (large units);
+  // sharded ones keep their rank's share of the main plan
+  const NbPlanDev& bp = s->nranks == 1 ? s->bplan : s->plan;
+  FFM_CUDA(launch_nb(bp, f64, false, w.pos, lj, w.ipos, ilj, w.bbox, nullptr, nullptr,
                      w.epart, B, st));
   TermPlanDev tp = s->tp;
   if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
   FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
-  FFM_CUDA(launch_reduce(nb_slots(s->plan), tp, B, w.epart, w.term_e, energies_d, status_d,
+  FFM_CUDA(launch_reduce(nb_slots(bp), tp, B, w.epart, w.term_e, energies_d, status_d,
                          s->plan.n, st));
   FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                          s->d_sp_s, status_d, st));

@@ -142,6 +142,10 @@ def test_landmarks_and_constant(E):
 
 
 def test_batch_equals_single_evaluations(golden):
+    """eval_batch sweeps with the batch plan (the largest super-unit that
+    divides np), single evaluations with the system's own plan: FP64 agrees
+    to roundoff of the summation order; FP32 tiles are evaluated by
+    different warp splits there, so FP32 agrees to FP32 roundoff."""
     import torch
 
     from paper_1810_03358_b200.engine import engine_for
@@ -156,7 +160,11 @@ def test_batch_equals_single_evaluations(golden):
         en = en.cpu().numpy()
         for b in range(B):
             e1, st1, _ = eng.eval_host(batch[b], prec)
-            np.testing.assert_allclose(en[b], e1, rtol=1e-12, atol=1e-9)
+            if prec == 0:
+                np.testing.assert_allclose(en[b], e1, rtol=1e-12, atol=1e-9)
+            else:
+                np.testing.assert_allclose(en[b], e1, rtol=1e-6,
+                                           atol=1e-6 * float(np.sum(np.abs(e1))))
         assert np.all(st.cpu().numpy()[:, 0] == -1)
 
 
