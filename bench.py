@@ -471,6 +471,14 @@ def optimizer_comparison(natoms, iters, methods=("sd", "fgm", "cg", "lbfgs", "wi
                "fgm": lambda: fgm(o, s.coords.ravel(), ls, stop),
                "cg": lambda: cg(o, s.coords.ravel(), "prp+", ls, stop),
                "lbfgs": lambda: lbfgs(o, s.coords.ravel(), m=5, linesearch=ls, stop=stop)}
+        if name != "wiggle":  # warm-up: capture the method's graph outside the timing
+            warm = StopCriteria(max_iterations=2, gradient_norm_rtol=1e-6)
+            {"sd": lambda: steepest_descent(o, s.coords.ravel(), ls, warm),
+             "fgm": lambda: fgm(o, s.coords.ravel(), ls, warm),
+             "cg": lambda: cg(o, s.coords.ravel(), "prp+", ls, warm),
+             "lbfgs": lambda: lbfgs(o, s.coords.ravel(), m=5, linesearch=ls, stop=warm)}[name]()
+            o.value_calls = o.grad_calls = 0
+            ls.reset()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         if name == "wiggle":

@@ -237,6 +237,11 @@ typedef struct {
 
 int ffm_lbfgs_create(ffm_system_t* sys, int precision, const ffm_lbfgs_config* cfg,
                      ffm_lbfgs_t** out);
+/* change the run-time fields of a run's configuration (budgets, threshold,
+ * line-search constants, CG variant, momentum) so the captured graph is
+ * reused; m, chunk, method, momentum_kind, fixed_step and whether ls_par
+ * seeds from the slope shape the graph and must match (FFM_EINVAL). */
+int ffm_lbfgs_configure(ffm_lbfgs_t* run, const ffm_lbfgs_config* cfg);
 /* start point: x_d, g_d device (3n) float64; f, |g| as computed by the
  * caller; warm_h = the line searcher's current warm-start step */
 int ffm_lbfgs_start(ffm_lbfgs_t* run, const double* x_d, const double* g_d, double f,

@@ -1483,12 +1483,11 @@ void lbfgs_free(ffm_lbfgs* L) {
 
 extern "C" {
 
-int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg,
-                     ffm_lbfgs_t** out) {
-  if (!s || !cfg || !out) return fail(FFM_EINVAL, "NULL argument");
-  *out = nullptr;
-  if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
-  if (s->nranks != 1) return fail(FFM_EINVAL, "graph-resident L-BFGS needs an unsharded system");
+}  // extern "C"
+
+namespace {
+
+int check_config(const ffm_lbfgs_config* cfg) {
   if (cfg->m < 1 || cfg->m > kMaxLbfgsPairs) return fail(FFM_EINVAL, "memory depth m out of range");
   if (cfg->ls_kind != 0 && cfg->ls_kind != 1) return fail(FFM_EINVAL, "bad line-search kind");
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
@@ -1500,12 +1499,19 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
     return fail(FFM_EINVAL, "bad fixed-step configuration");
   if (cfg->method == kMethodCg && (cfg->cg_kind < 0 || cfg->cg_kind > 6 || cfg->restart_period < 1))
     return fail(FFM_EINVAL, "bad CG variant");
-  DeviceGuard guard(s->device);
-  auto* L = new ffm_lbfgs();
-  L->sys = s;
-  L->device = s->device;
-  L->prec = precision;
-  MinConfig& c = L->cfg;
+  return FFM_OK;
+}
+
+// fields that shape the captured graph (buffer sizes, which kernels are
+// captured, host constants baked into launches); the rest is read from the
+// device state at run time and may change between runs (ffm_lbfgs_configure)
+bool same_structure(const MinConfig& c, const ffm_lbfgs_config* cfg) {
+  return c.m == cfg->m && c.chunk == cfg->chunk && c.method == cfg->method &&
+         c.momentum_kind == cfg->momentum_kind && c.fixed_step == cfg->fixed_step &&
+         c.ls_needs_grad == (cfg->ls_kind == 1 && cfg->use_gradient_start);
+}
+
+void set_config(MinConfig& c, const ffm_lbfgs_config* cfg) {
   c.m = cfg->m;
   c.ls_kind = cfg->ls_kind;
   c.K = cfg->K;
@@ -1527,6 +1533,26 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   c.fixed_step = cfg->fixed_step;
   c.momentum = cfg->momentum;
   c.ls_needs_grad = cfg->ls_kind == 1 && cfg->use_gradient_start;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg,
+                     ffm_lbfgs_t** out) {
+  if (!s || !cfg || !out) return fail(FFM_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
+  if (s->nranks != 1) return fail(FFM_EINVAL, "graph-resident L-BFGS needs an unsharded system");
+  FFM_TRYR(check_config(cfg));
+  DeviceGuard guard(s->device);
+  auto* L = new ffm_lbfgs();
+  L->sys = s;
+  L->device = s->device;
+  L->prec = precision;
+  MinConfig& c = L->cfg;
+  set_config(c, cfg);
   c.horizon = 0;
   c.sched = nullptr;
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
@@ -1561,6 +1587,19 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
     }
   L->rec_h.resize((size_t)(c.chunk + 1) * kMinRecWidth);
   *out = L;
+  return FFM_OK;
+}
+
+int ffm_lbfgs_configure(ffm_lbfgs_t* L, const ffm_lbfgs_config* cfg) {
+  if (!L || !cfg) return fail(FFM_EINVAL, "NULL argument");
+  FFM_TRYR(check_config(cfg));
+  if (!same_structure(L->cfg, cfg))
+    return fail(FFM_EINVAL, "configuration changes the graph structure: create a new run");
+  const long long horizon = L->cfg.horizon;
+  const double* sched = L->cfg.sched;
+  set_config(L->cfg, cfg);
+  L->cfg.horizon = horizon;
+  L->cfg.sched = sched;
   return FFM_OK;
 }
 

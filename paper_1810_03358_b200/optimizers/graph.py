@@ -110,12 +110,16 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         fixed_step=float(step) if method in (FIXED, OFGM) else 0.0,
         momentum=float(momentum) if method == FIXED else 0.0,
         momentum_kind=int(momentum_kind) if method == FIXED else 0, reserved2=0)
-    key = tuple(getattr(cfg, name) for name, _ in cfg._fields_)
+    # one captured graph per structure (ffm_lbfgs_configure: budgets,
+    # tolerances and line-search constants are run-time state)
+    key = (cfg.m, cfg.chunk, cfg.method, cfg.momentum_kind, cfg.fixed_step,
+           int(cfg.ls_kind == 1 and cfg.use_gradient_start))
     cache = oracle.__dict__.setdefault("_graph_runs", {})
     gr = cache.get(key)
     if gr is None:
         gr = cache[key] = _GraphRun(oracle.engine, oracle.precision, cfg)
     lib, h = gr.lib, gr.handle
+    N.check(lib.ffm_lbfgs_configure(h, C.byref(cfg)), "ffm_lbfgs_configure")
     if method == OFGM:
         t = np.ascontiguousarray(schedule, dtype=np.float64)
         N.check(lib.ffm_lbfgs_set_schedule(h, t.ctypes.data, len(t)), "ffm_lbfgs_set_schedule")

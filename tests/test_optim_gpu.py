@@ -345,3 +345,29 @@ def test_graph_ofgm_line_search_variants(golden, monkeypatch, ls):
     assert ra == rb
     assert a.status == b.status == "horizon_complete"
     assert a.f == b.f and np.array_equal(a.x, b.x)
+
+
+def test_graph_reused_across_stop_criteria(golden, monkeypatch):
+    """A captured graph is reused for runs that differ only in run-time
+    configuration (budgets, tolerances, CG variant): results equal those of
+    a fresh capture, and only one graph is built per structure."""
+    from paper_1810_03358_b200.optimizers import StopCriteria, cg, lbfgs, make_linesearch
+    from paper_1810_03358_b200.oracle import MolecularOracle
+
+    monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+    s = golden_system(golden, "conv200")
+    x0 = s.coords.ravel()
+    o = MolecularOracle(s)
+    lbfgs(o, x0, m=5, linesearch=make_linesearch("par"),
+          stop=StopCriteria(max_iterations=4, gradient_norm_rtol=0.0))
+    cg(o, x0, "fr", make_linesearch("par"), StopCriteria(max_iterations=3, gradient_norm_rtol=0.0))
+    stop = StopCriteria(max_iterations=40, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
+    a = lbfgs(o, x0, m=5, linesearch=make_linesearch("par"), stop=stop)
+    c = cg(o, x0, "prp+", make_linesearch("par"), stop)
+    assert len(o._graph_runs) == 2
+    b = lbfgs(MolecularOracle(s), x0, m=5, linesearch=make_linesearch("par"), stop=stop)
+    d = cg(MolecularOracle(s), x0, "prp+", make_linesearch("par"), stop)
+    for u, v in ((a, b), (c, d)):
+        assert [(r.f, r.grad_norm, r.step) for r in u.trace.records] == \
+            [(r.f, r.grad_norm, r.step) for r in v.trace.records]
+        assert np.array_equal(u.x, v.x) and u.status == v.status
