@@ -138,11 +138,18 @@ __device__ inline bool dihedral_term(P3 ci, P3 cj, P3 ck, P3 cl, const double* V
   const double y = dot(m, b2) / b2n;
   const double x = dot(n1, n2);
   const double phi = atan2(y, x);
-  *e = 0.5 * (V[0] * (1.0 + cos(phi)) + V[1] * (1.0 - cos(2.0 * phi)) +
-              V[2] * (1.0 + cos(3.0 * phi)) + V[3] * (1.0 - cos(4.0 * phi)));
+  // cos / sin of phi .. 4 phi from one sincos by the angle-addition
+  // recurrences (eight libm calls in the reference; the multiples agree with
+  // them to a few ulp, far inside the FP64 tolerance): the term blocks are
+  // the latency-critical items of a small-system evaluation
+  double s1, c1;
+  sincos(phi, &s1, &c1);
+  const double c2 = c1 * c1 - s1 * s1, s2 = 2.0 * s1 * c1;
+  const double c3 = c2 * c1 - s2 * s1, s3 = s2 * c1 + c2 * s1;
+  const double c4 = c2 * c2 - s2 * s2, s4 = 2.0 * s2 * c2;
+  *e = 0.5 * (V[0] * (1.0 + c1) + V[1] * (1.0 - c2) + V[2] * (1.0 + c3) + V[3] * (1.0 - c4));
   if (!grad) return true;
-  const double dedphi = 0.5 * (-V[0] * sin(phi) + 2.0 * V[1] * sin(2.0 * phi) -
-                               3.0 * V[2] * sin(3.0 * phi) + 4.0 * V[3] * sin(4.0 * phi));
+  const double dedphi = 0.5 * (-V[0] * s1 + 2.0 * V[1] * s2 - 3.0 * V[2] * s3 + 4.0 * V[3] * s4);
   const P3 cI = {-(b2n / n1sq) * n1.x, -(b2n / n1sq) * n1.y, -(b2n / n1sq) * n1.z};
   const P3 cL = {(b2n / n2sq) * n2.x, (b2n / n2sq) * n2.y, (b2n / n2sq) * n2.z};
   const double p = dot(b1, b2) / b2sq;
