@@ -777,6 +777,64 @@ int ffm_system_info(const ffm_system_t* s, int64_t* info) {
 }
 
 // The launch sequence of one evaluation (no host synchronisation).
+// The one-launch small-system evaluation (ffm_small.cu) of a tile-mode,
+// unsharded system with every term; false when it does not apply.
+// trial_*: a line-search trial of a graph-resident driver (see
+// SmallEvalArgs), else all null.
+static bool small_fused_applies(const ffm_system* s) {
+  return s->plan.ntiles > 0 && s->plan.n > 0 && s->nranks == 1;
+}
+
+static int issue_small(ffm_system* s, int precision, bool grad, const double* coords_d,
+                       double* grad_d, double* energies_d, int64_t* status_d, cudaStream_t st,
+                       bool* launched, double* trial_out = nullptr,
+                       const double* trial_x = nullptr, const double* trial_r = nullptr,
+                       const double* trial_h = nullptr, MinState* ls_state = nullptr,
+                       cudaGraphConditionalHandle ls_loop = 0) {
+  *launched = false;
+  Work& w = s->w[precision];
+  const bool f64 = precision == FFM_F64;
+  int& grid = s->small_grid[precision][grad ? 1 : 0];
+  SmallEvalArgs a;
+  a.plan = s->plan;
+  a.tp = s->tp;
+  a.nterm_blocks = term_blocks(s->tp);
+  a.coords = coords_d;
+  a.qt = s->d_qt;
+  a.pos = w.pos;
+  a.ipos = w.ipos;
+  a.lj = f64 ? (const void*)s->d_lj64 : (const void*)s->d_lj32;
+  a.ilj = f64 ? (const void*)s->d_ilj64 : (const void*)s->d_ilj32;
+  a.ipart = w.ipart;
+  a.jpart = w.jpart;
+  a.epart = w.epart;
+  a.term_part = w.term_e;
+  a.term_f = w.term_f;
+  a.trow_ptr = s->d_trow_ptr;
+  a.tcol_ptr = s->d_tcol_ptr;
+  a.tcol_idx = s->d_tcol_idx;
+  a.slot_ptr = s->d_slot_ptr;
+  a.slot_idx = s->d_slot_idx;
+  a.sp_ptr = s->d_sp_ptr;
+  a.sp_j = s->d_sp_j;
+  a.sp_s = s->d_sp_s;
+  a.grad = grad_d;
+  a.energies = energies_d;
+  a.status = status_d;
+  a.phase_clock = s->phase_clock;
+  a.trial_out = trial_out;
+  a.trial_x = trial_x;
+  a.trial_r = trial_r;
+  a.trial_h = trial_h;
+  a.ls_state = ls_state;
+  a.ls_loop = ls_loop;
+  if (grid == 0) grid = small_eval_grid(a, f64, grad, s->device);
+  if (grid <= 0) return FFM_OK;
+  FFM_CUDA(launch_small_eval(a, f64, grad, grid, st));
+  *launched = true;
+  return FFM_OK;
+}
+
 static int issue_eval(ffm_system* s, int precision, int flags, const double* coords_d,
                       double* grad_d, double* energies_d, int64_t* status_d, cudaStream_t st) {
   const bool grad = (flags & FFM_GRAD) != 0;
@@ -790,41 +848,11 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
   if (!do_nb || s->rank != 0) tp.nscaled = 0;
   const bool time_nb = (flags & FFM_TIME_NB) != 0 && do_nb;
   // small system evaluated whole: one cooperative launch (ffm_small.cu)
-  if (s->plan.ntiles > 0 && s->plan.n > 0 && s->nranks == 1 && do_nb && do_terms && !time_nb &&
-      !(flags & FFM_NO_FUSE)) {
-    int& grid = s->small_grid[precision][grad ? 1 : 0];
-    SmallEvalArgs a;
-    a.plan = s->plan;
-    a.tp = tp;
-    a.nterm_blocks = term_blocks(tp);
-    a.coords = coords_d;
-    a.qt = s->d_qt;
-    a.pos = w.pos;
-    a.ipos = w.ipos;
-    a.lj = lj;
-    a.ilj = ilj;
-    a.ipart = w.ipart;
-    a.jpart = w.jpart;
-    a.epart = w.epart;
-    a.term_part = w.term_e;
-    a.term_f = w.term_f;
-    a.trow_ptr = s->d_trow_ptr;
-    a.tcol_ptr = s->d_tcol_ptr;
-    a.tcol_idx = s->d_tcol_idx;
-    a.slot_ptr = s->d_slot_ptr;
-    a.slot_idx = s->d_slot_idx;
-    a.sp_ptr = s->d_sp_ptr;
-    a.sp_j = s->d_sp_j;
-    a.sp_s = s->d_sp_s;
-    a.grad = grad_d;
-    a.energies = energies_d;
-    a.status = status_d;
-    a.phase_clock = s->phase_clock;
-    if (grid == 0) grid = small_eval_grid(a, f64, grad, s->device);
-    if (grid > 0) {
-      FFM_CUDA(launch_small_eval(a, f64, grad, grid, st));
-      return FFM_OK;
-    }
+  if (small_fused_applies(s) && do_nb && do_terms && !time_nb && !(flags & FFM_NO_FUSE)) {
+    bool launched = false;
+    FFM_TRYR(issue_small(s, precision, grad, coords_d, grad_d, energies_d, status_d, st,
+                         &launched));
+    if (launched) return FFM_OK;
   }
   FFM_CUDA(launch_pack(s->plan.n, s->plan.np, 1, f64, coords_d, s->d_qt, w.pos, w.ipos,
                        status_d, st));
@@ -1144,8 +1172,16 @@ int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls)
 
 int cap_trial(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hloop) {
   MinState* S = L->S;
-  // phi(h) = f(x + h r): lincomb(1.0, x, h, r)  (FGM: from w)
+  // phi(h) = f(x + h r): lincomb(1.0, x, h, r)  (FGM: from w, OFGM: from y)
   const double* base = (L->cfg.method == kMethodFgm || L->cfg.method == kMethodOfgm) ? L->xn : L->x;
+  if (small_fused_applies(L->sys)) {
+    // small systems: the trial point, its evaluation and the probe
+    // controller in one cooperative launch (was axpby + evaluation + ls_step)
+    bool launched = false;
+    FFM_TRYR(issue_small(L->sys, L->prec, false, L->xt, nullptr, L->en, L->stw, st, &launched,
+                         L->xt, base, L->r, &S->h_trial, S, hloop));
+    if (launched) return FFM_OK;
+  }
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, base, &S->h_trial, 0.0, L->r, L->xt, st));
   FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY, L->xt, nullptr, L->en, L->stw, st));
   FFM_CUDA(launch_min_ls_step(S, L->en, L->stw, hloop, st));

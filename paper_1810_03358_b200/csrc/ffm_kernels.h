@@ -116,6 +116,16 @@ struct SmallEvalArgs {
   double* energies;
   int64_t* status;
   unsigned long long* phase_clock;  // null, or [grid][6] timestamps (tuning aid)
+  // line-search trial of a graph-resident driver (null trial_out: a plain
+  // evaluation of coords): the point x_t = lincomb(1, trial_x, *trial_h,
+  // trial_r) is formed into trial_out and evaluated, then the probe
+  // controller runs on ls_state and sets the probe loop's condition ls_loop
+  double* trial_out;
+  const double* trial_x;
+  const double* trial_r;
+  const double* trial_h;
+  struct MinState* ls_state;
+  cudaGraphConditionalHandle ls_loop;
 };
 // grid size (co-resident CTAs, at most what the work needs); 0 on error
 int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device);

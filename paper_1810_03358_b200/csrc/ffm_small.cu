@@ -23,6 +23,7 @@
 
 #include "ffm_device.cuh"
 #include "ffm_kernels.h"
+#include "ffm_min_dev.cuh"
 #include "ffm_tile.cuh"
 
 namespace ffm {
@@ -61,9 +62,18 @@ small_eval_kernel(SmallEvalArgs a) {
   };
   stamp(0);
 
-  // P0
-  for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs)
-    pack_item<T>(k, n, plan.np, 1, a.coords, a.qt, pos, ipos, a.status);
+  // P0 (a line-search trial first forms its point x_t = lincomb(1, x, h, r),
+  // the axpby of the host-driven loop, into the trial buffer)
+  const double* coords = a.trial_out ? a.trial_out : a.coords;
+  const double th = a.trial_out ? *a.trial_h : 0.0;
+  for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs) {
+    if (a.trial_out && k < n)
+      for (int c = 0; c < 3; ++c) {
+        const int64_t q = 3 * k + c;
+        a.trial_out[q] = fma(th, a.trial_r[q], 1.0 * a.trial_x[q]);
+      }
+    pack_item<T>(k, n, plan.np, 1, coords, a.qt, pos, ipos, a.status);
+  }
   grid.sync();
   stamp(1);
 
@@ -76,7 +86,7 @@ small_eval_kernel(SmallEvalArgs a) {
       tile_cta<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
                                 static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it, 0, tsm);
     else
-      term_block(a.tp, GRAD, a.coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
+      term_block(a.tp, GRAD, coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
                  a.nterm_blocks, sh);
   }
   __syncthreads();
@@ -111,7 +121,12 @@ small_eval_kernel(SmallEvalArgs a) {
     grid.sync();
     if (blockIdx.x == 0 && threadIdx.x == 0) a.status[kStNbSuspect] = 1;  // as the chain leaves it
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) finalize_entry(n, a.status);
+  // the CTA that reduced the energies finalises the status words and, for a
+  // line-search trial, runs the probe controller (ffm_min_dev.cuh)
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    finalize_entry(n, a.status);
+    if (a.ls_state) mindev::ls_step(a.ls_state, a.energies, a.status, a.ls_loop);
+  }
   stamp(5);
 }
 
