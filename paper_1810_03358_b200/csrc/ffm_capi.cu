@@ -888,7 +888,8 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
         s->plan.ntiles ? s->d_trow_ptr : nullptr, s->d_tcol_ptr, s->d_tcol_idx, w.ipart,
         w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f, s->tp.slot_sc0, do_nb,
         do_terms && s->rank == 0, do_nb && s->rank == 0, grad_d,
-        do_nb ? nb_slots(s->plan) : 0, tp, w.epart, w.term_e, energies_d, status_d, st));
+        do_nb ? nb_slots(s->plan) : 0, tp, w.epart, w.term_e, energies_d, status_d, s->rank,
+        s->nranks, st));
     FFM_CUDA(launch_finder(s->plan.n, s->plan.np, 1, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                            s->d_sp_s, status_d, st));
     return FFM_OK;

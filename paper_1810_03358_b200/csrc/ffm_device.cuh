@@ -314,7 +314,10 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
                                              const int* __restrict__ slot_idx,
                                              const double* __restrict__ term_f, int slot_sc0,
                                              bool use_nb, bool use_terms, bool use_sc,
-                                             double* __restrict__ grad, double (*part)[3][32]) {
+                                             double* __restrict__ grad, double (*part)[3][32],
+                                             int rank = 0, int nranks = 1) {
+  // row-sharded plans (ffm_system_set_shard): units / tiles are dealt
+  // round-robin, the slots of other ranks' ones hold exact zeros -- skip them
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int a0 = g << 5;
   double g0 = 0.0, g1 = 0.0, g2 = 0.0;
@@ -326,8 +329,9 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
     for (int k = warp; k < nt; k += NW) {
       const bool isrow = k < nr;
       const int st = isrow ? kIB : kJB;
-      const T* p = isrow ? ipart + (size_t)(r0 + k) * 3 * kIB + row
-                         : jpart + (size_t)tcol_idx[c0 + k - nr] * 3 * kJB + lane;
+      const int t = isrow ? r0 + k : tcol_idx[c0 + k - nr];
+      if (nranks > 1 && t % nranks != rank) continue;
+      const T* p = isrow ? ipart + (size_t)t * 3 * kIB + row : jpart + (size_t)t * 3 * kJB + lane;
       g0 += (double)p[0];
       g1 += (double)p[st];
       g2 += (double)p[2 * st];
@@ -336,8 +340,9 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
     const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
 #pragma unroll 4
     for (int k = warp; k <= nb; k += NW) {
-      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
-                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
+      const int u = k < ni ? unit_index[b * nb + b + k] : unit_index[(k - ni) * nb + b];
+      if (nranks > 1 && u % nranks != rank) continue;
+      const T* p = (k < ni ? ipart : jpart) + (size_t)u * 3 * S;
       g0 += (double)p[off];
       g1 += (double)p[S + off];
       g2 += (double)p[2 * S + off];

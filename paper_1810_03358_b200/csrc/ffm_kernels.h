@@ -61,7 +61,7 @@ cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* uni
                                  bool use_nb, bool use_terms, bool use_sc, double* grad,
                                  int nslots, const TermPlanDev& tp, const double* epart,
                                  const double* term_part, double* energies, int64_t* status,
-                                 cudaStream_t st);
+                                 int rank, int nranks, cudaStream_t st);
 
 // exact first coincident pair (reference loop order), only when flagged;
 // the last block then converts the status sentinels to -1.

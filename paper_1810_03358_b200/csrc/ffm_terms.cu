@@ -120,7 +120,8 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                      int slot_sc0, bool use_nb, bool use_terms, bool use_sc,
                      double* __restrict__ grad, int nslots, int nterm_blocks,
                      const double* __restrict__ epart, const double* __restrict__ term_part,
-                     double* __restrict__ energies, int64_t* __restrict__ status) {
+                     double* __restrict__ energies, int64_t* __restrict__ status, int rank,
+                     int nranks) {
   __shared__ double part[NW][3][32];
   if ((int)blockIdx.x == (n + 31) >> 5) {
     reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
@@ -129,7 +130,7 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
   }
   gather_group<T, NW>(blockIdx.x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart,
                       jpart, slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
-                      grad, part);
+                      grad, part, rank, nranks);
 }
 
 template <typename T>
@@ -139,7 +140,7 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
                                const double* term_f, int slot_sc0, bool use_nb, bool use_terms,
                                bool use_sc, double* grad, int nslots, int nterm_blocks,
                                const double* epart, const double* term_part, double* energies,
-                               int64_t* status, cudaStream_t st) {
+                               int64_t* status, int rank, int nranks, cudaStream_t st) {
   const int blocks = (n + 31) / 32 + 1;
   const T* ip = static_cast<const T*>(ipart);
   const T* jp = static_cast<const T*>(jpart);
@@ -148,12 +149,12 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
     gather_reduce_kernel<T, kGatherWarpsTiles><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
-        energies, status);
+        energies, status, rank, nranks);
   else
     gather_reduce_kernel<T, kGatherWarpsUnits><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
-        energies, status);
+        energies, status, rank, nranks);
   return cudaGetLastError();
 }
 
@@ -164,15 +165,16 @@ cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* uni
                                  bool use_nb, bool use_terms, bool use_sc, double* grad,
                                  int nslots, const TermPlanDev& tp, const double* epart,
                                  const double* term_part, double* energies, int64_t* status,
-                                 cudaStream_t st) {
+                                 int rank, int nranks, cudaStream_t st) {
   if (fp64)
     return launch_gr_t<double>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
                                slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
                                grad, nslots, term_blocks(tp), epart, term_part, energies, status,
-                               st);
+                               rank, nranks, st);
   return launch_gr_t<float>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
                             slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc, grad,
-                            nslots, term_blocks(tp), epart, term_part, energies, status, st);
+                            nslots, term_blocks(tp), epart, term_part, energies, status, rank,
+                            nranks, st);
 }
 
 // ---------------------------------------------------------- energy reduction
