@@ -5,8 +5,14 @@ of W evaluates the units u = r, r + W, r + 2W, ... (heaviest first, so every
 rank gets the same work to within one unit) and rank 0 also the O(N) bonded
 and 1-4 terms.  Each rank therefore produces a *partial* gradient over all
 atoms and partial energies; one NCCL all-reduce (SUM) of the packed
-[gradient | energies] vector over NVLink completes them on every rank, and
-one tiny all-reduce (MIN) merges the error words.  Coordinates are
+[gradient | energies | error words] vector over NVLink completes them on
+every rank.  The error words ride in the same sum: a rank that reports an
+error contributes (key + 1, 1), the others (0, 0), and every reporting rank
+reports the same key -- bonded terms are evaluated by rank 0 alone, and a
+coincident pair is located by the finder over the whole triangle (every
+rank holds all coordinates), so any rank that flags one finds the same,
+globally first pair; key = sum / count - 1 is exact in float64 (keys <
+2^53 / W).  Coordinates are
 replicated: every rank runs the same optimiser on the same all-reduced
 numbers, so no broadcast is needed per step.
 
@@ -24,7 +30,6 @@ import torch.distributed as dist
 
 from . import _native as N
 
-INT64_MAX = np.iinfo(np.int64).max
 
 
 def shard_units(nunits: int, rank: int, world: int):
@@ -40,46 +45,47 @@ def unit_order(nb: int):
 
 
 class ShardCombiner:
-    """All-reduce of one rank's partial evaluation."""
+    """All-reduce of one rank's partial evaluation (one collective)."""
+
+    SLOTS = (N.ST_NB_BAD_I, N.ST_BOND, N.ST_ANGLE, N.ST_DIHEDRAL)
 
     def __init__(self, n, device, group=None):
         self.n = n
         self.group = group
-        self.buf = torch.empty(3 * n + N.FFM_NTERMS, dtype=torch.float64, device=device)
-        self.keys = torch.empty(4, dtype=torch.int64, device=device)
+        # [gradient (3n) | energies (5) | error (key + 1) x 4 | reporting ranks x 4]
+        self.buf = torch.empty(3 * n + N.FFM_NTERMS + 8, dtype=torch.float64, device=device)
 
     def combine(self, grad, energies, status):
         """grad (3n,) or None, energies (5,), status (8,) int64 -- local
         partials in, global values out (in place on grad/energies/status)."""
-        n3 = 3 * self.n
+        n3, ne = 3 * self.n, N.FFM_NTERMS
+        b = self.buf
         if grad is not None:
-            self.buf[:n3].copy_(grad.reshape(-1))
+            b[:n3].copy_(grad.reshape(-1))
         else:
-            self.buf[:n3].zero_()
-        self.buf[n3:].copy_(energies)
-        dist.all_reduce(self.buf, op=dist.ReduceOp.SUM, group=self.group)
-        if grad is not None:
-            grad.reshape(-1).copy_(self.buf[:n3])
-        energies.copy_(self.buf[n3:])
-        # error words: first coincident pair as one key i * n + j, first bad
-        # bonded terms; sentinel INT64_MAX for "clean"
+            b[:n3].zero_()
+        b[n3:n3 + ne].copy_(energies)
         st = status
-        big = torch.full_like(st[:1], INT64_MAX)
-        key = torch.where(st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1] >= 0,
-                          st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1] * self.n + st[N.ST_NB_BAD_J:N.ST_NB_BAD_J + 1],
-                          big)
-        self.keys[0:1].copy_(key)
-        for k, slot in enumerate((N.ST_BOND, N.ST_ANGLE, N.ST_DIHEDRAL), start=1):
-            v = st[slot:slot + 1]
-            self.keys[k:k + 1].copy_(torch.where(v >= 0, v, big))
-        dist.all_reduce(self.keys, op=dist.ReduceOp.MIN, group=self.group)
-        k0 = self.keys[0:1]
-        clean = k0 == INT64_MAX
-        st[N.ST_NB_BAD_I:N.ST_NB_BAD_I + 1].copy_(torch.where(clean, -1, k0 // self.n))
-        st[N.ST_NB_BAD_J:N.ST_NB_BAD_J + 1].copy_(torch.where(clean, -1, k0 % self.n))
-        for k, slot in enumerate((N.ST_BOND, N.ST_ANGLE, N.ST_DIHEDRAL), start=1):
-            v = self.keys[k:k + 1]
-            st[slot:slot + 1].copy_(torch.where(v == INT64_MAX, -1, v))
+        # error keys: the first coincident pair as i * n + j, the first bad
+        # bond / angle / dihedral; -1 = clean
+        keys = torch.stack([torch.where(st[N.ST_NB_BAD_I] >= 0,
+                                        st[N.ST_NB_BAD_I] * self.n + st[N.ST_NB_BAD_J],
+                                        st[N.ST_NB_BAD_I]),
+                            st[N.ST_BOND], st[N.ST_ANGLE], st[N.ST_DIHEDRAL]])
+        rep = keys >= 0
+        b[n3 + ne:n3 + ne + 4].copy_(torch.where(rep, keys + 1, 0))
+        b[n3 + ne + 4:].copy_(rep)
+        dist.all_reduce(b, op=dist.ReduceOp.SUM, group=self.group)
+        if grad is not None:
+            grad.reshape(-1).copy_(b[:n3])
+        energies.copy_(b[n3:n3 + ne])
+        cnt = b[n3 + ne + 4:]
+        key = torch.where(cnt > 0, torch.round(b[n3 + ne:n3 + ne + 4] / cnt.clamp(min=1.0)) - 1,
+                          -1.0).to(torch.int64)
+        k0 = key[0]
+        st[N.ST_NB_BAD_I].copy_(torch.where(k0 >= 0, k0 // self.n, -1))
+        st[N.ST_NB_BAD_J].copy_(torch.where(k0 >= 0, k0 % self.n, -1))
+        st[N.ST_BOND:N.ST_DIHEDRAL + 1].copy_(key[1:])
         return grad, energies, status
 
 

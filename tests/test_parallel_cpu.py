@@ -33,7 +33,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, golden_path, q):
+def _worker(rank, world, port, golden_path, q, both=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -57,8 +57,9 @@ def _worker(rank, world, port, golden_path, q):
         grad = torch.from_numpy((gn + gb).reshape(-1).copy())
         energies = torch.tensor([es, eb, et, ec, ev], dtype=torch.float64)
         status = torch.full((N.FFM_STATUS_WORDS,), -1, dtype=torch.int64)
-        if rank == 1:  # pretend rank 1 saw a coincident pair and a bad angle
+        if rank == 1 or both:  # pretend rank 1 (or every rank) found the first coincident pair
             status[N.ST_NB_BAD_I], status[N.ST_NB_BAD_J] = 7, 9
+        if rank == 0:  # and rank 0, which evaluates the bonded terms, a bad angle
             status[N.ST_ANGLE] = 4
         comb = ShardCombiner(n, "cpu")
         comb.combine(grad, energies, status)
@@ -67,13 +68,17 @@ def _worker(rank, world, port, golden_path, q):
         dist.destroy_process_group()
 
 
-def test_two_rank_combine_equals_full_evaluation(golden):
+@pytest.mark.parametrize("both", [False, True])
+def test_two_rank_combine_equals_full_evaluation(golden, both):
+    """One SUM all-reduce completes gradient, energies and the error words
+    (a key reported by one rank or by both)."""
     from conftest import GOLDEN
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, str(GOLDEN), q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, str(GOLDEN), q, both))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
