@@ -62,13 +62,20 @@ struct Work {
   double* term_e = nullptr;  // [batch][nterm_e]
   int te_batch = 0;
   double* term_f = nullptr;  // [nslots][3]
+  double* escratch = nullptr;  // split energy reduction: [kMaxEnergyParts][3] + counter
 };
+
+// the split energy reduction's counter sits after its [kMaxEnergyParts][3] partials
+inline unsigned* ecount(Work& w) {
+  return reinterpret_cast<unsigned*>(w.escratch + (size_t)kMaxEnergyParts * 3);
+}
 
 }  // namespace
 
 struct ffm_system {
   int device = 0;
   NbPlanDev plan{};
+  int S0 = 0;  // the super-unit edge chosen at creation (single-rank plan)
   // batched (multi-candidate, energy-only) sweeps: super-units as large as
   // divide np -- with B geometries per launch the grid is large whatever the
   // unit size, so larger units amortise their overheads (configs[3])
@@ -175,7 +182,8 @@ void free_all(ffm_system* s) {
   if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
-    void* wp[] = {w.pos, w.ipos, w.bbox, w.ipart, w.jpart, w.epart, w.term_e, w.term_f};
+    void* wp[] = {w.pos, w.ipos, w.bbox, w.ipart, w.jpart, w.epart, w.term_e, w.term_f,
+                  w.escratch};
     for (void* p : wp)
       if (p) cudaFree(p);
   }
@@ -203,6 +211,49 @@ int choose_S(int64_t n) {
     if (nb * (nb + 1) / 2 >= 1700) return S;
   }
   return 256;
+}
+
+// (Re)build the super-unit tables of edge S (a divisor of np): units in
+// evaluation order, off-diagonal first (full work), diagonal last (half
+// work), and the (row, column) -> unit index map of the gather.
+int build_units(ffm_system* s, int S) {
+  NbPlanDev& p = s->plan;
+  p.S = S;
+  p.nb = p.np / S;
+  p.nunits = p.nb * (p.nb + 1) / 2;
+  std::vector<int2> urc;
+  std::vector<int> uidx((size_t)p.nb * p.nb, -1);
+  for (int r = 0; r < p.nb; ++r)
+    for (int c = r + 1; c < p.nb; ++c) urc.push_back(make_int2(r, c));
+  for (int r = 0; r < p.nb; ++r) urc.push_back(make_int2(r, r));
+  for (size_t u = 0; u < urc.size(); ++u) uidx[(size_t)urc[u].x * p.nb + urc[u].y] = (int)u;
+  if (s->d_unit_rc) cudaFree(s->d_unit_rc);
+  if (s->d_unit_index) cudaFree(s->d_unit_index);
+  s->d_unit_rc = nullptr;
+  s->d_unit_index = nullptr;
+  FFM_TRYR(upload(&s->d_unit_rc, urc));
+  FFM_TRYR(upload(&s->d_unit_index, uidx));
+  p.unit_rc = s->d_unit_rc;
+  p.unit_list = nullptr;
+  if (p.ntiles == 0) p.nlaunch = p.n > 0 ? p.nunits : 0;
+  return FFM_OK;
+}
+
+// Super-unit edge of a row-sharded plan: every rank should still see about
+// six waves of units (the single-GPU rule of choose_S, per rank), so the
+// edge shrinks with the shard count -- 100k atoms: 1024 up to 2 ranks, 512
+// at 4 and 8 (at S = 1024 eight ranks would get 606 units each, 2.05 waves
+// of ~265 us units: a third wave almost empty).  Only edges dividing np.
+#ifndef FFM_SHARD_UNITS
+#define FFM_SHARD_UNITS 1700  // units per rank wanted (~6 waves of 296 CTA slots)
+#endif
+int choose_S_sharded(const NbPlanDev& p, int S0, int nranks) {
+  for (int S : {1024, 768, 512, 256}) {
+    if (S > S0 || p.np % S) continue;
+    const int64_t nb = p.np / S;
+    if (nb * (nb + 1) / 2 >= (int64_t)FFM_SHARD_UNITS * nranks) return S;
+  }
+  return p.np % 256 == 0 ? 256 : S0;
 }
 
 // rebuild the term plan device view (after set_terms or creation)
@@ -427,6 +478,13 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
     FFM_CUDA(cudaMemcpy(w.epart, init.data(), bytes, cudaMemcpyHostToDevice));
     w.e_batch = batch;
   }
+  if (!w.escratch) {
+    const size_t bytes = (size_t)kMaxEnergyParts * 3 * sizeof(double) + 64;
+    if (cudaMalloc(&w.escratch, bytes) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for the energy reduction scratch");
+    FFM_CUDA(cudaMemset(w.escratch, 0, bytes));
+    FFM_CUDA(cudaDeviceSynchronize());
+  }
   if (w.te_batch < batch) {
     if (w.term_e) cudaFree(w.term_e);
     w.term_e = nullptr;
@@ -479,7 +537,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   s->device = device;
   NbPlanDev& p = s->plan;
   p.n = (int)n;
-  p.S = choose_S(n);
+  p.S = s->S0 = choose_S(n);
   p.nb = (int)std::max<int64_t>(1, (n + p.S - 1) / p.S);
   p.np = p.nb * p.S;
   p.nunits = p.nb * (p.nb + 1) / 2;
@@ -622,15 +680,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_sc_s, s->scaled_s));
 
   // ---- units: off-diagonal first (full work), diagonal last (half work)
-  std::vector<int2> urc;
-  std::vector<int> uidx((size_t)p.nb * p.nb, -1);
-  for (int r = 0; r < p.nb; ++r)
-    for (int c = r + 1; c < p.nb; ++c) urc.push_back(make_int2(r, c));
-  for (int r = 0; r < p.nb; ++r) urc.push_back(make_int2(r, r));
-  for (size_t u = 0; u < urc.size(); ++u) uidx[(size_t)urc[u].x * p.nb + urc[u].y] = (int)u;
-  FFM_TRY(upload(&s->d_unit_rc, urc));
-  FFM_TRY(upload(&s->d_unit_index, uidx));
-  p.unit_rc = s->d_unit_rc;
+  FFM_TRY(build_units(s, p.S));
   {  // the batch plan: the largest unit edge that divides np (units mode)
     NbPlanDev& b = s->bplan;
     b = p;
@@ -717,6 +767,16 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
       if (rc) return rc;
       s->plan.tile_list = s->d_tile_list;
     }
+  } else {
+    // re-plan the super-unit edge for this shard count (the single-rank
+    // edge is kept from creation: s->S0)
+    const int S = nranks == 1 ? s->S0 : choose_S_sharded(s->plan, s->S0, nranks);
+    if (S != s->plan.S) {
+      int rc = build_units(s, S);
+      if (rc) return rc;
+    }
+  }
+  if (s->plan.ntiles > 0) {
   } else if (nranks == 1) {
     s->plan.unit_list = nullptr;
     s->plan.nlaunch = s->plan.nunits;
@@ -889,13 +949,13 @@ static int issue_eval(ffm_system* s, int precision, int flags, const double* coo
         w.jpart, s->d_slot_ptr, s->d_slot_idx, w.term_f, s->tp.slot_sc0, do_nb,
         do_terms && s->rank == 0, do_nb && s->rank == 0, grad_d,
         do_nb ? nb_slots(s->plan) : 0, tp, w.epart, w.term_e, energies_d, status_d, s->rank,
-        s->nranks, st));
+        s->nranks, w.escratch, ecount(w), st));
     FFM_CUDA(launch_finder(s->plan.n, s->plan.np, 1, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                            s->d_sp_s, status_d, st));
     return FFM_OK;
   }
   FFM_CUDA(launch_reduce(do_nb ? nb_slots(s->plan) : 0, tp, 1, w.epart, w.term_e, energies_d,
-                         status_d, s->plan.n, st));
+                         status_d, s->plan.n, w.escratch, ecount(w), st));
   FFM_CUDA(launch_finder(do_nb ? s->plan.n : 0, s->plan.np, 1, f64, w.pos, s->d_sp_ptr,
                          s->d_sp_j, s->d_sp_s, status_d, st));
   return FFM_OK;
@@ -1017,7 +1077,7 @@ int ffm_eval_batch(ffm_system_t* s, int precision, int64_t batch, const double* 
   if (s->rank != 0) tp.nbond = tp.nangle = tp.ndih = tp.nscaled = 0;
   FFM_CUDA(launch_terms(tp, false, B, coords_d, w.term_e, nullptr, status_d, st));
   FFM_CUDA(launch_reduce(nb_slots(bp), tp, B, w.epart, w.term_e, energies_d, status_d,
-                         s->plan.n, st));
+                         s->plan.n, w.escratch, ecount(w), st));
   FFM_CUDA(launch_finder(s->plan.n, s->plan.np, B, f64, w.pos, s->d_sp_ptr, s->d_sp_j,
                          s->d_sp_s, status_d, st));
   return FFM_OK;

@@ -458,6 +458,75 @@ __device__ __forceinline__ void reduce_entry(int nunits, int nterm_blocks,
   }
 }
 
+// The same reduction over many slots (a sharded or fine super-unit plan has
+// tens of thousands) by `nparts` blocks: block `part` sums its contiguous
+// slice of the slots into scratch[part]; the last block to finish (atomic
+// counter, reset for the next evaluation) adds the parts in part order plus
+// the term partials and writes energies / status exactly as reduce_entry
+// does.  Fixed order throughout: bit-identical run to run.
+__device__ __forceinline__ void reduce_split(int nunits, int nterm_blocks,
+                                             const double* __restrict__ epart,
+                                             const double* __restrict__ term_part,
+                                             double* __restrict__ energies,
+                                             int64_t* __restrict__ status, double* sh,
+                                             double* scratch, unsigned* counter, int part,
+                                             int nparts, int finalize_n) {
+  __shared__ int last;
+  const int chunk = (nunits + nparts - 1) / nparts;
+  const int u0 = part * chunk, u1 = min(nunits, u0 + chunk);
+  double ec = 0.0, ev = 0.0, mr = DBL_MAX;
+  for (int u = u0 + threadIdx.x; u < u1; u += blockDim.x) {
+    ec += epart[3 * u];
+    ev += epart[3 * u + 1];
+    mr = fmin(mr, epart[3 * u + 2]);
+  }
+  ec = tree_sum(ec, sh);
+  ev = tree_sum(ev, sh);
+  mr = tree_min(mr, sh);
+  if (threadIdx.x == 0) {
+    scratch[3 * part] = ec;
+    scratch[3 * part + 1] = ev;
+    scratch[3 * part + 2] = mr;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == (unsigned)(nparts - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double es = 0.0, eb = 0.0, et = 0.0, tc = 0.0, tv = 0.0;
+  for (int k = threadIdx.x; k < nterm_blocks; k += blockDim.x) {
+    const double* p = term_part + 5 * (size_t)k;
+    es += p[0];
+    eb += p[1];
+    et += p[2];
+    tc += p[3];
+    tv += p[4];
+  }
+  es = tree_sum(es, sh);
+  eb = tree_sum(eb, sh);
+  et = tree_sum(et, sh);
+  tc = tree_sum(tc, sh);
+  tv = tree_sum(tv, sh);
+  if (threadIdx.x == 0) {
+    double sc = 0.0, sv = 0.0, m = DBL_MAX;
+    for (int q = 0; q < nparts; ++q) {
+      sc += __ldcg(scratch + 3 * q);
+      sv += __ldcg(scratch + 3 * q + 1);
+      m = fmin(m, __ldcg(scratch + 3 * q + 2));
+    }
+    sc += tc;
+    sv += tv;
+    energies[0] = es;
+    energies[1] = eb;
+    energies[2] = et;
+    energies[3] = sc;
+    energies[4] = sv;
+    if (!isfinite(sc) || !isfinite(sv) || m < kRmin * kRmin) status[kStNbSuspect] = 1;
+    if (finalize_n >= 0 && status[kStNbSuspect] == 0) finalize_entry(finalize_n, status);
+    *counter = 0u;
+  }
+}
+
 // ------------------------------------------------------------ pair finder
 // Exact restatement of the coincidence test of ffmin/kernels.py:294-302 for
 // row i of the upper triangle (only run when the sweep flagged a suspect):

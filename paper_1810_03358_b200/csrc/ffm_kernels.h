@@ -45,9 +45,15 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
 // energies[batch][5] = (stretch, bend, torsion, coulomb, vdw); flags suspect
 // coincidences for the finder
 // (clean entries are finalised here: sentinels -> -1; n = atoms)
+// batch 1 with escratch: split over energy_parts(nunits) blocks (reduce_split)
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
                           const double* term_part, double* energies, int64_t* status, int n,
-                          cudaStream_t st);
+                          double* escratch, unsigned* ecount, cudaStream_t st);
+// blocks of the split energy reduction: one per kEnergySlotsPerPart slots;
+// escratch holds kMaxEnergyParts x 3 doubles, ecount one counter (zeroed)
+constexpr int kEnergySlotsPerPart = 2048;
+constexpr int kMaxEnergyParts = 64;
+int energy_parts(int nslots);
 
 // batch 1: the gradient gather (gather_group, ffm_device.cuh: tile mode
 // when trow_ptr is set, else super-unit mode) and the energy reduction in
@@ -61,7 +67,8 @@ cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* uni
                                  bool use_nb, bool use_terms, bool use_sc, double* grad,
                                  int nslots, const TermPlanDev& tp, const double* epart,
                                  const double* term_part, double* energies, int64_t* status,
-                                 int rank, int nranks, cudaStream_t st);
+                                 int rank, int nranks, double* escratch, unsigned* ecount,
+                                 cudaStream_t st);
 
 // exact first coincident pair (reference loop order), only when flagged;
 // the last block then converts the status sentinels to -1.

@@ -121,11 +121,16 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                      double* __restrict__ grad, int nslots, int nterm_blocks,
                      const double* __restrict__ epart, const double* __restrict__ term_part,
                      double* __restrict__ energies, int64_t* __restrict__ status, int rank,
-                     int nranks) {
+                     int nranks, double* __restrict__ escratch, unsigned* ecount, int nparts) {
   __shared__ double part[NW][3][32];
-  if ((int)blockIdx.x == (n + 31) >> 5) {
-    reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
-                 true, n);
+  const int ngroups = (n + 31) >> 5;
+  if ((int)blockIdx.x >= ngroups) {  // the energy reduction: nparts blocks
+    if (nparts == 1)  // (the fused small-system kernel's order: identical bits)
+      reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
+                   true, n);
+    else
+      reduce_split(nslots, nterm_blocks, epart, term_part, energies, status, &part[0][0][0],
+                   escratch, ecount, blockIdx.x - ngroups, nparts, n);
     return;
   }
   gather_group<T, NW>(blockIdx.x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart,
@@ -140,8 +145,10 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
                                const double* term_f, int slot_sc0, bool use_nb, bool use_terms,
                                bool use_sc, double* grad, int nslots, int nterm_blocks,
                                const double* epart, const double* term_part, double* energies,
-                               int64_t* status, int rank, int nranks, cudaStream_t st) {
-  const int blocks = (n + 31) / 32 + 1;
+                               int64_t* status, int rank, int nranks, double* escratch,
+                               unsigned* ecount, cudaStream_t st) {
+  const int nparts = energy_parts(nslots);
+  const int blocks = (n + 31) / 32 + nparts;
   const T* ip = static_cast<const T*>(ipart);
   const T* jp = static_cast<const T*>(jpart);
   count_launch();
@@ -149,12 +156,12 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
     gather_reduce_kernel<T, kGatherWarpsTiles><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
-        energies, status, rank, nranks);
+        energies, status, rank, nranks, escratch, ecount, nparts);
   else
     gather_reduce_kernel<T, kGatherWarpsUnits><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
-        energies, status, rank, nranks);
+        energies, status, rank, nranks, escratch, ecount, nparts);
   return cudaGetLastError();
 }
 
@@ -165,16 +172,17 @@ cudaError_t launch_gather_reduce(int n, int S, int nb, bool fp64, const int* uni
                                  bool use_nb, bool use_terms, bool use_sc, double* grad,
                                  int nslots, const TermPlanDev& tp, const double* epart,
                                  const double* term_part, double* energies, int64_t* status,
-                                 int rank, int nranks, cudaStream_t st) {
+                                 int rank, int nranks, double* escratch, unsigned* ecount,
+                                 cudaStream_t st) {
   if (fp64)
     return launch_gr_t<double>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
                                slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
                                grad, nslots, term_blocks(tp), epart, term_part, energies, status,
-                               rank, nranks, st);
+                               rank, nranks, escratch, ecount, st);
   return launch_gr_t<float>(n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart, jpart,
                             slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc, grad,
                             nslots, term_blocks(tp), epart, term_part, energies, status, rank,
-                            nranks, st);
+                            nranks, escratch, ecount, st);
 }
 
 // ---------------------------------------------------------- energy reduction
@@ -187,12 +195,30 @@ reduce_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
                n);
 }
 
+__global__ void __launch_bounds__(kRedThreads)
+reduce_split_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
+                    const double* __restrict__ term_part, double* __restrict__ energies,
+                    int64_t* __restrict__ status, int n, double* escratch, unsigned* ecount) {
+  __shared__ double sh[32];
+  reduce_split(nunits, nterm_blocks, epart, term_part, energies, status, sh, escratch, ecount,
+               blockIdx.x, gridDim.x, n);
+}
+
+int energy_parts(int nslots) {
+  const int p = (nslots + kEnergySlotsPerPart - 1) / kEnergySlotsPerPart;
+  return p < 1 ? 1 : (p > kMaxEnergyParts ? kMaxEnergyParts : p);
+}
+
 cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const double* epart,
                           const double* term_part, double* energies, int64_t* status, int n,
-                          cudaStream_t st) {
+                          double* escratch, unsigned* ecount, cudaStream_t st) {
   count_launch();
-  reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, term_blocks(tp), epart, term_part,
-                                                energies, status, n);
+  if (batch == 1 && escratch && energy_parts(nunits) > 1)
+    reduce_split_kernel<<<energy_parts(nunits), kRedThreads, 0, st>>>(
+        nunits, term_blocks(tp), epart, term_part, energies, status, n, escratch, ecount);
+  else
+    reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, term_blocks(tp), epart, term_part,
+                                                  energies, status, n);
   return cudaGetLastError();
 }
 

@@ -261,7 +261,7 @@ def test_full_size_properties():
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_row_shards_sum_to_the_full_evaluation(world):
+def test_row_shards_sum_to_the_full_evaluation(world, n=20000):
     """ffm_system_set_shard on one GPU: the partial gradients / energies of
     all ranks, summed, equal the unsharded evaluation (what the NCCL
     all-reduce of parallel.ShardCombiner computes on W GPUs)."""
@@ -271,7 +271,7 @@ def test_row_shards_sum_to_the_full_evaluation(world):
     from paper_1810_03358_b200.engine import DeviceSystem
     from paper_1810_03358_b200.synth import make_globule_system
 
-    s = make_globule_system(20000, seed=4)
+    s = make_globule_system(n, seed=4)
     c = torch.from_numpy(s.coords.copy()).cuda()
     full = DeviceSystem(s.topology)
     g_full = torch.empty_like(c)
@@ -292,6 +292,30 @@ def test_row_shards_sum_to_the_full_evaluation(world):
         eng.close()
     assert torch.allclose(e_sum, e_full, rtol=1e-12)
     assert float((g_sum - g_full).abs().max()) <= 1e-11 * float(g_full.abs().max())
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_sharded_plan_replans_super_units(world):
+    """60k atoms: the single-GPU plan uses 1024-atom super-units; a sharded
+    plan shrinks them (each rank keeps ~6 waves of units) and the rank sums
+    still equal the full evaluation; back to one rank restores the edge."""
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(60000, seed=2)
+    eng = DeviceSystem(s.topology)
+    S0 = eng.info["S"]
+    assert S0 == 1024
+    N.check(eng.lib.ffm_system_set_shard(eng.handle, 0, world), "set_shard")
+    info = np.zeros(8, np.int64)
+    N.check(eng.lib.ffm_system_info(eng.handle, info.ctypes.data), "info")
+    assert info[2] < S0 and info[4] >= 1700 * world
+    N.check(eng.lib.ffm_system_set_shard(eng.handle, 0, 1), "set_shard")
+    N.check(eng.lib.ffm_system_info(eng.handle, info.ctypes.data), "info")
+    assert info[2] == S0
+    eng.close()
+    test_row_shards_sum_to_the_full_evaluation(world, n=60000)
 
 
 def test_kernel_backend_farfield_functions(golden):
