@@ -218,8 +218,8 @@ typedef struct {
    * hs, cd, ls, dy; restart every restart_period iterations), 2 = steepest
    * descent (ffmin/optimizers/gradient.py, Eq. (4)), 3 = FGM with the theta
    * schedule and best-point tracking (ffmin/optimizers/fgm.py, Algorithm 1).
-   * m is ignored (but must be in range) for methods 1..5 (5 = OFGM, see
-   * ffm_lbfgs_set_schedule). */
+   * m is ignored (but must be in range) for methods 1..6 (5 = OFGM, see
+   * ffm_lbfgs_set_schedule; 6 = wiggle, below). */
   int32_t method;
   int32_t cg_kind;
   int32_t restart_period;
@@ -233,6 +233,14 @@ typedef struct {
   double momentum;
   int32_t momentum_kind;
   int32_t reserved2;
+  /* method 6 = gradient-free atom wiggle (ffmin/optimizers/wiggle.py): probe
+   * step h, far-field linearisation cutoff (0 = exact probes), exact
+   * re-evaluation every epoch_iterations iterations (incremental mode); the
+   * atom of each iteration comes from ffm_lbfgs_set_atoms. */
+  double wiggle_h;
+  double wiggle_cutoff;
+  int32_t wiggle_epoch;
+  int32_t reserved3;
 } ffm_lbfgs_config;
 
 int ffm_lbfgs_create(ffm_system_t* sys, int precision, const ffm_lbfgs_config* cfg,
@@ -265,6 +273,9 @@ int ffm_lbfgs_result(ffm_lbfgs_t* run, double* x_d, double* g_d, void* stream);
  * (len = N + 1, ofgm_schedule), before ffm_lbfgs_start; fixed_step = 1/L
  * selects the fixed-step variant, 0 the line-searched one */
 int ffm_lbfgs_set_schedule(ffm_lbfgs_t* run, const double* t_h, int64_t len);
+/* wiggle (method 6): the atoms of the next ffm_lbfgs_run launch, one per
+ * iteration (count >= cfg.chunk; drawn by the caller's generator) */
+int ffm_lbfgs_set_atoms(ffm_lbfgs_t* run, const int32_t* atoms_h, int64_t count);
 /* copy the best point seen so far out (device pointer, 3n; FGM's result
  * unless the run converged -- OptimizationRun.finish_best) */
 int ffm_lbfgs_best(ffm_lbfgs_t* run, double* x_d, void* stream);

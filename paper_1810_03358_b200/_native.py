@@ -68,6 +68,7 @@ SIGNATURES = {
     "ffm_lbfgs_result": (_I, [_P, _P, _P, _P]),
     "ffm_lbfgs_best": (_I, [_P, _P, _P]),
     "ffm_lbfgs_set_schedule": (_I, [_P, _P, _I64]),
+    "ffm_lbfgs_set_atoms": (_I, [_P, _P, _I64]),
     "ffm_lbfgs_destroy": (_I, [_P]),
 }
 
@@ -83,14 +84,17 @@ class LbfgsConfig(C.Structure):
                 ("k_minus", C.c_double), ("trust", C.c_double), ("method", C.c_int32),
                 ("cg_kind", C.c_int32), ("restart_period", C.c_int32), ("reserved", C.c_int32),
                 ("fixed_step", C.c_double), ("momentum", C.c_double),
-                ("momentum_kind", C.c_int32), ("reserved2", C.c_int32)]
+                ("momentum_kind", C.c_int32), ("reserved2", C.c_int32),
+                ("wiggle_h", C.c_double), ("wiggle_cutoff", C.c_double),
+                ("wiggle_epoch", C.c_int32), ("reserved3", C.c_int32)]
 
 
 LBFGS_STATUS = {0: None, 1: "converged", 2: "iteration_budget", 3: "linesearch_failure",
                 4: "oracle_budget", 5: "horizon_complete"}
 LBFGS_REC_WIDTH = 8
 # ffm_lbfgs_config.method / cg_kind codes
-METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM, METHOD_FIXED, METHOD_OFGM = 0, 1, 2, 3, 4, 5
+METHOD_LBFGS, METHOD_CG, METHOD_SD, METHOD_FGM, METHOD_FIXED, METHOD_OFGM, METHOD_WIGGLE = (
+    0, 1, 2, 3, 4, 5, 6)
 CG_KINDS = ("fr", "prp", "prp+", "hs", "cd", "ls", "dy")
 
 _lock = threading.Lock()

@@ -1182,6 +1182,10 @@ struct ffm_lbfgs {
   double* en = nullptr;      // energies of the last evaluation
   int64_t* stw = nullptr;    // its status words
   cudaStream_t cap[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  // wiggle: probe scratch (atoms6, newpos6, out6, st6, atoms1, newpos1,
+  // out1, st1) and the atoms of a launch
+  void* wbuf = nullptr;
+  int* wig_atoms = nullptr;
   double* gsum = nullptr;    // OFGM: running weighted gradient sum
   double* anchor = nullptr;  // OFGM: x0
   double* sched = nullptr;   // OFGM: t[0..N] (device)
@@ -1412,6 +1416,90 @@ int cap_ofgm(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaStream_t c4, cu
   return FFM_OK;
 }
 
+// wiggle scratch layout inside L->wbuf (8-byte slots)
+struct WigBufs {
+  int* atoms6;
+  double* newpos6;
+  double* out6;
+  int64_t* st6;
+  int* atoms1;
+  double* newpos1;
+  double* out1;
+  int64_t* st1;
+};
+constexpr size_t kWigBufBytes = 8 * (8 + 18 + 36 + 18 + 8 + 3 + 6 + 3);
+WigBufs wig_bufs(void* base) {
+  double* p = static_cast<double*>(base);
+  WigBufs b;
+  b.atoms6 = reinterpret_cast<int*>(p);
+  b.newpos6 = p + 8;
+  b.out6 = p + 26;
+  b.st6 = reinterpret_cast<int64_t*>(p + 62);
+  b.atoms1 = reinterpret_cast<int*>(p + 80);
+  b.newpos1 = p + 88;
+  b.out1 = p + 91;
+  b.st1 = reinterpret_cast<int64_t*>(p + 97);
+  return b;
+}
+
+// gradient-free wiggle (ffmin/optimizers/wiggle.py): six axis probes, the
+// parabola-vertex probe (IF), the exact check of the best candidate (IF),
+// the epoch re-evaluation (IF) and the record -- one iteration inside the
+// IF(go) body; c3 captures the nested bodies
+int cap_wiggle(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdir) {
+  MinState* S = L->S;
+  ffm_system* s = L->sys;
+  const WigBufs b = wig_bufs(L->wbuf);
+  const double lin = L->cfg.wig_cutoff;
+  auto delta = [&](int k, const int* atoms, const double* newpos, double lc, double* out,
+                   int64_t* stw, cudaStream_t q) {
+    return launch_atom_delta(s->tp, L->x, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s, s->d_aterm_ptr,
+                             s->d_aterm_idx, k, atoms, newpos, lc, out, stw, q);
+  };
+  FFM_CUDA(launch_wig_prep(S, L->x, b.atoms6, b.newpos6, st));
+  FFM_CUDA(delta(6, b.atoms6, b.newpos6, lin, b.out6, b.st6, st));
+  cudaGraphConditionalHandle hv, hx, he;
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&hv, bdir, 0, 0));
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&hx, bdir, 0, 0));
+  FFM_CUDA(cudaGraphConditionalHandleCreate(&he, bdir, 0, 0));
+  FFM_CUDA(launch_wig_ctrl1(S, b.out6, b.st6, b.atoms1, hv, st));
+  cudaGraph_t body = nullptr, tmp = nullptr;
+  cudaError_t e;
+  int rc = FFM_OK;
+  // the vertex probe
+  FFM_TRYR(add_conditional(st, hv, cudaGraphCondTypeIf, &body));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  if (launch_wig_pos(S, L->x, b.newpos1, 0, c3) != cudaSuccess ||
+      delta(1, b.atoms1, b.newpos1, lin, b.out1, b.st1, c3) != cudaSuccess ||
+      launch_wig_ctrl_v(S, b.out1, b.st1, c3) != cudaSuccess)
+    rc = fail(FFM_ECUDA, "wiggle vertex probe");
+  e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  FFM_CUDA(launch_wig_ctrl2(S, hx, st));
+  // the exact check of the chosen move
+  FFM_TRYR(add_conditional(st, hx, cudaGraphCondTypeIf, &body));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  if (launch_wig_pos(S, L->x, b.newpos1, 1, c3) != cudaSuccess ||
+      delta(1, b.atoms1, b.newpos1, 0.0, b.out1, b.st1, c3) != cudaSuccess ||
+      launch_wig_ctrl3(S, b.out1, b.st1, L->x, c3) != cudaSuccess)
+    rc = fail(FFM_ECUDA, "wiggle exact probe");
+  e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  FFM_CUDA(launch_wig_end(S, he, st));
+  // the epoch re-evaluation (incremental probes)
+  FFM_TRYR(add_conditional(st, he, cudaGraphCondTypeIf, &body));
+  FFM_CUDA(cudaStreamBeginCaptureToGraph(c3, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  rc = issue_eval(s, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, c3);
+  if (!rc && launch_wig_epoch(S, L->en, L->stw, c3) != cudaSuccess) rc = fail(FFM_ECUDA, "wig_epoch");
+  e = cudaStreamEndCapture(c3, &tmp);
+  if (rc) return rc;
+  FFM_CUDA(e);
+  FFM_CUDA(launch_wig_record(S, L->rec, st));
+  return FFM_OK;
+}
+
 int cap_accept(ffm_lbfgs* L, cudaStream_t st) {
   MinState* S = L->S;
   if (L->cfg.method == kMethodFgm) {  // x+ = lincomb(1, w, h, r); no gradient at x+
@@ -1521,6 +1609,8 @@ int lbfgs_build(ffm_lbfgs* L) {
       FFM_G(cap_fixed(L, c2, c3, bdir));
     else if (L->cfg.method == kMethodOfgm)
       FFM_G(cap_ofgm(L, c2, c3, c4, bdir));
+    else if (L->cfg.method == kMethodWiggle)
+      FFM_G(cap_wiggle(L, c2, c3, bdir));
     else
       FFM_G(cap_direction(L, c2, hls));
     FFM_GC(cudaStreamEndCapture(c2, &tmp));
@@ -1570,7 +1660,7 @@ int lbfgs_build(ffm_lbfgs* L) {
 void lbfgs_free(ffm_lbfgs* L) {
   if (L->exec) cudaGraphExecDestroy(L->exec);
   for (void* p : {(void*)L->S, (void*)L->rec, (void*)L->buf, (void*)L->scratch, (void*)L->en,
-                  (void*)L->stw, (void*)L->sched})
+                  (void*)L->stw, (void*)L->sched, L->wbuf, (void*)L->wig_atoms})
     if (p) cudaFree(p);
   for (cudaStream_t c : L->cap)
     if (c) cudaStreamDestroy(c);
@@ -1590,7 +1680,10 @@ int check_config(const ffm_lbfgs_config* cfg) {
   if (cfg->ls_kind == 1 && (cfg->K < 2 || cfg->K > kLsMaxPoints - 2))
     return fail(FFM_EINVAL, "ls_par K out of range");
   if (cfg->chunk < 1) return fail(FFM_EINVAL, "chunk must be >= 1");
-  if (cfg->method < kMethodLbfgs || cfg->method > kMethodOfgm) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method < kMethodLbfgs || cfg->method > kMethodWiggle) return fail(FFM_EINVAL, "bad method");
+  if (cfg->method == kMethodWiggle && (!(cfg->wiggle_h > 0.0) || cfg->wiggle_epoch < 1 ||
+                                       cfg->wiggle_cutoff < 0.0))
+    return fail(FFM_EINVAL, "bad wiggle configuration");
   if (cfg->method == kMethodFixed &&
       (cfg->momentum_kind < 0 || cfg->momentum_kind > 3 || !(cfg->fixed_step > 0.0)))
     return fail(FFM_EINVAL, "bad fixed-step configuration");
@@ -1605,7 +1698,8 @@ int check_config(const ffm_lbfgs_config* cfg) {
 bool same_structure(const MinConfig& c, const ffm_lbfgs_config* cfg) {
   return c.m == cfg->m && c.chunk == cfg->chunk && c.method == cfg->method &&
          c.momentum_kind == cfg->momentum_kind && c.fixed_step == cfg->fixed_step &&
-         c.ls_needs_grad == (cfg->ls_kind == 1 && cfg->use_gradient_start);
+         c.ls_needs_grad == (cfg->ls_kind == 1 && cfg->use_gradient_start) &&
+         (c.wig_cutoff > 0.0) == (cfg->wiggle_cutoff > 0.0);
 }
 
 void set_config(MinConfig& c, const ffm_lbfgs_config* cfg) {
@@ -1630,6 +1724,9 @@ void set_config(MinConfig& c, const ffm_lbfgs_config* cfg) {
   c.fixed_step = cfg->fixed_step;
   c.momentum = cfg->momentum;
   c.ls_needs_grad = cfg->ls_kind == 1 && cfg->use_gradient_start;
+  c.wig_h = cfg->wiggle_h;
+  c.wig_cutoff = cfg->wiggle_cutoff;
+  c.wig_epoch = cfg->wiggle_epoch;
 }
 
 }  // namespace
@@ -1652,6 +1749,17 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   set_config(c, cfg);
   c.horizon = 0;
   c.sched = nullptr;
+  c.wig_atoms = nullptr;
+  if (c.method == kMethodWiggle) {
+    if (cudaMalloc(&L->wbuf, kWigBufBytes) != cudaSuccess ||
+        cudaMalloc(&L->wig_atoms, (size_t)c.chunk * sizeof(int)) != cudaSuccess ||
+        cudaMemset(L->wig_atoms, 0, (size_t)c.chunk * sizeof(int)) != cudaSuccess) {
+      lbfgs_free(L);
+      delete L;
+      return fail(FFM_ENOMEM, "cudaMalloc failed for the wiggle run");
+    }
+    c.wig_atoms = L->wig_atoms;
+  }
   L->n = 3 * (int64_t)std::max(1, s->plan.n);
   const int64_t n = L->n;
   const size_t nbuf = (size_t)n * (12 + 2 * (c.m + 1));
@@ -1694,9 +1802,11 @@ int ffm_lbfgs_configure(ffm_lbfgs_t* L, const ffm_lbfgs_config* cfg) {
     return fail(FFM_EINVAL, "configuration changes the graph structure: create a new run");
   const long long horizon = L->cfg.horizon;
   const double* sched = L->cfg.sched;
+  const int* atoms = L->cfg.wig_atoms;
   set_config(L->cfg, cfg);
   L->cfg.horizon = horizon;
   L->cfg.sched = sched;
+  L->cfg.wig_atoms = atoms;
   return FFM_OK;
 }
 
@@ -1800,6 +1910,18 @@ int ffm_lbfgs_set_schedule(ffm_lbfgs_t* L, const double* t_h, int64_t len) {
   FFM_CUDA(cudaMemcpy(L->sched, t_h, (size_t)len * sizeof(double), cudaMemcpyHostToDevice));
   L->cfg.horizon = len - 1;
   L->cfg.sched = L->sched;
+  return FFM_OK;
+}
+
+int ffm_lbfgs_set_atoms(ffm_lbfgs_t* L, const int32_t* atoms_h, int64_t count) {
+  if (!L || !atoms_h) return fail(FFM_EINVAL, "NULL argument");
+  if (L->cfg.method != kMethodWiggle) return fail(FFM_EINVAL, "not a wiggle run");
+  if (count < L->cfg.chunk) return fail(FFM_EINVAL, "need one atom per iteration of a launch");
+  for (int64_t k = 0; k < L->cfg.chunk; ++k)
+    if (atoms_h[k] < 0 || atoms_h[k] >= L->sys->plan.n) return fail(FFM_EINVAL, "atom out of range");
+  DeviceGuard guard(L->device);
+  FFM_CUDA(cudaMemcpy(L->wig_atoms, atoms_h, (size_t)L->cfg.chunk * sizeof(int),
+                      cudaMemcpyHostToDevice));
   return FFM_OK;
 }
 

@@ -206,6 +206,22 @@ cudaError_t launch_ofgm_x(MinState* S, int64_t n, const double* y, const double*
                           int from_ls, cudaStream_t st);
 cudaError_t launch_ofgm_post(MinState* S, const double* en, const int64_t* stw, double* rec,
                              int from_en, cudaStream_t st);
+// gradient-free wiggle (ffmin/optimizers/wiggle.py): probe positions, the
+// three decisions (vertex probe hv, exact check hx, epoch re-evaluation he)
+cudaError_t launch_wig_prep(MinState* S, const double* coords, int* atoms6, double* newpos6,
+                            cudaStream_t st);
+cudaError_t launch_wig_ctrl1(MinState* S, const double* out, const int64_t* stw, int* atoms1,
+                             cudaGraphConditionalHandle hv, cudaStream_t st);
+cudaError_t launch_wig_pos(MinState* S, const double* coords, double* newpos1, int which,
+                           cudaStream_t st);
+cudaError_t launch_wig_ctrl_v(MinState* S, const double* out, const int64_t* stw,
+                              cudaStream_t st);
+cudaError_t launch_wig_ctrl2(MinState* S, cudaGraphConditionalHandle hx, cudaStream_t st);
+cudaError_t launch_wig_ctrl3(MinState* S, const double* out, const int64_t* stw, double* coords,
+                             cudaStream_t st);
+cudaError_t launch_wig_end(MinState* S, cudaGraphConditionalHandle he, cudaStream_t st);
+cudaError_t launch_wig_epoch(MinState* S, const double* en, const int64_t* stw, cudaStream_t st);
+cudaError_t launch_wig_record(MinState* S, double* rec, cudaStream_t st);
 cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
                              const double* x_new, double* best, cudaStream_t st);
 cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const double* y_tmp,

@@ -36,11 +36,13 @@ struct MinConfig {
   long long horizon;
   const double* sched;
   int ls_needs_grad;   // the line search seeds from the slope (ls_par + gradient start)
-  int pad2;
+  int wig_epoch;       // wiggle: exact re-evaluation period (incremental probes)
+  double wig_h, wig_cutoff;  // wiggle: probe step, linearisation cutoff (0: exact probes)
+  const int* wig_atoms;      // wiggle: the atom of each iteration of a launch
 };
 
 enum : int { kMethodLbfgs = 0, kMethodCg = 1, kMethodSd = 2, kMethodFgm = 3, kMethodFixed = 4,
-             kMethodOfgm = 5 };
+             kMethodOfgm = 5, kMethodWiggle = 6 };
 
 // run status codes (host maps them to the reference's strings)
 enum : int { kMinNone = 0, kMinConverged = 1, kMinIterBudget = 2, kMinLsFailure = 3,
@@ -91,6 +93,10 @@ struct MinState {
   double f_init;  // f(x0): the fixed-step divergence test
   // OFGM: t_k, 1 - 1/t_{k+1}, 2/t_{k+1}, 1/t_{k+1}; the iteration's step
   double oc[4], step;
+  // wiggle (ffmin/optimizers/wiggle.py): the iteration's atom, its six axis
+  // probe values, vertex probe, chosen move and outcome
+  int wig_atom, wig_vtx, wig_best, wig_moved;
+  double wig_pv[6], wig_vertex[3], wig_dv, wig_delta[3], wig_est;
 };
 
 }  // namespace ffm

@@ -528,6 +528,166 @@ __global__ void ofgm_post_kernel(MinState* S, const double* en, const int64_t* s
   }
 }
 
+// ---- gradient-free atom wiggle (ffmin/optimizers/wiggle.py)
+constexpr double kWigAcceptMargin = 1e-9;  // wiggle.py ACCEPT_MARGIN
+
+// a probe's energy change (out row of atom_delta_kernel); +inf when the move
+// hit degenerate geometry (the reference catches the evaluation error)
+__device__ inline double wig_value(const double* o, const int64_t* st, bool lin) {
+  if (st[0] >= 0 || st[1] >= 0 || st[2] >= 0) return (double)INFINITY;
+  double v = o[2] + o[3] + o[4] + o[0] + o[1];  // float(o[2]) + ... left to right
+  if (lin) v += o[5];
+  return v;
+}
+
+// the iteration's atom and its six axis probes (+-h along x, y, z)
+__global__ void wig_prep_kernel(MinState* S, const double* __restrict__ coords,
+                                int* __restrict__ atoms6, double* __restrict__ newpos6) {
+  const int a = S->c.wig_atoms[S->iters_launch - 1];
+  S->wig_atom = a;
+  const double h = S->c.wig_h;
+  for (int i = 0; i < 6; ++i) {
+    const int axis = i >> 1;
+    const double step = (i & 1) ? 1.0 * h : -1.0 * h;
+    atoms6[i] = a;
+    for (int c = 0; c < 3; ++c) newpos6[3 * i + c] = coords[3 * a + c] + (c == axis ? step : 0.0);
+  }
+}
+
+// the six probe values -> per-axis parabola vertex (fit_parabola through
+// (-h, dm), (0, 0), (h, dp); without an interior minimum the best probe
+// offset); a non-zero vertex is probed next (hv)
+__global__ void wig_ctrl1_kernel(MinState* S, const double* __restrict__ out,
+                                 const int64_t* __restrict__ st, int* __restrict__ atoms1,
+                                 cudaGraphConditionalHandle hv) {
+  const bool lin = S->c.wig_cutoff > 0.0;
+  const int w = lin ? 6 : 5;
+  const double h = S->c.wig_h;
+  for (int i = 0; i < 6; ++i) S->wig_pv[i] = wig_value(out + w * i, st + 3 * i, lin);
+  S->vcalls += 6;
+  bool any = false;
+  for (int axis = 0; axis < 3; ++axis) {
+    const double dm = S->wig_pv[2 * axis], dp = S->wig_pv[2 * axis + 1];
+    bool have = false;
+    double v = 0.0;
+    if (isfinite(dm) && isfinite(dp)) {
+      const double x0 = -h, x1 = 0.0, x2 = h, f0 = dm, f1 = 0.0, f2 = dp;
+      const double s01 = (f1 - f0) / (x1 - x0);
+      const double s12 = (f2 - f1) / (x2 - x1);
+      const double curv = (s12 - s01) / (x2 - x0);
+      double mx = fabs(f0);
+      if (fabs(f1) > mx) mx = fabs(f1);
+      if (fabs(f2) > mx) mx = fabs(f2);
+      const bool degenerate = fabs(curv) < 1e-12 * mx;
+      if (!(curv <= 0.0 || degenerate)) {
+        have = true;
+        v = 0.5 * (x0 + x1) - s01 / (2.0 * curv);
+      }
+    }
+    double vx;
+    if (!have) {  // min(choices): (value, offset) tuples, lexicographic
+      double bv = 0.0, bo = 0.0;
+      if (isfinite(dm) && (dm < bv || (dm == bv && -h < bo))) bv = dm, bo = -h;
+      if (isfinite(dp) && (dp < bv || (dp == bv && h < bo))) bv = dp, bo = h;
+      vx = bo;
+    } else {  // min(max(v, -10 h), 10 h), Python's first-maximum semantics
+      const double lo = -10.0 * h, hi = 10.0 * h;
+      const double t = lo > v ? lo : v;
+      vx = hi < t ? hi : t;
+    }
+    S->wig_vertex[axis] = vx;
+    any = any || vx != 0.0;
+  }
+  S->wig_vtx = any ? 1 : 0;
+  S->wig_dv = (double)INFINITY;
+  atoms1[0] = S->wig_atom;  // the single-candidate probes (vertex, exact)
+  cudaGraphSetConditional(hv, any ? 1u : 0u);
+}
+
+// newpos1 = coords[atom] + (vertex | delta)  (which = 0: vertex, 1: delta)
+__global__ void wig_pos_kernel(const MinState* S, const double* __restrict__ coords,
+                               double* __restrict__ newpos1, int which) {
+  const int a = S->wig_atom;
+  const double* d = which ? S->wig_delta : S->wig_vertex;
+  for (int c = 0; c < 3; ++c) newpos1[c] = coords[3 * a + c] + d[c];
+}
+
+__global__ void wig_ctrl_v_kernel(MinState* S, const double* __restrict__ out,
+                                  const int64_t* __restrict__ st) {
+  S->wig_dv = wig_value(out, st, S->c.wig_cutoff > 0.0);
+  S->vcalls++;
+}
+
+// the candidate of least estimated change (axis probes in order, then the
+// vertex; first minimum as min(..., key=...)); a clear decrease is checked
+// exactly next (hx)
+__global__ void wig_ctrl2_kernel(MinState* S, cudaGraphConditionalHandle hx) {
+  const double h = S->c.wig_h;
+  int best = -1;
+  double bv = 0.0;
+  for (int i = 0; i < 6; ++i)
+    if (isfinite(S->wig_pv[i]) && (best < 0 || S->wig_pv[i] < bv)) best = i, bv = S->wig_pv[i];
+  if (S->wig_vtx && isfinite(S->wig_dv) && (best < 0 || S->wig_dv < bv)) best = 6, bv = S->wig_dv;
+  S->wig_best = best;
+  S->wig_moved = 0;
+  unsigned go = 0;
+  if (best >= 0) {
+    for (int c = 0; c < 3; ++c)
+      S->wig_delta[c] = best == 6 ? S->wig_vertex[c]
+                                  : (c == (best >> 1) ? ((best & 1) ? 1.0 * h : -1.0 * h) : 0.0);
+    S->wig_est = bv;
+    go = bv < -kWigAcceptMargin ? 1u : 0u;
+  }
+  cudaGraphSetConditional(hx, go);
+}
+
+// the exact change decides: coords[atom] += delta, e += exact
+__global__ void wig_ctrl3_kernel(MinState* S, const double* __restrict__ out,
+                                 const int64_t* __restrict__ st, double* __restrict__ coords) {
+  const double exact = wig_value(out, st, false);
+  if (isfinite(exact)) S->vcalls++;
+  if (exact < -kWigAcceptMargin) {
+    const int a = S->wig_atom;
+    for (int c = 0; c < 3; ++c) coords[3 * a + c] = coords[3 * a + c] + S->wig_delta[c];
+    S->f = S->f + exact;
+    S->wig_moved = 1;
+  }
+}
+
+// end of an iteration: k, the epoch re-evaluation (he), then the record
+__global__ void wig_end_kernel(MinState* S, cudaGraphConditionalHandle he) {
+  S->k++;
+  const bool epoch = S->c.wig_cutoff > 0.0 && S->k % S->c.wig_epoch == 0;
+  cudaGraphSetConditional(he, epoch ? 1u : 0u);
+}
+
+__global__ void wig_epoch_kernel(MinState* S, const double* en, const int64_t* stw) {
+  if (bad_status(stw, false)) {
+    set_err(S, kMinErrEval, stw, false);
+    return;
+  }
+  S->f = en[0] + en[1] + en[2] + en[3] + en[4];
+  S->vcalls++;
+}
+
+// record (k, e, -, step, calls, -, t, best): the move's components ride in
+// columns 2, 3, 5 (NaN in 2 when nothing moved); the host takes the norm
+__global__ void wig_record_kernel(MinState* S, double* rec) {
+  if (S->err) return;
+  if (S->f < S->best_f) S->best_f = S->f;
+  double* r = rec + S->nrec * kMinRecWidth;
+  const bool m = S->wig_moved != 0;
+  r[0] = (double)S->k;
+  r[1] = S->f;
+  r[2] = m ? S->wig_delta[0] : (double)NAN;
+  r[3] = m ? S->wig_delta[1] : 0.0;
+  r[4] = (double)S->vcalls;
+  r[5] = m ? S->wig_delta[2] : 0.0;
+  r[6] = (double)(globaltimer() - S->t_launch);
+  r[7] = S->best_f;
+  S->nrec++;
+}
+
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
@@ -594,6 +754,38 @@ cudaError_t launch_fgm_accept(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(fgm_accept_kernel, S, rec);
 }
 cudaError_t launch_ofgm_pre(MinState* S, cudaStream_t st) { FFM_ONE(ofgm_pre_kernel, S); }
+cudaError_t launch_wig_prep(MinState* S, const double* coords, int* atoms6, double* newpos6,
+                            cudaStream_t st) {
+  FFM_ONE(wig_prep_kernel, S, coords, atoms6, newpos6);
+}
+cudaError_t launch_wig_ctrl1(MinState* S, const double* out, const int64_t* stw, int* atoms1,
+                             cudaGraphConditionalHandle hv, cudaStream_t st) {
+  FFM_ONE(wig_ctrl1_kernel, S, out, stw, atoms1, hv);
+}
+cudaError_t launch_wig_pos(MinState* S, const double* coords, double* newpos1, int which,
+                           cudaStream_t st) {
+  FFM_ONE(wig_pos_kernel, S, coords, newpos1, which);
+}
+cudaError_t launch_wig_ctrl_v(MinState* S, const double* out, const int64_t* stw,
+                              cudaStream_t st) {
+  FFM_ONE(wig_ctrl_v_kernel, S, out, stw);
+}
+cudaError_t launch_wig_ctrl2(MinState* S, cudaGraphConditionalHandle hx, cudaStream_t st) {
+  FFM_ONE(wig_ctrl2_kernel, S, hx);
+}
+cudaError_t launch_wig_ctrl3(MinState* S, const double* out, const int64_t* stw, double* coords,
+                             cudaStream_t st) {
+  FFM_ONE(wig_ctrl3_kernel, S, out, stw, coords);
+}
+cudaError_t launch_wig_end(MinState* S, cudaGraphConditionalHandle he, cudaStream_t st) {
+  FFM_ONE(wig_end_kernel, S, he);
+}
+cudaError_t launch_wig_epoch(MinState* S, const double* en, const int64_t* stw, cudaStream_t st) {
+  FFM_ONE(wig_epoch_kernel, S, en, stw);
+}
+cudaError_t launch_wig_record(MinState* S, double* rec, cudaStream_t st) {
+  FFM_ONE(wig_record_kernel, S, rec);
+}
 cudaError_t launch_ofgm_dir(MinState* S, cudaGraphConditionalHandle hz,
                             cudaGraphConditionalHandle hnz, cudaStream_t st) {
   FFM_ONE(ofgm_dir_kernel, S, hz, hnz);

@@ -59,3 +59,31 @@ def test_wiggle_tracks_reference(golden, name):
     # every accepted move strictly lowered the energy
     assert all(b < a for a, b, st in zip(f, f[1:], steps[1:]) if st > 0)
     assert math.isnan(res.grad_norm)
+
+
+@pytest.mark.parametrize("inc", [True, False])
+def test_graph_wiggle_equals_host_loop(golden, monkeypatch, inc):
+    """The graph-resident wiggle (probe batches, parabola vertex, exact check,
+    epoch re-evaluation as conditional nodes) makes the host loop's
+    decisions with its arithmetic: identical records, coordinates, calls."""
+    from paper_1810_03358_b200.optimizers import StopCriteria
+    from paper_1810_03358_b200.optimizers.wiggle import WiggleConfig, atom_wiggle
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(900, seed=6)
+    cfg = WiggleConfig(h=0.05, seed=3, epoch_iterations=25, use_incremental_coulomb=inc,
+                       cutoff=7.0)
+    out = []
+    for host in (True, False):
+        if host:
+            monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
+        else:
+            monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
+        out.append(atom_wiggle(s, cfg, StopCriteria(max_iterations=150, gradient_norm_rtol=0.0)))
+    a, b = out
+    ra = [(r.iteration, r.f, r.step, r.value_calls, r.best_f) for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.step, r.value_calls, r.best_f) for r in b.trace.records]
+    assert len(ra) == len(rb) == 151
+    assert ra == rb
+    assert a.f == b.f and a.status == b.status and np.array_equal(a.x, b.x)
+    assert sum(1 for r in a.trace.records if r.step > 0) > 10  # moves were made
