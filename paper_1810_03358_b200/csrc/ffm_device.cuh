@@ -336,12 +336,21 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
       g1 += (double)p[st];
       g2 += (double)p[2 * st];
     }
-  } else if (use_nb) {  // super-unit mode: [unit][3][S] rows and columns
+  } else if (use_nb && nranks == 1) {  // super-unit mode: [unit][3][S] rows and columns
     const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
 #pragma unroll 4
     for (int k = warp; k <= nb; k += NW) {
+      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
+                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
+      g0 += (double)p[off];
+      g1 += (double)p[S + off];
+      g2 += (double)p[2 * S + off];
+    }
+  } else if (use_nb) {  // the same, this rank's units only
+    const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
+    for (int k = warp; k <= nb; k += NW) {
       const int u = k < ni ? unit_index[b * nb + b + k] : unit_index[(k - ni) * nb + b];
-      if (nranks > 1 && u % nranks != rank) continue;
+      if (u % nranks != rank) continue;
       const T* p = (k < ni ? ipart : jpart) + (size_t)u * 3 * S;
       g0 += (double)p[off];
       g1 += (double)p[S + off];
