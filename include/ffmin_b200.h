@@ -96,6 +96,18 @@ int ffm_system_destroy(ffm_system_t* sys);
  * paper_1810_03358_b200.parallel).  nranks = 1 restores the full sweep. */
 int ffm_system_set_shard(ffm_system_t* sys, int rank, int nranks);
 
+/* The NCCL communicator (ncclComm_t, e.g. torch's ProcessGroupNCCL
+ * _comm_ptr()) of a sharded system's ranks.  With it attached, every
+ * ffm_eval / ffm_eval_host of the sharded system -- and every evaluation
+ * inside the graph-resident drivers, which then accept sharded systems --
+ * completes on the device with one all-reduce of [gradient | energies |
+ * error words] on the evaluation's stream (what parallel.ShardCombiner does
+ * from Python; capturable in CUDA graphs), so it returns global values.
+ * ffm_eval_batch keeps returning the rank's partial energies.  The library
+ * resolves ncclAllReduce from the libnccl.so.2 already loaded in the
+ * process.  NULL detaches. */
+int ffm_system_set_comm(ffm_system_t* sys, void* nccl_comm);
+
 /* Device time of the pair sweep of the last FFM_TIME_NB evaluation
  * (CUDA events on the evaluation's stream; synchronises on them). */
 int ffm_system_nb_ms(ffm_system_t* sys, float* ms_h);

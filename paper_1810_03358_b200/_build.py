@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs.append(str(obj))
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
-          *objs], verbose)
+          *objs, "-ldl"], verbose)
     os.replace(tmp, LIB)
     for o in objs:
         os.remove(o)

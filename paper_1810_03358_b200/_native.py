@@ -62,6 +62,7 @@ SIGNATURES = {
     "ffm_lbfgs_two_loop": (_I, [_I64, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
     "ffm_lbfgs_create": (_I, [_P, _I, _P, C.POINTER(_P)]),
     "ffm_lbfgs_configure": (_I, [_P, _P]),
+    "ffm_system_set_comm": (_I, [_P, _P]),
     "ffm_lbfgs_start": (_I, [_P, _P, _P, _D, _D, _D, _P]),
     "ffm_lbfgs_run": (_I, [_P, _P]),
     "ffm_lbfgs_poll": (_I, [_P, _P, _P, _P, _I64, _P, _P]),

@@ -1,5 +1,8 @@
 // ffm_capi.cu -- the extern "C" boundary (include/ffmin_b200.h): system
 // plans resident in HBM, workspace management and launch sequencing.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -13,6 +16,24 @@
 #include "../../include/ffmin_b200.h"
 #include "ffm_kernels.h"
 #include "ffm_min.cuh"
+
+// ncclAllReduce from the libnccl.so.2 the process has loaded (torch's), or
+// any the loader finds; resolved once
+using AllReduceFn = ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                     ncclComm_t, cudaStream_t);
+static AllReduceFn nccl_allreduce() {
+  static AllReduceFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) fn = reinterpret_cast<AllReduceFn>(dlsym(h, "ncclAllReduce"));
+    if (!fn) fn = reinterpret_cast<AllReduceFn>(dlsym(RTLD_DEFAULT, "ncclAllReduce"));
+  }
+  return fn;
+}
+
 
 using namespace ffm;
 
@@ -76,6 +97,9 @@ struct ffm_system {
   int device = 0;
   NbPlanDev plan{};
   int S0 = 0;  // the super-unit edge chosen at creation (single-rank plan)
+  // sharded evaluations completed on the device (ffm_system_set_comm)
+  void* comm = nullptr;
+  double* d_comb = nullptr;  // [3n + 13]
   // batched (multi-candidate, energy-only) sweeps: super-units as large as
   // divide np -- with B geometries per launch the grid is large whatever the
   // unit size, so larger units amortise their overheads (configs[3])
@@ -162,7 +186,7 @@ struct ffm_system {
 namespace {
 
 void free_all(ffm_system* s) {
-  void* ptrs[] = {s->d_unit_rc, s->d_unit_rc_b, s->d_unit_index, s->d_spt_ptr, s->d_spt_m,
+  void* ptrs[] = {s->d_comb, s->d_unit_rc, s->d_unit_rc_b, s->d_unit_index, s->d_spt_ptr, s->d_spt_m,
                   s->d_spt_mask,
                   s->d_sp_ptr, s->d_sp_j, s->d_sp_s, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
                   s->d_qt, s->d_lj32, s->d_lj64, s->d_ilj32, s->d_ilj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
@@ -804,6 +828,23 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
   return FFM_OK;
 }
 
+int ffm_system_set_comm(ffm_system_t* s, void* comm) {
+  if (!s) return fail(FFM_EINVAL, "NULL argument");
+  DeviceGuard guard(s->device);
+  FFM_CUDA(cudaDeviceSynchronize());
+  drop_graphs(s);
+  s->comm = nullptr;
+  if (!comm) return FFM_OK;
+  if (!nccl_allreduce()) return fail(FFM_EINVAL, "ncclAllReduce not found (libnccl.so.2 not loaded)");
+  if (!s->d_comb) {
+    const size_t bytes = ((size_t)3 * s->plan.n + FFM_NTERMS + 8) * sizeof(double);
+    if (cudaMalloc(&s->d_comb, bytes) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for the all-reduce buffer");
+  }
+  s->comm = comm;
+  return FFM_OK;
+}
+
 int ffm_debug_phase_clock(ffm_system_t* s, void* clock_d, int* grids) {
   if (!s || !grids) return fail(FFM_EINVAL, "NULL argument");
   s->phase_clock = static_cast<unsigned long long*>(clock_d);
@@ -895,8 +936,31 @@ static int issue_small(ffm_system* s, int precision, bool grad, const double* co
   return FFM_OK;
 }
 
+static int issue_eval_local(ffm_system* s, int precision, int flags, const double* coords_d,
+                            double* grad_d, double* energies_d, int64_t* status_d,
+                            cudaStream_t st);
+
+// One evaluation; a sharded system with a communicator completes it on the
+// device: encode, one NCCL all-reduce, decode (parallel.py's ShardCombiner)
 static int issue_eval(ffm_system* s, int precision, int flags, const double* coords_d,
                       double* grad_d, double* energies_d, int64_t* status_d, cudaStream_t st) {
+  FFM_TRYR(issue_eval_local(s, precision, flags, coords_d, grad_d, energies_d, status_d, st));
+  if (s->nranks <= 1 || !s->comm) return FFM_OK;
+  const bool grad = (flags & FFM_GRAD) != 0;
+  const int64_t n = s->plan.n, n3 = 3 * n;
+  double* buf = grad ? s->d_comb : s->d_comb + n3;
+  const size_t count = (size_t)(grad ? n3 : 0) + FFM_NTERMS + 8;
+  FFM_CUDA(launch_combine_encode(n, grad ? grad_d : nullptr, energies_d, status_d, s->d_comb, st));
+  const ncclResult_t r = nccl_allreduce()(buf, buf, count, ncclFloat64, ncclSum,
+                                          static_cast<ncclComm_t>(s->comm), st);
+  if (r != ncclSuccess) return fail(FFM_ECUDA, "ncclAllReduce failed (" + std::to_string((int)r) + ")");
+  FFM_CUDA(launch_combine_decode(n, s->d_comb, grad ? grad_d : nullptr, energies_d, status_d, st));
+  return FFM_OK;
+}
+
+static int issue_eval_local(ffm_system* s, int precision, int flags, const double* coords_d,
+                            double* grad_d, double* energies_d, int64_t* status_d,
+                            cudaStream_t st) {
   const bool grad = (flags & FFM_GRAD) != 0;
   Work& w = s->w[precision];
   const bool f64 = precision == FFM_F64;
@@ -1738,7 +1802,9 @@ int ffm_lbfgs_create(ffm_system_t* s, int precision, const ffm_lbfgs_config* cfg
   if (!s || !cfg || !out) return fail(FFM_EINVAL, "NULL argument");
   *out = nullptr;
   if (precision != FFM_F64 && precision != FFM_F32) return fail(FFM_EINVAL, "bad precision");
-  if (s->nranks != 1) return fail(FFM_EINVAL, "graph-resident L-BFGS needs an unsharded system");
+  if (s->nranks != 1 && !s->comm)
+    return fail(FFM_EINVAL, "graph-resident drivers need an unsharded system or a communicator "
+                            "(ffm_system_set_comm)");
   FFM_TRYR(check_config(cfg));
   DeviceGuard guard(s->device);
   auto* L = new ffm_lbfgs();

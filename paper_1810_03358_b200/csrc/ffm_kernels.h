@@ -139,6 +139,14 @@ int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device);
 cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int grid,
                               cudaStream_t st);
 
+// ---- sharded evaluations completed on the device (ffm_vec.cu): pack the
+// rank's partial [gradient | energies | error words] into buf (3n + 13
+// doubles; grad null: the 13-word tail only), and unpack the all-reduced sums
+cudaError_t launch_combine_encode(int64_t natoms, const double* grad, const double* energies,
+                                  const int64_t* status, double* buf, cudaStream_t st);
+cudaError_t launch_combine_decode(int64_t natoms, const double* buf, double* grad,
+                                  double* energies, int64_t* status, cudaStream_t st);
+
 // ---- vector algebra (ffm_vec.cu) ----
 int vec_reduce_blocks();
 cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,

@@ -5,7 +5,11 @@
 // leave the device.  All reductions use a fixed grid and a fixed combination
 // order, so every dot product -- and therefore every optimiser trace -- is
 // bit-identical run to run.
+#include <cmath>
+
 #include <cooperative_groups.h>
+
+#include "../../include/ffmin_b200.h"
 #include "ffm_kernels.h"
 
 namespace cg = cooperative_groups;
@@ -340,6 +344,81 @@ cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* id
   count_launch();
   return cudaLaunchCooperativeKernel((void*)two_loop_dev_kernel, two_loop_grid(n), kVecThreads,
                                      args, 0, st);
+}
+
+}  // namespace ffm
+
+
+namespace ffm {
+
+// ---- device-side completion of a sharded evaluation (ffm_system_set_comm)
+// buf = [gradient (3n) | energies (5) | error (key + 1) x 4 | reporting x 4];
+// a rank reporting an error adds (key + 1, 1), and all reporting ranks
+// report the same key (parallel.py), so key = sum / count - 1 exactly.
+constexpr int kCombTail = FFM_NTERMS + 8;
+
+__global__ void combine_encode_kernel(int64_t n3, int64_t natoms, const double* __restrict__ grad,
+                                      const double* __restrict__ energies,
+                                      const int64_t* __restrict__ status, double* __restrict__ buf) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (grad)
+    for (int64_t i = i0; i < n3; i += (int64_t)gridDim.x * blockDim.x) buf[i] = grad[i];
+  if (i0 == 0) {
+    double* t = buf + n3;
+    for (int q = 0; q < FFM_NTERMS; ++q) t[q] = energies[q];
+    const int64_t keys[4] = {status[FFM_ST_NB_BAD_I] >= 0
+                                 ? status[FFM_ST_NB_BAD_I] * natoms + status[FFM_ST_NB_BAD_J]
+                                 : -1,
+                             status[FFM_ST_BOND], status[FFM_ST_ANGLE], status[FFM_ST_DIHEDRAL]};
+    for (int q = 0; q < 4; ++q) {
+      t[FFM_NTERMS + q] = keys[q] >= 0 ? (double)(keys[q] + 1) : 0.0;
+      t[FFM_NTERMS + 4 + q] = keys[q] >= 0 ? 1.0 : 0.0;
+    }
+  }
+}
+
+__global__ void combine_decode_kernel(int64_t n3, int64_t natoms, const double* __restrict__ buf,
+                                      double* __restrict__ grad, double* __restrict__ energies,
+                                      int64_t* __restrict__ status) {
+  const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (grad)
+    for (int64_t i = i0; i < n3; i += (int64_t)gridDim.x * blockDim.x) grad[i] = buf[i];
+  if (i0 == 0) {
+    const double* t = buf + n3;
+    for (int q = 0; q < FFM_NTERMS; ++q) energies[q] = t[q];
+    int64_t key[4];
+    for (int q = 0; q < 4; ++q) {
+      const double c = t[FFM_NTERMS + 4 + q];
+      key[q] = c > 0.0 ? (int64_t)llround(t[FFM_NTERMS + q] / c) - 1 : -1;
+    }
+    status[FFM_ST_NB_BAD_I] = key[0] >= 0 ? key[0] / natoms : -1;
+    status[FFM_ST_NB_BAD_J] = key[0] >= 0 ? key[0] % natoms : -1;
+    status[FFM_ST_BOND] = key[1];
+    status[FFM_ST_ANGLE] = key[2];
+    status[FFM_ST_DIHEDRAL] = key[3];
+  }
+}
+
+static int comb_blocks(int64_t n3) {
+  int64_t b = (n3 + 255) / 256;
+  if (b > 1184) b = 1184;
+  return b < 1 ? 1 : (int)b;
+}
+
+cudaError_t launch_combine_encode(int64_t natoms, const double* grad, const double* energies,
+                                  const int64_t* status, double* buf, cudaStream_t st) {
+  count_launch();
+  combine_encode_kernel<<<grad ? comb_blocks(3 * natoms) : 1, 256, 0, st>>>(
+      3 * natoms, natoms, grad, energies, status, buf);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_combine_decode(int64_t natoms, const double* buf, double* grad,
+                                  double* energies, int64_t* status, cudaStream_t st) {
+  count_launch();
+  combine_decode_kernel<<<grad ? comb_blocks(3 * natoms) : 1, 256, 0, st>>>(
+      3 * natoms, natoms, buf, grad, energies, status);
+  return cudaGetLastError();
 }
 
 }  // namespace ffm

@@ -29,10 +29,16 @@ def eligible_fixed(oracle, ops) -> bool:
     """The device molecular oracle (and FFMIN_B200_HOST_LOOP unset): the
     fixed-step drivers run in the graph."""
     from ..oracle import MolecularOracle
+    from ..parallel import ShardedMolecularOracle
 
     if os.environ.get("FFMIN_B200_HOST_LOOP"):
         return False
-    return ops.space == "device" and type(oracle) is MolecularOracle
+    if ops.space != "device":
+        return False
+    # a row-sharded oracle qualifies when its evaluations complete on the
+    # device (NCCL communicator attached): the all-reduce is captured too
+    return type(oracle) is MolecularOracle or (
+        type(oracle) is ShardedMolecularOracle and oracle.native)
 
 
 def eligible(oracle, ops, linesearch, m: int = 1) -> bool:

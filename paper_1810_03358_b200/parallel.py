@@ -91,9 +91,12 @@ class ShardCombiner:
 
 class ShardedSystem:
     """This rank's engine handle (a private DeviceSystem with a shard) plus
-    the combiner; evaluates like engine.DeviceSystem.eval, globally."""
+    the completion of its partial evaluations: on the device (the group's
+    NCCL communicator attached to the engine, ffm_system_set_comm: one
+    all-reduce inside every evaluation, capturable in the graph-resident
+    drivers) or, for other backends, by ShardCombiner from Python."""
 
-    def __init__(self, topo, group=None, device=None):
+    def __init__(self, topo, group=None, device=None, native=True):
         from .engine import DeviceSystem
 
         self.rank = dist.get_rank(group)
@@ -103,7 +106,25 @@ class ShardedSystem:
                 "ffm_system_set_shard")
         self.n = topo.natoms
         self.device = self.engine.device
+        self.handle = self.engine.handle
+        self.lib = self.engine.lib
         self.combiner = ShardCombiner(self.n, self.device, group)
+        self.native = native and self._attach_comm(group)
+
+    def _attach_comm(self, group):
+        """The group's ncclComm_t, if its backend is NCCL (created eagerly
+        by a one-element all-reduce)."""
+        try:
+            pg = group if group is not None else dist.distributed_c10d._get_default_group()
+            probe = torch.zeros(1, device=self.device)
+            dist.all_reduce(probe, group=group)
+            backend = pg._get_backend(self.device)
+            ptr = int(backend._comm_ptr())
+        except Exception:
+            return False
+        if not ptr:
+            return False
+        return self.engine.lib.ffm_system_set_comm(self.handle, C.c_void_p(ptr)) == 0
 
     def new_outputs(self):
         return self.engine.new_outputs()
@@ -112,7 +133,8 @@ class ShardedSystem:
              flags=None):
         energies, status = self.engine.eval(coords, precision, grad=grad, energies=energies,
                                             status=status, flags=flags)
-        self.combiner.combine(grad, energies, status)
+        if not self.native:
+            self.combiner.combine(grad, energies, status)
         return energies, status
 
 
@@ -122,13 +144,13 @@ class ShardedMolecularOracle:
 
     space = "device"
 
-    def __init__(self, system, dtype=np.float64, group=None, device=None):
+    def __init__(self, system, dtype=np.float64, group=None, device=None, native=True):
         from .engine import precision_of
         from .oracle import MolecularOracle
 
         self._base = MolecularOracle.__new__(MolecularOracle)
         MolecularOracle.__init__(self._base, system, dtype, device=device)
-        self._base.engine = ShardedSystem(system.topology, group, device)
+        self._base.engine = ShardedSystem(system.topology, group, device, native)
         self.system = system
         self.n = 3 * system.natoms
         self.device = self._base.device
@@ -141,9 +163,22 @@ class ShardedMolecularOracle:
     def value_calls(self):
         return self._base.value_calls
 
+    @value_calls.setter
+    def value_calls(self, v):
+        self._base.value_calls = v
+
     @property
     def grad_calls(self):
         return self._base.grad_calls
+
+    @grad_calls.setter
+    def grad_calls(self, v):
+        self._base.grad_calls = v
+
+    @property
+    def native(self):
+        """Evaluations complete on the device (graph-resident drivers apply)."""
+        return self._base.engine.native
 
     def value(self, x):
         return self._base.value(x)
