@@ -18,14 +18,7 @@ namespace ffm {
 #ifndef FFM_UNROLL64
 #define FFM_UNROLL64 0  // 0: 4 with gradient, 8 energy-only (measured best)
 #endif
-#ifndef FFM_UNROLL_SMALL
-#define FFM_UNROLL_SMALL 4
-#endif
 constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
-// tile-mode / fused small-system sweeps: a few warps run each tile once, so
-// a cold instruction cache, not the FMA pipe, bounds them; a short loop body
-// (a few KB instead of ~25 KB fully unrolled) is faster there
-constexpr int kStepUnrollSmall = FFM_UNROLL_SMALL;
 constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/SM)
 #ifndef FFM_F64FORM
 #define FFM_F64FORM 2  // FP64 energy/gradient algebra variant (see warp_tile; 2 measured best)
@@ -64,10 +57,7 @@ __device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restric
 // i-atom pairs held per pass: FP32 keeps both packed pairs (4 i-atoms per
 // lane) live; FP64 sweeps them one after the other so the kernel fits 128
 // registers and two CTAs per SM
-#ifndef FFM_NP32
-#define FFM_NP32 2
-#endif
-template <typename T> struct PairsPerPass { static constexpr int value = FFM_NP32; };
+template <typename T> struct PairsPerPass { static constexpr int value = 2; };
 template <> struct PairsPerPass<double> { static constexpr int value = 1; };
 
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
