@@ -109,7 +109,8 @@ struct ffm_system {
   int nspt = 0;
   // device tables
   int2* d_unit_rc = nullptr;
-  int* d_unit_index = nullptr;
+  int* d_unit_index = nullptr;  // the gather's unit lists (build_units)
+  int2* d_unit_ks = nullptr;
   int* d_spt_ptr = nullptr;
   int* d_spt_m = nullptr;
   uint32_t* d_spt_mask = nullptr;
@@ -186,7 +187,8 @@ struct ffm_system {
 namespace {
 
 void free_all(ffm_system* s) {
-  void* ptrs[] = {s->d_comb, s->d_unit_rc, s->d_unit_rc_b, s->d_unit_index, s->d_spt_ptr, s->d_spt_m,
+  void* ptrs[] = {s->d_comb, s->d_unit_rc, s->d_unit_rc_b, s->d_unit_index, s->d_unit_ks,
+                  s->d_spt_ptr, s->d_spt_m,
                   s->d_spt_mask,
                   s->d_sp_ptr, s->d_sp_j, s->d_sp_s, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
                   s->d_qt, s->d_lj32, s->d_lj64, s->d_ilj32, s->d_ilj64, s->d_q, s->d_sigma, s->d_eps, s->d_sc_idx,
@@ -238,29 +240,90 @@ int choose_S(int64_t n) {
 }
 
 // (Re)build the super-unit tables of edge S (a divisor of np): units in
-// evaluation order, off-diagonal first (full work), diagonal last (half
-// work), and the (row, column) -> unit index map of the gather.
-int build_units(ffm_system* s, int S) {
+// evaluation order -- off-diagonal first (full work), then the last `nsplit`
+// off-diagonal units as two halves each (rows [0, nsub/2) and [nsub/2, nsub):
+// the final wave runs in half-size pieces, so its tail is half as long),
+// then the diagonal units (half work) -- and the gather's unit lists
+// (gather_group: the units holding each super-block half's rows, then the
+// units holding each super-block's columns).
+int build_units(ffm_system* s, int S, int nsplit) {
   NbPlanDev& p = s->plan;
   p.S = S;
   p.nb = p.np / S;
-  p.nunits = p.nb * (p.nb + 1) / 2;
-  std::vector<int2> urc;
-  std::vector<int> uidx((size_t)p.nb * p.nb, -1);
-  for (int r = 0; r < p.nb; ++r)
-    for (int c = r + 1; c < p.nb; ++c) urc.push_back(make_int2(r, c));
-  for (int r = 0; r < p.nb; ++r) urc.push_back(make_int2(r, r));
-  for (size_t u = 0; u < urc.size(); ++u) uidx[(size_t)urc[u].x * p.nb + urc[u].y] = (int)u;
-  if (s->d_unit_rc) cudaFree(s->d_unit_rc);
+  const int nb = p.nb, nsub = S / kIB, hs = nsub / 2;
+  const int noff = nb * (nb - 1) / 2;
+  if (nsplit > noff) nsplit = noff;
+  if (nsub < 2) nsplit = 0;
+  std::vector<int2> urc, uks;
+  std::vector<int> half0((size_t)nb * nb, -1), half1((size_t)nb * nb, -1);
+  int k = 0;
+  for (int r = 0; r < nb; ++r)
+    for (int c = r + 1; c < nb; ++c, ++k) {
+      const size_t key = (size_t)r * nb + c;
+      if (k < noff - nsplit) {
+        half0[key] = half1[key] = (int)urc.size();
+        urc.push_back(make_int2(r, c));
+        uks.push_back(make_int2(0, nsub));
+      } else {
+        half0[key] = (int)urc.size();
+        urc.push_back(make_int2(r, c));
+        uks.push_back(make_int2(0, hs));
+        half1[key] = (int)urc.size();
+        urc.push_back(make_int2(r, c));
+        uks.push_back(make_int2(hs, nsub));
+      }
+    }
+  for (int r = 0; r < nb; ++r) {
+    half0[(size_t)r * nb + r] = half1[(size_t)r * nb + r] = (int)urc.size();
+    urc.push_back(make_int2(r, r));
+    uks.push_back(make_int2(0, nsub));
+  }
+  p.nunits = (int)urc.size();
+  // gather lists: [row ptr (2 nb + 1) | column ptr (nb + 1) | rows | columns]
+  std::vector<int> rptr(2 * nb + 1, 0), cptr(nb + 1, 0), rows, cols;
+  for (int b = 0; b < nb; ++b)
+    for (int h = 0; h < 2; ++h) {
+      for (int cc = b; cc < nb; ++cc) rows.push_back((h ? half1 : half0)[(size_t)b * nb + cc]);
+      rptr[2 * b + h + 1] = (int)rows.size();
+    }
+  for (int b = 0; b < nb; ++b) {
+    for (int r = 0; r <= b; ++r) {
+      const size_t key = (size_t)r * nb + b;
+      cols.push_back(half0[key]);
+      if (half1[key] != half0[key]) cols.push_back(half1[key]);
+    }
+    cptr[b + 1] = (int)cols.size();
+  }
+  std::vector<int> lists;
+  lists.insert(lists.end(), rptr.begin(), rptr.end());
+  lists.insert(lists.end(), cptr.begin(), cptr.end());
+  lists.insert(lists.end(), rows.begin(), rows.end());
+  lists.insert(lists.end(), cols.begin(), cols.end());
+  for (int2** d : {&s->d_unit_rc, &s->d_unit_ks})
+    if (*d) cudaFree(*d), *d = nullptr;
   if (s->d_unit_index) cudaFree(s->d_unit_index);
-  s->d_unit_rc = nullptr;
   s->d_unit_index = nullptr;
   FFM_TRYR(upload(&s->d_unit_rc, urc));
-  FFM_TRYR(upload(&s->d_unit_index, uidx));
+  FFM_TRYR(upload(&s->d_unit_ks, uks));
+  FFM_TRYR(upload(&s->d_unit_index, lists));
   p.unit_rc = s->d_unit_rc;
+  p.unit_ks = s->d_unit_ks;
   p.unit_list = nullptr;
   if (p.ntiles == 0) p.nlaunch = p.n > 0 ? p.nunits : 0;
   return FFM_OK;
+}
+
+// units of the last wave split in halves: one wave of CTA slots (2 per SM)
+// per rank, since the units are dealt round-robin -- for S = 1024 only: a
+// half unit of S <= 512 pays the whole per-unit overhead for one or two
+// tiles per warp (measured, tools/mid_sweep.py A/B: 100k atoms, S = 1024
+// 4.41 -> 4.37 ms; 10k, S = 256 70.0 -> 71.8 us; 30k, S = 512 426 -> 433 us)
+int split_count(const ffm_system* s, int S, int nranks) {
+  if (const char* f = getenv("FFM_SPLIT_UNITS")) return atoi(f);  // tuning / tests
+  if (S < 1024) return 0;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device);
+  return 2 * sms * nranks;
 }
 
 // Super-unit edge of a row-sharded plan: every rank should still see about
@@ -403,7 +466,7 @@ int nb_slots(const NbPlanDev& p) { return p.ntiles ? p.ntiles : p.nunits; }
 bool use_tiles(const NbPlanDev& p, int device) {
   if (const char* f = getenv("FFM_FORCE_TILES")) return atoi(f) != 0;  // tuning / tests
   (void)device;
-  return p.nunits < 150;
+  return p.nb * (p.nb + 1) / 2 < 150;  // whole units (before the last wave's split)
 }
 
 int build_tiles(ffm_system* s) {
@@ -704,7 +767,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_sc_s, s->scaled_s));
 
   // ---- units: off-diagonal first (full work), diagonal last (half work)
-  FFM_TRY(build_units(s, p.S));
+  FFM_TRY(build_units(s, p.S, split_count(s, p.S, 1)));
   {  // the batch plan: the largest unit edge that divides np (units mode)
     NbPlanDev& b = s->bplan;
     b = p;
@@ -722,6 +785,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
     for (int r = 0; r < b.nb; ++r) brc.push_back(make_int2(r, r));
     FFM_TRY(upload(&s->d_unit_rc_b, brc));
     b.unit_rc = s->d_unit_rc_b;
+    b.unit_ks = nullptr;  // whole units
     b.unit_list = nullptr;
     b.ntiles = 0;
     b.tiles = nullptr;
@@ -795,10 +859,8 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
     // re-plan the super-unit edge for this shard count (the single-rank
     // edge is kept from creation: s->S0)
     const int S = nranks == 1 ? s->S0 : choose_S_sharded(s->plan, s->S0, nranks);
-    if (S != s->plan.S) {
-      int rc = build_units(s, S);
-      if (rc) return rc;
-    }
+    int rc = build_units(s, S, split_count(s, S, nranks));
+    if (rc) return rc;
   }
   if (s->plan.ntiles > 0) {
   } else if (nranks == 1) {

@@ -297,7 +297,7 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
 // straddles a super-block or a tile row) by the NW warps of a block
 // (block-uniform call, contains __syncthreads).  The group's partial
 // entries -- super-unit mode: the i-rows of units (b, b..nb-1) then the
-// j-columns of units (0..b, b); tile mode: the i-rows of the tiles of its
+// j-columns of units (0..b, b), from the plan's unit lists; tile mode: the i-rows of the tiles of its
 // sub-block row, then the j-columns of the tiles of its j-block -- are dealt
 // to the warps (entry k to warp k mod NW, 128-byte coalesced rows, all
 // three components); the NW warp sums and the atom's term slots are then
@@ -336,25 +336,37 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
       g1 += (double)p[st];
       g2 += (double)p[2 * st];
     }
-  } else if (use_nb && nranks == 1) {  // super-unit mode: [unit][3][S] rows and columns
-    const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
+  } else if (use_nb) {  // super-unit mode: [unit][3][S] rows and columns
+    // unit_index = [row lists' ptr (2 nb + 1) | column lists' ptr (nb + 1) |
+    // row lists | column lists]: the units holding the rows of super-block
+    // b's half h (units of the last wave come in halves), then the units
+    // holding its columns (both halves of a split unit)
+    const int* urow_ptr = unit_index;
+    const int* ucol_ptr = unit_index + 2 * nb + 1;
+    const int* urow_idx = unit_index + 3 * nb + 2;
+    const int* ucol_idx = urow_idx + urow_ptr[2 * nb];
+    const int b = a0 / S, offr = a0 - b * S, off = offr + lane;
+    const int h = (offr / kIB) >= (S / kIB) / 2 ? 1 : 0;
+    const int r0 = urow_ptr[2 * b + h], nr = urow_ptr[2 * b + h + 1] - r0;
+    const int c0 = ucol_ptr[b], nt = nr + ucol_ptr[b + 1] - c0;
+    if (nranks == 1) {
 #pragma unroll 4
-    for (int k = warp; k <= nb; k += NW) {
-      const T* p = k < ni ? ipart + (size_t)unit_index[b * nb + b + k] * 3 * S
-                          : jpart + (size_t)unit_index[(k - ni) * nb + b] * 3 * S;
-      g0 += (double)p[off];
-      g1 += (double)p[S + off];
-      g2 += (double)p[2 * S + off];
-    }
-  } else if (use_nb) {  // the same, this rank's units only
-    const int b = a0 / S, off = a0 - b * S + lane, ni = nb - b;
-    for (int k = warp; k <= nb; k += NW) {
-      const int u = k < ni ? unit_index[b * nb + b + k] : unit_index[(k - ni) * nb + b];
-      if (u % nranks != rank) continue;
-      const T* p = (k < ni ? ipart : jpart) + (size_t)u * 3 * S;
-      g0 += (double)p[off];
-      g1 += (double)p[S + off];
-      g2 += (double)p[2 * S + off];
+      for (int k = warp; k < nt; k += NW) {
+        const T* p = k < nr ? ipart + (size_t)urow_idx[r0 + k] * 3 * S
+                            : jpart + (size_t)ucol_idx[c0 + k - nr] * 3 * S;
+        g0 += (double)p[off];
+        g1 += (double)p[S + off];
+        g2 += (double)p[2 * S + off];
+      }
+    } else {  // this rank's units only
+      for (int k = warp; k < nt; k += NW) {
+        const int u = k < nr ? urow_idx[r0 + k] : ucol_idx[c0 + k - nr];
+        if (u % nranks != rank) continue;
+        const T* p = (k < nr ? ipart : jpart) + (size_t)u * 3 * S;
+        g0 += (double)p[off];
+        g1 += (double)p[S + off];
+        g2 += (double)p[2 * S + off];
+      }
     }
   }
   part[warp][0][lane] = g0;

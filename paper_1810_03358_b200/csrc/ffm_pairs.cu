@@ -252,7 +252,8 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   const T cut2 = T(plan.cut2);
   const int nsub = S / kIB, njb = S / kJB;
   constexpr int NP = PairsPerPass<T>::value;
-  for (int ks = 0; ks < nsub; ++ks) {
+  const int2 kr = plan.unit_ks ? plan.unit_ks[u] : make_int2(0, nsub);
+  for (int ks = kr.x; ks < kr.y; ++ks) {
     const int ib = i0 + ks * kIB;
     const int kk = ib / kIB;
     const int e_beg = plan.spt_ptr[kk], e_end = plan.spt_ptr[kk + 1];

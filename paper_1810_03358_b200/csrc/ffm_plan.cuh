@@ -18,6 +18,8 @@ struct NbPlanDev {
   int nb;       // np / S
   int nunits;   // nb * (nb + 1) / 2
   const int2* unit_rc;       // [nunits] (row block, column block)
+  const int2* unit_ks;       // [nunits] sub-block rows [ks0, ks1) a unit covers (the last
+                             // wave's units come in halves), or null = all
   const int* unit_list;      // units this launch evaluates (row sharding), or null = all
   int nlaunch;               // number of CTAs along x (= nunits without sharding)
   const int* spt_ptr;        // [np/128 + 1] special tiles per i-sub-block

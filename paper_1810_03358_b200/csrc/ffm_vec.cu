@@ -355,8 +355,6 @@ namespace ffm {
 // buf = [gradient (3n) | energies (5) | error (key + 1) x 4 | reporting x 4];
 // a rank reporting an error adds (key + 1, 1), and all reporting ranks
 // report the same key (parallel.py), so key = sum / count - 1 exactly.
-constexpr int kCombTail = FFM_NTERMS + 8;
-
 __global__ void combine_encode_kernel(int64_t n3, int64_t natoms, const double* __restrict__ grad,
                                       const double* __restrict__ energies,
                                       const int64_t* __restrict__ status, double* __restrict__ buf) {

@@ -516,3 +516,43 @@ def test_fused_small_evaluation_equals_kernel_chain(golden, name):
             assert np.array_equal(s_f, s_c), (prec, grad, s_f, s_c)
             if grad:
                 assert np.array_equal(g_f, g_c, equal_nan=True)
+
+
+@pytest.mark.parametrize("S", [256, 512, 1024])
+def test_split_last_wave_units(S, monkeypatch):
+    """Units of the last wave evaluated in halves (rows [0, nsub/2) and
+    [nsub/2, nsub) as separate units with their own partial slots; the
+    gather's unit lists take both): forced on small systems of every unit
+    edge, against the oracle and summed over row shards."""
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    import torch
+
+    monkeypatch.setenv("FFM_FORCE_S", str(S))
+    monkeypatch.setenv("FFM_FORCE_TILES", "0")
+    monkeypatch.setenv("FFM_SPLIT_UNITS", "7")
+    s = make_globule_system(4700, seed=12)
+    info = DeviceSystem(s.topology).info
+    nb = info["np"] // S
+    assert info["units"] == nb * (nb + 1) // 2 + 7
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    gmax = np.max(np.abs(g_ref))
+    for dt, et, gt in ((np.float64, 1e-10, 1e-10), (np.float32, 1e-5, 1e-4)):
+        bd, g = energy_and_gradient(s, dt)
+        got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+        assert _rel(got, e_ref) <= et
+        assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
+    c = torch.from_numpy(s.coords.copy()).cuda()
+    g_sum = torch.zeros_like(c)
+    for rank in range(3):
+        eng = DeviceSystem(s.topology)
+        N.check(eng.lib.ffm_system_set_shard(eng.handle, rank, 3), "set_shard")
+        g = torch.empty_like(c)
+        eng.eval(c, N.FFM_F64, grad=g)
+        g_sum += g
+        eng.close()
+    assert float((g_sum.cpu().numpy().ravel() - np.ravel(g_ref)).__abs__().max()) <= 1e-10 * gmax
