@@ -1,9 +1,11 @@
 """Fixed-step descent, steepest descent and momentum methods
 (mirrors ffmin/optimizers/gradient.py: Eq. (2), (4), (9), (10), (11)).
 
-All vector updates go through the run's vector space (vecops): on the
-molecular oracle that is HBM and the engine's axpby kernel; the host only
-sees f, ||g|| and the stop decisions.
+All vector updates go through the run's vector space (vecops).  With the
+molecular oracle every driver here runs its iterations as one conditional
+CUDA graph (optimizers/graph.py): no value reaches the host between polls;
+the loops below are the graph's bit-exact specification and serve other
+oracles.
 """
 
 from __future__ import annotations

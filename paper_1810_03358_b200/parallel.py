@@ -16,8 +16,12 @@ globally first pair; key = sum / count - 1 is exact in float64 (keys <
 replicated: every rank runs the same optimiser on the same all-reduced
 numbers, so no broadcast is needed per step.
 
-The reduction logic (``ShardCombiner``) is independent of CUDA and is
-exercised with the gloo backend on CPU tensors in tests/test_parallel_cpu.py.
+With an NCCL process group the engine does this itself: the group's
+communicator is attached (ffm_system_set_comm) and every evaluation ends
+with encode / ncclAllReduce / decode kernels on its stream, so the
+graph-resident drivers capture the all-reduce too.  ``ShardCombiner`` is
+the same reduction in torch for other backends; it is exercised with gloo
+on CPU tensors in tests/test_parallel_cpu.py.
 """
 
 from __future__ import annotations
