@@ -345,7 +345,10 @@ def main():
                      "frac": achieved / flop_peak, "traffic": nb_traffic(n),
                      "flop_per_pair": FLOP_PER_PAIR, "fma_pipe_frac": fma_frac,
                      "nb_ms": nb32, "nb_ms_f64": nb64,
-                     "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt"},
+                     "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt",
+                     "bound_note": "not a dense contraction (north star): the pair sweep is bound "
+                                   "by the FP32 FMA pipe; DRAM traffic is under 2% of its time "
+                                   "and tensor cores do not apply"},
         "roofline_f64": {"bound": "fp64-pipe", "kernel": "nb_units_kernel<double,GRAD>",
                          "achieved": nb_pairs_per_rank * FP64_OPS_PER_PAIR / (nb64 * 1e-3) / 1e12,
                          "peak": DFMA_PEAK / 1e12, "unit": "T fp64-pipe ops/s",
