@@ -96,6 +96,7 @@ struct MinState {
   // wiggle (ffmin/optimizers/wiggle.py): the iteration's atom, its six axis
   // probe values, vertex probe, chosen move and outcome
   int wig_atom, wig_vtx, wig_best, wig_moved;
+  int ls_more, pad3;  // the probe controller's loop decision (small-system probe loop)
   double wig_pv[6], wig_vertex[3], wig_dv, wig_delta[3], wig_est;
 };
 

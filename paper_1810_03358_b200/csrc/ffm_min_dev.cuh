@@ -218,6 +218,7 @@ __device__ inline bool ls_on_value(MinState* S, double f) {
 __device__ inline void ls_step(MinState* S, const double* en, const int64_t* stw,
                                cudaGraphConditionalHandle hloop) {
   S->vcalls++;
+  S->ls_more = 0;
   if (bad_status(stw, false)) {
     set_err(S, kMinErrEval, stw, false);
     cudaGraphSetConditional(hloop, 0);
@@ -235,6 +236,7 @@ __device__ inline void ls_step(MinState* S, const double* en, const int64_t* stw
       S->warm = S->found ? fabs(S->res_h) : S->c.h0;
     }
   }
+  S->ls_more = more ? 1 : 0;
   cudaGraphSetConditional(hloop, more ? 1u : 0u);
 }
 

@@ -62,72 +62,81 @@ small_eval_kernel(SmallEvalArgs a) {
   };
   stamp(0);
 
-  // P0 (a line-search trial first forms its point x_t = lincomb(1, x, h, r),
-  // the axpby of the host-driven loop, into the trial buffer)
-  const double* coords = a.trial_out ? a.trial_out : a.coords;
-  const double th = a.trial_out ? *a.trial_h : 0.0;
-  for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs) {
-    if (a.trial_out && k < n)
-      for (int c = 0; c < 3; ++c) {
-        const int64_t q = 3 * k + c;
-        a.trial_out[q] = fma(th, a.trial_r[q], 1.0 * a.trial_x[q]);
-      }
-    pack_item<T>(k, n, plan.np, 1, coords, a.qt, pos, ipos, a.status);
-  }
-  grid.sync();
-  stamp(1);
-
-  // P1: CTA items -- the pair tiles (one CTA each, the longer items, first)
-  // and the bonded / scaled-pair term blocks, dealt round-robin so a CTA
-  // with a tile does not also run a term block when the grid covers both
-  const int nitems = plan.nlaunch + a.nterm_blocks;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    if (it < plan.nlaunch)
-      tile_cta<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
-                                static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it, 0, tsm);
-    else
-      term_block(a.tp, GRAD, coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
-                 a.nterm_blocks, sh);
-  }
-  __syncthreads();
-  stamp(2);
-  grid.sync();
-  stamp(3);
-
-  // P2: the finder decision, made identically by every CTA: a coincident
-  // pair shows as a non-finite tile partial (FP32) or a closest-pair r^2
-  // below RMIN^2 (FP64), or was flagged by the scaled-pair terms
-  int suspect = a.status[kStNbSuspect] != 0;
-  for (int t = threadIdx.x; t < plan.ntiles && !suspect; t += kSmallThreads) {
-    const double* e = a.epart + 3 * (size_t)t;
-    if (!isfinite(e[0]) || !isfinite(e[1]) || e[2] < kRmin * kRmin) suspect = 1;
-  }
-  suspect = __syncthreads_or(suspect);
-  if (GRAD)  // 32-atom groups, the same 4-warp split as the chain's gather
-    for (int g = blockIdx.x; g < ((n + 31) >> 5); g += gridDim.x)
-      gather_group<T, kGatherWarpsTiles>(g, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr,
-                                         a.tcol_idx, ipart, jpart, a.slot_ptr, a.slot_idx,
-                                         a.term_f, a.tp.slot_sc0, true, true, true, a.grad,
-                                         gpart);
-  if (blockIdx.x == gridDim.x - 1)  // the gather groups fill the first CTAs
-    reduce_entry(plan.ntiles, a.nterm_blocks, a.epart, a.term_part, a.energies, a.status, 0, red,
-                 false);
-  __syncthreads();
-  stamp(4);
-  if (suspect) {  // P3 (uniform across the grid)
+  // a line-search trial repeats the whole evaluation for every probe the
+  // controller asks for (one launch per search instead of one per probe:
+  // each probe would cost a conditional-node relaunch and a cooperative
+  // launch, ~6 us, on systems whose evaluation takes ~10 us)
+  for (;;) {
+    // P0 (a line-search trial first forms its point x_t = lincomb(1, x, h, r),
+    // the axpby of the host-driven loop, into the trial buffer)
+    const double* coords = a.trial_out ? a.trial_out : a.coords;
+    const double th = a.trial_out ? *(volatile const double*)a.trial_h : 0.0;
+    for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs) {
+      if (a.trial_out && k < n)
+        for (int c = 0; c < 3; ++c) {
+          const int64_t q = 3 * k + c;
+          a.trial_out[q] = fma(th, a.trial_r[q], 1.0 * a.trial_x[q]);
+        }
+      pack_item<T>(k, n, plan.np, 1, coords, a.qt, pos, ipos, a.status);
+    }
     grid.sync();
-    for (int64_t i = gt; i < n; i += gs)
-      finder_row<T>((int)i, n, pos, a.sp_ptr, a.sp_j, a.sp_s, a.status);
+    stamp(1);
+
+    // P1: CTA items -- the pair tiles (one CTA each, the longer items, first)
+    // and the bonded / scaled-pair term blocks, dealt round-robin so a CTA
+    // with a tile does not also run a term block when the grid covers both
+    const int nitems = plan.nlaunch + a.nterm_blocks;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      if (it < plan.nlaunch)
+        tile_cta<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
+                                  static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it, 0, tsm);
+      else
+        term_block(a.tp, GRAD, coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
+                   a.nterm_blocks, sh);
+    }
+    __syncthreads();
+    stamp(2);
     grid.sync();
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.status[kStNbSuspect] = 1;  // as the chain leaves it
+    stamp(3);
+
+    // P2: the finder decision, made identically by every CTA: a coincident
+    // pair shows as a non-finite tile partial (FP32) or a closest-pair r^2
+    // below RMIN^2 (FP64), or was flagged by the scaled-pair terms
+    int suspect = a.status[kStNbSuspect] != 0;
+    for (int t = threadIdx.x; t < plan.ntiles && !suspect; t += kSmallThreads) {
+      const double* e = a.epart + 3 * (size_t)t;
+      if (!isfinite(e[0]) || !isfinite(e[1]) || e[2] < kRmin * kRmin) suspect = 1;
+    }
+    suspect = __syncthreads_or(suspect);
+    if (GRAD)  // 32-atom groups, the same 4-warp split as the chain's gather
+      for (int g = blockIdx.x; g < ((n + 31) >> 5); g += gridDim.x)
+        gather_group<T, kGatherWarpsTiles>(g, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr,
+                                           a.tcol_idx, ipart, jpart, a.slot_ptr, a.slot_idx,
+                                           a.term_f, a.tp.slot_sc0, true, true, true, a.grad,
+                                           gpart);
+    if (blockIdx.x == gridDim.x - 1)  // the gather groups fill the first CTAs
+      reduce_entry(plan.ntiles, a.nterm_blocks, a.epart, a.term_part, a.energies, a.status, 0, red,
+                   false);
+    __syncthreads();
+    stamp(4);
+    if (suspect) {  // P3 (uniform across the grid)
+      grid.sync();
+      for (int64_t i = gt; i < n; i += gs)
+        finder_row<T>((int)i, n, pos, a.sp_ptr, a.sp_j, a.sp_s, a.status);
+      grid.sync();
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.status[kStNbSuspect] = 1;  // as the chain leaves it
+    }
+    // the CTA that reduced the energies finalises the status words and, for a
+    // line-search trial, runs the probe controller (ffm_min_dev.cuh)
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+      finalize_entry(n, a.status);
+      if (a.ls_state) mindev::ls_step(a.ls_state, a.energies, a.status, a.ls_loop);
+    }
+    stamp(5);
+    if (!a.ls_state) break;
+    grid.sync();  // the controller's decision and next step are visible to all CTAs
+    if (!*(volatile int*)&a.ls_state->ls_more) break;
   }
-  // the CTA that reduced the energies finalises the status words and, for a
-  // line-search trial, runs the probe controller (ffm_min_dev.cuh)
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-    finalize_entry(n, a.status);
-    if (a.ls_state) mindev::ls_step(a.ls_state, a.energies, a.status, a.ls_loop);
-  }
-  stamp(5);
 }
 
 template <typename T, bool GRAD, bool CUTOFF>
