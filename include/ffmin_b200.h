@@ -202,15 +202,19 @@ int ffm_lbfgs_two_loop(int64_t n, int count, const int32_t* order_h, const doubl
                        const double* S_d, const double* Y_d, const double* g_d, double* d_d,
                        double* scratch_d, void* stream);
 
-/* ---- graph-resident L-BFGS (ffmin/optimizers/lbfgs.py:93-128) ----
+/* ---- graph-resident minimisers (ffmin/optimizers/*.py) ----
  *
- * The whole iteration -- direction (two-loop recursion), the line search
- * (ls_par / ls_h with the LineSearcher warm start and retry,
- * ffmin/linesearch.py, ffmin/optimizers/common.py), the gradient at the new
- * point, the curvature-guarded memory update and the convergence test -- runs
- * as one CUDA graph with conditional nodes; no value crosses to the host
- * between iterations.  The host launches chunks of iterations and reads the
- * trace records after each chunk.  Single-rank systems only. */
+ * The whole iteration of a driver -- for L-BFGS (ffmin/optimizers/lbfgs.py:
+ * 93-128) the direction (two-loop recursion), the line search (ls_par /
+ * ls_h with the LineSearcher warm start and retry, ffmin/linesearch.py,
+ * ffmin/optimizers/common.py), the gradient at the new point, the
+ * curvature-guarded memory update and the convergence test; likewise for
+ * nonlinear CG, steepest descent, FGM, OFGM, the fixed-step family and the
+ * gradient-free wiggle (cfg.method) -- runs as one CUDA graph with
+ * conditional nodes; no value crosses to the host between iterations.  The
+ * host launches chunks of iterations and reads the trace records after each
+ * chunk.  Unsharded systems, or sharded ones with a communicator
+ * (ffm_system_set_comm).  The "lbfgs" in the names is historical. */
 typedef struct ffm_lbfgs ffm_lbfgs_t;
 
 typedef struct {
