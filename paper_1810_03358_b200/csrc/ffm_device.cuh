@@ -391,6 +391,73 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
   __syncthreads();  // part is reused by the block's next group
 }
 
+// Super-unit mode gather of a 128-atom span (one sub-block of one super-
+// block: atoms 128 g .. 128 g + 127) by the NW warps of a block: the same
+// entries and the same warp split as gather_group (entry k to warp k mod NW;
+// per atom the warp sums in warp order, then the term slots), so identical
+// bits -- but each warp reads 512 contiguous bytes per entry and component
+// (four 128-byte rows) instead of 128, which the DRAM pages reward.
+// part: NW x 3 x 128 doubles of shared memory.
+template <typename T, int NW>
+__device__ __forceinline__ void gather_span128(int g, int n, int S, int nb,
+                                               const int* __restrict__ unit_index,
+                                               const T* __restrict__ ipart,
+                                               const T* __restrict__ jpart,
+                                               const int* __restrict__ slot_ptr,
+                                               const int* __restrict__ slot_idx,
+                                               const double* __restrict__ term_f, int slot_sc0,
+                                               bool use_nb, bool use_terms, bool use_sc,
+                                               double* __restrict__ grad,
+                                               double (*part)[3][128], int rank, int nranks) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int a0 = g * 128;
+  double acc[4][3];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = acc[q][2] = 0.0;
+  if (use_nb) {
+    const int* urow_ptr = unit_index;
+    const int* ucol_ptr = unit_index + 2 * nb + 1;
+    const int* urow_idx = unit_index + 3 * nb + 2;
+    const int* ucol_idx = urow_idx + urow_ptr[2 * nb];
+    const int b = a0 / S, offr = a0 - b * S;
+    const int h = (offr / kIB) >= (S / kIB) / 2 ? 1 : 0;
+    const int r0 = urow_ptr[2 * b + h], nr = urow_ptr[2 * b + h + 1] - r0;
+    const int c0 = ucol_ptr[b], nt = nr + ucol_ptr[b + 1] - c0;
+#pragma unroll 2
+    for (int k = warp; k < nt; k += NW) {
+      const int u = k < nr ? urow_idx[r0 + k] : ucol_idx[c0 + k - nr];
+      if (nranks > 1 && u % nranks != rank) continue;
+      const T* p = (k < nr ? ipart : jpart) + (size_t)u * 3 * S + offr + lane;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        acc[q][0] += (double)p[32 * q];
+        acc[q][1] += (double)p[S + 32 * q];
+        acc[q][2] += (double)p[2 * S + 32 * q];
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) part[warp][c][32 * q + lane] = acc[q][c];
+  __syncthreads();
+  for (int x = threadIdx.x; x < 384; x += NW * 32) {
+    const int l = x / 3, c = x - 3 * l, a = a0 + l;
+    if (a < n) {
+      double v = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) v += part[w][c][l];
+      for (int s = slot_ptr[a]; s < slot_ptr[a + 1]; ++s) {
+        const int k = slot_idx[s];
+        if (k < slot_sc0 ? !use_terms : !use_sc) continue;
+        v += term_f[3 * (size_t)k + c];
+      }
+      grad[3 * (size_t)a + c] = v;
+    }
+  }
+  __syncthreads();
+}
+
 // status sentinels -> the reference's conventions (-1 = clean)
 __device__ __forceinline__ void finalize_entry(int n, int64_t* s) {
   if (s[kStNbKey] != kSentinel) {

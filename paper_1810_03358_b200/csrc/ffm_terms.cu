@@ -110,7 +110,7 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
 // reduces the energies (reduce_entry), so results are bit-identical run to
 // run.  Super-unit mode uses 8 warps per group, tile mode 4 (the same split
 // as the fused small-system kernel, so both produce the same bits).
-template <typename T, int NW>
+template <typename T, int NW, int SPAN>
 __global__ void __launch_bounds__(NW * 32)
 gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                      const int* __restrict__ trow_ptr, const int* __restrict__ tcol_ptr,
@@ -122,8 +122,11 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                      const double* __restrict__ epart, const double* __restrict__ term_part,
                      double* __restrict__ energies, int64_t* __restrict__ status, int rank,
                      int nranks, double* __restrict__ escratch, unsigned* ecount, int nparts) {
-  __shared__ double part[NW][3][32];
-  const int ngroups = (n + 31) >> 5;
+  // 128-atom spans (gather_span128, super-unit mode, large systems) or
+  // 32-atom groups (gather_group: more blocks in flight for smaller ones)
+  constexpr int kSpan = SPAN;
+  __shared__ double part[NW][3][kSpan];
+  const int ngroups = (n + kSpan - 1) / kSpan;
   if ((int)blockIdx.x >= ngroups) {  // the energy reduction: nparts blocks
     if (nparts == 1)  // (the fused small-system kernel's order: identical bits)
       reduce_entry(nslots, nterm_blocks, epart, term_part, energies, status, 0, &part[0][0][0],
@@ -133,9 +136,14 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                    escratch, ecount, blockIdx.x - ngroups, nparts, n);
     return;
   }
-  gather_group<T, NW>(blockIdx.x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart,
-                      jpart, slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
-                      grad, part, rank, nranks);
+  if constexpr (kSpan == 128)
+    gather_span128<T, NW>(blockIdx.x, n, S, nb, unit_index, ipart, jpart, slot_ptr, slot_idx,
+                          term_f, slot_sc0, use_nb, use_terms, use_sc, grad, part, rank,
+                          nranks);
+  else
+    gather_group<T, NW>(blockIdx.x, n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ipart,
+                        jpart, slot_ptr, slot_idx, term_f, slot_sc0, use_nb, use_terms, use_sc,
+                        grad, reinterpret_cast<double (*)[3][32]>(part), rank, nranks);
 }
 
 template <typename T>
@@ -148,17 +156,25 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
                                int64_t* status, int rank, int nranks, double* escratch,
                                unsigned* ecount, cudaStream_t st) {
   const int nparts = energy_parts(nslots);
-  const int blocks = (n + 31) / 32 + nparts;
+  // 128-atom spans from 40k atoms on (100k: 4479 -> 4467 us per evaluation;
+  // at 10k the 4x fewer blocks cost 4 us: tools/mid_sweep.py A/B)
+  const bool span = !trow_ptr && n >= 40000;
+  const int blocks = (span ? (n + 127) / 128 : (n + 31) / 32) + nparts;
   const T* ip = static_cast<const T*>(ipart);
   const T* jp = static_cast<const T*>(jpart);
   count_launch();
-  if (trow_ptr)
-    gather_reduce_kernel<T, kGatherWarpsTiles><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
+  if (span)
+    gather_reduce_kernel<T, kGatherWarpsUnits, 128><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
+        n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
+        slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
+        energies, status, rank, nranks, escratch, ecount, nparts);
+  else if (trow_ptr)
+    gather_reduce_kernel<T, kGatherWarpsTiles, 32><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
         energies, status, rank, nranks, escratch, ecount, nparts);
   else
-    gather_reduce_kernel<T, kGatherWarpsUnits><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
+    gather_reduce_kernel<T, kGatherWarpsUnits, 32><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
         energies, status, rank, nranks, escratch, ecount, nparts);
