@@ -10,13 +10,13 @@
 namespace ffm {
 
 #ifndef FFM_MINB64
-#define FFM_MINB64 2  // FP64: two CTAs per SM (<= 128 registers)
+#define FFM_MINB64 1  // FP64: one CTA per SM, four i-atoms per lane (~245 registers)
 #endif
 #ifndef FFM_UNROLL
 #define FFM_UNROLL 32
 #endif
 #ifndef FFM_UNROLL64
-#define FFM_UNROLL64 0  // 0: 4 with gradient, 8 energy-only (measured best)
+#define FFM_UNROLL64 8  // FP64 steps unrolled (measured best with four i-atoms per lane)
 #endif
 constexpr int kStepUnroll = FFM_UNROLL;  // steps of the 32-step tile loop unrolled
 constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/SM)
@@ -54,11 +54,16 @@ __device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restric
   return {d.x, d.y};
 }
 
-// i-atom pairs held per pass: FP32 keeps both packed pairs (4 i-atoms per
-// lane) live; FP64 sweeps them one after the other so the kernel fits 128
-// registers and two CTAs per SM
+// i-atom pairs held per pass: both packed pairs (4 i-atoms per lane) live.
+// FP64 then needs ~245 registers, i.e. one 8-warp CTA per SM, and the
+// doubled independent work per step outruns two CTAs of two i-atoms per
+// lane (100k atoms: 12.80 -> 11.71 ms with 8 steps unrolled; tools/
+// build_lib_variant.sh A/B: NP64, MINB64, UNROLL64)
 template <typename T> struct PairsPerPass { static constexpr int value = 2; };
-template <> struct PairsPerPass<double> { static constexpr int value = 1; };
+#ifndef FFM_NP64
+#define FFM_NP64 2
+#endif
+template <> struct PairsPerPass<double> { static constexpr int value = FFM_NP64; };
 
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
 // j-block, so step t of lane l reads entry l + t (atom (l + t) mod 32) with
