@@ -90,8 +90,8 @@ int ffm_system_destroy(ffm_system_t* sys);
 
 /* Row sharding over `nranks` GPUs (one process per GPU): this handle then
  * evaluates only its share of the S x S super-units of the pair triangle
- * (units dealt round-robin, heaviest first) and, on rank 0 only, the O(N)
- * bonded / 1-4 terms.  Gradients and energies of an evaluation are partial
+ * (units dealt heaviest first to the least-loaded rank, rank 0 counted with
+ * its O(N) work) and, on rank 0 only, the O(N) bonded / 1-4 terms.  Gradients and energies of an evaluation are partial
  * sums; the caller all-reduces them (NCCL over NVLink in
  * paper_1810_03358_b200.parallel).  nranks = 1 restores the full sweep. */
 int ffm_system_set_shard(ffm_system_t* sys, int rank, int nranks);

@@ -149,6 +149,7 @@ struct ffm_system {
   int small_grid[2][2] = {{0, 0}, {0, 0}};
   unsigned long long* phase_clock = nullptr;  // ffm_debug_phase_clock (tuning aid)
   int* d_unit_list = nullptr;
+  std::vector<char> unit_live;  // host: slot holds a real unit (build_units)
   // small-system tile mode (NbPlanDev::ntiles > 0)
   int2* d_tiles = nullptr;
   int* d_tile_list = nullptr;
@@ -246,37 +247,77 @@ int choose_S(int64_t n) {
 // then the diagonal units (half work) -- and the gather's unit lists
 // (gather_group: the units holding each super-block half's rows, then the
 // units holding each super-block's columns).
-int build_units(ffm_system* s, int S, int nsplit) {
+//
+// Row-sharded plans (nranks > 1) deal the units in that order to the rank
+// with the least work so far (counted in 128 x 32 tiles; ties go to the
+// lowest rank), rank 0 starting at the tile-equivalent of the O(N) bonded
+// and 1-4 work only it evaluates; unit slot u then belongs to rank
+// u % nranks (the gather's ownership test), each rank's units keep their
+// order, and slots a shorter rank leaves over hold null units (never
+// launched: zero partials, energy slot (0, 0, 1e30)).  s->unit_live marks
+// the real ones.
+#ifndef FFM_TERM_PAIRS_PER_ATOM
+#define FFM_TERM_PAIRS_PER_ATOM 400  // measured: rank 0 ran 31-45 us longer at 100k
+#endif
+int build_units(ffm_system* s, int S, int nsplit, int nranks) {
   NbPlanDev& p = s->plan;
   p.S = S;
   p.nb = p.np / S;
-  const int nb = p.nb, nsub = S / kIB, hs = nsub / 2;
+  const int nb = p.nb, nsub = S / kIB, hs = nsub / 2, njb = S / kJB;
   const int noff = nb * (nb - 1) / 2;
   if (nsplit > noff) nsplit = noff;
   if (nsub < 2) nsplit = 0;
-  std::vector<int2> urc, uks;
-  std::vector<int> half0((size_t)nb * nb, -1), half1((size_t)nb * nb, -1);
-  int k = 0;
-  for (int r = 0; r < nb; ++r)
+  std::vector<int2> lrc, lks;  // logical order
+  for (int r = 0, k = 0; r < nb; ++r)
     for (int c = r + 1; c < nb; ++c, ++k) {
-      const size_t key = (size_t)r * nb + c;
       if (k < noff - nsplit) {
-        half0[key] = half1[key] = (int)urc.size();
-        urc.push_back(make_int2(r, c));
-        uks.push_back(make_int2(0, nsub));
+        lrc.push_back(make_int2(r, c));
+        lks.push_back(make_int2(0, nsub));
       } else {
-        half0[key] = (int)urc.size();
-        urc.push_back(make_int2(r, c));
-        uks.push_back(make_int2(0, hs));
-        half1[key] = (int)urc.size();
-        urc.push_back(make_int2(r, c));
-        uks.push_back(make_int2(hs, nsub));
+        lrc.push_back(make_int2(r, c));
+        lks.push_back(make_int2(0, hs));
+        lrc.push_back(make_int2(r, c));
+        lks.push_back(make_int2(hs, nsub));
       }
     }
   for (int r = 0; r < nb; ++r) {
-    half0[(size_t)r * nb + r] = half1[(size_t)r * nb + r] = (int)urc.size();
-    urc.push_back(make_int2(r, r));
-    uks.push_back(make_int2(0, nsub));
+    lrc.push_back(make_int2(r, r));
+    lks.push_back(make_int2(0, nsub));
+  }
+  // slot of each logical unit (identity for one rank)
+  std::vector<int> slot(lrc.size());
+  int nslot = (int)lrc.size();
+  if (nranks > 1) {
+    int term_pairs = FFM_TERM_PAIRS_PER_ATOM;
+    if (const char* f = getenv("FFM_TERM_PAIRS_PER_ATOM")) term_pairs = atoi(f);  // tuning aid
+    std::vector<double> load(nranks, 0.0);
+    std::vector<int> count(nranks, 0);
+    load[0] = (double)term_pairs * p.n / (kIB * kJB);
+    for (size_t k = 0; k < lrc.size(); ++k) {
+      int tiles = 0;
+      for (int ks = lks[k].x; ks < lks[k].y; ++ks)
+        tiles += lrc[k].x == lrc[k].y ? njb - (kIB / kJB) * ks : njb;
+      int r = 0;
+      for (int q = 1; q < nranks; ++q)
+        if (load[q] < load[r]) r = q;
+      load[r] += tiles;
+      slot[k] = count[r]++ * nranks + r;
+    }
+    nslot = *std::max_element(count.begin(), count.end()) * nranks;
+  } else {
+    for (size_t k = 0; k < slot.size(); ++k) slot[k] = (int)k;
+  }
+  std::vector<int2> urc(nslot, make_int2(0, 0)), uks(nslot, make_int2(0, 0));
+  s->unit_live.assign(nslot, 0);
+  std::vector<int> half0((size_t)nb * nb, -1), half1((size_t)nb * nb, -1);
+  for (size_t k = 0; k < lrc.size(); ++k) {
+    const int u = slot[k];
+    urc[u] = lrc[k];
+    uks[u] = lks[k];
+    s->unit_live[u] = 1;
+    const size_t key = (size_t)lrc[k].x * nb + lrc[k].y;
+    if (lks[k].x == 0 && lks[k].y == nsub) half0[key] = half1[key] = u;
+    else (lks[k].x == 0 ? half0 : half1)[key] = u;
   }
   p.nunits = (int)urc.size();
   // gather lists: [row ptr (2 nb + 1) | column ptr (nb + 1) | rows | columns]
@@ -314,7 +355,7 @@ int build_units(ffm_system* s, int S, int nsplit) {
 }
 
 // units of the last wave split in halves: one wave of CTA slots (2 per SM)
-// per rank, since the units are dealt round-robin -- for S = 1024 only: a
+// per rank, since every rank gets an equal share of them -- for S = 1024 only: a
 // half unit of S <= 512 pays the whole per-unit overhead for one or two
 // tiles per warp (measured, tools/mid_sweep.py A/B: 100k atoms, S = 1024
 // 4.41 -> 4.37 ms; 10k, S = 256 70.0 -> 71.8 us; 30k, S = 512 426 -> 433 us)
@@ -767,7 +808,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
   FFM_TRY(upload(&s->d_sc_s, s->scaled_s));
 
   // ---- units: off-diagonal first (full work), diagonal last (half work)
-  FFM_TRY(build_units(s, p.S, split_count(s, p.S, 1)));
+  FFM_TRY(build_units(s, p.S, split_count(s, p.S, 1), 1));
   {  // the batch plan: the largest unit edge that divides np (units mode)
     NbPlanDev& b = s->bplan;
     b = p;
@@ -859,7 +900,7 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
     // re-plan the super-unit edge for this shard count (the single-rank
     // edge is kept from creation: s->S0)
     const int S = nranks == 1 ? s->S0 : choose_S_sharded(s->plan, s->S0, nranks);
-    int rc = build_units(s, S, split_count(s, S, nranks));
+    int rc = build_units(s, S, split_count(s, S, nranks), nranks);
     if (rc) return rc;
   }
   if (s->plan.ntiles > 0) {
@@ -867,14 +908,18 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
     s->plan.unit_list = nullptr;
     s->plan.nlaunch = s->plan.nunits;
   } else {
-    // units are ordered heavy (off-diagonal) first: dealing them round-robin
-    // gives every rank the same work to within one unit
+    // this rank's slots (u % nranks == rank, build_units), null units skipped
     std::vector<int> mine;
-    for (int u = rank; u < s->plan.nunits; u += nranks) mine.push_back(u);
+    for (int u = rank; u < s->plan.nunits; u += nranks)
+      if (s->unit_live[u]) mine.push_back(u);
+    if (mine.empty()) {
+      mine.push_back(0);
+      s->plan.nlaunch = 0;
+    }
     int rc = upload(&s->d_unit_list, mine);
     if (rc) return rc;
     s->plan.unit_list = s->d_unit_list;
-    s->plan.nlaunch = (int)mine.size();
+    if (s->plan.nlaunch != 0) s->plan.nlaunch = (int)mine.size();
   }
   // drop the partial buffers so stale slots of other ranks read as zero
   for (auto& w : s->w) {

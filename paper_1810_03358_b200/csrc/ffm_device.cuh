@@ -316,8 +316,8 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
                                              bool use_nb, bool use_terms, bool use_sc,
                                              double* __restrict__ grad, double (*part)[3][32],
                                              int rank = 0, int nranks = 1) {
-  // row-sharded plans (ffm_system_set_shard): units / tiles are dealt
-  // round-robin, the slots of other ranks' ones hold exact zeros -- skip them
+  // row-sharded plans (ffm_system_set_shard): unit / tile slot u belongs to
+  // rank u % nranks, the slots of other ranks' ones hold exact zeros -- skip them
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int a0 = g << 5;
   double g0 = 0.0, g1 = 0.0, g2 = 0.0;
