@@ -124,7 +124,7 @@ cudaError_t launch_bbox(int n, int np, int batch, bool fp64, const void* pos, vo
   return cudaGetLastError();
 }
 
-template <typename T>
+template <int NW>
 __device__ __forceinline__ double block_sum(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -132,10 +132,11 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double s = 0.0;
-  for (int w = 0; w < kWarps; ++w) s += red[w];
+  for (int w = 0; w < NW; ++w) s += red[w];
   return s;
 }
 
+template <int NW>
 __device__ __forceinline__ double block_min(double v, double* red) {
   for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -143,7 +144,7 @@ __device__ __forceinline__ double block_min(double v, double* red) {
   if (lane == 0) red[warp] = v;
   __syncthreads();
   double s = red[0];
-  for (int w = 1; w < kWarps; ++w) s = fmin(s, red[w]);
+  for (int w = 1; w < NW; ++w) s = fmin(s, red[w]);
   return s;
 }
 
@@ -169,8 +170,12 @@ __device__ unsigned long long* g_unit_clock = nullptr;
 #ifndef FFM_MINB
 #define FFM_MINB 2
 #endif
-template <typename T, bool GRAD, bool CUTOFF>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? FFM_MINB : FFM_MINB64)
+// NW warps per CTA: 8 for FP32 (two CTAs per SM), 4 for FP64 (two CTAs per
+// SM, so one CTA's staging / reduction phases overlap the other's pair loop;
+// one 8-warp FP64 CTA fills the register file alone -- measured 4 vs 8
+// warps: 100k 11.72 -> 11.43 ms, 20k 571 -> 505 us, 10k 168 -> 159 us)
+template <typename T, bool GRAD, bool CUTOFF, int NW>
+__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? FFM_MINB : (NW == kWarps ? FFM_MINB64 : 2))
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, const T* __restrict__ bbox,
@@ -180,7 +185,8 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   using V4 = typename Vec4T<T>::type;
   using V2 = typename Vec2T<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double red[kWarps];
+  constexpr int kNT = NW * 32;
+  __shared__ double red[NW];
   const int S = plan.S;
   V4* sj = reinterpret_cast<V4*>(smem_raw);   // [2S]: each j-block stored twice
   // FP32 stores each j-block twice (immediate-offset addressing in the hot
@@ -189,7 +195,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   constexpr int kRep = kDbl ? 2 : 1;
   V2* sl = reinterpret_cast<V2*>(sj + kRep * S);  // [kRep S]
   T* jacc = reinterpret_cast<T*>(sl + kRep * S);  // [3][S]      (GRAD)
-  T* ired = jacc + 3 * S;                      // [kWarps][3][kIB] (GRAD)
+  T* ired = jacc + 3 * S;                      // [NW][3][kIB] (GRAD)
 
   FFM_STAMP(0);
   const int u = plan.unit_list ? plan.unit_list[blockIdx.x] : blockIdx.x;
@@ -217,7 +223,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     __syncthreads();
     if (cull) {
       if (GRAD)
-        for (int x = tid; x < 3 * S; x += kThreads) {
+        for (int x = tid; x < 3 * S; x += kNT) {
           ipart[(size_t)u * 3 * S + x] = T(0);
           jpart[(size_t)u * 3 * S + x] = T(0);
         }
@@ -231,7 +237,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     }
   }
 
-  for (int e = tid; e < kRep * S; e += kThreads) {
+  for (int e = tid; e < kRep * S; e += kNT) {
     const int a = kDbl ? j0 + (e >> 6) * kJB + (e & 31) : j0 + e;
     V4 p = pos[a];
     p.x = -p.x;
@@ -243,7 +249,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     sl[e] = l;
   }
   if (GRAD)
-    for (int a = tid; a < 3 * S; a += kThreads) jacc[a] = T(0);
+    for (int a = tid; a < 3 * S; a += kNT) jacc[a] = T(0);
   __syncthreads();
   FFM_STAMP(1);
 
@@ -285,7 +291,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
     V ec2 = P::zero(), ev2 = P::zero();
-    for (int m = warp; m < njb; m += kWarps) {
+    for (int m = warp; m < njb; m += NW) {
       const int jb = j0 + m * kJB;
       if (diag && jb + kJB <= ib) continue;  // whole tile has j < i
       if (CUTOFF) {  // tile-level culling
@@ -329,7 +335,7 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
       Ev += double(P::lo(ev2)) + double(P::hi(ev2));
       ec2 = P::zero();
       ev2 = P::zero();
-      if (ks == 0 && m < 32) FFM_STAMP(10 + m / kWarps);
+      if (ks == 0 && m < 32) FFM_STAMP(10 + m / NW);
     }
     if (GRAD) {
 #pragma unroll
@@ -346,11 +352,11 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
     if (GRAD) {
       // cross-warp reduction of the i-rows of this sub-block (fixed order)
       __syncthreads();
-      for (int x = tid; x < 3 * kIB; x += kThreads) {
+      for (int x = tid; x < 3 * kIB; x += kNT) {
         const int c = x / kIB, a = x - c * kIB;
         T s = T(0);
 #pragma unroll
-        for (int w = 0; w < kWarps; ++w) s += ired[w * 3 * kIB + x];
+        for (int w = 0; w < NW; ++w) s += ired[w * 3 * kIB + x];
         // F = -gradient
         ipart[((size_t)u * 3 + c) * S + ks * kIB + a] = -s;
       }
@@ -359,11 +365,11 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
   }
   if (GRAD) {
     __syncthreads();
-    for (int x = tid; x < 3 * S; x += kThreads) jpart[(size_t)u * 3 * S + x] = jacc[x];
+    for (int x = tid; x < 3 * S; x += kNT) jpart[(size_t)u * 3 * S + x] = jacc[x];
   }
-  const double ec = block_sum<T>(Ec, red);
-  const double ev = block_sum<T>(Ev, red) / LjIScale<T>::value;
-  const double mr = block_min(double(minr2), red);
+  const double ec = block_sum<NW>(Ec, red);
+  const double ev = block_sum<NW>(Ev, red) / LjIScale<T>::value;
+  const double mr = block_min<NW>(double(minr2), red);
   if (tid == 0) {
     double* e = epart + ((size_t)bidx * plan.nunits + u) * 3;
     e[0] = ec;
@@ -405,20 +411,20 @@ static cudaError_t launch_tiles_t(const NbPlanDev& plan, const void* pos, const 
   return cudaGetLastError();
 }
 
-size_t nb_smem_bytes(int S, bool fp64, bool grad) {
+size_t nb_smem_bytes(int S, bool fp64, bool grad, int nw) {
   const size_t t = fp64 ? 8 : 4;
   size_t b = (size_t)(fp64 ? 1 : 2) * S * (4 * t + 2 * t);  // j-block copies, see nb_units_kernel
-  if (grad) b += (size_t)3 * S * t + (size_t)kWarps * 3 * kIB * t;
+  if (grad) b += (size_t)3 * S * t + (size_t)nw * 3 * kIB * t;
   return b;
 }
 
-template <typename T, bool GRAD, bool CUTOFF>
-static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const void* lj,
+template <typename T, bool GRAD, bool CUTOFF, int NW>
+static cudaError_t launch_nb_w(const NbPlanDev& plan, const void* pos, const void* lj,
                                const void* ipos, const void* ilj, const void* bbox,
                                void* ipart, void* jpart, double* epart, int batch,
                                cudaStream_t st) {
-  const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD);
-  auto k = nb_units_kernel<T, GRAD, CUTOFF>;
+  const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD, NW);
+  auto k = nb_units_kernel<T, GRAD, CUTOFF, NW>;
   // opt in once, for the largest super-unit (not a stream operation, so it
   // must not sit inside a graph capture)
   static int opted = -1;
@@ -426,18 +432,46 @@ static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const voi
   cudaGetDevice(&dev);
   if (opted != dev) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)nb_smem_bytes(1024, sizeof(T) == 8, GRAD));
+                                         (int)nb_smem_bytes(1024, sizeof(T) == 8, GRAD, NW));
     if (e != cudaSuccess) return e;
     opted = dev;
   }
   if (plan.nlaunch == 0) return cudaSuccess;
   dim3 grid(plan.nlaunch, batch);
-  count_launch(), k<<<grid, kThreads, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
+  count_launch(), k<<<grid, NW * 32, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
                                   static_cast<const typename Vec2T<T>::type*>(lj),
                                   static_cast<const T*>(ipos), static_cast<const T*>(ilj),
                                   static_cast<const T*>(bbox), static_cast<T*>(ipart),
                                   static_cast<T*>(jpart), epart);
   return cudaGetLastError();
+}
+
+// warps per CTA of an FP64 sweep of super-unit edge S (FFM_F64_WARPS = 4 / 8
+// forces one: tuning aid)
+#ifndef FFM_F64_NW4_MAXS
+#define FFM_F64_NW4_MAXS 1024
+#endif
+int nb_warps(int S, bool fp64) {
+  if (!fp64) return kWarps;
+  static const int forced = [] {
+    const char* f = getenv("FFM_F64_WARPS");
+    return f ? atoi(f) : 0;
+  }();
+  if (forced == 4 || forced == kWarps) return forced;
+  return S <= FFM_F64_NW4_MAXS ? 4 : kWarps;
+}
+
+template <typename T, bool GRAD, bool CUTOFF>
+static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const void* lj,
+                               const void* ipos, const void* ilj, const void* bbox,
+                               void* ipart, void* jpart, double* epart, int batch,
+                               cudaStream_t st) {
+  if constexpr (sizeof(T) == 8)
+    if (nb_warps(plan.S, true) == 4)
+      return launch_nb_w<T, GRAD, CUTOFF, 4>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart,
+                                             epart, batch, st);
+  return launch_nb_w<T, GRAD, CUTOFF, kWarps>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart,
+                                              epart, batch, st);
 }
 
 cudaError_t launch_nb(const NbPlanDev& plan, bool fp64, bool grad, const void* pos,

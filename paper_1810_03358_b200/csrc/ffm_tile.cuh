@@ -10,7 +10,7 @@
 namespace ffm {
 
 #ifndef FFM_MINB64
-#define FFM_MINB64 1  // FP64: one CTA per SM, four i-atoms per lane (~245 registers)
+#define FFM_MINB64 1  // FP64 8-warp CTAs (FFM_F64_WARPS=8 only): one per SM (~245 registers)
 #endif
 #ifndef FFM_UNROLL
 #define FFM_UNROLL 32
@@ -55,10 +55,11 @@ __device__ __forceinline__ Pk<double>::V ld_pair<double>(const double* __restric
 }
 
 // i-atom pairs held per pass: both packed pairs (4 i-atoms per lane) live.
-// FP64 then needs ~245 registers, i.e. one 8-warp CTA per SM, and the
-// doubled independent work per step outruns two CTAs of two i-atoms per
-// lane (100k atoms: 12.80 -> 11.71 ms with 8 steps unrolled; tools/
-// build_lib_variant.sh A/B: NP64, MINB64, UNROLL64)
+// FP64 then needs ~245 registers, i.e. eight warps per SM (two 4-warp
+// CTAs: nb_warps), and the doubled independent work per step outruns two
+// CTAs of two i-atoms per lane (100k atoms: 12.80 -> 11.71 ms with 8 steps
+// unrolled, 11.43 ms as two 4-warp CTAs; tools/build_lib_variant.sh A/B:
+// NP64, MINB64, UNROLL64)
 template <typename T> struct PairsPerPass { static constexpr int value = 2; };
 #ifndef FFM_NP64
 #define FFM_NP64 2
