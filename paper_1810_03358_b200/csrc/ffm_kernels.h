@@ -12,7 +12,7 @@ extern std::atomic<long long> g_launch_count;
 inline void count_launch(long long k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
 
 size_t nb_smem_bytes(int S, bool fp64, bool grad, int nw);
-int nb_warps(int S, bool fp64);  // warps per CTA of the super-unit sweep
+int nb_warps(int S, bool fp64, int nlaunch);  // warps per CTA of the super-unit sweep
 
 // all-pairs sweep over every super-unit; batch > 1 only without GRAD.
 // pos/lj: j-side records; ipos/ilj: the same data in the i-side pair layout

@@ -175,7 +175,7 @@ __device__ unsigned long long* g_unit_clock = nullptr;
 // one 8-warp FP64 CTA fills the register file alone -- measured 4 vs 8
 // warps: 100k 11.72 -> 11.43 ms, 20k 571 -> 505 us, 10k 168 -> 159 us)
 template <typename T, bool GRAD, bool CUTOFF, int NW>
-__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? FFM_MINB : (NW == kWarps ? FFM_MINB64 : 2))
+__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? FFM_MINB * kWarps / NW : (NW == kWarps ? FFM_MINB64 : 2))
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, const T* __restrict__ bbox,
@@ -446,13 +446,24 @@ static cudaError_t launch_nb_w(const NbPlanDev& plan, const void* pos, const voi
   return cudaGetLastError();
 }
 
-// warps per CTA of an FP64 sweep of super-unit edge S (FFM_F64_WARPS = 4 / 8
-// forces one: tuning aid)
+// warps per CTA of a sweep of super-unit edge S and nlaunch units
+// (FFM_F64_WARPS / FFM_F32_WARPS = 4 / 8 force one: tuning aid)
 #ifndef FFM_F64_NW4_MAXS
 #define FFM_F64_NW4_MAXS 1024
 #endif
-int nb_warps(int S, bool fp64) {
-  if (!fp64) return kWarps;
+// FP32: 4-warp CTAs (four per SM) only for many 256-atom units -- measured
+// (tools/mid_sweep.py, FFM_F32_WARPS A/B): 20k atoms (3160 units) 219 ->
+// 205 us; 10k (820 units) and S = 512 (30k) unchanged or slower
+int nb_warps(int S, bool fp64, int nlaunch) {
+  if (!fp64) {
+    static const int forced32 = [] {
+      const char* f = getenv("FFM_F32_WARPS");
+      return f ? atoi(f) : 0;
+    }();
+    if (forced32 == kWarps || (forced32 == 4 && S <= 512)) return forced32;
+    if (S > 256) return kWarps;
+    return nlaunch >= 2000 ? 4 : kWarps;
+  }
   static const int forced = [] {
     const char* f = getenv("FFM_F64_WARPS");
     return f ? atoi(f) : 0;
@@ -466,10 +477,9 @@ static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const voi
                                const void* ipos, const void* ilj, const void* bbox,
                                void* ipart, void* jpart, double* epart, int batch,
                                cudaStream_t st) {
-  if constexpr (sizeof(T) == 8)
-    if (nb_warps(plan.S, true) == 4)
-      return launch_nb_w<T, GRAD, CUTOFF, 4>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart,
-                                             epart, batch, st);
+  if (nb_warps(plan.S, sizeof(T) == 8, plan.nlaunch) == 4)
+    return launch_nb_w<T, GRAD, CUTOFF, 4>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart, epart,
+                                           batch, st);
   return launch_nb_w<T, GRAD, CUTOFF, kWarps>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart,
                                               epart, batch, st);
 }
