@@ -228,7 +228,7 @@ void drop_graphs(ffm_system* s) {
 int choose_S(int64_t n) {
   if (const char* f = getenv("FFM_FORCE_S")) {  // tuning aid; njb = S / 32 must fit 32 bits
     const int v = atoi(f);
-    if (v >= 256 && v <= 1024 && v % 256 == 0) return v;
+    if (v >= 128 && v <= 1024 && v % 128 == 0) return v;
   }
   // largest super-unit that still gives ~6 waves of units on 148 SMs x 2
   // CTAs: bigger units amortise the per-sub-block reductions, more units

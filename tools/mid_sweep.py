@@ -15,7 +15,7 @@ from paper_1810_03358_b200.synth import make_globule_system
 sizes = [int(a) for a in sys.argv[1:]] or [3000, 5000, 10000, 20000, 30000]
 only = os.environ.get("VARIANTS")
 PREC = N.FFM_F64 if os.environ.get("PREC") == "f64" else N.FFM_F32
-variants = [("auto", {}), ("S256", {"FFM_FORCE_S": "256", "FFM_FORCE_TILES": "0"}),
+variants = [("auto", {}), ("S128", {"FFM_FORCE_S": "128", "FFM_FORCE_TILES": "0"}), ("S256", {"FFM_FORCE_S": "256", "FFM_FORCE_TILES": "0"}),
             ("tiles256", {"FFM_FORCE_S": "256", "FFM_FORCE_TILES": "1"}),
             ("S512", {"FFM_FORCE_S": "512", "FFM_FORCE_TILES": "0"}),
             ("tiles", {"FFM_FORCE_TILES": "1"})]
