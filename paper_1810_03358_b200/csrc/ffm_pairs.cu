@@ -174,8 +174,15 @@ __device__ unsigned long long* g_unit_clock = nullptr;
 // SM, so one CTA's staging / reduction phases overlap the other's pair loop;
 // one 8-warp FP64 CTA fills the register file alone -- measured 4 vs 8
 // warps: 100k 11.72 -> 11.43 ms, 20k 571 -> 505 us, 10k 168 -> 159 us)
+#ifndef FFM_MINB64E
+#define FFM_MINB64E 3  // FP64 energy-only 4-warp CTAs per SM (no force accumulators)
+#endif
+#ifndef FFM_MINB32E
+#define FFM_MINB32E FFM_MINB  // FP32 energy-only 8-warp CTAs per SM
+#endif
 template <typename T, bool GRAD, bool CUTOFF, int NW>
-__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? FFM_MINB * kWarps / NW : (NW == kWarps ? FFM_MINB64 : 2))
+__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? (GRAD ? FFM_MINB : FFM_MINB32E) * kWarps / NW
+                                  : (NW == kWarps ? FFM_MINB64 : (GRAD ? 2 : FFM_MINB64E)))
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, const T* __restrict__ bbox,
