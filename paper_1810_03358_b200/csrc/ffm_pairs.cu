@@ -177,11 +177,13 @@ __device__ unsigned long long* g_unit_clock = nullptr;
 #ifndef FFM_MINB64E
 #define FFM_MINB64E 3  // FP64 energy-only 4-warp CTAs per SM (no force accumulators)
 #endif
-#ifndef FFM_MINB32E
-#define FFM_MINB32E FFM_MINB  // FP32 energy-only 8-warp CTAs per SM
-#endif
-template <typename T, bool GRAD, bool CUTOFF, int NW>
-__global__ void __launch_bounds__(NW * 32, sizeof(T) == 4 ? (GRAD ? FFM_MINB : FFM_MINB32E) * kWarps / NW
+// OCC > 0 overrides the CTAs per SM the registers are bounded for: FP32
+// energy-only sweeps of units up to 512 atoms run three 8-warp CTAs per SM
+// (79 registers, no spills; 10k atoms 45.6 -> 43.3 us, while at S = 1024
+// the third CTA measured 1% slower: profiles/r01_energy_occupancy_ab.log)
+template <typename T, bool GRAD, bool CUTOFF, int NW, int OCC = 0>
+__global__ void __launch_bounds__(NW * 32, OCC > 0 ? OCC
+                                  : sizeof(T) == 4 ? FFM_MINB * kWarps / NW
                                   : (NW == kWarps ? FFM_MINB64 : (GRAD ? 2 : FFM_MINB64E)))
 nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
@@ -425,13 +427,13 @@ size_t nb_smem_bytes(int S, bool fp64, bool grad, int nw) {
   return b;
 }
 
-template <typename T, bool GRAD, bool CUTOFF, int NW>
+template <typename T, bool GRAD, bool CUTOFF, int NW, int OCC = 0>
 static cudaError_t launch_nb_w(const NbPlanDev& plan, const void* pos, const void* lj,
                                const void* ipos, const void* ilj, const void* bbox,
                                void* ipart, void* jpart, double* epart, int batch,
                                cudaStream_t st) {
   const size_t smem = nb_smem_bytes(plan.S, sizeof(T) == 8, GRAD, NW);
-  auto k = nb_units_kernel<T, GRAD, CUTOFF, NW>;
+  auto k = nb_units_kernel<T, GRAD, CUTOFF, NW, OCC>;
   // opt in once, for the largest super-unit (not a stream operation, so it
   // must not sit inside a graph capture)
   static int opted = -1;
@@ -484,6 +486,10 @@ static cudaError_t launch_nb_t(const NbPlanDev& plan, const void* pos, const voi
                                const void* ipos, const void* ilj, const void* bbox,
                                void* ipart, void* jpart, double* epart, int batch,
                                cudaStream_t st) {
+  if constexpr (sizeof(T) == 4 && !GRAD)
+    if (plan.S <= 512)
+      return launch_nb_w<T, GRAD, CUTOFF, kWarps, 3>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart,
+                                                     epart, batch, st);
   if (nb_warps(plan.S, sizeof(T) == 8, plan.nlaunch) == 4)
     return launch_nb_w<T, GRAD, CUTOFF, 4>(plan, pos, lj, ipos, ilj, bbox, ipart, jpart, epart,
                                            batch, st);

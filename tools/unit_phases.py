@@ -54,3 +54,15 @@ for name, sel in (("first wave", first), ("later", ~first)):
     print(f"  {name:10s} ({sel.sum()} CTAs): total {np.nanmedian(X[:, 14] - X[:, 0]):6.2f} us; "
           f"jload {row[0]:.2f}; sub-blocks " + " ".join(f"{v:.2f}" for v in row[1:-1]) +
           f"; tail {row[-1]:.2f}; sub0 tiles(w0) " + " ".join(f"{v:.2f}" for v in tiles))
+# slot occupancy: CTA-time over (2 CTA slots per SM x SMs x span), and the
+# end-time profile of the last CTAs (the tail)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+dur = T[:, 14] - T[:, 0]
+span = np.nanmax(T[:, 14])
+print(f"  slot occupancy {np.nansum(dur) / (2 * sms * span):.3f} "
+      f"(CTA-us {np.nansum(dur):.0f} over {2 * sms} slots x {span:.1f} us)")
+ends = np.sort(T[:, 14])
+for q in (0.5, 0.75, 0.9, 0.97, 1.0):
+    print(f"  {q:.2f} of CTAs done by {ends[min(len(ends) - 1, int(q * len(ends)))]:.1f} us")
+starts = np.sort(T[:, 0])
+print(f"  last CTA started at {starts[-1]:.1f} us")
