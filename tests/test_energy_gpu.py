@@ -223,11 +223,14 @@ def test_missing_native_library_fails_loudly(tmp_path):
 
 # ------------------------------------------------------- full-size checks
 
-@pytest.mark.parametrize("n", [30000, 100000])
+@pytest.mark.parametrize("n", [10000, 20000, 30000, 100000])
 def test_full_size_against_threaded_oracle(n):
     """BASELINE sizes: the whole FP32 / FP64 gradient against the C oracle
-    run on all host cores."""
-    from paper_1810_03358_b200.energy import energy_and_gradient
+    run on all host cores, and the energy-only sweep's energies (the line
+    search's probes).  10k: 8-warp FP32 / 4-warp FP64 CTAs on 256-atom
+    units, three FP32 energy-only CTAs per SM; 20k: 4-warp FP32 CTAs (many
+    256-atom units); 30k: 512-atom units; 100k: 1024-atom units."""
+    from paper_1810_03358_b200.energy import energy_and_gradient, energy_total
     from paper_1810_03358_b200.synth import make_globule_system
 
     s = make_globule_system(n, seed=1)
@@ -240,6 +243,9 @@ def test_full_size_against_threaded_oracle(n):
         got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
         assert _rel(got, e_ref) <= et, (dt, got, e_ref)
         assert np.max(np.abs(g - g_ref)) <= gt * gmax
+        be = energy_total(s, dt)
+        got_e = np.array([be.stretch, be.bend, be.torsion, be.coulomb, be.vdw])
+        assert _rel(got_e, e_ref) <= et, (dt, got_e, e_ref)
 
 
 def test_full_size_properties():
