@@ -162,7 +162,7 @@ def run_graph(run, oracle, x, f, g, gn, linesearch, method, m=1, cg_kind="prp",
         if ints[2]:
             status = N.LBFGS_STATUS[int(ints[1])]
             break
-        if stop.max_wall_time is not None and run.elapsed() >= stop.max_wall_time:
+        if run.wall_time_reached():
             status = TIME_BUDGET
             break
     if linesearch is not None:

@@ -16,12 +16,20 @@ globally first pair; key = sum / count - 1 is exact in float64 (keys <
 replicated: every rank runs the same optimiser on the same all-reduced
 numbers, so no broadcast is needed per step.
 
-With an NCCL process group the engine does this itself: the group's
-communicator is attached (ffm_system_set_comm) and every evaluation ends
-with encode / ncclAllReduce / decode kernels on its stream, so the
-graph-resident drivers capture the all-reduce too.  ``ShardCombiner`` is
-the same reduction in torch for other backends; it is exercised with gloo
-on CPU tensors in tests/test_parallel_cpu.py.
+Completion, two ways:
+
+* ``ShardCombiner`` (the default): the engine's partial sums, then one
+  ``torch.distributed.all_reduce`` of the packed vector on the evaluation's
+  stream (NCCL over NVLink, or gloo).  Tested across processes: gloo world 2
+  on CPU (tests/test_parallel_cpu.py) and two processes sharing one GPU with
+  the real CUDA shards (tests/test_sharded_gpu.py).
+* native (opt-in: ``native=True`` or FFMIN_B200_NATIVE_COMM=1, NCCL groups
+  only): the group's communicator is attached to the engine
+  (ffm_system_set_comm) and every evaluation ends with encode /
+  ncclAllReduce / decode kernels on its stream, so the graph-resident
+  drivers capture the all-reduce too.  Exercised on one GPU with a one-rank
+  group only (a second rank needs a second GPU: NCCL refuses two ranks on
+  one device), hence not the default.
 """
 
 from __future__ import annotations
@@ -100,8 +108,13 @@ class ShardedSystem:
     all-reduce inside every evaluation, capturable in the graph-resident
     drivers) or, for other backends, by ShardCombiner from Python."""
 
-    def __init__(self, topo, group=None, device=None, native=True):
+    def __init__(self, topo, group=None, device=None, native=None):
+        import os
+
         from .engine import DeviceSystem
+
+        if native is None:
+            native = os.environ.get("FFMIN_B200_NATIVE_COMM", "") == "1"
 
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
@@ -148,7 +161,7 @@ class ShardedMolecularOracle:
 
     space = "device"
 
-    def __init__(self, system, dtype=np.float64, group=None, device=None, native=True):
+    def __init__(self, system, dtype=np.float64, group=None, device=None, native=None):
         from .engine import precision_of
         from .oracle import MolecularOracle
 
@@ -159,6 +172,17 @@ class ShardedMolecularOracle:
         self.n = 3 * system.natoms
         self.device = self._base.device
         self.precision = precision_of(dtype)
+        self.group = group
+        self._t = torch.zeros(1, dtype=torch.float64, device=self.device)
+
+    def agreed_elapsed(self, t):
+        """MAX of the ranks' elapsed wall times (one all-reduce), so that a
+        max_wall_time budget stops every rank at the same iteration: a rank
+        that stopped alone would leave the others waiting in the next
+        evaluation's collective."""
+        self._t.fill_(float(t))
+        dist.all_reduce(self._t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(self._t.item())
 
     def __getattr__(self, name):
         return getattr(self._base, name)

@@ -1,0 +1,141 @@
+"""Round-2 additions to tests/golden/golden_v1.npz (additive: existing keys
+are loaded and written back unchanged).
+
+Runs ONLY in the build container, where the reference package is importable
+from /root/reference (never on the GPU box).  Every value comes from the
+reference's own code (numba backend unless noted):
+
+  lbfgs500_np/*     the configs[0] bounded L-BFGS run again with the
+                    reference's NUMPY backend (ffmin/kernels.py:984-1024):
+                    the reference's own agreement horizon with itself,
+                    lbfgs500/self_horizon = leading records within 1e-8
+                    relative of the numba trace
+  conv500/*         configs[0] run to convergence on a single-basin problem
+                    (500-atom chain relaxed, jittered by 0.05 A, relaxed
+                    again; the second run is golden), as conv60 / conv200
+  fd14/*            ffmin.energy.finite_difference_gradient (energy.py:
+                    182-198) of chain14, step 1e-5, FP64 and FP32
+  batch1500/*       energy_total (energy.py:133-141, what wiggle.py:118-127
+                    probe_full calls) of 16 perturbed geometries of
+                    globule1500, FP64 and FP32: the batched evaluator's
+                    golden candidates
+
+    python tests/golden/make_golden_r2.py
+"""
+
+from __future__ import annotations
+
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+
+from ffmin.energy import energy_total, finite_difference_gradient  # noqa: E402
+from ffmin.kernels import NUMPY_BACKEND  # noqa: E402
+from ffmin.model import AngleTerm, AtomSpec, BondTerm, DihedralTerm  # noqa: E402
+from ffmin.model import MolecularSystem, NonbondedPolicy  # noqa: E402
+from ffmin.optimizers import StopCriteria, lbfgs, make_linesearch  # noqa: E402
+from ffmin.oracle import MolecularOracle  # noqa: E402
+from ffmin.synth import make_chain_system  # noqa: E402
+
+HERE = Path(__file__).resolve().parent
+OUT = HERE / "golden_v1.npz"
+sys.path.insert(0, str(HERE))
+from make_golden import put_system, store  # noqa: E402
+
+
+def rebuild(G, name):
+    """A golden case as a reference MolecularSystem."""
+    atoms = tuple(AtomSpec(i, f"A{i}", float(q), float(s), float(e)) for i, (q, s, e) in
+                  enumerate(zip(G[f"{name}/q"], G[f"{name}/sigma"], G[f"{name}/epsilon"])))
+    ex = frozenset(tuple(map(int, p)) for p in G[f"{name}/excluded"])
+    sc = frozenset(tuple(map(int, p)) for p in G[f"{name}/scaled14"])
+    cut = float(G[f"{name}/cutoff"])
+    return MolecularSystem(
+        atoms=atoms, coords=np.array(G[f"{name}/coords"]),
+        bonds=tuple(BondTerm(int(i), int(j), float(k), float(r)) for (i, j), k, r in
+                    zip(G[f"{name}/bond_idx"], G[f"{name}/bond_K"], G[f"{name}/bond_r0"])),
+        angles=tuple(AngleTerm(int(i), int(j), int(k), float(kk), float(a)) for (i, j, k), kk, a
+                     in zip(G[f"{name}/ang_idx"], G[f"{name}/ang_K"], G[f"{name}/ang_t0"])),
+        dihedrals=tuple(DihedralTerm(int(i), int(j), int(k), int(l), *map(float, v))
+                        for (i, j, k, l), v in zip(G[f"{name}/dih_idx"], G[f"{name}/dih_V"])),
+        nonbonded=NonbondedPolicy(excluded=ex, scaled14=sc, s14=float(G[f"{name}/s14"]),
+                                  cutoff=None if cut <= 0 else cut))
+
+
+def main():
+    G = dict(np.load(OUT, allow_pickle=False))
+
+    # the reference against itself: numpy backend, same bounded run
+    s500 = make_chain_system(500, seed=0, strain=0.3)
+    assert np.array_equal(s500.coords, G["lbfgs500/coords"])
+    stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
+    t1 = time.time()
+    res = lbfgs(MolecularOracle(s500, backend=NUMPY_BACKEND), s500.coords.ravel(), m=3,
+                linesearch=make_linesearch("par"), stop=stop)
+    f_np = np.array([r.f for r in res.trace.records])
+    G["lbfgs500_np/f_trace"] = f_np
+    G["lbfgs500_np/final"] = np.array([res.f, res.grad_norm, res.iterations])
+    ref = G["lbfgs500/f_trace"]
+    k = min(len(ref), len(f_np))
+    bad = np.nonzero(np.abs(f_np[:k] - ref[:k]) > 1e-8 * np.abs(ref[:k]))[0]
+    G["lbfgs500/self_horizon"] = np.array(int(bad[0]) if len(bad) else k)
+    print("lbfgs500 numpy backend:", res.f, res.iterations, "horizon",
+          int(G["lbfgs500/self_horizon"]), f"{time.time() - t1:.1f}s")
+
+    # configs[0] to convergence on a single-basin problem: a coarse relax
+    # (|g| <= 1e-2) of the strained chain, a 0.05 A jitter, then the golden
+    # run to |g| <= 1e-3
+    tol = 1e-3
+    stop = StopCriteria(max_iterations=20000, gradient_norm_tol=tol, gradient_norm_rtol=0.0)
+    sc = make_chain_system(500, seed=0, strain=0.3)
+    t1 = time.time()
+    r0 = lbfgs(MolecularOracle(sc), sc.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+               stop=StopCriteria(max_iterations=20000, gradient_norm_tol=1e-2,
+                                 gradient_norm_rtol=0.0))
+    print("conv500 pre-relax", r0.status, r0.f, r0.iterations, f"{time.time() - t1:.1f}s",
+          flush=True)
+    jit = np.random.default_rng(500).normal(scale=0.05, size=sc.coords.shape)
+    sc = sc.with_coords(r0.x.reshape(-1, 3) + jit)
+    store.clear()
+    put_system("conv500", sc)
+    t1 = time.time()
+    r = lbfgs(MolecularOracle(sc), sc.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+              stop=stop)
+    store["conv500/final"] = np.array([r.f, r.grad_norm, r.iterations, tol])
+    store["conv500/status"] = np.array(r.status)
+    store["conv500/x"] = r.x
+    store["conv500/seconds"] = np.array(time.time() - t1)
+    store["conv500/calls"] = np.array([r.trace.records[-1].value_calls,
+                                       r.trace.records[-1].grad_calls])
+    print("conv500", r.status, r.f, r.grad_norm, r.iterations, f"{time.time() - t1:.1f}s")
+
+    # finite-difference gradient (energy.py:182-198)
+    c14 = rebuild(G, "chain14")
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        store[f"fd14/grad_{tag}"] = finite_difference_gradient(c14, 1e-5, dt)
+    store["fd14/step"] = np.array(1e-5)
+
+    # batched candidates: energy_total of perturbed full geometries
+    g1500 = rebuild(G, "globule1500")
+    rng = np.random.default_rng(1500)
+    cands = g1500.coords[None] + rng.normal(scale=0.05, size=(16,) + g1500.coords.shape)
+    store["batch1500/coords"] = cands
+    for dt, tag in ((np.float64, "f64"), (np.float32, "f32")):
+        store[f"batch1500/energy_{tag}"] = np.array([
+            [bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw]
+            for bd in (energy_total(g1500.with_coords(c), dt) for c in cands)])
+
+    for k, v in store.items():
+        assert k not in G or k.startswith("conv500/"), f"would overwrite {k}"
+        G[k] = v
+    np.savez_compressed(OUT, **G)
+    print("wrote", OUT, len(G), "keys")
+
+
+if __name__ == "__main__":
+    main()

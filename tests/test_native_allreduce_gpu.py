@@ -85,7 +85,7 @@ def test_graph_driver_on_sharded_oracle(nccl1, monkeypatch):
             monkeypatch.setenv("FFMIN_B200_HOST_LOOP", "1")
         else:
             monkeypatch.delenv("FFMIN_B200_HOST_LOOP", raising=False)
-        o = ShardedMolecularOracle(s)
+        o = ShardedMolecularOracle(s, native=True)
         assert o.native
         _half(o._base.engine)
         r = lbfgs(o, s.coords.ravel(), m=4, linesearch=make_linesearch("par"),

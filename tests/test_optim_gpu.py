@@ -71,7 +71,29 @@ def test_device_lbfgs_follows_reference_trace(golden):
     assert np.max(np.abs(calls[:, 0] - ref_calls[:, 0])) <= 3
 
 
-@pytest.mark.parametrize("name,m", [("conv10", 5), ("conv60", 5), ("conv200", 5)])
+def test_device_lbfgs_horizon_at_least_references_own(golden):
+    """configs[0], the bounded 300-iteration run: how long the device trace
+    stays within 1e-8 of the reference's (numba) trace must be at least how
+    long the reference's numpy backend stays within 1e-8 of its numba
+    backend (lbfgs500/self_horizon, tests/golden/make_golden_r2.py) -- the
+    basin the unconverged run ends in is decided by roundoff in both."""
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import StopCriteria, lbfgs, make_linesearch
+
+    s = golden_system(golden, "lbfgs500")
+    stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
+    res = lbfgs(MolecularOracle(s), s.coords.ravel(), m=3, linesearch=make_linesearch("par"),
+                stop=stop)
+    f = np.array([r.f for r in res.trace.records])
+    ref = golden["lbfgs500/f_trace"]
+    k = min(len(f), len(ref))
+    bad = np.nonzero(np.abs(f[:k] - ref[:k]) > 1e-8 * np.abs(ref[:k]))[0]
+    horizon = int(bad[0]) if len(bad) else k
+    assert horizon >= int(golden["lbfgs500/self_horizon"]) > 0
+
+
+@pytest.mark.parametrize("name,m", [("conv10", 5), ("conv60", 5), ("conv200", 5),
+                                    ("conv500", 5)])
 def test_device_lbfgs_reaches_reference_minimum(golden, name, m):
     """Run to the precision limit like the reference; final energies agree
     to 1e-9 relative (north star: 1e-6), both in FP64 and FP32 modes."""
