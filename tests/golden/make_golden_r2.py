@@ -72,35 +72,46 @@ def main():
 
     # the reference against itself: numpy backend, same bounded run
     s500 = make_chain_system(500, seed=0, strain=0.3)
+    redo_np = "lbfgs500_np/f_trace" not in G
     assert np.array_equal(s500.coords, G["lbfgs500/coords"])
     stop = StopCriteria(max_iterations=300, gradient_norm_tol=1e-3, gradient_norm_rtol=0.0)
     t1 = time.time()
-    res = lbfgs(MolecularOracle(s500, backend=NUMPY_BACKEND), s500.coords.ravel(), m=3,
-                linesearch=make_linesearch("par"), stop=stop)
-    f_np = np.array([r.f for r in res.trace.records])
-    G["lbfgs500_np/f_trace"] = f_np
-    G["lbfgs500_np/final"] = np.array([res.f, res.grad_norm, res.iterations])
+    if redo_np:
+        res = lbfgs(MolecularOracle(s500, backend=NUMPY_BACKEND), s500.coords.ravel(), m=3,
+                    linesearch=make_linesearch("par"), stop=stop)
+        G["lbfgs500_np/f_trace"] = np.array([r.f for r in res.trace.records])
+        G["lbfgs500_np/final"] = np.array([res.f, res.grad_norm, res.iterations])
+    f_np = G["lbfgs500_np/f_trace"]
     ref = G["lbfgs500/f_trace"]
     k = min(len(ref), len(f_np))
     bad = np.nonzero(np.abs(f_np[:k] - ref[:k]) > 1e-8 * np.abs(ref[:k]))[0]
     G["lbfgs500/self_horizon"] = np.array(int(bad[0]) if len(bad) else k)
-    print("lbfgs500 numpy backend:", res.f, res.iterations, "horizon",
+    print("lbfgs500 numpy backend:", G["lbfgs500_np/final"], "horizon",
           int(G["lbfgs500/self_horizon"]), f"{time.time() - t1:.1f}s")
 
-    # configs[0] to convergence on a single-basin problem: a coarse relax
-    # (|g| <= 1e-2) of the strained chain, a 0.05 A jitter, then the golden
-    # run to |g| <= 1e-3
+    # configs[0] to convergence on a single-basin problem.  The strained
+    # 500-atom chain relaxes slowly through many basins (stage A: 20000
+    # iterations to f = -2495.6; stage B from a 0.05 A jitter of that: 16836
+    # iterations to |g| <= 1e-3, f = -3242.66 -- both far too long to follow
+    # under any roundoff change), so the golden run (stage C) starts from a
+    # 0.05 A jitter of stage B's minimum, like conv60 / conv200.  Stage B's
+    # point is kept as conv500_pre/x, so reruns skip A and B.
     tol = 1e-3
     stop = StopCriteria(max_iterations=20000, gradient_norm_tol=tol, gradient_norm_rtol=0.0)
     sc = make_chain_system(500, seed=0, strain=0.3)
-    t1 = time.time()
-    r0 = lbfgs(MolecularOracle(sc), sc.coords.ravel(), m=5, linesearch=make_linesearch("par"),
-               stop=StopCriteria(max_iterations=20000, gradient_norm_tol=1e-2,
-                                 gradient_norm_rtol=0.0))
-    print("conv500 pre-relax", r0.status, r0.f, r0.iterations, f"{time.time() - t1:.1f}s",
-          flush=True)
-    jit = np.random.default_rng(500).normal(scale=0.05, size=sc.coords.shape)
-    sc = sc.with_coords(r0.x.reshape(-1, 3) + jit)
+    if "conv500_pre/x" not in G:
+        t1 = time.time()
+        rA = lbfgs(MolecularOracle(sc), sc.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+                   stop=StopCriteria(max_iterations=20000, gradient_norm_tol=1e-2,
+                                     gradient_norm_rtol=0.0))
+        jit = np.random.default_rng(500).normal(scale=0.05, size=sc.coords.shape)
+        rB = lbfgs(MolecularOracle(sc), (rA.x.reshape(-1, 3) + jit).ravel(), m=5,
+                   linesearch=make_linesearch("par"), stop=stop)
+        G["conv500_pre/x"] = rB.x
+        print("conv500 stages A, B", rA.f, rB.f, rB.iterations, f"{time.time() - t1:.1f}s",
+              flush=True)
+    jit = np.random.default_rng(501).normal(scale=0.05, size=sc.coords.shape)
+    sc = sc.with_coords(G["conv500_pre/x"].reshape(-1, 3) + jit)
     store.clear()
     put_system("conv500", sc)
     t1 = time.time()
@@ -131,7 +142,8 @@ def main():
             for bd in (energy_total(g1500.with_coords(c), dt) for c in cands)])
 
     for k, v in store.items():
-        assert k not in G or k.startswith("conv500/"), f"would overwrite {k}"
+        assert k not in G or k.startswith(("conv500/", "fd14/", "batch1500/")), \
+            f"would overwrite {k}"
         G[k] = v
     np.savez_compressed(OUT, **G)
     print("wrote", OUT, len(G), "keys")
