@@ -49,6 +49,10 @@ FMA_SLOTS_PER_PAIR = 24  # FP32 lane-ops on the FMA pipe per pair (SASS: 2 x 12 
 FP64_OPS_PER_PAIR = 32  # FP64-pipe operations per pair (ncu: fp64 pipe 66.9% at 12.87 ms)
 DFMA_PEAK = 18.49e12  # measured DFMA/s (63.6 per clk per SM, profiles/r01_pipes_microbench.txt)
 NOMINAL_FP32_FLOPS = 2 * 128 * 148 * 1965e6  # 128 FFMA lanes / clk / SM at the max SM clock
+# the pair loop's instruction mix alone (tools/microbench/pairmix.cu: warp_tile's
+# arithmetic on shared-memory data at the sweep's occupancy, no global memory,
+# masks or reductions), profiles/r02_pipes_microbench.txt
+MIX_CEILING_PAIRS = 1.268e12
 
 
 def parse():
@@ -100,7 +104,7 @@ def world_from_env(args):
 def nb_traffic(n):
     """DRAM bytes per pair-sweep launch from the committed ncu capture."""
     try:
-        d = json.loads((ROOT / "profiles" / "r01_nb_traffic.json").read_text())
+        d = json.loads((ROOT / "profiles" / "r02_nb_traffic.json").read_text())
         return d["dram_bytes_per_launch"] if d.get("natoms") == n else None
     except Exception:
         return None
@@ -421,6 +425,10 @@ def main():
                      "flop_per_pair": FLOP_PER_PAIR, "fma_pipe_frac": fma_frac,
                      "nb_ms": nb32, "nb_ms_f64": nb64,
                      "frac_of_nominal": achieved / NOMINAL_FP32_FLOPS,
+                     "frac_of_mix_ceiling": nb_pairs_per_rank / (nb32 * 1e-3) / MIX_CEILING_PAIRS,
+                     "mix_ceiling_note": "the sweep's instruction mix alone reaches 1.268e12 "
+                                         "pairs/s (81.7% of the FMA pipe; 3-source FFMA2 are "
+                                         "register-read bound), profiles/r02_pipes_microbench.txt",
                      "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt "
                                     "(MEASURED_PEAKS.json has no FP32 figure); frac_of_nominal: "
                                     "128 FMA/clk/SM x 148 SMs x 1965 MHz = 74.4 TFLOP/s",

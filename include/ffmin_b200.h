@@ -142,8 +142,12 @@ int ffm_eval_host(ffm_system_t* sys, int precision, int flags, const double* coo
 
 /* Energies of `batch` candidate geometries of the same system
  * (coords_d: [batch][n][3]); energies_d: [batch][5]; status_d: [batch][8].
- * The batched evaluator behind the gradient-free drivers (probe_full in
- * ffmin/optimizers/wiggle.py:118-127). */
+ * The batched form of energy_total (ffmin/energy.py:133-141) that
+ * probe_full (ffmin/optimizers/wiggle.py:118-127) calls once per candidate:
+ * B full geometries per launch (BASELINE configs[3], finite-difference
+ * gradients).  The atom-wiggle driver itself probes with exact single-atom
+ * deltas (ffm_atom_delta below), which equal probe_full's
+ * energy_total(moved) - e_run up to that difference's roundoff. */
 int ffm_eval_batch(ffm_system_t* sys, int precision, int64_t batch, const double* coords_d,
                    double* energies_d, int64_t* status_d, void* stream);
 
