@@ -155,3 +155,34 @@ def test_every_driver_reproduces_reference_trace(golden, name):
     assert np.array_equal(calls, golden[f"drv30/{name}/calls"])
     assert np.array_equal(res.x, golden[f"drv30/{name}/x"])
     assert res.status == str(golden[f"drv30/{name}/status"])
+
+
+def test_wall_time_budget_uses_the_agreed_elapsed_time():
+    """A row-sharded oracle runs the same driver on every rank and every
+    evaluation ends in a collective, so the max_wall_time test must use the
+    ranks' agreed (MAX) elapsed time (ShardedMolecularOracle.agreed_elapsed):
+    an oracle whose agreement reports an expired budget stops the run at the
+    next budget check even though the local clock has not run out, and one
+    that reports none lets it run to its iteration budget."""
+    from paper_1810_03358_b200.optimizers.common import TIME_BUDGET
+
+    class Agreeing(FunctionOracle):
+        def __init__(self, remote):  # Rosenbrock: no line-search failure in 3 steps
+            super().__init__(
+                2, lambda x: float((1 - x[0]) ** 2 + 100 * (x[1] - x[0] ** 2) ** 2),
+                lambda x: np.array([-2 * (1 - x[0]) - 400 * x[0] * (x[1] - x[0] ** 2),
+                                    200 * (x[1] - x[0] ** 2)]))
+            self.remote = remote
+            self.asked = 0
+
+        def agreed_elapsed(self, t):
+            self.asked += 1
+            return max(t, self.remote)
+
+    for remote, want in ((1e9, TIME_BUDGET), (0.0, "iteration_budget")):
+        o = Agreeing(remote)
+        res = lbfgs(o, np.array([-1.2, 1.0]), m=2, linesearch=make_linesearch("par"),
+                    stop=StopCriteria(max_iterations=3, max_wall_time=60.0,
+                                      gradient_norm_rtol=0.0, gradient_norm_tol=0.0))
+        assert res.status == want and o.asked >= 1
+        assert res.iterations == (0 if remote else 3)

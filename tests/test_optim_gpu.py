@@ -118,6 +118,32 @@ def test_device_lbfgs_reaches_reference_minimum(golden, name, m):
     assert f32_in_f64 == pytest.approx(ref_f, rel=1e-4)
 
 
+@pytest.mark.parametrize("n,iters", [(10000, 8), (100000, 1)])
+def test_device_lbfgs_at_benchmark_sizes_tracks_oracle(n, iters):
+    """configs[2] / configs[4] sizes: the graph-resident FP64 L-BFGS on the
+    10k / 100k-atom globules of bench.py against oracle/optim.py (the
+    reference driver restated, lbfgs.py:78-128, on the threaded C oracle):
+    same f trace (1e-9 relative) and oracle call counts, iterate within
+    1e-6 A."""
+    import oracle as O
+    import oracle.optim as OO
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.optimizers import StopCriteria, lbfgs, make_linesearch
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(n, seed=1)
+    res = lbfgs(MolecularOracle(s), s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
+                stop=StopCriteria(max_iterations=iters, gradient_norm_rtol=0.0))
+    ref = OO.lbfgs(O.Arrays.from_system(s), s.coords.ravel(), m=5, max_iterations=iters,
+                   threads=O.host_threads())
+    f = np.array([r.f for r in res.trace.records])
+    assert len(f) == len(ref["f_trace"]) == iters + 1
+    np.testing.assert_allclose(f, ref["f_trace"], rtol=1e-9, atol=0)
+    calls = [(r.value_calls, r.grad_calls) for r in res.trace.records]
+    assert calls == [tuple(c) for c in ref["calls"]]
+    assert np.max(np.abs(res.x - ref["x"])) <= 1e-6
+
+
 def test_device_results_stay_on_device():
     import torch
 
