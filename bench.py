@@ -547,6 +547,46 @@ def run_extras(rank, world, local, native=False):
     # configs[4]: L-BFGS iterations on the 100k-atom system (1 GPU)
     out["lbfgs_100k"] = optimizer_comparison(100000, iters=10, methods=("lbfgs",),
                                              dtype=np.float32, cpu_iters=1)
+    out["shard_compute_100k"] = shard_compute(local)
+    return out
+
+
+def shard_compute(local, n=100_000):
+    """configs[4] on one GPU: every rank's partial FP32 evaluation of a W-way
+    row-sharded 100k plan (ffm_system_set_shard), timed alone with CUDA
+    events -- the compute each GPU of a W-GPU job runs, without the
+    all-reduce (24n bytes per evaluation) and without waiting on other
+    ranks."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(n, seed=0)
+    dev = torch.device("cuda", local)
+    c = torch.from_numpy(np.array(s.coords)).to(dev)
+    g = torch.empty_like(c)
+    eng = DeviceSystem(s.topology, local)
+    en, st = eng.new_outputs()
+    out = {"natoms": n, "what": "per-rank partial evaluation (FP32 energy+gradient), ms, "
+                                "each rank's share timed alone on one GPU; no collective"}
+    for W in (1, 2, 4, 8):
+        ms = []
+        for rank in range(W):
+            N.check(eng.lib.ffm_system_set_shard(eng.handle, rank, W), "set_shard")
+            for _ in range(2):
+                eng.eval(c, N.FFM_F32, grad=g, energies=en, status=st)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                eng.eval(c, N.FFM_F32, grad=g, energies=en, status=st)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1) / 5)
+        out[f"W{W}"] = {"max_rank_ms": max(ms), "min_rank_ms": min(ms)}
+    eng.close()
     return out
 
 
