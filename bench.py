@@ -49,10 +49,11 @@ FMA_SLOTS_PER_PAIR = 24  # FP32 lane-ops on the FMA pipe per pair (SASS: 2 x 12 
 FP64_OPS_PER_PAIR = 32  # FP64-pipe operations per pair (ncu: fp64 pipe 66.9% at 12.87 ms)
 DFMA_PEAK = 18.49e12  # measured DFMA/s (63.6 per clk per SM, profiles/r01_pipes_microbench.txt)
 NOMINAL_FP32_FLOPS = 2 * 128 * 148 * 1965e6  # 128 FFMA lanes / clk / SM at the max SM clock
-# the pair loop's instruction mix alone (tools/microbench/pairmix.cu: warp_tile's
-# arithmetic on shared-memory data at the sweep's occupancy, no global memory,
-# masks or reductions), profiles/r02_pipes_microbench.txt
-MIX_CEILING_PAIRS = 1.268e12
+# the tile loop alone (tools/microbench/pairmix.cu: the sweep's warp_tile on a
+# restaged shared-memory j-block at the sweep's occupancy, no global memory,
+# masks, staging or reductions), ncu pipe activity, profiles/r02_pipes_microbench.txt
+MIX_CEILING = {"fp32_fma_pipe_active": 0.788, "fp64_pipe_active": 0.745}
+SWEEP_NCU = {"fp32_fma_pipe_active": 0.756, "fp64_pipe_active": 0.746}  # r02 ncu, 100k
 
 
 def parse():
@@ -425,10 +426,11 @@ def main():
                      "flop_per_pair": FLOP_PER_PAIR, "fma_pipe_frac": fma_frac,
                      "nb_ms": nb32, "nb_ms_f64": nb64,
                      "frac_of_nominal": achieved / NOMINAL_FP32_FLOPS,
-                     "frac_of_mix_ceiling": nb_pairs_per_rank / (nb32 * 1e-3) / MIX_CEILING_PAIRS,
-                     "mix_ceiling_note": "the sweep's instruction mix alone reaches 1.268e12 "
-                                         "pairs/s (81.7% of the FMA pipe; 3-source FFMA2 are "
-                                         "register-read bound), profiles/r02_pipes_microbench.txt",
+                     "mix_ceiling": {"fma_pipe_active_tile_loop_alone": MIX_CEILING["fp32_fma_pipe_active"],
+                                     "fma_pipe_active_sweep": SWEEP_NCU["fp32_fma_pipe_active"],
+                                     "source": "ncu, profiles/r02_pipes_microbench.txt: the sweep's "
+                                               "tile loop in isolation keeps the FMA pipe 78.8% "
+                                               "busy; the 100k sweep 75.6%"},
                      "peak_source": "measured FFMA throughput, profiles/r01_pipes_microbench.txt "
                                     "(MEASURED_PEAKS.json has no FP32 figure); frac_of_nominal: "
                                     "128 FMA/clk/SM x 148 SMs x 1965 MHz = 74.4 TFLOP/s",
@@ -439,7 +441,10 @@ def main():
                          "achieved": nb_pairs_per_rank * FP64_OPS_PER_PAIR / (nb64 * 1e-3) / 1e12,
                          "peak": DFMA_PEAK / 1e12, "unit": "T fp64-pipe ops/s",
                          "frac": nb_pairs_per_rank * FP64_OPS_PER_PAIR / (nb64 * 1e-3) / DFMA_PEAK,
-                         "ops_per_pair": FP64_OPS_PER_PAIR, "nb_ms": nb64},
+                         "ops_per_pair": FP64_OPS_PER_PAIR, "nb_ms": nb64,
+                         "mix_ceiling": {"fp64_pipe_active_tile_loop_alone": MIX_CEILING["fp64_pipe_active"],
+                                         "fp64_pipe_active_sweep": SWEEP_NCU["fp64_pipe_active"],
+                                         "source": "ncu, profiles/r02_pipes_microbench.txt"}},
         "gpu_launches": int(launches),
         "clocks": clocks,
     }

@@ -1,99 +1,89 @@
-// Instruction-mix ceiling of the FP32 pair loop (tuning aid, not product):
-// warp_tile's per-pair arithmetic (ffm_tile.cuh, FP32, energy + gradient,
-// 4 i-atoms per lane as two packed pairs) run on register / shared-memory
-// data only, at the sweep's occupancy (8-warp CTAs, 2 per SM, 128 registers),
-// to see how busy this mix can keep the FMA pipe by itself:
-// (j-records from the doubled shared-memory block and the j-gradient column's
-// three 64-bit lane shuffles per step, as in the real loop; without the
-// shuffles ptxas hoists across the unrolled steps and spills)
-// Reports pairs/s and FMA-pipe lane-ops (24 per pair in the sweep's SASS) as a
-// fraction of 128 / clk / SM at the clock given on the command line.
+// Instruction-mix ceiling of the pair loop (tuning aid, not product): the
+// sweep's own warp_tile (ffm_tile.cuh, energy + gradient, unmasked, 4 i-atoms
+// per lane) called tile after tile on a shared-memory j-block restaged per
+// tile, at the
+// sweep's occupancy (FP32: 8-warp CTAs, 2 per SM; FP64: 4-warp CTAs, 2 per
+// SM) with no global memory traffic, masks, special-tile lookups, unit
+// staging or cross-warp reductions.  Reports pairs/s and the pipe fraction
+// it implies: FP32 24 FMA-pipe lane-ops per pair of 128 / clk / SM, FP64 32
+// FP64-pipe ops per pair of 64 / clk / SM, at the clock given (MHz).
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
-#include "../../paper_1810_03358_b200/csrc/ffm_common.cuh"
+#include "../../paper_1810_03358_b200/csrc/ffm_tile.cuh"
 using namespace ffm;
-using P = Pk<float>;
-using V = P::V;
-constexpr int kTiles = 256;  // tiles of 32 steps per warp
+constexpr int kTiles = 256;  // tiles per warp
 
-__global__ void __launch_bounds__(256, 2) k_pairs(float* out, float seed) {
-  __shared__ float4 sj[8][64];
-  __shared__ float2 sl[8][64];
+template <typename T, int NW, bool DBL = true>
+__global__ void __launch_bounds__(NW * 32, 2) k_tiles(T* out, T seed) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  using V4 = typename Vec4T<T>::type;
+  using V2 = typename Vec2T<T>::type;
+  __shared__ V4 sj[NW][64];
+  __shared__ V2 sl[NW][64];
+  __shared__ T jacc[NW][3 * 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float4 p = make_float4(-(lane * 0.37f + seed), -(lane * 0.11f), -(lane * 0.23f), 0.3f);
-  float2 l = make_float2(1.1f + lane * 1e-3f, -0.9f);
-  sj[w][lane] = p; sj[w][lane + 32] = p; sl[w][lane] = l; sl[w][lane + 32] = l;
+  V4 p;
+  p.x = -(lane * T(0.37) + seed);
+  p.y = -(lane * T(0.11));
+  p.z = -(lane * T(0.23));
+  p.w = T(0.3);
+  V2 l;
+  l.x = T(1.1) + lane * T(1e-3);
+  l.y = T(-0.9);
+  sj[w][lane] = p;
+  sj[w][lane + 32] = p;
+  sl[w][lane] = l;
+  sl[w][lane + 32] = l;
+  jacc[w][lane] = jacc[w][32 + lane] = jacc[w][64 + lane] = T(0);
   __syncwarp();
   V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2], F[2][3];
   for (int pp = 0; pp < 2; ++pp) {
-    xi[pp] = P::make(10.f + lane + pp, 11.f + lane); yi[pp] = P::make(3.f * pp, 1.f);
-    zi[pp] = P::make(2.f, 5.f + pp); qi[pp] = P::make(0.2f, -0.3f);
-    ai[pp] = P::make(6.f, 6.5f); bi[pp] = P::make(1.f, 1.2f);
+    xi[pp] = P::make(T(10) + lane + pp, T(11) + lane);
+    yi[pp] = P::make(T(3) * pp, T(1));
+    zi[pp] = P::make(T(2), T(5) + pp);
+    qi[pp] = P::make(T(0.2), T(-0.3));
+    ai[pp] = P::make(T(6), T(6.5));
+    bi[pp] = P::make(T(1), T(1.2));
     F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
   }
-  V ec2 = P::zero(), ev2 = P::zero();
-  const float4* J = sj[w] + lane;
-  const float2* L = sl[w] + lane;
-  const int src = (lane + 1) & 31;
+  const uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
+  T minr2 = T(1e30);
+  double acc = 0.0;
   for (int tile = 0; tile < kTiles; ++tile) {
-    V gx = P::zero(), gy = P::zero(), gz = P::zero();
-#pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      float4 pj;
-      float2 lj;
-      pj = J[t];
-      lj = L[t];
-      V dx[2], dy[2], dz[2], r2[2], A[2], nB[2], Q[2], ri[2], i2[2];
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        dx[pp] = P::add(xi[pp], P::bc(pj.x)); dy[pp] = P::add(yi[pp], P::bc(pj.y));
-        dz[pp] = P::add(zi[pp], P::bc(pj.z));
-        r2[pp] = P::mul(dx[pp], dx[pp]); r2[pp] = P::fma(dy[pp], dy[pp], r2[pp]);
-        r2[pp] = P::fma(dz[pp], dz[pp], r2[pp]);
-      }
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        A[pp] = P::mul(ai[pp], P::bc(lj.x)); nB[pp] = P::mul(bi[pp], P::bc(lj.y));
-        Q[pp] = P::mul(qi[pp], P::bc(pj.w));
-        ri[pp] = P::rsqrt(r2[pp]); i2[pp] = P::rcp_or_sq(r2[pp], ri[pp]);
-      }
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        const V i4 = P::mul(i2[pp], i2[pp]), i6 = P::mul(i4, i2[pp]);
-        const V u = P::mul(A[pp], i6), v = P::add(u, nB[pp]), ecp = P::mul(Q[pp], ri[pp]);
-        ec2 = P::add(ec2, ecp);
-        const V pw = P::add(u, v);
-        ev2 = P::fma(v, i6, ev2);
-        const V g = P::mul(P::fma(pw, i6, ecp), i2[pp]);
-        F[pp][0] = P::fma(g, dx[pp], F[pp][0]); F[pp][1] = P::fma(g, dy[pp], F[pp][1]);
-        F[pp][2] = P::fma(g, dz[pp], F[pp][2]);
-        gx = P::fma(g, dx[pp], gx); gy = P::fma(g, dy[pp], gy); gz = P::fma(g, dz[pp], gz);
-      }
-      {
-        gx = __shfl_sync(0xffffffffu, gx, src); gy = __shfl_sync(0xffffffffu, gy, src);
-        gz = __shfl_sync(0xffffffffu, gz, src);
-      }
-    }
-    ec2 = P::add(ec2, P::add(gx, P::add(gy, gz)));
+    // a new j-block every tile (as the sweep stages one): nothing of the
+    // tile's arithmetic is loop-invariant for the compiler to hoist
+    p.x -= T(1e-3);
+    l.x += T(1e-6);
+    __syncwarp();
+    sj[w][lane] = p;
+    sj[w][lane + 32] = p;
+    sl[w][lane] = l;
+    sl[w][lane + 32] = l;
+    __syncwarp();
+    V ec2 = P::zero(), ev2 = P::zero();
+    warp_tile<T, true, false, false, 2, DBL>(sj[w], sl[w], lane, xi, yi, zi, qi, ai, bi, F, ec2,
+                                             ev2, jacc[w], 32, mk, T(0), minr2);
+    acc += double(P::lo(ec2)) + double(P::hi(ev2));
+    __syncwarp();
   }
-  float s = P::lo(ec2) + P::hi(ev2);
+  T s = T(acc) + minr2;
   for (int pp = 0; pp < 2; ++pp) s += P::lo(F[pp][0]) + P::hi(F[pp][1]) + P::lo(F[pp][2]);
-  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s + jacc[w][lane];
 }
 
 int main(int argc, char** argv) {
   const double mhz = argc > 1 ? atof(argv[1]) : 1965.0;
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-  const int blocks = sms * 2 * 8, threads = 256;  // 8 waves of the 2-CTA/SM residency
-  float* out;
-  cudaMalloc(&out, sizeof(float) * blocks * threads);
+  double* out;
+  cudaMalloc(&out, sizeof(double) * sms * 2 * 8 * 256);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const double pairs = (double)blocks * threads * 4 * 32 * kTiles;  // 4 i-atoms per lane
-  auto run = [&](const char* name, auto launch) {
+  auto run = [&](const char* name, int blocks, int threads, double ops, double lanes,
+                 auto launch) {
     for (int w = 0; w < 3; ++w) launch();
     cudaEventRecord(e0);
     for (int r = 0; r < 5; ++r) launch();
@@ -102,11 +92,27 @@ int main(int argc, char** argv) {
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= 5;
+    const double pairs = (double)blocks * threads * 4 * 32 * kTiles;
     const double rate = pairs / (ms * 1e-3);
-    printf("%-6s %8.3f ms  %.4e pairs/s  FMA-pipe %5.1f%% of 128/clk/SM at %.0f MHz\n", name, ms,
-           rate, 100.0 * rate * 24 / (128.0 * sms * mhz * 1e6), mhz);
+    printf("%-5s %8.3f ms  %.4e pairs/s  pipe %5.1f%% of %.0f/clk/SM at %.0f MHz\n", name, ms,
+           rate, 100.0 * rate * ops / (lanes * sms * mhz * 1e6), lanes, mhz);
   };
-  run("pairmix", [&] { k_pairs<<<blocks, threads>>>(out, 0.5f); });
+  const int b32 = sms * 2 * 8, b64 = sms * 2 * 8;
+  run("fp32", b32, 256, 24, 128,
+      [&] { k_tiles<float, 8><<<b32, 256>>>(reinterpret_cast<float*>(out), 0.5f); });
+  run("fp64", b64, 128, 32, 64, [&] { k_tiles<double, 4><<<b64, 128>>>(out, 0.5); });
+  // the same at the sweep's FP64 residency (two 4-warp CTAs per SM: extra
+  // dynamic shared memory keeps a third out), doubled / single j-block copy
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, 0);
+  const int pad = maxsm / 2 - 20 * 1024;
+  cudaFuncSetAttribute(k_tiles<double, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, pad);
+  cudaFuncSetAttribute(k_tiles<double, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       pad);
+  run("fp64/2", b64, 128, 32, 64,
+      [&] { k_tiles<double, 4, true><<<b64, 128, pad>>>(out, 0.5); });
+  run("fp64/2s", b64, 128, 32, 64,
+      [&] { k_tiles<double, 4, false><<<b64, 128, pad>>>(out, 0.5); });
   cudaError_t err = cudaGetLastError();
   printf("status: %s\n", cudaGetErrorString(err));
   return err != cudaSuccess;
