@@ -52,13 +52,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src in SOURCES:
         obj = LIB_DIR / (Path(src).stem + ".o")
-        cmd = [nvcc_path(), *NVCC_FLAGS, *EXTRA.get(src, ()), "-c", "-o", str(obj),
-               str(CSRC / src)]
-        _run(cmd, verbose)
+        cmds.append([nvcc_path(), *NVCC_FLAGS, *EXTRA.get(src, ()), "-c", "-o", str(obj),
+                     str(CSRC / src)])
         objs.append(str(obj))
+    # the translation units are independent: compile them in parallel
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as pool:
+        for f in [pool.submit(_run, c, verbose) for c in cmds]:
+            f.result()
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
           *objs, "-ldl"], verbose)
