@@ -12,6 +12,16 @@
 
 namespace ffm {
 
+// Programmatic dependent launch (PDL, launch_k in ffm_kernels.h): a kernel
+// may be scheduled while its stream predecessor is still finishing; every
+// kernel calls pdl_wait() before touching memory (griddepcontrol.wait: the
+// predecessor grid has completed and its writes are visible -- a no-op for
+// kernels launched without PDL), then lets its own dependents launch early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // ffmin/constants.py:10, 13, 16
 constexpr double kCoulomb = 1389.38757;
 constexpr double kRmin = 1e-12;

@@ -4,12 +4,43 @@
 #include "ffm_plan.cuh"
 
 #include <atomic>
+#include <cstdlib>
+#include <utility>
 
 namespace ffm {
 
 // every kernel launch of the engine, for the benchmark's gpu_launches claim
 extern std::atomic<long long> g_launch_count;
 inline void count_launch(long long k = 1) { g_launch_count.fetch_add(k, std::memory_order_relaxed); }
+
+// Kernel launch with programmatic stream serialization (PDL): the next
+// kernel of a dependent chain is scheduled onto SMs freed by its
+// predecessor's last wave and starts the moment the predecessor completes
+// (pdl_wait, ffm_common.cuh), instead of after a full launch latency --
+// inside the captured evaluation / minimiser graphs too.  FFM_PDL=0 turns
+// it off (plain launches).
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* f = getenv("FFM_PDL");
+    return f ? atoi(f) != 0 : true;
+  }();
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                            cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 size_t nb_smem_bytes(int S, bool fp64, bool grad, int nw);
 int nb_warps(int S, bool fp64, int nlaunch);  // warps per CTA of the super-unit sweep

@@ -21,6 +21,8 @@ namespace {
 using namespace mindev;
 
 __global__ void min_launch_begin_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->iters_launch = 0;
   S->pause = 0;
   S->nrec = 0;
@@ -30,6 +32,8 @@ __global__ void min_launch_begin_kernel(MinState* S) {
 __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir,
                                     cudaGraphConditionalHandle hls,
                                     cudaGraphConditionalHandle hacc) {
+  pdl_wait();
+  pdl_launch_dependents();
   cudaGraphSetConditional(hls, 0);
   cudaGraphSetConditional(hacc, 0);
   unsigned go = 0;
@@ -57,6 +61,8 @@ __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir
 
 // after d (two-loop or antigradient) and <d, d>
 __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->c.method == kMethodSd) {
     // r = div(lincomb(-1, g), |g|)  (ffmin/optimizers/gradient.py, Eq. (4))
     S->dn = S->gn;
@@ -93,6 +99,8 @@ __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
 
 // after r = d / |d| and slope = <g, r>: LineSearcher.search, first attempt
 __global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) {  // an evaluation before the search failed (OFGM: value(y))
     cudaGraphSetConditional(hloop, 0);
     return;
@@ -106,11 +114,15 @@ __global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop
 
 __global__ void min_ls_step_kernel(MinState* S, const double* en, const int64_t* stw,
                                    cudaGraphConditionalHandle hloop) {
+  pdl_wait();
+  pdl_launch_dependents();
   ls_step(S, en, stw, hloop);
 }
 
 // lbfgs.py: what a line-search result does to the iteration
 __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditionalHandle hacc) {
+  pdl_wait();
+  pdl_launch_dependents();
   unsigned acc = 0;
   if (!S->err && S->c.method == kMethodFgm) {
     // ffmin/optimizers/fgm.py: a failed search stops the run, or records an
@@ -183,6 +195,8 @@ __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditiona
 
 // after the gradient at x_new and <g_new, g_new>
 __global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->gcalls++;
   if (bad_status(stw, true)) {
     set_err(S, kMinErrEval, stw, true);
@@ -193,6 +207,8 @@ __global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
 
 // after <s,y>, <s,s>, <y,y>: LbfgsMemory._commit
 __global__ void min_commit_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->store_slot = -1;
   if (S->err) return;
   const double sy = S->sy, ss = S->ss, yy = S->yy;
@@ -224,6 +240,8 @@ __global__ void min_store_kernel(const MinState* S, int64_t n, const double* __r
                                  double* __restrict__ ring_y, const double* __restrict__ x_new,
                                  const double* __restrict__ g_new, double* __restrict__ x,
                                  double* __restrict__ g) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   const int slot = S->store_slot;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -255,6 +273,8 @@ __device__ double cg_beta_of(int kind, const double* d) {
 }
 
 __global__ void min_cg_beta_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   S->since_restart++;
   if (S->since_restart >= S->c.restart_period) {
@@ -271,6 +291,8 @@ __global__ void min_cg_beta_kernel(MinState* S) {
 // in place (each element reads its old p first)
 __global__ void cg_update_kernel(const MinState* S, int64_t n, const double* __restrict__ g_new,
                                  double* __restrict__ p) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   const double beta = S->beta;
   const bool use_beta = S->cg_else && isfinite(beta);
@@ -284,6 +306,8 @@ __global__ void cg_update_kernel(const MinState* S, int64_t n, const double* __r
 // descent test dot(p+, -g+) <= 0 (= -<p+, g+>, the negation is exact) or a
 // non-finite beta: restart p+ = -g+
 __global__ void min_cg_check_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->cg_reset = 0;
   if (S->err || !S->cg_else) return;
   if (!isfinite(S->beta) || -S->pg <= 0.0) {
@@ -295,6 +319,8 @@ __global__ void min_cg_check_kernel(MinState* S) {
 // dst = lincomb(-1, src) when *flag (device-decided restarts)
 __global__ void select_neg_kernel(const int* flag, const int* err, int64_t n,
                                   const double* __restrict__ src, double* __restrict__ dst) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (!*flag || *err) return;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -305,6 +331,8 @@ __global__ void select_neg_kernel(const int* flag, const int* err, int64_t n,
 // theta_k and beta_k from theta_{k-1}; the caller then forms
 // w = lincomb(1, x, beta, lincomb(1, x, -1, x_prev))
 __global__ void fgm_pre_kernel(MinState* S, cudaGraphConditionalHandle heval) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double tp = S->theta_prev;
   const double theta = 0.5 * tp * (sqrt(tp * tp + 4.0) - tp);
   S->theta = theta;
@@ -318,6 +346,8 @@ __global__ void fgm_pre_kernel(MinState* S, cudaGraphConditionalHandle heval) {
 // |g_w| and the convergence test, then the search direction scale
 __global__ void fgm_post_eval_kernel(MinState* S, const double* en, const int64_t* stw,
                                      cudaGraphConditionalHandle hls) {
+  pdl_wait();
+  pdl_launch_dependents();
   cudaGraphSetConditional(hls, 0);
   if (S->k > 0) {
     S->vcalls++;
@@ -350,6 +380,8 @@ __global__ void fgm_post_eval_kernel(MinState* S, const double* en, const int64_
 }
 
 __global__ void fgm_accept_kernel(MinState* S, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->f = S->res_f;
   S->theta_prev = S->theta;
   S->k++;
@@ -365,6 +397,8 @@ __global__ void fgm_accept_kernel(MinState* S, double* rec) {
 __global__ void fgm_shift_kernel(const MinState* S, int64_t n, double* __restrict__ x,
                                  double* __restrict__ x_prev, const double* __restrict__ w,
                                  const double* __restrict__ x_new, double* __restrict__ best) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   const int mode = S->fgm_mode, bs = S->best_src;
   if (mode == 0 && bs == 0) return;
@@ -381,6 +415,8 @@ __global__ void fgm_shift_kernel(const MinState* S, int64_t n, double* __restric
 // ---- fixed-step family (ffmin/optimizers/gradient.py): GD, heavy ball,
 // Nesterov (NAG, NAG-SC).  coef(k) and whether the gradient at w is needed
 __global__ void mom_pre_kernel(MinState* S, cudaGraphConditionalHandle heval, int has_eval) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int kind = S->c.momentum_kind;
   const double k = (double)S->k;
   S->beta = kind == 2 ? (k - 1.0) / (k + 2.0) : S->c.momentum;
@@ -391,6 +427,8 @@ __global__ void mom_pre_kernel(MinState* S, cudaGraphConditionalHandle heval, in
 
 // after grad f(w) (Nesterov schemes, k > 0): oracle.gradient(w)
 __global__ void mom_wcheck_kernel(MinState* S, const int64_t* stw) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->gcalls++;
   if (bad_status(stw, true)) set_err(S, kMinErrEval, stw, true);
 }
@@ -398,6 +436,8 @@ __global__ void mom_wcheck_kernel(MinState* S, const int64_t* stw) {
 // after f (and grad f) at x+ and <g, g>: call counts, error / divergence
 // tests, record, convergence
 __global__ void mom_post_kernel(MinState* S, const double* en, const int64_t* stw, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   const int kind = S->c.momentum_kind;
   const bool wform = kind >= 2;
@@ -429,6 +469,8 @@ __global__ void mom_post_kernel(MinState* S, const double* en, const int64_t* st
 // the schedule coefficients of iteration k (host arithmetic: 1.0 - 1.0 / t,
 // 2.0 / t, 1.0 / t)
 __global__ void ofgm_pre_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double tk = S->c.sched[S->k], tk1 = S->c.sched[S->k + 1];
   S->oc[0] = tk;
   S->oc[1] = 1.0 - 1.0 / tk1;
@@ -443,6 +485,8 @@ __global__ void ofgm_pre_kernel(MinState* S) {
 // search along -d / |d| from y (hnz)
 __global__ void ofgm_dir_kernel(MinState* S, cudaGraphConditionalHandle hz,
                                 cudaGraphConditionalHandle hnz) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double dn = sqrt(S->dd);
   S->dn = dn;
   if (dn == 0.0) {
@@ -459,6 +503,8 @@ __global__ void ofgm_dir_kernel(MinState* S, cudaGraphConditionalHandle hz,
 // after an energy-only evaluation: value(y) (which = 0: f_y, seeds the
 // search) or value(x) with x = y (which = 1: f)
 __global__ void ofgm_value_kernel(MinState* S, const double* en, const int64_t* stw, int which) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   S->vcalls++;
   if (bad_status(stw, false)) {
@@ -471,6 +517,8 @@ __global__ void ofgm_value_kernel(MinState* S, const double* en, const int64_t* 
 
 // after a gradient evaluation (gradient(y) for the slope, gradient(x))
 __global__ void ofgm_gcheck_kernel(MinState* S, const int64_t* stw) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   S->gcalls++;
   if (bad_status(stw, true)) set_err(S, kMinErrEval, stw, true);
@@ -478,6 +526,8 @@ __global__ void ofgm_gcheck_kernel(MinState* S, const int64_t* stw) {
 
 // the search result: x = lincomb(1, y, h, r) when found, else x = y with f_y
 __global__ void ofgm_ls_post_kernel(MinState* S) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   if (S->found) {
     S->step = S->res_h;
@@ -490,6 +540,8 @@ __global__ void ofgm_ls_post_kernel(MinState* S) {
 
 __global__ void ofgm_x_kernel(const MinState* S, int64_t n, const double* __restrict__ y,
                               const double* __restrict__ r, double* __restrict__ x, int from_ls) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   const bool move = from_ls && S->found;
   const double h = S->res_h;
@@ -502,6 +554,8 @@ __global__ void ofgm_x_kernel(const MinState* S, int64_t n, const double* __rest
 // variant's value_and_gradient(x) supplies f and both call counts)
 __global__ void ofgm_post_kernel(MinState* S, const double* en, const int64_t* stw, double* rec,
                                  int from_en) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   if (from_en) {
     S->vcalls++;
@@ -543,6 +597,8 @@ __device__ inline double wig_value(const double* o, const int64_t* st, bool lin)
 // the iteration's atom and its six axis probes (+-h along x, y, z)
 __global__ void wig_prep_kernel(MinState* S, const double* __restrict__ coords,
                                 int* __restrict__ atoms6, double* __restrict__ newpos6) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int a = S->c.wig_atoms[S->iters_launch - 1];
   S->wig_atom = a;
   const double h = S->c.wig_h;
@@ -560,6 +616,8 @@ __global__ void wig_prep_kernel(MinState* S, const double* __restrict__ coords,
 __global__ void wig_ctrl1_kernel(MinState* S, const double* __restrict__ out,
                                  const int64_t* __restrict__ st, int* __restrict__ atoms1,
                                  cudaGraphConditionalHandle hv) {
+  pdl_wait();
+  pdl_launch_dependents();
   const bool lin = S->c.wig_cutoff > 0.0;
   const int w = lin ? 6 : 5;
   const double h = S->c.wig_h;
@@ -607,6 +665,8 @@ __global__ void wig_ctrl1_kernel(MinState* S, const double* __restrict__ out,
 // newpos1 = coords[atom] + (vertex | delta)  (which = 0: vertex, 1: delta)
 __global__ void wig_pos_kernel(const MinState* S, const double* __restrict__ coords,
                                double* __restrict__ newpos1, int which) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int a = S->wig_atom;
   const double* d = which ? S->wig_delta : S->wig_vertex;
   for (int c = 0; c < 3; ++c) newpos1[c] = coords[3 * a + c] + d[c];
@@ -614,6 +674,8 @@ __global__ void wig_pos_kernel(const MinState* S, const double* __restrict__ coo
 
 __global__ void wig_ctrl_v_kernel(MinState* S, const double* __restrict__ out,
                                   const int64_t* __restrict__ st) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->wig_dv = wig_value(out, st, S->c.wig_cutoff > 0.0);
   S->vcalls++;
 }
@@ -622,6 +684,8 @@ __global__ void wig_ctrl_v_kernel(MinState* S, const double* __restrict__ out,
 // vertex; first minimum as min(..., key=...)); a clear decrease is checked
 // exactly next (hx)
 __global__ void wig_ctrl2_kernel(MinState* S, cudaGraphConditionalHandle hx) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double h = S->c.wig_h;
   int best = -1;
   double bv = 0.0;
@@ -644,6 +708,8 @@ __global__ void wig_ctrl2_kernel(MinState* S, cudaGraphConditionalHandle hx) {
 // the exact change decides: coords[atom] += delta, e += exact
 __global__ void wig_ctrl3_kernel(MinState* S, const double* __restrict__ out,
                                  const int64_t* __restrict__ st, double* __restrict__ coords) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double exact = wig_value(out, st, false);
   if (isfinite(exact)) S->vcalls++;
   if (exact < -kWigAcceptMargin) {
@@ -656,12 +722,16 @@ __global__ void wig_ctrl3_kernel(MinState* S, const double* __restrict__ out,
 
 // end of an iteration: k, the epoch re-evaluation (he), then the record
 __global__ void wig_end_kernel(MinState* S, cudaGraphConditionalHandle he) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->k++;
   const bool epoch = S->c.wig_cutoff > 0.0 && S->k % S->c.wig_epoch == 0;
   cudaGraphSetConditional(he, epoch ? 1u : 0u);
 }
 
 __global__ void wig_epoch_kernel(MinState* S, const double* en, const int64_t* stw) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (bad_status(stw, false)) {
     set_err(S, kMinErrEval, stw, false);
     return;
@@ -673,6 +743,8 @@ __global__ void wig_epoch_kernel(MinState* S, const double* en, const int64_t* s
 // record (k, e, -, step, calls, -, t, best): the move's components ride in
 // columns 2, 3, 5 (NaN in 2 when nothing moved); the host takes the norm
 __global__ void wig_record_kernel(MinState* S, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   if (S->f < S->best_f) S->best_f = S->f;
   double* r = rec + S->nrec * kMinRecWidth;
@@ -689,6 +761,8 @@ __global__ void wig_record_kernel(MinState* S, double* rec) {
 }
 
 __global__ void min_iter_end_kernel(MinState* S, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
   if (S->err) return;
   S->f = S->res_f;
   S->gn = sqrt(S->gg);
@@ -702,6 +776,8 @@ __global__ void min_iter_end_kernel(MinState* S, double* rec) {
 }
 
 __global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) {
+  pdl_wait();
+  pdl_launch_dependents();
   S->fgm_mode = 0;  // consumed by fgm_shift_kernel
   S->best_src = 0;
   cudaGraphSetConditional(hout, (!S->done && !S->pause) ? 1u : 0u);
@@ -712,7 +788,7 @@ __global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) 
 #define FFM_ONE(kern, ...)                   \
   do {                                       \
     count_launch();                          \
-    kern<<<1, 1, 0, st>>>(__VA_ARGS__);      \
+    launch_k(kern, 1, 1, 0, st, __VA_ARGS__);      \
     return cudaGetLastError();               \
   } while (0)
 
@@ -831,28 +907,28 @@ static int vec_blocks(int64_t n) {
 cudaError_t launch_cg_update(MinState* S, int64_t n, const double* g_new, double* p,
                              cudaStream_t st) {
   count_launch();
-  cg_update_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, g_new, p);
+  launch_k(cg_update_kernel, vec_blocks(n), 256, 0, st, S, n, g_new, p);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ofgm_x(MinState* S, int64_t n, const double* y, const double* r, double* x,
                           int from_ls, cudaStream_t st) {
   count_launch();
-  ofgm_x_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, y, r, x, from_ls);
+  launch_k(ofgm_x_kernel, vec_blocks(n), 256, 0, st, S, n, y, r, x, from_ls);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fgm_shift(MinState* S, int64_t n, double* x, double* x_prev, const double* w,
                              const double* x_new, double* best, cudaStream_t st) {
   count_launch();
-  fgm_shift_kernel<<<vec_blocks(n), 256, 0, st>>>(S, n, x, x_prev, w, x_new, best);
+  launch_k(fgm_shift_kernel, vec_blocks(n), 256, 0, st, S, n, x, x_prev, w, x_new, best);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_neg(MinState* S, int64_t n, const double* src, double* dst,
                               cudaStream_t st) {
   count_launch();
-  select_neg_kernel<<<vec_blocks(n), 256, 0, st>>>(&S->cg_reset, &S->err, n, src, dst);
+  launch_k(select_neg_kernel, vec_blocks(n), 256, 0, st, &S->cg_reset, &S->err, n, src, dst);
   return cudaGetLastError();
 }
 
@@ -863,7 +939,7 @@ cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const 
   if (blocks > 1184) blocks = 1184;
   if (blocks < 1) blocks = 1;
   count_launch();
-  min_store_kernel<<<(int)blocks, 256, 0, st>>>(S, n, s_tmp, y_tmp, ring_s, ring_y, x_new, g_new,
+  launch_k(min_store_kernel, (int)blocks, 256, 0, st, S, n, s_tmp, y_tmp, ring_s, ring_y, x_new, g_new,
                                                 x, g);
   return cudaGetLastError();
 }

@@ -82,6 +82,8 @@ __device__ __forceinline__ void box_union_warp(const T* __restrict__ bbox, int f
 template <typename T>
 __global__ void bbox_kernel(int n, int np, int batch, const typename Vec4T<T>::type* __restrict__ pos,
                             T* __restrict__ bbox) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int nbox = np / kJB;
@@ -116,10 +118,10 @@ cudaError_t launch_bbox(int n, int np, int batch, bool fp64, const void* pos, vo
   const int blocks = (int)((threads + 255) / 256);
   count_launch();
   if (fp64)
-    bbox_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<const double4*>(pos),
+    launch_k(bbox_kernel<double>, blocks, 256, 0, st, n, np, batch, static_cast<const double4*>(pos),
                                                 static_cast<double*>(bbox));
   else
-    bbox_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<const float4*>(pos),
+    launch_k(bbox_kernel<float>, blocks, 256, 0, st, n, np, batch, static_cast<const float4*>(pos),
                                                static_cast<float*>(bbox));
   return cudaGetLastError();
 }
@@ -189,6 +191,8 @@ nb_units_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, const T* __restrict__ bbox,
                 T* __restrict__ ipart, T* __restrict__ jpart, double* __restrict__ epart) {
+  pdl_wait();  // (no early pdl_launch_dependents: the dependents' waiting CTAs
+               // measured 2% slower at 10k atoms than launching at completion)
   using P = Pk<T>;
   using V = typename P::V;
   using V4 = typename Vec4T<T>::type;
@@ -401,6 +405,8 @@ nb_tiles_kernel(NbPlanDev plan, const typename Vec4T<T>::type* __restrict__ pos,
                 const typename Vec2T<T>::type* __restrict__ lj, const T* __restrict__ ipos,
                 const T* __restrict__ ilj, T* __restrict__ ipart, T* __restrict__ jpart,
                 double* __restrict__ epart) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ TileSmem<T> sm;
   tile_cta<T, GRAD, CUTOFF>(plan, pos, lj, ipos, ilj, ipart, jpart, epart, blockIdx.x, blockIdx.y,
                             sm);
@@ -413,7 +419,7 @@ static cudaError_t launch_tiles_t(const NbPlanDev& plan, const void* pos, const 
   if (plan.nlaunch == 0) return cudaSuccess;
   dim3 grid(plan.nlaunch, batch);  // one CTA per tile
   count_launch();
-  nb_tiles_kernel<T, GRAD, CUTOFF><<<grid, kTileWarps * 32, 0, st>>>(
+  launch_k(nb_tiles_kernel<T, GRAD, CUTOFF>, grid, kTileWarps * 32, 0, st, 
       plan, static_cast<const typename Vec4T<T>::type*>(pos),
       static_cast<const typename Vec2T<T>::type*>(lj), static_cast<const T*>(ipos),
       static_cast<const T*>(ilj), static_cast<T*>(ipart), static_cast<T*>(jpart), epart);
@@ -447,7 +453,7 @@ static cudaError_t launch_nb_w(const NbPlanDev& plan, const void* pos, const voi
   }
   if (plan.nlaunch == 0) return cudaSuccess;
   dim3 grid(plan.nlaunch, batch);
-  count_launch(), k<<<grid, NW * 32, smem, st>>>(plan, static_cast<const typename Vec4T<T>::type*>(pos),
+  count_launch(), launch_k(k, grid, NW * 32, smem, st, plan, static_cast<const typename Vec4T<T>::type*>(pos),
                                   static_cast<const typename Vec2T<T>::type*>(lj),
                                   static_cast<const T*>(ipos), static_cast<const T*>(ilj),
                                   static_cast<const T*>(bbox), static_cast<T*>(ipart),

@@ -14,6 +14,8 @@ __global__ void pack_kernel(int n, int np, int batch, const double* __restrict__
                             const double* __restrict__ qt,
                             typename Vec4T<T>::type* __restrict__ pos, T* __restrict__ ipos,
                             int64_t* __restrict__ status) {
+  pdl_wait();
+  pdl_launch_dependents();
   pack_item<T>((int64_t)blockIdx.x * blockDim.x + threadIdx.x, n, np, batch, coords, qt, pos,
                ipos, status);
 }
@@ -21,6 +23,8 @@ __global__ void pack_kernel(int n, int np, int batch, const double* __restrict__
 template <typename T>
 __global__ void pad_kernel(int n, int np, int batch, typename Vec4T<T>::type* __restrict__ pos,
                            T* __restrict__ ipos) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int npad = np - n;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= (int64_t)npad * batch) return;
@@ -36,11 +40,11 @@ cudaError_t launch_pack(int n, int np, int batch, bool fp64, const double* coord
   const int64_t tot = (int64_t)n * batch > batch ? (int64_t)n * batch : batch;
   const int blocks = (int)((tot + 255) / 256);
   if (fp64)
-    count_launch(), pack_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+    count_launch(), launch_k(pack_kernel<double>, blocks, 256, 0, st, n, np, batch, coords, qt,
                                                 static_cast<double4*>(pos),
                                                 static_cast<double*>(ipos), status);
   else
-    count_launch(), pack_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, coords, qt,
+    count_launch(), launch_k(pack_kernel<float>, blocks, 256, 0, st, n, np, batch, coords, qt,
                                                static_cast<float4*>(pos),
                                                static_cast<float*>(ipos), status);
   return cudaGetLastError();
@@ -52,10 +56,10 @@ cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipo
   if (tot <= 0) return cudaSuccess;
   const int blocks = (int)((tot + 255) / 256);
   if (fp64)
-    count_launch(), pad_kernel<double><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<double4*>(pos),
+    count_launch(), launch_k(pad_kernel<double>, blocks, 256, 0, st, n, np, batch, static_cast<double4*>(pos),
                                                static_cast<double*>(ipos));
   else
-    count_launch(), pad_kernel<float><<<blocks, 256, 0, st>>>(n, np, batch, static_cast<float4*>(pos),
+    count_launch(), launch_k(pad_kernel<float>, blocks, 256, 0, st, n, np, batch, static_cast<float4*>(pos),
                                               static_cast<float*>(ipos));
   return cudaGetLastError();
 }
@@ -64,6 +68,8 @@ cudaError_t launch_pad(int n, int np, int batch, bool fp64, void* pos, void* ipo
 // records and scaled by LjIScale<T> (see ffm_common.cuh)
 template <typename T>
 __global__ void ilj_kernel(int np, const double2* __restrict__ lj64, T* __restrict__ ilj) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= np) return;
   ilj[ipos_index(a, np, 0)] = T(LjIScale<T>::value * lj64[a].x);
@@ -74,9 +80,9 @@ cudaError_t launch_ilj(int np, bool fp64, const void* lj64, void* ilj, cudaStrea
   const int blocks = (np + 255) / 256;
   const double2* src = static_cast<const double2*>(lj64);
   if (fp64)
-    count_launch(), ilj_kernel<double><<<blocks, 256, 0, st>>>(np, src, static_cast<double*>(ilj));
+    count_launch(), launch_k(ilj_kernel<double>, blocks, 256, 0, st, np, src, static_cast<double*>(ilj));
   else
-    count_launch(), ilj_kernel<float><<<blocks, 256, 0, st>>>(np, src, static_cast<float*>(ilj));
+    count_launch(), launch_k(ilj_kernel<float>, blocks, 256, 0, st, np, src, static_cast<float*>(ilj));
   return cudaGetLastError();
 }
 
@@ -85,6 +91,8 @@ __global__ void __launch_bounds__(kTermThreads)
 terms_kernel(TermPlanDev tp, bool grad, const double* __restrict__ coords,
              double* __restrict__ term_part, double* __restrict__ term_f,
              int64_t* __restrict__ status) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[5][kTermThreads / 32];
   term_block(tp, grad, coords, term_part, term_f, status, blockIdx.y, blockIdx.x, gridDim.x, sh);
 }
@@ -100,7 +108,7 @@ cudaError_t launch_terms(const TermPlanDev& tp, bool grad, int batch, const doub
   if (nblk == 0) return cudaSuccess;
   dim3 grid(nblk, batch);
   count_launch();
-  terms_kernel<<<grid, kTermThreads, 0, st>>>(tp, grad, coords, term_part, term_f, status);
+  launch_k(terms_kernel, grid, kTermThreads, 0, st, tp, grad, coords, term_part, term_f, status);
   return cudaGetLastError();
 }
 
@@ -122,6 +130,8 @@ gather_reduce_kernel(int n, int S, int nb, const int* __restrict__ unit_index,
                      const double* __restrict__ epart, const double* __restrict__ term_part,
                      double* __restrict__ energies, int64_t* __restrict__ status, int rank,
                      int nranks, double* __restrict__ escratch, unsigned* ecount, int nparts) {
+  pdl_wait();
+  pdl_launch_dependents();
   // 128-atom spans (gather_span128, super-unit mode, large systems) or
   // 32-atom groups (gather_group: more blocks in flight for smaller ones)
   constexpr int kSpan = SPAN;
@@ -164,17 +174,17 @@ static cudaError_t launch_gr_t(int n, int S, int nb, const int* unit_index, cons
   const T* jp = static_cast<const T*>(jpart);
   count_launch();
   if (span)
-    gather_reduce_kernel<T, kGatherWarpsUnits, 128><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
+    launch_k(gather_reduce_kernel<T, kGatherWarpsUnits, 128>, blocks, kGatherWarpsUnits * 32, 0, st, 
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
         energies, status, rank, nranks, escratch, ecount, nparts);
   else if (trow_ptr)
-    gather_reduce_kernel<T, kGatherWarpsTiles, 32><<<blocks, kGatherWarpsTiles * 32, 0, st>>>(
+    launch_k(gather_reduce_kernel<T, kGatherWarpsTiles, 32>, blocks, kGatherWarpsTiles * 32, 0, st, 
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
         energies, status, rank, nranks, escratch, ecount, nparts);
   else
-    gather_reduce_kernel<T, kGatherWarpsUnits, 32><<<blocks, kGatherWarpsUnits * 32, 0, st>>>(
+    launch_k(gather_reduce_kernel<T, kGatherWarpsUnits, 32>, blocks, kGatherWarpsUnits * 32, 0, st, 
         n, S, nb, unit_index, trow_ptr, tcol_ptr, tcol_idx, ip, jp, slot_ptr, slot_idx, term_f,
         slot_sc0, use_nb, use_terms, use_sc, grad, nslots, nterm_blocks, epart, term_part,
         energies, status, rank, nranks, escratch, ecount, nparts);
@@ -206,6 +216,8 @@ __global__ void __launch_bounds__(kRedThreads)
 reduce_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
               const double* __restrict__ term_part, double* __restrict__ energies,
               int64_t* __restrict__ status, int n) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[32];
   reduce_entry(nunits, nterm_blocks, epart, term_part, energies, status, blockIdx.x, sh, true,
                n);
@@ -215,6 +227,8 @@ __global__ void __launch_bounds__(kRedThreads)
 reduce_split_kernel(int nunits, int nterm_blocks, const double* __restrict__ epart,
                     const double* __restrict__ term_part, double* __restrict__ energies,
                     int64_t* __restrict__ status, int n, double* escratch, unsigned* ecount) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[32];
   reduce_split(nunits, nterm_blocks, epart, term_part, energies, status, sh, escratch, ecount,
                blockIdx.x, gridDim.x, n);
@@ -230,10 +244,10 @@ cudaError_t launch_reduce(int nunits, const TermPlanDev& tp, int batch, const do
                           double* escratch, unsigned* ecount, cudaStream_t st) {
   count_launch();
   if (batch == 1 && escratch && energy_parts(nunits) > 1)
-    reduce_split_kernel<<<energy_parts(nunits), kRedThreads, 0, st>>>(
+    launch_k(reduce_split_kernel, energy_parts(nunits), kRedThreads, 0, st, 
         nunits, term_blocks(tp), epart, term_part, energies, status, n, escratch, ecount);
   else
-    reduce_kernel<<<batch, kRedThreads, 0, st>>>(nunits, term_blocks(tp), epart, term_part,
+    launch_k(reduce_kernel, batch, kRedThreads, 0, st, nunits, term_blocks(tp), epart, term_part,
                                                   energies, status, n);
   return cudaGetLastError();
 }
@@ -243,6 +257,8 @@ template <typename T>
 __global__ void finder_kernel(int n, int np, const typename Vec4T<T>::type* __restrict__ pos,
                               const int* __restrict__ sp_ptr, const int* __restrict__ sp_j,
                               const double* __restrict__ sp_s, int64_t* __restrict__ status) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int b = blockIdx.y;
   int64_t* s = status + (size_t)b * kStWords;
   // clean entries were finalised by the reduction (reduce_entry)
@@ -269,10 +285,10 @@ cudaError_t launch_finder(int n, int np, int batch, bool fp64, const void* pos,
   dim3 grid((n + 127) / 128, batch);
   if (n == 0) return cudaSuccess;  // nothing to find; the reduction finalised
   if (fp64)
-    count_launch(), finder_kernel<double><<<grid, 128, 0, st>>>(n, np, static_cast<const double4*>(pos),
+    count_launch(), launch_k(finder_kernel<double>, grid, 128, 0, st, n, np, static_cast<const double4*>(pos),
                                                 sp_ptr, sp_j, sp_s, status);
   else
-    count_launch(), finder_kernel<float><<<grid, 128, 0, st>>>(n, np, static_cast<const float4*>(pos), sp_ptr,
+    count_launch(), launch_k(finder_kernel<float>, grid, 128, 0, st, n, np, static_cast<const float4*>(pos), sp_ptr,
                                                sp_j, sp_s, status);
   return cudaGetLastError();
 }
@@ -293,6 +309,8 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
                   const int* __restrict__ aterm_idx, const int* __restrict__ atoms,
                   const double* __restrict__ newpos, double lin_cutoff,
                   double* __restrict__ out, int64_t* __restrict__ status) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[32];
   __shared__ long long bad[3];
   const int k = blockIdx.x;
@@ -441,7 +459,7 @@ cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* atoms, const double* newpos, double lin_cutoff,
                               double* out, int64_t* status, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
-  count_launch(), atom_delta_kernel<<<ncand, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s,
+  count_launch(), launch_k(atom_delta_kernel, ncand, kDeltaThreads, 0, st, tp, coords, fsp_ptr, fsp_j, fsp_s,
                                                      aterm_ptr, aterm_idx, atoms, newpos, lin_cutoff,
                                                      out, status);
   return cudaGetLastError();
@@ -455,6 +473,8 @@ farfield_kernel(TermPlanDev tp, const double* __restrict__ coords,
                 const double* __restrict__ fsp_s, int a, double cutoff,
                 double* __restrict__ e0_coef, uint8_t* __restrict__ near_mask,
                 int64_t* __restrict__ bad) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[32];
   __shared__ long long first_bad;
   if (threadIdx.x == 0) first_bad = kSentinel;
@@ -507,7 +527,7 @@ cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const i
                             double* e0_coef, uint8_t* near_mask, int64_t* bad,
                             cudaStream_t st) {
   count_launch();
-  farfield_kernel<<<1, kDeltaThreads, 0, st>>>(tp, coords, fsp_ptr, fsp_j, fsp_s, atom, cutoff,
+  launch_k(farfield_kernel, 1, kDeltaThreads, 0, st, tp, coords, fsp_ptr, fsp_j, fsp_s, atom, cutoff,
                                                e0_coef, near_mask, bad);
   return cudaGetLastError();
 }

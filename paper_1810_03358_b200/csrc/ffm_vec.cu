@@ -35,6 +35,8 @@ __device__ __forceinline__ double block_sum256(double v, double* sh) {
 __global__ void __launch_bounds__(kVecThreads)
 dot_partial_kernel(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
                    double* __restrict__ part) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[kVecThreads / 32];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * kVecThreads + threadIdx.x; i < n;
@@ -46,6 +48,8 @@ dot_partial_kernel(int64_t n, const double* __restrict__ x, const double* __rest
 
 __global__ void __launch_bounds__(kVecThreads)
 dot_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[kVecThreads / 32];
   double acc = 0.0;
   for (int i = threadIdx.x; i < kVecBlocks; i += kVecThreads) acc += part[i];
@@ -55,8 +59,8 @@ dot_final_kernel(const double* __restrict__ part, double* __restrict__ out) {
 
 cudaError_t launch_dot(int64_t n, const double* x, const double* y, double* part,
                        double* out, cudaStream_t st) {
-  count_launch(); dot_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, x, y, part);
-  count_launch(); dot_final_kernel<<<1, kVecThreads, 0, st>>>(part, out);
+  count_launch(); launch_k(dot_partial_kernel, kVecBlocks, kVecThreads, 0, st, n, x, y, part);
+  count_launch(); launch_k(dot_final_kernel, 1, kVecThreads, 0, st, part, out);
   return cudaGetLastError();
 }
 
@@ -70,6 +74,8 @@ struct DotArgs {
 
 __global__ void __launch_bounds__(kVecThreads)
 dots_partial_kernel(int64_t n, DotArgs A, double* __restrict__ part) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[kVecThreads / 32];
   for (int q = 0; q < A.k; ++q) {
     double acc = 0.0;
@@ -85,6 +91,8 @@ dots_partial_kernel(int64_t n, DotArgs A, double* __restrict__ part) {
 
 __global__ void __launch_bounds__(kVecThreads)
 dots_final_kernel(int k, const double* __restrict__ part, double* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
   __shared__ double sh[kVecThreads / 32];
   for (int q = 0; q < k; ++q) {
     double acc = 0.0;
@@ -104,9 +112,9 @@ cudaError_t launch_dots(int64_t n, int k, const double* const* x, const double* 
     A.y[q] = y[q];
   }
   count_launch();
-  dots_partial_kernel<<<kVecBlocks, kVecThreads, 0, st>>>(n, A, part);
+  launch_k(dots_partial_kernel, kVecBlocks, kVecThreads, 0, st, n, A, part);
   count_launch();
-  dots_final_kernel<<<1, kVecThreads, 0, st>>>(k, part, out);
+  launch_k(dots_final_kernel, 1, kVecThreads, 0, st, k, part, out);
   return cudaGetLastError();
 }
 
@@ -116,6 +124,8 @@ __global__ void axpby_kernel(int64_t n, const double* __restrict__ a_dev, double
                              double sa, const double* __restrict__ x,
                              const double* __restrict__ b_dev, double b_host,
                              const double* __restrict__ y, double* __restrict__ z) {
+  pdl_wait();
+  pdl_launch_dependents();
   const double a = a_dev ? *a_dev : a_host;
   const double b = b_dev ? *b_dev : b_host;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -132,7 +142,7 @@ cudaError_t launch_axpby(int64_t n, const double* a_dev, double a_host, double s
   int64_t blocks = (n + 255) / 256;
   if (blocks > 4 * kVecBlocks) blocks = 4 * kVecBlocks;
   if (blocks < 1) blocks = 1;
-  count_launch(); axpby_kernel<<<(int)blocks, 256, 0, st>>>(n, a_dev, a_host, sa, x, b_dev, b_host, y, z);
+  count_launch(); launch_k(axpby_kernel, (int)blocks, 256, 0, st, n, a_dev, a_host, sa, x, b_dev, b_host, y, z);
   return cudaGetLastError();
 }
 
@@ -358,6 +368,8 @@ namespace ffm {
 __global__ void combine_encode_kernel(int64_t n3, int64_t natoms, const double* __restrict__ grad,
                                       const double* __restrict__ energies,
                                       const int64_t* __restrict__ status, double* __restrict__ buf) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (grad)
     for (int64_t i = i0; i < n3; i += (int64_t)gridDim.x * blockDim.x) buf[i] = grad[i];
@@ -378,6 +390,8 @@ __global__ void combine_encode_kernel(int64_t n3, int64_t natoms, const double* 
 __global__ void combine_decode_kernel(int64_t n3, int64_t natoms, const double* __restrict__ buf,
                                       double* __restrict__ grad, double* __restrict__ energies,
                                       int64_t* __restrict__ status) {
+  pdl_wait();
+  pdl_launch_dependents();
   const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (grad)
     for (int64_t i = i0; i < n3; i += (int64_t)gridDim.x * blockDim.x) grad[i] = buf[i];
@@ -406,7 +420,7 @@ static int comb_blocks(int64_t n3) {
 cudaError_t launch_combine_encode(int64_t natoms, const double* grad, const double* energies,
                                   const int64_t* status, double* buf, cudaStream_t st) {
   count_launch();
-  combine_encode_kernel<<<grad ? comb_blocks(3 * natoms) : 1, 256, 0, st>>>(
+  launch_k(combine_encode_kernel, grad ? comb_blocks(3 * natoms) : 1, 256, 0, st, 
       3 * natoms, natoms, grad, energies, status, buf);
   return cudaGetLastError();
 }
@@ -414,7 +428,7 @@ cudaError_t launch_combine_encode(int64_t natoms, const double* grad, const doub
 cudaError_t launch_combine_decode(int64_t natoms, const double* buf, double* grad,
                                   double* energies, int64_t* status, cudaStream_t st) {
   count_launch();
-  combine_decode_kernel<<<grad ? comb_blocks(3 * natoms) : 1, 256, 0, st>>>(
+  launch_k(combine_decode_kernel, grad ? comb_blocks(3 * natoms) : 1, 256, 0, st, 
       3 * natoms, natoms, buf, grad, energies, status);
   return cudaGetLastError();
 }
