@@ -26,6 +26,9 @@ constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/S
 #ifndef FFM_RCP
 #define FFM_RCP 1  // FP32 r^-2 from MUFU.RCP instead of an FMA-pipe multiply
 #endif
+#ifndef FFM_EFACTOR
+#define FFM_EFACTOR 1  // energy-only tiles: i-side parameters factored out (warp_tile_energy)
+#endif
 
 template <typename T>
 __device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
@@ -66,6 +69,96 @@ template <typename T> struct PairsPerPass { static constexpr int value = 2; };
 #endif
 template <> struct PairsPerPass<double> { static constexpr int value = FFM_NP64; };
 
+// Energy-only 128 x 32 tile (line-search probes, batched candidates,
+// energy_total): the i-side parameters are factored out of the pair sums,
+//   E_coul(i) = q~_i sum_j q~_j / r,   s E_lj(i) = s a_i sum_j a_j / r^12 - s b_i sum_j b_j / r^6,
+// so a pair costs the geometry, r^-1 (MUFU.RSQ), r^-2 = (r^-1)^2, r^-6,
+// r^-12 and three accumulations with broadcast j operands: 13 FMA-pipe
+// lane-ops and one MUFU instead of 15 and two, without the per-pair
+// coefficient products (100k FP32 2.46 -> 2.19 ms, FP64 6.98 -> 6.47 ms;
+// profiles/r02_energy_factor_ab.log).  Inactive pairs (mask, cutoff) get
+// r^-1 = r^-2 = 0.  The three per-i-atom sums are folded into ec2 / ev2 at
+// the end of the tile.
+#ifndef FFM_ERCP
+#define FFM_ERCP 0  // FP32 energy-only r^-2 via MUFU.RCP: 0 none (measured best), 1 all, 2 first pair
+#endif
+template <typename T, bool CUTOFF, bool MASKED, int NP, bool DOUBLED, int UNR, int NSTEP>
+__device__ __forceinline__ void warp_tile_energy(
+    const typename Vec4T<T>::type* __restrict__ J,
+    const typename Vec2T<T>::type* __restrict__ L, int lane,
+    const typename Pk<T>::V (&xi)[NP], const typename Pk<T>::V (&yi)[NP],
+    const typename Pk<T>::V (&zi)[NP], const typename Pk<T>::V (&qi)[NP],
+    const typename Pk<T>::V (&ai)[NP], const typename Pk<T>::V (&bi)[NP],
+    typename Pk<T>::V& ec2, typename Pk<T>::V& ev2, const uint32_t (&mk)[2 * NP], T cut2,
+    T& minr2, int t0) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  constexpr bool f32 = sizeof(T) == 4;
+  V sc[NP], sa[NP], sb[NP];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) sc[pp] = sa[pp] = sb[pp] = P::zero();
+  if (DOUBLED) {
+    J += lane + t0;
+    L += lane + t0;
+  }
+#pragma unroll(UNR ? UNR : sizeof(T) == 8 ? (kStepUnroll64 ? kStepUnroll64 : 8) : kStepUnroll)
+  for (int ts = 0; ts < NSTEP; ++ts) {
+    const int t = t0 + ts;
+    const int jt = DOUBLED ? ts : ((lane + t) & 31);
+    const auto pj = J[jt];  // (-x, -y, -z, q~) of atom (lane + t) mod 32
+    const auto lj = L[jt];  // (a, -b)
+    V r2[NP], ri[NP], i2[NP];
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const V dx = P::add(xi[pp], P::bc(pj.x));
+      const V dy = P::add(yi[pp], P::bc(pj.y));
+      const V dz = P::add(zi[pp], P::bc(pj.z));
+      r2[pp] = P::mul(dx, dx);
+      r2[pp] = P::fma(dy, dy, r2[pp]);
+      r2[pp] = P::fma(dz, dz, r2[pp]);
+    }
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      bool a0 = true, a1 = true;
+      if (MASKED) {
+        const int jj = (lane + t) & 31;
+        a0 = (mk[2 * pp] >> jj) & 1u;
+        a1 = (mk[2 * pp + 1] >> jj) & 1u;
+        r2[pp] = P::make(a0 ? P::lo(r2[pp]) : T(1), a1 ? P::hi(r2[pp]) : T(1));
+      }
+      if constexpr (sizeof(T) == 8) minr2 = fmin(minr2, fmin(P::lo(r2[pp]), P::hi(r2[pp])));
+      if (CUTOFF) {
+        a0 = a0 && P::lo(r2[pp]) <= cut2;
+        a1 = a1 && P::hi(r2[pp]) <= cut2;
+      }
+      ri[pp] = P::rsqrt(r2[pp]);
+      const bool rcp = f32 && (FFM_ERCP == 1 || (FFM_ERCP == 2 && pp == 0));
+      if (rcp) i2[pp] = P::rcp_or_sq(r2[pp], ri[pp]);
+      if (MASKED || CUTOFF) {
+        ri[pp] = P::make(a0 ? P::lo(ri[pp]) : T(0), a1 ? P::hi(ri[pp]) : T(0));
+        if (rcp) i2[pp] = P::make(a0 ? P::lo(i2[pp]) : T(0), a1 ? P::hi(i2[pp]) : T(0));
+      }
+    }
+#pragma unroll
+    for (int pp = 0; pp < NP; ++pp) {
+      const bool rcp = f32 && (FFM_ERCP == 1 || (FFM_ERCP == 2 && pp == 0));
+      if (!rcp) i2[pp] = P::mul(ri[pp], ri[pp]);
+      const V i4 = P::mul(i2[pp], i2[pp]);
+      const V i6 = P::mul(i4, i2[pp]);
+      const V i12 = P::mul(i6, i6);
+      sc[pp] = P::fma(P::bc(pj.w), ri[pp], sc[pp]);   // sum q~_j / r
+      sa[pp] = P::fma(P::bc(lj.x), i12, sa[pp]);      // sum a_j / r^12
+      sb[pp] = P::fma(P::bc(lj.y), i6, sb[pp]);       // -sum b_j / r^6
+    }
+  }
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    ec2 = P::fma(qi[pp], sc[pp], ec2);
+    ev2 = P::fma(ai[pp], sa[pp], ev2);
+    ev2 = P::fma(bi[pp], sb[pp], ev2);
+  }
+}
+
 // One 128 x 32 warp tile.  J/L point at the doubled 64-entry copy of the
 // j-block, so step t of lane l reads entry l + t (atom (l + t) mod 32) with
 // an immediate offset.  MASKED tiles carry per-lane activity bitmasks
@@ -89,6 +182,13 @@ __device__ __forceinline__ void warp_tile(
     const uint32_t (&mk)[2 * NP], T cut2, T& minr2, int t0 = 0) {
   using P = Pk<T>;
   using V = typename P::V;
+#if FFM_EFACTOR
+  if constexpr (!GRAD) {
+    warp_tile_energy<T, CUTOFF, MASKED, NP, DOUBLED, UNR, NSTEP>(
+        J, L, lane, xi, yi, zi, qi, ai, bi, ec2, ev2, mk, cut2, minr2, t0);
+    return;
+  }
+#endif
   V gx = P::zero(), gy = P::zero(), gz = P::zero();
   const int src = (lane + 1) & 31;
   if (DOUBLED) {  // j-block stored twice: entry lane + t is an immediate offset
