@@ -27,13 +27,17 @@ constexpr double kCoulomb = 1389.38757;
 constexpr double kRmin = 1e-12;
 constexpr double kDegenerateEps = 1e-12;
 
-// FP32 i-side LJ records (ilj) carry a factor 6: the FP32 pair kernel then
-// forms 6A/r^6 and 6B directly, so the gradient needs no separate scaling
-// multiply (12 A/r^12 - 6 B/r^6 = (6A/r^6 + 6(A/r^6 - B))/r^6), and the vdW
-// energy sum is divided by 6 once per super-unit.  FP64 keeps scale 1 (its
-// register-bound schedule measured faster with the explicit multiply).
+// The i-side LJ records (ilj) carry a factor 6: the pair kernel then forms
+// 6A/r^6 and 6B directly, so the gradient needs no separate scaling multiply
+// (12 A/r^12 - 6 B/r^6 = (6A/r^6 + 6(A/r^6 - B))/r^6), and the vdW energy
+// sum is divided by 6 once per super-unit.  (FP64 took it in round 2 with the
+// 4-warp CTAs: 100k energy+gradient 11.43 -> 11.25 ms; round 1's 8-warp FP64
+// kernel had measured the explicit multiply faster.)
+#ifndef FFM_F64SCALE
+#define FFM_F64SCALE 1  // FP64 i-side LJ scaled by 6 as well (w = fma(pw, r^-6, ecp))
+#endif
 template <typename T> struct LjIScale { static constexpr double value = 6.0; };
-template <> struct LjIScale<double> { static constexpr double value = 1.0; };
+template <> struct LjIScale<double> { static constexpr double value = FFM_F64SCALE ? 6.0 : 1.0; };
 
 // Pair-kernel tiling:
 //   a warp tile is 128 i-atoms (4 per lane, two packed pairs) x 32 j-atoms;

@@ -30,6 +30,22 @@ constexpr int kStepUnroll64 = FFM_UNROLL64;  // FP64 (register-bound at 2 CTAs/S
 #define FFM_EFACTOR 1  // energy-only tiles: i-side parameters factored out (warp_tile_energy)
 #endif
 
+// FP64 min r^2 of a tile (the close-contact flag that sends an evaluation
+// to the exact finder).  FFM_F64IMIN: tracked on the high words of the
+// non-negative doubles with integer min (ALU pipe, not the FP64 pipe); the
+// result (low word 0) is <= the true minimum, so the flag stays conservative.
+#ifndef FFM_F64IMIN
+#define FFM_F64IMIN 1  // (FP64 100k energy-only sweep 6.50 -> 5.67 ms: the fmin pair was on the FP64 pipe)
+#endif
+__device__ __forceinline__ double min_r2_track(double m, double a, double b) {
+#if FFM_F64IMIN
+  const int h = min(min(__double2hiint(a), __double2hiint(b)), __double2hiint(m));
+  return __hiloint2double(h, 0);
+#else
+  return fmin(m, fmin(a, b));
+#endif
+}
+
 template <typename T>
 __device__ __forceinline__ typename Pk<T>::V shfl_rot(typename Pk<T>::V v, int src);
 
@@ -126,7 +142,7 @@ __device__ __forceinline__ void warp_tile_energy(
         a1 = (mk[2 * pp + 1] >> jj) & 1u;
         r2[pp] = P::make(a0 ? P::lo(r2[pp]) : T(1), a1 ? P::hi(r2[pp]) : T(1));
       }
-      if constexpr (sizeof(T) == 8) minr2 = fmin(minr2, fmin(P::lo(r2[pp]), P::hi(r2[pp])));
+      if constexpr (sizeof(T) == 8) minr2 = min_r2_track(minr2, P::lo(r2[pp]), P::hi(r2[pp]));
       if (CUTOFF) {
         a0 = a0 && P::lo(r2[pp]) <= cut2;
         a1 = a1 && P::hi(r2[pp]) <= cut2;
@@ -227,7 +243,7 @@ __device__ __forceinline__ void warp_tile(
         nB[pp] = P::make(a0 ? P::lo(nB[pp]) : T(0), a1 ? P::hi(nB[pp]) : T(0));
         Q[pp] = P::make(a0 ? P::lo(Q[pp]) : T(0), a1 ? P::hi(Q[pp]) : T(0));
       }
-      if constexpr (sizeof(T) == 8) minr2 = fmin(minr2, fmin(P::lo(r2[pp]), P::hi(r2[pp])));
+      if constexpr (sizeof(T) == 8) minr2 = min_r2_track(minr2, P::lo(r2[pp]), P::hi(r2[pp]));
       if (CUTOFF) {
         const bool c0 = P::lo(r2[pp]) <= cut2;
         const bool c1 = P::hi(r2[pp]) <= cut2;
@@ -267,9 +283,9 @@ __device__ __forceinline__ void warp_tile(
       if (GRAD) {
         // g = -(dE/dr)/r = (C q q / r + 12 A / r^12 - 6 B / r^6) / r^2
         V w;
-        if constexpr (sizeof(T) == 4) {
+        if constexpr (sizeof(T) == 4 || FFM_F64SCALE) {
           w = P::fma(pw, i6, ecp);         // s = 6: no separate scaling multiply
-        } else {                           // FP64 (s = 1): measured faster this way
+        } else {                           // FP64 with FFM_F64SCALE = 0 (s = 1)
           const V k = P::mul(pw, i6);
           w = P::fma(k, P::bc(T(6)), ecp);
         }
