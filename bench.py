@@ -46,14 +46,14 @@ METRIC = "pair-interactions/sec (energy+grad)"
 NATOMS = 100_000
 FLOP_PER_PAIR = 38  # 27 FP32 ops (10 of them FMA -> +10) + 1 rsqrt, DESIGN.md
 FMA_SLOTS_PER_PAIR = 24  # FP32 lane-ops on the FMA pipe per pair (SASS: 2 x 12 packed FFMA2/FMUL2/FADD2 per 2 pairs; r^-2 on MUFU)
-FP64_OPS_PER_PAIR = 32  # FP64-pipe operations per pair (ncu: fp64 pipe 66.9% at 12.87 ms)
+FP64_OPS_PER_PAIR = 29  # FP64-pipe operations per pair (SASS of the unmasked tile: 29 DFMA/DMUL/DADD per pair)
 DFMA_PEAK = 18.49e12  # measured DFMA/s (63.6 per clk per SM, profiles/r01_pipes_microbench.txt)
 NOMINAL_FP32_FLOPS = 2 * 128 * 148 * 1965e6  # 128 FFMA lanes / clk / SM at the max SM clock
 # the tile loop alone (tools/microbench/pairmix.cu: the sweep's warp_tile on a
 # restaged shared-memory j-block at the sweep's occupancy, no global memory,
 # masks, staging or reductions), ncu pipe activity, profiles/r02_pipes_microbench.txt
-MIX_CEILING = {"fp32_fma_pipe_active": 0.788, "fp64_pipe_active": 0.745}
-SWEEP_NCU = {"fp32_fma_pipe_active": 0.756, "fp64_pipe_active": 0.746}  # r02 ncu, 100k
+MIX_CEILING = {"fp32_fma_pipe_active": 0.788, "fp64_pipe_active": 0.764}
+SWEEP_NCU = {"fp32_fma_pipe_active": 0.756, "fp64_pipe_active": 0.737}  # r02 ncu, 100k
 
 
 def parse():
