@@ -151,7 +151,7 @@ struct ffm_system {
   int* d_unit_list = nullptr;
   std::vector<char> unit_live;  // host: slot holds a real unit (build_units)
   // small-system tile mode (NbPlanDev::ntiles > 0)
-  int2* d_tiles = nullptr;
+  int4* d_tiles = nullptr;
   int* d_tile_list = nullptr;
   int* d_trow_ptr = nullptr;  // [np/128 + 1] tiles of each i-sub-block (contiguous)
   int* d_tcol_ptr = nullptr;  // [np/32 + 1] tiles of each j-block ...
@@ -510,17 +510,20 @@ bool use_tiles(const NbPlanDev& p, int device) {
   return p.nb * (p.nb + 1) / 2 < 150;  // whole units (before the last wave's split)
 }
 
-int build_tiles(ffm_system* s) {
+int build_tiles(ffm_system* s, const std::vector<int>& spt_ptr, const std::vector<int>& spt_m) {
   NbPlanDev& p = s->plan;
   const int nkk = p.np / kIB, nmg = p.np / kJB;
-  std::vector<int2> tiles;
+  std::vector<int4> tiles;
   std::vector<int> rptr(nkk + 1, 0);
   std::vector<std::vector<int>> col(nmg);
   for (int kk = 0; kk < nkk; ++kk) {
     for (int mg = 4 * kk; mg < nmg; ++mg) {
       if (kk * kIB >= p.n || mg * kJB >= p.n) continue;  // padding only
       col[mg].push_back((int)tiles.size());
-      tiles.push_back(make_int2(kk, mg));
+      int spe = -1;  // the tile's special-pair mask entry (ffm_plan.cuh)
+      for (int e = spt_ptr[kk]; e < spt_ptr[kk + 1]; ++e)
+        if (spt_m[e] == mg) spe = e;
+      tiles.push_back(make_int4(kk, mg, spe, 0));
     }
     rptr[kk + 1] = (int)tiles.size();
   }
@@ -530,7 +533,7 @@ int build_tiles(ffm_system* s) {
     cidx.insert(cidx.end(), col[mg].begin(), col[mg].end());
   }
   if (cidx.empty()) cidx.push_back(0);
-  if (tiles.empty()) tiles.push_back(make_int2(0, 0));  // n = 0: never launched
+  if (tiles.empty()) tiles.push_back(make_int4(0, 0, -1, 0));  // n = 0: never launched
   FFM_TRYR(upload(&s->d_tiles, tiles));
   FFM_TRYR(upload(&s->d_trow_ptr, rptr));
   FFM_TRYR(upload(&s->d_tcol_ptr, cptr));
@@ -832,7 +835,7 @@ int ffm_system_create(ffm_system_t** out, int device, int64_t n, const double* q
     b.tiles = nullptr;
     b.tile_list = nullptr;
   }
-  if (n > 0 && use_tiles(p, device)) FFM_TRY(build_tiles(s));
+  if (n > 0 && use_tiles(p, device)) FFM_TRY(build_tiles(s, spt_ptr, spt_m));
   p.spt_ptr = s->bplan.spt_ptr = s->d_spt_ptr;
   p.spt_m = s->bplan.spt_m = s->d_spt_m;
   p.spt_mask = s->bplan.spt_mask = s->d_spt_mask;

@@ -65,7 +65,7 @@ __device__ __forceinline__ void pack_item(int64_t k, int n, int np, int batch,
     s[kStDihedral] = kSentinel;
     s[kStNbSuspect] = 0;
     s[kStNbKey] = kSentinel;
-    s[7] = 0;
+    s[kStCount] = 0;
   }
 }
 
@@ -499,6 +499,11 @@ __device__ __forceinline__ double tree_min(double v, double* sh) {
   return s;
 }
 
+#ifndef FFM_RED_UNROLL
+#define FFM_RED_UNROLL 2  // (8 changed the fused small kernel's register allocation: spills)
+#endif
+constexpr int kRedUnroll = FFM_RED_UNROLL;
+constexpr int kRedUnroll4 = FFM_RED_UNROLL < 4 ? FFM_RED_UNROLL : 4;
 // flag_suspect: mark a possible coincidence (non-finite sums, closest pair
 // below RMIN) in the status words for the finder
 __device__ __forceinline__ void reduce_entry(int nunits, int nterm_blocks,
@@ -510,11 +515,15 @@ __device__ __forceinline__ void reduce_entry(int nunits, int nterm_blocks,
   epart += (size_t)b * nunits * 3;
   term_part += (size_t)b * nterm_blocks * 5;
   double ec = 0.0, ev = 0.0, mr = DBL_MAX, es = 0.0, eb = 0.0, et = 0.0;
+  // (unrolled: a thread's partial loads are independent and go out
+  // together; the sums keep their order)
+#pragma unroll kRedUnroll
   for (int u = threadIdx.x; u < nunits; u += blockDim.x) {
     ec += epart[3 * u];
     ev += epart[3 * u + 1];
     mr = fmin(mr, epart[3 * u + 2]);
   }
+#pragma unroll kRedUnroll4
   for (int k = threadIdx.x; k < nterm_blocks; k += blockDim.x) {
     const double* p = term_part + 5 * (size_t)k;
     es += p[0];

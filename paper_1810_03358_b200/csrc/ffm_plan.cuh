@@ -31,7 +31,8 @@ struct NbPlanDev {
   // small systems (ntiles > 0): the sweep runs one warp per 128 x 32 tile
   // instead of per super-unit (nb_tiles_kernel); nlaunch then counts tiles
   int ntiles;
-  const int2* tiles;         // [ntiles] (i-sub-block, global j-block), row-major
+  const int4* tiles;         // [ntiles] (i-sub-block, global j-block, special-pair
+                             // mask entry or -1, 0), row-major
   const int* tile_list;      // tiles this launch evaluates (row sharding), or null = all
 };
 

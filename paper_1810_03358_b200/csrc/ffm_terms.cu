@@ -265,12 +265,12 @@ __global__ void finder_kernel(int n, int np, const typename Vec4T<T>::type* __re
   if (*(volatile int64_t*)(s + kStNbSuspect) == 0) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) finder_row<T>(i, n, pos + (size_t)b * np, sp_ptr, sp_j, sp_s, s);
-  // the entry's last finder block converts the sentinels (status word 7
-  // counts finished blocks; reset for the next evaluation)
+  // the entry's last finder block converts the sentinels (status word
+  // kStCount counts finished blocks; reset for the next evaluation)
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(s + 7);
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(s + kStCount);
     if (atomicAdd(cnt, 1ull) == gridDim.x - 1) {
       __threadfence();
       finalize_entry(n, s);

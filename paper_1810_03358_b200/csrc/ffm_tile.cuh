@@ -361,8 +361,11 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
   const int t = plan.tile_list ? plan.tile_list[slot] : slot;
   __syncthreads();  // a CTA running several tiles: the previous one is done with sm
-  const int2 tk = plan.tiles[t];
-  const int kk = tk.x, mg = tk.y;
+  // a lone tile is latency-bound: one round trip for the tile record (its
+  // special-pair mask entry resolved on the host), then every load the tile
+  // needs -- j-block staging, the special-pair mask, the i-rows -- at once
+  const int4 tk = plan.tiles[t];
+  const int kk = tk.x, mg = tk.y, spe = tk.z;
   const int ib = kk * kIB, jb = mg * kJB;
   pos += (size_t)bidx * plan.np;
   ipos += (size_t)bidx * 4 * plan.np;
@@ -381,6 +384,18 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
     sm.sl[lane + 32] = l;
   }
   constexpr int NP = PairsPerPass<T>::value;
+  static_assert(NP == 2, "tile_cta holds all four i-atoms of a lane in one pass");
+  V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
+#pragma unroll
+  for (int pp = 0; pp < NP; ++pp) {
+    const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
+    xi[pp] = ld_pair<T>(ipos, r);
+    yi[pp] = ld_pair<T>(ipos, half + r);
+    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+    ai[pp] = ld_pair<T>(ilj, r);
+    bi[pp] = ld_pair<T>(ilj, half + r);
+  }
   bool masked = jb < ib + kIB;  // straddles the diagonal
   uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
   if (masked) {
@@ -390,22 +405,10 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
       mk[p] = d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
     }
   }
-  // this tile's special-pair mask, if any: the row's special-tile list is
-  // searched 32 entries per step by the whole warp (one round of loads, not
-  // a chain of dependent ones -- a lone tile is latency-bound)
-  {
-    const int e_end = plan.spt_ptr[kk + 1];
-    for (int e0 = plan.spt_ptr[kk]; e0 < e_end; e0 += 32) {
-      const int e = e0 + lane;
-      const uint32_t hit = __ballot_sync(0xffffffffu, e < e_end && plan.spt_m[e] == mg);
-      if (hit) {
-        const int ef = e0 + __ffs(hit) - 1;
-        masked = true;
+  if (spe >= 0) {  // this tile's special pairs (excluded / scaled)
+    masked = true;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)ef * kIB + 32 * p + lane];
-        break;
-      }
-    }
+    for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)spe * kIB + 32 * p + lane];
   }
   const T cut2 = T(plan.cut2);
   T minr2 = T(1e30);
@@ -414,18 +417,8 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
   if (GRAD) jacc[lane] = jacc[32 + lane] = jacc[64 + lane] = T(0);
   __syncthreads();  // sj / sl staged
   const int t0 = q * kTileSteps;
-  for (int p0 = 0; p0 < 2; p0 += NP) {
-    V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
-#pragma unroll
-    for (int pp = 0; pp < NP; ++pp) {
-      const int64_t r = (int64_t)kk * 64 + (p0 + pp) * 32 + lane;
-      xi[pp] = ld_pair<T>(ipos, r);
-      yi[pp] = ld_pair<T>(ipos, half + r);
-      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
-      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
-      ai[pp] = ld_pair<T>(ilj, r);
-      bi[pp] = ld_pair<T>(ilj, half + r);
-    }
+  {
+    constexpr int p0 = 0;
     V F[NP][3];
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
