@@ -154,7 +154,7 @@ struct SmallEvalArgs {
   double* grad;
   double* energies;
   int64_t* status;
-  unsigned long long* phase_clock;  // null, or [grid][6] timestamps (tuning aid)
+  unsigned long long* phase_clock;  // null, or [grid][8] timestamps (tuning aid)
   // line-search trial of a graph-resident driver (null trial_out: a plain
   // evaluation of coords): the point x_t = lincomb(1, trial_x, *trial_h,
   // trial_r) is formed into trial_out and evaluated, then the probe

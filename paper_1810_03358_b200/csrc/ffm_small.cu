@@ -51,8 +51,9 @@ small_eval_kernel(SmallEvalArgs a) {
   T* ipos = static_cast<T*>(a.ipos);
   T* ipart = static_cast<T*>(a.ipart);
   T* jpart = static_cast<T*>(a.jpart);
-  // optional phase clock (tools/time_small_phases.py): [CTA][6] globaltimer stamps
-  unsigned long long* clk = a.phase_clock ? a.phase_clock + 6 * blockIdx.x : nullptr;
+  // optional phase clock (tools/time_small_phases.py): [CTA][8] globaltimer
+  // stamps (slots 0-5 used)
+  unsigned long long* clk = a.phase_clock ? a.phase_clock + 8 * blockIdx.x : nullptr;
   auto stamp = [&](int k) {
     if (clk && threadIdx.x == 0) {
       unsigned long long t;
@@ -85,6 +86,9 @@ small_eval_kernel(SmallEvalArgs a) {
     // P1: CTA items -- the pair tiles (one CTA each, the longer items, first)
     // and the bonded / scaled-pair term blocks, dealt round-robin so a CTA
     // with a tile does not also run a term block when the grid covers both
+    // (a cp.async double-buffered variant that fetched a CTA's next tile
+    // during the current one measured no faster: a tile's loads are not its
+    // critical path, profiles/r02_small_tile_loads.log)
     const int nitems = plan.nlaunch + a.nterm_blocks;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       if (it < plan.nlaunch)

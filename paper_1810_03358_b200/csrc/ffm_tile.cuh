@@ -344,95 +344,43 @@ struct TileSmem {
   double ered[kTileWarps][3];
 };
 
-// tile_cta evaluates launch slot `slot` of batch entry bidx with the whole
-// CTA (kTileWarps warps; block-uniform call, contains __syncthreads)
+// The compute and epilogue of one tile once the CTA has staged its j-block
+// (sm.sj / sm.sl, negated, stored twice), zeroed sm.jacc and passed a
+// barrier, with the lane's four i-atoms and masks in registers: warp q
+// evaluates rotation steps 8q .. 8q + 7; warp partials are combined in warp
+// order (block-uniform, contains __syncthreads).
 template <typename T, bool GRAD, bool CUTOFF>
-__device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
-                                         const typename Vec4T<T>::type* __restrict__ pos,
-                                         const typename Vec2T<T>::type* __restrict__ lj,
-                                         const T* __restrict__ ipos, const T* __restrict__ ilj,
-                                         T* __restrict__ ipart, T* __restrict__ jpart,
-                                         double* __restrict__ epart, int slot, int bidx,
-                                         TileSmem<T>& sm) {
+__device__ __forceinline__ void tile_body(const NbPlanDev& plan, TileSmem<T>& sm,
+                                          const typename Pk<T>::V (&xi)[2],
+                                          const typename Pk<T>::V (&yi)[2],
+                                          const typename Pk<T>::V (&zi)[2],
+                                          const typename Pk<T>::V (&qi)[2],
+                                          const typename Pk<T>::V (&ai)[2],
+                                          const typename Pk<T>::V (&bi)[2],
+                                          const uint32_t (&mk)[4], bool masked, int t, int bidx,
+                                          T* __restrict__ ipart, T* __restrict__ jpart,
+                                          double* __restrict__ epart) {
   using P = Pk<T>;
   using V = typename P::V;
-  using V4 = typename Vec4T<T>::type;
-  using V2 = typename Vec2T<T>::type;
+  constexpr int NP = 2;
   const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
-  const int t = plan.tile_list ? plan.tile_list[slot] : slot;
-  __syncthreads();  // a CTA running several tiles: the previous one is done with sm
-  // a lone tile is latency-bound: one round trip for the tile record (its
-  // special-pair mask entry resolved on the host), then every load the tile
-  // needs -- j-block staging, the special-pair mask, the i-rows -- at once
-  const int4 tk = plan.tiles[t];
-  const int kk = tk.x, mg = tk.y, spe = tk.z;
-  const int ib = kk * kIB, jb = mg * kJB;
-  pos += (size_t)bidx * plan.np;
-  ipos += (size_t)bidx * 4 * plan.np;
-  const int64_t half = plan.np >> 1;
-  if (q == 0) {
-    V4 p = pos[jb + lane];
-    p.x = -p.x;
-    p.y = -p.y;
-    p.z = -p.z;
-    sm.sj[lane] = p;
-    sm.sj[lane + 32] = p;
-  } else if (q == 1) {
-    V2 l = lj[jb + lane];
-    l.y = -l.y;
-    sm.sl[lane] = l;
-    sm.sl[lane + 32] = l;
-  }
-  constexpr int NP = PairsPerPass<T>::value;
-  static_assert(NP == 2, "tile_cta holds all four i-atoms of a lane in one pass");
-  V xi[NP], yi[NP], zi[NP], qi[NP], ai[NP], bi[NP];
-#pragma unroll
-  for (int pp = 0; pp < NP; ++pp) {
-    const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
-    xi[pp] = ld_pair<T>(ipos, r);
-    yi[pp] = ld_pair<T>(ipos, half + r);
-    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
-    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
-    ai[pp] = ld_pair<T>(ilj, r);
-    bi[pp] = ld_pair<T>(ilj, half + r);
-  }
-  bool masked = jb < ib + kIB;  // straddles the diagonal
-  uint32_t mk[4] = {~0u, ~0u, ~0u, ~0u};
-  if (masked) {
-#pragma unroll
-    for (int p = 0; p < 4; ++p) {
-      const int d = ib + lane + 32 * p - jb;  // pair active iff jj > d
-      mk[p] = d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
-    }
-  }
-  if (spe >= 0) {  // this tile's special pairs (excluded / scaled)
-    masked = true;
-#pragma unroll
-    for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)spe * kIB + 32 * p + lane];
-  }
   const T cut2 = T(plan.cut2);
   T minr2 = T(1e30);
   double ec = 0.0, ev = 0.0;
   T* jacc = sm.jacc[q];
-  if (GRAD) jacc[lane] = jacc[32 + lane] = jacc[64 + lane] = T(0);
-  __syncthreads();  // sj / sl staged
   const int t0 = q * kTileSteps;
   {
-    constexpr int p0 = 0;
     V F[NP][3];
 #pragma unroll
     for (int pp = 0; pp < NP; ++pp) F[pp][0] = F[pp][1] = F[pp][2] = P::zero();
     V ec2 = P::zero(), ev2 = P::zero();
-    uint32_t mkp[2 * NP];
-#pragma unroll
-    for (int x = 0; x < 2 * NP; ++x) mkp[x] = mk[2 * p0 + x];
     if (masked)
       warp_tile<T, GRAD, CUTOFF, true, NP, true, kTileSteps, kTileSteps>(
-          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mkp, cut2, minr2,
+          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mk, cut2, minr2,
           t0);
     else
       warp_tile<T, GRAD, CUTOFF, false, NP, true, kTileSteps, kTileSteps>(
-          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mkp, cut2, minr2,
+          sm.sj, sm.sl, lane, xi, yi, zi, qi, ai, bi, F, ec2, ev2, jacc, kJB, mk, cut2, minr2,
           t0);
     ec += double(P::lo(ec2)) + double(P::hi(ec2));
     ev += double(P::lo(ev2)) + double(P::hi(ev2));
@@ -441,8 +389,8 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
       for (int pp = 0; pp < NP; ++pp)
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          sm.fred[q][c * kIB + lane + 64 * (p0 + pp)] = P::lo(F[pp][c]);
-          sm.fred[q][c * kIB + lane + 64 * (p0 + pp) + 32] = P::hi(F[pp][c]);
+          sm.fred[q][c * kIB + lane + 64 * pp] = P::lo(F[pp][c]);
+          sm.fred[q][c * kIB + lane + 64 * pp + 32] = P::hi(F[pp][c]);
         }
     }
   }
@@ -489,6 +437,81 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
       jp[tid] = g;
     }
   }
+}
+
+// diagonal mask of a tile (pair (i, j) active iff j > i) for the lane's rows
+__device__ __forceinline__ bool tile_diag_mask(int ib, int jb, int lane, uint32_t (&mk)[4]) {
+  const bool masked = jb < ib + kIB;  // straddles the diagonal
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int d = ib + lane + 32 * p - jb;  // pair active iff jj > d
+    mk[p] = !masked || d < 0 ? ~0u : (d >= 31 ? 0u : ~((2u << d) - 1u));
+  }
+  return masked;
+}
+
+// tile_cta evaluates launch slot `slot` of batch entry bidx with the whole
+// CTA (kTileWarps warps; block-uniform call, contains __syncthreads)
+template <typename T, bool GRAD, bool CUTOFF>
+__device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
+                                         const typename Vec4T<T>::type* __restrict__ pos,
+                                         const typename Vec2T<T>::type* __restrict__ lj,
+                                         const T* __restrict__ ipos, const T* __restrict__ ilj,
+                                         T* __restrict__ ipart, T* __restrict__ jpart,
+                                         double* __restrict__ epart, int slot, int bidx,
+                                         TileSmem<T>& sm) {
+  using P = Pk<T>;
+  using V = typename P::V;
+  using V4 = typename Vec4T<T>::type;
+  using V2 = typename Vec2T<T>::type;
+  const int lane = threadIdx.x & 31, q = threadIdx.x >> 5;
+  const int t = plan.tile_list ? plan.tile_list[slot] : slot;
+  __syncthreads();  // a CTA running several tiles: the previous one is done with sm
+  // a lone tile is latency-bound: one round trip for the tile record (its
+  // special-pair mask entry resolved on the host), then every load the tile
+  // needs -- j-block staging, the special-pair mask, the i-rows -- at once
+  const int4 tk = plan.tiles[t];
+  const int kk = tk.x, mg = tk.y, spe = tk.z;
+  const int ib = kk * kIB, jb = mg * kJB;
+  pos += (size_t)bidx * plan.np;
+  ipos += (size_t)bidx * 4 * plan.np;
+  const int64_t half = plan.np >> 1;
+  if (q == 0) {
+    V4 p = pos[jb + lane];
+    p.x = -p.x;
+    p.y = -p.y;
+    p.z = -p.z;
+    sm.sj[lane] = p;
+    sm.sj[lane + 32] = p;
+  } else if (q == 1) {
+    V2 l = lj[jb + lane];
+    l.y = -l.y;
+    sm.sl[lane] = l;
+    sm.sl[lane + 32] = l;
+  }
+  static_assert(PairsPerPass<T>::value == 2, "a tile lane holds its four i-atoms in one pass");
+  V xi[2], yi[2], zi[2], qi[2], ai[2], bi[2];
+#pragma unroll
+  for (int pp = 0; pp < 2; ++pp) {
+    const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
+    xi[pp] = ld_pair<T>(ipos, r);
+    yi[pp] = ld_pair<T>(ipos, half + r);
+    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+    ai[pp] = ld_pair<T>(ilj, r);
+    bi[pp] = ld_pair<T>(ilj, half + r);
+  }
+  uint32_t mk[4];
+  bool masked = tile_diag_mask(ib, jb, lane, mk);
+  if (spe >= 0) {  // this tile's special pairs (excluded / scaled)
+    masked = true;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) mk[p] &= ~plan.spt_mask[(size_t)spe * kIB + 32 * p + lane];
+  }
+  if (GRAD) sm.jacc[q][lane] = sm.jacc[q][32 + lane] = sm.jacc[q][64 + lane] = T(0);
+  __syncthreads();  // sj / sl staged
+  tile_body<T, GRAD, CUTOFF>(plan, sm, xi, yi, zi, qi, ai, bi, mk, masked, t, bidx, ipart, jpart,
+                             epart);
 }
 
 }  // namespace ffm

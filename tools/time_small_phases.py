@@ -21,7 +21,7 @@ fl = N.FFM_ENERGY | (N.FFM_GRAD if grad else 0) | N.FFM_NO_GRAPH
 eng.eval(c, prec, grad=g if grad else None, energies=en, status=st, flags=fl)
 torch.cuda.synchronize()
 grids = np.zeros(4, np.int32)
-clk = torch.zeros((8192, 6), dtype=torch.int64, device="cuda")
+clk = torch.zeros((8192, 8), dtype=torch.int64, device="cuda")
 N.check(eng.lib.ffm_debug_phase_clock(eng.handle, N.ptr(clk), grids.ctypes.data), "clk")
 G = int(grids[2 * prec + grad])
 for rep in range(5):
