@@ -137,13 +137,14 @@ __device__ inline bool dihedral_term(P3 ci, P3 cj, P3 ck, P3 cl, const double* V
   const P3 m = cross(n1, n2);
   const double y = dot(m, b2) / b2n;
   const double x = dot(n1, n2);
-  const double phi = atan2(y, x);
-  // cos / sin of phi .. 4 phi from one sincos by the angle-addition
-  // recurrences (eight libm calls in the reference; the multiples agree with
-  // them to a few ulp, far inside the FP64 tolerance): the term blocks are
-  // the latency-critical items of a small-system evaluation
-  double s1, c1;
-  sincos(phi, &s1, &c1);
+  // phi = atan2(y, x) in the reference; since m = n1 x n2 is parallel to b2,
+  // x^2 + y^2 = |n1|^2 |n2|^2, so cos phi = x / (|n1| |n2|) and sin phi =
+  // y / (|n1| |n2|) directly (no atan2 / sincos chains: the term blocks are
+  // the latency-critical items of a small-system evaluation).  cos / sin of
+  // 2 phi .. 4 phi by the angle-addition recurrences (eight libm calls in
+  // the reference; they agree to a few ulp, far inside the FP64 tolerance)
+  const double inv = 1.0 / (n1n * n2n);
+  const double c1 = x * inv, s1 = y * inv;
   const double c2 = c1 * c1 - s1 * s1, s2 = 2.0 * s1 * c1;
   const double c3 = c2 * c1 - s2 * s1, s3 = s2 * c1 + c2 * s1;
   const double c4 = c2 * c2 - s2 * s2, s4 = 2.0 * s2 * c2;
