@@ -96,6 +96,15 @@ int ffm_system_destroy(ffm_system_t* sys);
  * paper_1810_03358_b200.parallel).  nranks = 1 restores the full sweep. */
 int ffm_system_set_shard(ffm_system_t* sys, int rank, int nranks);
 
+/* Super-unit edge S of the pair sweep's plan (units mode only: a multiple
+ * of 128 in [128, 1024] dividing the padded atom count; FFM_EINVAL in tile
+ * mode).  ffm_preferred_edge gives the edge an n-atom system evaluated
+ * mostly in `precision` runs best with (0: tile mode): the creation default,
+ * except 128 for FP64 mid-size systems.  No reference counterpart (tuning of
+ * this engine's plan); paper_1810_03358_b200.engine.engine_for applies it. */
+int ffm_preferred_edge(int64_t n, int precision, int* edge);
+int ffm_system_set_edge(ffm_system_t* sys, int S);
+
 /* The NCCL communicator (ncclComm_t, e.g. torch's ProcessGroupNCCL
  * _comm_ptr()) of a sharded system's ranks.  With it attached, every
  * ffm_eval / ffm_eval_host of the sharded system -- and every evaluation

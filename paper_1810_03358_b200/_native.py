@@ -45,6 +45,8 @@ SIGNATURES = {
     "ffm_system_set_terms": (_I, [_P, _I64, _P, _P, _P, _I64, _P, _P, _P, _I64, _P, _P]),
     "ffm_system_destroy": (_I, [_P]),
     "ffm_system_set_shard": (_I, [_P, _I, _I]),
+    "ffm_system_set_edge": (_I, [_P, _I]),
+    "ffm_preferred_edge": (_I, [_I64, _I, _P]),
     "ffm_system_info": (_I, [_P, _P]),
     "ffm_system_nb_ms": (_I, [_P, _P]),
     "ffm_launch_count": (C.c_longlong, []),

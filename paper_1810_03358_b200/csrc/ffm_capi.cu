@@ -938,6 +938,37 @@ int ffm_system_set_shard(ffm_system_t* s, int rank, int nranks) {
   return FFM_OK;
 }
 
+// FP64 sweeps of mid-size systems run faster on 128-atom super-units than on
+// the 256 choose_S picks for both precisions (tools/mid_sweep.py, one B200,
+// FP64 S = 256 vs 128, us per evaluation: energy+gradient 4500 atoms 66.9 ->
+// 49.4, 5000 67.0 -> 56.4, 6000 82.8 -> 68.6, 8000 114.3 -> 102.3, 10000
+// 155.0 -> 147.4, 12000 198.1 -> 198.2; energy only 4500 49.4 -> 31.0, 6000
+// 50.0 -> 41.2, 8000 63.9 -> 60.9, 10000 86.5 -> 86.4, 12000 109.3 -> 113.2;
+// graph-resident L-BFGS per iteration 5000 0.576 -> 0.451 ms, 8000 0.729 ->
+// 0.720, 10000 0.930 -> 0.937); FP32 is not (5000 atoms 37.5 -> 41.2 us)
+#ifndef FFM_F64_EDGE128_UNITS
+#define FFM_F64_EDGE128_UNITS 800  // S = 256 plans with fewer units switch to 128
+#endif
+int ffm_preferred_edge(int64_t n, int precision, int* edge) {
+  if (!edge || n < 0) return fail(FFM_EINVAL, "bad argument");
+  const int S = choose_S(n);
+  const int64_t nb = std::max<int64_t>(1, (n + S - 1) / S);
+  const int64_t units = nb * (nb + 1) / 2;
+  if (units < 150) *edge = 0;  // tile mode (use_tiles)
+  else if (precision == FFM_F64 && S == 256 && units < FFM_F64_EDGE128_UNITS) *edge = 128;
+  else *edge = S;
+  return FFM_OK;
+}
+
+int ffm_system_set_edge(ffm_system_t* s, int S) {
+  if (!s) return fail(FFM_EINVAL, "system is NULL");
+  if (s->plan.ntiles > 0) return fail(FFM_EINVAL, "a tile-mode plan has no super-unit edge");
+  if (S < 128 || S > 1024 || S % 128 || s->plan.np % S)
+    return fail(FFM_EINVAL, "edge must be a multiple of 128 in [128, 1024] dividing the padded atom count");
+  s->S0 = S;
+  return ffm_system_set_shard(s, s->rank, s->nranks);  // rebuilds the units with edge S0
+}
+
 int ffm_system_set_comm(ffm_system_t* s, void* comm) {
   if (!s) return fail(FFM_EINVAL, "NULL argument");
   DeviceGuard guard(s->device);

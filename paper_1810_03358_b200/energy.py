@@ -100,7 +100,7 @@ def raise_status(system, st, grad, order=None):
 
 def _eval(system, dtype, backend, grad, flags=None):
     _check_backend(backend)
-    eng = engine_for(system.topology)
+    eng = engine_for(system.topology, precision=dtype)
     return eng.eval_host(system.coords, precision_of(dtype), grad=grad, flags=flags)
 
 

@@ -10,6 +10,7 @@ is the CUDA code in csrc/.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 
 import numpy as np
@@ -70,14 +71,17 @@ class DeviceSystem:
                 h, len(topo.bond_K), _p(topo.bond_idx), _p(topo.bond_K), _p(topo.bond_r0),
                 len(topo.ang_K), _p(topo.ang_idx), _p(topo.ang_K), _p(topo.ang_t0),
                 len(topo.dih_V), _p(topo.dih_idx), _p(topo.dih_V)), "ffm_system_set_terms")
-        info = np.zeros(8, np.int64)
-        N.check(self.lib.ffm_system_info(h, _p(info)), "ffm_system_info")
-        self.info = dict(zip(("n", "np", "S", "blocks", "units", "special_tiles",
-                              "scaled_pairs", "device"), info.tolist()))
+        self.refresh_info()
         self._lock = threading.Lock()
         # host-path result buffers
         self._h_en = np.zeros(N.FFM_NTERMS)
         self._h_st = np.zeros(N.FFM_STATUS_WORDS, np.int64)
+
+    def refresh_info(self):
+        info = np.zeros(8, np.int64)
+        N.check(self.lib.ffm_system_info(self.handle, _p(info)), "ffm_system_info")
+        self.info = dict(zip(("n", "np", "S", "blocks", "units", "special_tiles",
+                              "scaled_pairs", "device"), info.tolist()))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -180,13 +184,32 @@ class DeviceSystem:
             raise ValueError(f"coords must be a contiguous cuda float64 tensor ({self.n}, 3)")
 
 
-def engine_for(topo, device=None) -> DeviceSystem:
-    """The (cached) engine of a topology on a device."""
+def engine_for(topo, device=None, precision=None) -> DeviceSystem:
+    """The (cached) engine of a topology on a device.  ``precision`` (FFM_F64
+    / FFM_F32 / a NumPy dtype) names the precision the caller evaluates in:
+    where the engine's preferred super-unit edge for it differs from the
+    creation default (FP64 on mid-size systems, ffm_preferred_edge) the
+    caller gets a second cached engine planned with that edge."""
     require_cuda()
     idx = torch.cuda.current_device() if device is None else (
         device.index if isinstance(device, torch.device) else int(device))
-    eng = topo.engines.get(idx)
+    key = idx
+    edge = None
+    if precision is not None and os.environ.get("FFM_EDGE_PREF", "1") != "0":
+        lib = N.load()
+        want, dflt = C.c_int(0), C.c_int(0)
+        N.check(lib.ffm_preferred_edge(topo.natoms, precision_of(precision), C.byref(want)),
+                "ffm_preferred_edge")
+        N.check(lib.ffm_preferred_edge(topo.natoms, N.FFM_F32, C.byref(dflt)),
+                "ffm_preferred_edge")
+        if want.value != dflt.value:
+            key, edge = (idx, "edge", want.value), want.value
+    eng = topo.engines.get(key)
     if eng is None:
         eng = DeviceSystem(topo, idx)
-        topo.engines[idx] = eng
+        if edge is not None:
+            with torch.cuda.device(eng.device):
+                N.check(eng.lib.ffm_system_set_edge(eng.handle, edge), "ffm_system_set_edge")
+            eng.refresh_info()
+        topo.engines[key] = eng
     return eng

@@ -110,7 +110,7 @@ class MolecularOracle(ObjectiveOracle):
         self.dtype = np.dtype(dtype)
         self.backend = backend
         self.precision = precision_of(self.dtype)
-        self.engine = engine_for(system.topology, device)
+        self.engine = engine_for(system.topology, device, precision=self.precision)
         self.device = self.engine.device
         n = system.natoms
         # fixed device buffers: every evaluation replays the same captured

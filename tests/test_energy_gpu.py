@@ -562,3 +562,47 @@ def test_split_last_wave_units(S, monkeypatch):
         g_sum += g
         eng.close()
     assert float((g_sum.cpu().numpy().ravel() - np.ravel(g_ref)).__abs__().max()) <= 1e-10 * gmax
+
+
+def test_fp64_preferred_edge_engine():
+    """FP64 callers of a mid-size system get an engine planned on 128-atom
+    super-units (ffm_preferred_edge / ffm_system_set_edge); FP32 callers and
+    other sizes keep the default plan.  Both plans agree with the oracle."""
+    import ctypes as C
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.energy import energy_and_gradient
+    from paper_1810_03358_b200.engine import engine_for
+    from paper_1810_03358_b200.oracle import MolecularOracle
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    lib = N.load()
+    edge = C.c_int(-1)
+    for n, e64, e32 in ((500, 0, 0), (5000, 128, 256), (20000, 256, 256), (100000, 1024, 1024)):
+        N.check(lib.ffm_preferred_edge(n, N.FFM_F64, C.byref(edge)), "edge")
+        assert edge.value == e64, n
+        N.check(lib.ffm_preferred_edge(n, N.FFM_F32, C.byref(edge)), "edge")
+        assert edge.value == e32, n
+    s = make_globule_system(5000, seed=4)
+    e_def = engine_for(s.topology)
+    e64 = engine_for(s.topology, precision=np.float64)
+    assert e_def.info["S"] == 256 and e64.info["S"] == 128 and e64 is not e_def
+    assert engine_for(s.topology, precision=np.float32) is e_def
+    assert MolecularOracle(s).engine is e64
+    assert MolecularOracle(s, np.float32).engine is e_def
+    A = O.Arrays.from_system(s)
+    e_ref, g_ref, err = O.energy_and_gradient(A, s.coords, True, threads=O.host_threads())
+    assert err is None
+    bd, g = energy_and_gradient(s, np.float64)
+    got = np.array([bd.stretch, bd.bend, bd.torsion, bd.coulomb, bd.vdw])
+    assert _rel(got, e_ref) <= 1e-10
+    assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= 1e-10 * np.max(np.abs(g_ref))
+    en, st, g_def = e_def.eval_host(s.coords, N.FFM_F64, grad=True)
+    assert _rel(en, e_ref) <= 1e-10
+    # invalid edges are refused, the plan is unchanged
+    assert lib.ffm_system_set_edge(e64.handle, 192) != 0
+    assert lib.ffm_system_set_edge(e64.handle, 2048) != 0
+    small = engine_for(make_globule_system(600, seed=1).topology)  # tile mode
+    assert lib.ffm_system_set_edge(small.handle, 256) != 0
+    e64.refresh_info()
+    assert e64.info["S"] == 128

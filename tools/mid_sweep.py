@@ -31,7 +31,7 @@ for n in sizes:
         os.environ.update(env)
         eng = DeviceSystem(s.topology)
         en, st = eng.new_outputs()
-        fl = N.FFM_ENERGY | N.FFM_GRAD
+        fl = N.FFM_ENERGY | (0 if os.environ.get("GRAD") == "0" else N.FFM_GRAD)
         nb = []
         for k in range(8):
             eng.eval(c, PREC, grad=g, energies=en, status=st, flags=fl | N.FFM_TIME_NB)
