@@ -160,6 +160,8 @@ class MolecularOracle(ObjectiveOracle):
         # NumPy array owns it), the 104-byte result block alongside; one
         # synchronisation for both
         host = isinstance(x, np.ndarray)
+        if host and not x.flags.writeable:
+            x = x.copy()  # torch.from_numpy warns on read-only arrays
         self._x.view(-1).copy_(torch.from_numpy(x) if host else x)
         self.engine.eval(self._x, self.precision, grad=self._g if grad else None,
                          energies=self._en, status=self._st)
