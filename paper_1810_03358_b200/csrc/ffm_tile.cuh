@@ -147,7 +147,7 @@ __device__ __forceinline__ void warp_tile_energy(
         a0 = a0 && P::lo(r2[pp]) <= cut2;
         a1 = a1 && P::hi(r2[pp]) <= cut2;
       }
-      ri[pp] = P::rsqrt(r2[pp]);
+      ri[pp] = P::rsqrt_e(r2[pp]);
       const bool rcp = f32 && (FFM_ERCP == 1 || (FFM_ERCP == 2 && pp == 0));
       if (rcp) i2[pp] = P::rcp_or_sq(r2[pp], ri[pp]);
       if (MASKED || CUTOFF) {
