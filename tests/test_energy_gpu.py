@@ -388,10 +388,11 @@ def test_cutoff_culling_matches_oracle(cutoff):
         assert np.max(dg[m]) <= gt * gmax
 
 
-@pytest.mark.parametrize("S", [256, 512, 768, 1024])
+@pytest.mark.parametrize("S", [128, 256, 512, 768, 1024])
 def test_every_super_unit_size(S, monkeypatch):
-    """The unit size is picked from {256, 512, 768, 1024} by system size;
-    force each one (FFM_FORCE_S, read at plan creation) on one system, with
+    """The unit size is picked from {256, 512, 768, 1024} by system size
+    (128 for FP64 callers of mid-size systems, ffm_preferred_edge); force
+    each one (FFM_FORCE_S, read at plan creation) on one system, with
     special pairs and a ragged last block, and compare with the oracle."""
     from paper_1810_03358_b200.energy import energy_and_gradient
     from paper_1810_03358_b200.engine import DeviceSystem
