@@ -326,16 +326,38 @@ __device__ __forceinline__ void gather_group(int g, int n, int S, int nb,
     const int kk = a0 / kIB, mg = a0 / kJB, row = a0 - kk * kIB + lane;
     const int r0 = trow_ptr[kk], nr = trow_ptr[kk + 1] - r0;
     const int c0 = tcol_ptr[mg], nt = nr + tcol_ptr[mg + 1] - c0;
+    // the warp's entries k = warp, warp + NW, ... in order: its rows, then
+    // its columns, as two branch-free loops (with a per-entry branch -- row
+    // or column, this rank's or not -- ptxas kept each entry's loads behind
+    // the previous entry's sums; measured: no change in the evaluation time,
+    // profiles/r02_small_tile_loads.log)
+    int k = warp;
+    if (nranks == 1) {
 #pragma unroll 4
-    for (int k = warp; k < nt; k += NW) {
-      const bool isrow = k < nr;
-      const int st = isrow ? kIB : kJB;
-      const int t = isrow ? r0 + k : tcol_idx[c0 + k - nr];
-      if (nranks > 1 && t % nranks != rank) continue;
-      const T* p = isrow ? ipart + (size_t)t * 3 * kIB + row : jpart + (size_t)t * 3 * kJB + lane;
-      g0 += (double)p[0];
-      g1 += (double)p[st];
-      g2 += (double)p[2 * st];
+      for (; k < nr; k += NW) {
+        const T* p = ipart + (size_t)(r0 + k) * 3 * kIB + row;
+        g0 += (double)p[0];
+        g1 += (double)p[kIB];
+        g2 += (double)p[2 * kIB];
+      }
+#pragma unroll 4
+      for (; k < nt; k += NW) {
+        const T* p = jpart + (size_t)tcol_idx[c0 + k - nr] * 3 * kJB + lane;
+        g0 += (double)p[0];
+        g1 += (double)p[kJB];
+        g2 += (double)p[2 * kJB];
+      }
+    } else {  // this rank's tiles only
+      for (; k < nt; k += NW) {
+        const bool isrow = k < nr;
+        const int st = isrow ? kIB : kJB;
+        const int t = isrow ? r0 + k : tcol_idx[c0 + k - nr];
+        if (t % nranks != rank) continue;
+        const T* p = isrow ? ipart + (size_t)t * 3 * kIB + row : jpart + (size_t)t * 3 * kJB + lane;
+        g0 += (double)p[0];
+        g1 += (double)p[st];
+        g2 += (double)p[2 * st];
+      }
     }
   } else if (use_nb) {  // super-unit mode: [unit][3][S] rows and columns
     // unit_index = [row lists' ptr (2 nb + 1) | column lists' ptr (nb + 1) |
