@@ -381,7 +381,7 @@ int choose_S_sharded(const NbPlanDev& p, int S0, int nranks) {
     const int64_t nb = p.np / S;
     if (nb * (nb + 1) / 2 >= (int64_t)FFM_SHARD_UNITS * nranks) return S;
   }
-  return p.np % 256 == 0 ? 256 : S0;
+  return p.np % 256 == 0 ? std::min(256, S0) : S0;  // never above the single-rank edge
 }
 
 // rebuild the term plan device view (after set_terms or creation)
