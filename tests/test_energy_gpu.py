@@ -607,3 +607,35 @@ def test_fp64_preferred_edge_engine():
     assert lib.ffm_system_set_edge(small.handle, 256) != 0
     e64.refresh_info()
     assert e64.info["S"] == 128
+
+
+def test_edge_128_plan_shards():
+    """A 128-edge plan stays 128 when sharded, and its row shards sum to the
+    unsharded evaluation (FP64)."""
+    import torch
+
+    from paper_1810_03358_b200 import _native as N
+    from paper_1810_03358_b200.engine import DeviceSystem
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(5000, seed=9)
+    c = torch.from_numpy(s.coords.copy()).cuda()
+    full = DeviceSystem(s.topology)
+    N.check(full.lib.ffm_system_set_edge(full.handle, 128), "set_edge")
+    g_full = torch.empty_like(c)
+    e_full, _ = full.eval(c, N.FFM_F64, grad=g_full)
+    g_sum, e_sum = torch.zeros_like(c), torch.zeros(5, dtype=torch.float64, device="cuda")
+    for rank in range(2):
+        eng = DeviceSystem(s.topology)
+        N.check(eng.lib.ffm_system_set_edge(eng.handle, 128), "set_edge")
+        N.check(eng.lib.ffm_system_set_shard(eng.handle, rank, 2), "set_shard")
+        eng.refresh_info()
+        assert eng.info["S"] == 128
+        g = torch.empty_like(c)
+        en, _ = eng.eval(c, N.FFM_F64, grad=g)
+        g_sum += g
+        e_sum += en
+        eng.close()
+    gmax = float(g_full.abs().max())
+    assert float((g_sum - g_full).abs().max()) <= 1e-11 * gmax
+    assert float(((e_sum - e_full).abs() / e_full.abs().clamp_min(1e-12)).max()) <= 1e-12
