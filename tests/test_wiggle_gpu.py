@@ -87,3 +87,31 @@ def test_graph_wiggle_equals_host_loop(golden, monkeypatch, inc):
     assert ra == rb
     assert a.f == b.f and a.status == b.status and np.array_equal(a.x, b.x)
     assert sum(1 for r in a.trace.records if r.step > 0) > 10  # moves were made
+
+
+def test_exact_deltas_equal_full_recompute_at_scale():
+    """The wiggle's exact single-atom probes (O(n) device deltas) against the
+    reference's probe_full recipe -- total energy of the moved system minus
+    the running total (ffmin/optimizers/wiggle.py:118-127) -- on a 5000-atom
+    globule: they agree to the roundoff of the two totals."""
+    import oracle as O
+
+    from paper_1810_03358_b200.energy import energy_total, exact_delta_atom_move
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(5000, seed=3)
+    A = O.Arrays.from_system(s)
+    e0 = float(np.sum(O.energy_and_gradient(A, s.coords, False, threads=O.host_threads())[0]))
+    assert energy_total(s).total == pytest.approx(e0, rel=1e-11)
+    rng = np.random.default_rng(5)
+    for atom in rng.integers(0, s.natoms, size=6):
+        d = rng.normal(scale=0.2, size=3)
+        moved = s.coords.copy()
+        moved[atom] += d
+        e1 = float(np.sum(O.energy_and_gradient(A, moved, False, threads=O.host_threads())[0]))
+        full = e1 - e0  # probe_full
+        exact = exact_delta_atom_move(s, int(atom), d)
+        assert abs(exact - full) <= 1e-11 * abs(e0) + 1e-9, (atom, exact, full)
+        # the device total of the moved system gives the same difference
+        dev = energy_total(s.with_coords(moved)).total - energy_total(s).total
+        assert abs(dev - full) <= 1e-11 * abs(e0) + 1e-9
