@@ -107,6 +107,34 @@ template <> struct Pk<float> {
   static __device__ __forceinline__ V zero() { return 0ull; }
 };
 
+// Tuning aid (variant builds with -DFFM_MIN_STAMPS only): a timeline of
+// globaltimer stamps from the minimiser's controller kernels and the fused
+// small-system evaluation, [0] = count, then (tag, ns) pairs
+// (tools/lbfgs_timeline.py); each translation unit has its own pointer.
+#ifdef FFM_MIN_STAMPS
+static __device__ unsigned long long* g_mclk = nullptr;
+__device__ __forceinline__ void mstamp(int tag, bool last_block = false) {
+  if (g_mclk && threadIdx.x == 0 && blockIdx.x == (last_block ? gridDim.x - 1 : 0)) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    const unsigned long long k = atomicAdd(g_mclk, 1ull);
+    if (k < 200000) {
+      g_mclk[1 + 2 * k] = (unsigned long long)tag;
+      g_mclk[2 + 2 * k] = t;
+    }
+  }
+}
+#define FFM_MSTAMP(t) ::ffm::mstamp(t)
+#define FFM_MSTAMP_LAST(t) ::ffm::mstamp(t, true)
+#else
+#define FFM_MSTAMP_LAST(t) \
+  do {                     \
+  } while (0)
+#define FFM_MSTAMP(t) \
+  do {                \
+  } while (0)
+#endif
+
 #ifndef FFM_F64HALF
 #define FFM_F64HALF 1  // FP64 energy-only rsqrt Newton step: y / 2 by an exponent decrement
 #endif

@@ -33,6 +33,7 @@ __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir
                                     cudaGraphConditionalHandle hls,
                                     cudaGraphConditionalHandle hacc) {
   pdl_wait();
+  FFM_MSTAMP(1);
   pdl_launch_dependents();
   cudaGraphSetConditional(hls, 0);
   cudaGraphSetConditional(hacc, 0);
@@ -62,6 +63,7 @@ __global__ void min_it_begin_kernel(MinState* S, cudaGraphConditionalHandle hdir
 // after d (two-loop or antigradient) and <d, d>
 __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
   pdl_wait();
+  FFM_MSTAMP(2);
   pdl_launch_dependents();
   if (S->c.method == kMethodSd) {
     // r = div(lincomb(-1, g), |g|)  (ffmin/optimizers/gradient.py, Eq. (4))
@@ -100,6 +102,7 @@ __global__ void min_dir_kernel(MinState* S, cudaGraphConditionalHandle hls) {
 // after r = d / |d| and slope = <g, r>: LineSearcher.search, first attempt
 __global__ void min_ls_init_kernel(MinState* S, cudaGraphConditionalHandle hloop) {
   pdl_wait();
+  FFM_MSTAMP(3);
   pdl_launch_dependents();
   if (S->err) {  // an evaluation before the search failed (OFGM: value(y))
     cudaGraphSetConditional(hloop, 0);
@@ -122,6 +125,7 @@ __global__ void min_ls_step_kernel(MinState* S, const double* en, const int64_t*
 // lbfgs.py: what a line-search result does to the iteration
 __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditionalHandle hacc) {
   pdl_wait();
+  FFM_MSTAMP(7);
   pdl_launch_dependents();
   unsigned acc = 0;
   if (!S->err && S->c.method == kMethodFgm) {
@@ -208,6 +212,7 @@ __global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
 // after <s,y>, <s,s>, <y,y>: LbfgsMemory._commit
 __global__ void min_commit_kernel(MinState* S) {
   pdl_wait();
+  FFM_MSTAMP(8);
   pdl_launch_dependents();
   S->store_slot = -1;
   if (S->err) return;
@@ -777,6 +782,7 @@ __global__ void min_iter_end_kernel(MinState* S, double* rec) {
 
 __global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) {
   pdl_wait();
+  FFM_MSTAMP(9);
   pdl_launch_dependents();
   S->fgm_mode = 0;  // consumed by fgm_shift_kernel
   S->best_src = 0;
@@ -945,3 +951,9 @@ cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const 
 }
 
 }  // namespace ffm
+
+#ifdef FFM_MIN_STAMPS
+extern "C" int ffm_debug_min_clock_minimize(void* clock_d) {
+  return (int)cudaMemcpyToSymbol(ffm::g_mclk, &clock_d, sizeof(void*));
+}
+#endif

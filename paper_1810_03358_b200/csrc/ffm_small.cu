@@ -42,6 +42,9 @@ small_eval_kernel(SmallEvalArgs a) {
   __shared__ double gpart[kGatherWarpsTiles][3][32];
   __shared__ double sh[5][kTermThreads / 32];
   __shared__ double red[32];
+  __shared__ MinState ms;  // the probe controller's copy of the driver state
+  __shared__ int64_t st_s[kStWords];
+  __shared__ double en_s[5];  // stretch, bend, torsion, coulomb, vdw
   cg::grid_group grid = cg::this_grid();
   const NbPlanDev& plan = a.plan;
   const int n = plan.n;
@@ -62,6 +65,7 @@ small_eval_kernel(SmallEvalArgs a) {
     }
   };
   stamp(0);
+  FFM_MSTAMP(4);
 
   // a line-search trial repeats the whole evaluation for every probe the
   // controller asks for (one launch per search instead of one per probe:
@@ -82,6 +86,7 @@ small_eval_kernel(SmallEvalArgs a) {
     }
     grid.sync();
     stamp(1);
+    FFM_MSTAMP(10);
 
     // P1: CTA items -- the pair tiles (one CTA each, the longer items, first)
     // and the bonded / scaled-pair term blocks, dealt round-robin so a CTA
@@ -102,6 +107,7 @@ small_eval_kernel(SmallEvalArgs a) {
     stamp(2);
     grid.sync();
     stamp(3);
+    FFM_MSTAMP(11);
 
     // P2: the finder decision, made identically by every CTA: a coincident
     // pair shows as a non-finite tile partial (FP32) or a closest-pair r^2
@@ -136,13 +142,37 @@ small_eval_kernel(SmallEvalArgs a) {
     }
     // the CTA that reduced the energies finalises the status words and, for a
     // line-search trial, runs the probe controller (ffm_min_dev.cuh)
-    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
-      finalize_entry(n, a.status);
-      if (a.ls_state) mindev::ls_step(a.ls_state, a.energies, a.status, a.ls_loop);
+    FFM_MSTAMP_LAST(12);
+    if (blockIdx.x == gridDim.x - 1) {
+      // the probe controller works on a shared-memory copy of the driver
+      // state: its scalar logic is a chain of dependent reads and writes,
+      // ~4 us per probe as L2 round trips, one copy in and out instead
+      constexpr int kW = (int)(sizeof(MinState) / sizeof(unsigned long long));
+      static_assert(sizeof(MinState) % sizeof(unsigned long long) == 0, "MinState words");
+      unsigned long long* gw = reinterpret_cast<unsigned long long*>(a.ls_state);
+      unsigned long long* sw = reinterpret_cast<unsigned long long*>(&ms);
+      // (the status words and energies likewise: every input is read in one
+      // round trip, the outputs written back together)
+      if (a.ls_state)
+        for (int w = threadIdx.x; w < kW; w += kSmallThreads) sw[w] = gw[w];
+      if (threadIdx.x < kStWords) st_s[threadIdx.x] = a.status[threadIdx.x];
+      else if (threadIdx.x < kStWords + 5) en_s[threadIdx.x - kStWords] = a.energies[threadIdx.x - kStWords];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        finalize_entry(n, st_s);
+        if (a.ls_state) mindev::ls_step(&ms, en_s, st_s, a.ls_loop);
+      }
+      __syncthreads();
+      if (a.ls_state)
+        for (int w = threadIdx.x; w < kW; w += kSmallThreads) gw[w] = sw[w];
+      if (threadIdx.x < kStWords) a.status[threadIdx.x] = st_s[threadIdx.x];
     }
+    FFM_MSTAMP_LAST(13);
     stamp(5);
+    FFM_MSTAMP(5);
     if (!a.ls_state) break;
     grid.sync();  // the controller's decision and next step are visible to all CTAs
+    FFM_MSTAMP(14);
     if (!*(volatile int*)&a.ls_state->ls_more) break;
   }
 }
@@ -185,3 +215,9 @@ cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int 
 }
 
 }  // namespace ffm
+
+#ifdef FFM_MIN_STAMPS
+extern "C" int ffm_debug_min_clock_small(void* clock_d) {
+  return (int)cudaMemcpyToSymbol(ffm::g_mclk, &clock_d, sizeof(void*));
+}
+#endif

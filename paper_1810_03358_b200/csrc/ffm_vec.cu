@@ -102,6 +102,26 @@ dots_final_kernel(int k, const double* __restrict__ part, double* __restrict__ o
   }
 }
 
+// vectors this short are reduced by one block in one launch (the small
+// systems' minimiser graphs run ~3 of these per iteration: one node instead
+// of two, no partial round trip)
+constexpr int64_t kSmallVecN = 6144;
+
+__global__ void __launch_bounds__(kVecThreads)
+dots_small_kernel(int64_t n, DotArgs A, double* __restrict__ out) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ double sh[kVecThreads / 32];
+  for (int q = 0; q < A.k; ++q) {
+    double acc = 0.0;
+    const double* __restrict__ x = A.x[q];
+    const double* __restrict__ y = A.y[q];
+    for (int64_t i = threadIdx.x; i < n; i += kVecThreads) acc = fma(x[i], y[i], acc);
+    const double s = block_sum256(acc, sh);
+    if (threadIdx.x == 0) out[q] = s;
+  }
+}
+
 cudaError_t launch_dots(int64_t n, int k, const double* const* x, const double* const* y,
                         double* part, double* out, cudaStream_t st) {
   if (k < 1 || k > kMaxDots) return cudaErrorInvalidValue;
@@ -110,6 +130,11 @@ cudaError_t launch_dots(int64_t n, int k, const double* const* x, const double* 
   for (int q = 0; q < k; ++q) {
     A.x[q] = x[q];
     A.y[q] = y[q];
+  }
+  if (n <= kSmallVecN) {
+    count_launch();
+    launch_k(dots_small_kernel, 1, kVecThreads, 0, st, n, A, out);
+    return cudaGetLastError();
   }
   count_launch();
   launch_k(dots_partial_kernel, kVecBlocks, kVecThreads, 0, st, n, A, part);
@@ -170,6 +195,14 @@ __device__ __forceinline__ double grid_sum(const double* part) {
   return s;
 }
 
+// one-block grids (short vectors, two_loop_grid) are launched as plain
+// kernels and need only the block barrier; the global memory they exchange
+// through is then written and read by the same block
+__device__ __forceinline__ void grid_barrier(cg::grid_group& grid) {
+  if (gridDim.x == 1) __syncthreads();
+  else grid.sync();
+}
+
 __device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[kVecThreads / 32];
@@ -184,10 +217,10 @@ __device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
   double alpha[kMaxLbfgsPairs];
   int p = 0;
 
+  double a = 0.0, b = 0.0, c = 0.0;
   {  // phase 0: q = g;  <s_0, g>, <s_0, y_0>, <y_0, y_0>  (index 0 = newest)
     const double* s0 = A.S + (int64_t)A.idx[0] * n;
     const double* y0 = A.Y + (int64_t)A.idx[0] * n;
-    double a = 0.0, b = 0.0, c = 0.0;
     for (int64_t i = i0; i < n; i += stride) {
       const double v = A.g[i];
       A.q[i] = v;
@@ -198,21 +231,25 @@ __device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
     a = block_sum256(a, sh);
     b = block_sum256(b, sh);
     c = block_sum256(c, sh);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && gridDim.x > 1) {
       rot[blockIdx.x] = a;
       psy[blockIdx.x] = b;
       pyy[blockIdx.x] = c;
     }
   }
-  grid.sync();
-  if (threadIdx.x == 0) bc = grid_sum(psy) / grid_sum(pyy);
+  grid_barrier(grid);
+  // one-block grids: thread 0 already holds the block sums (grid_sum of one
+  // partial is 0 + it, the same bits), no global round trip per phase
+  const bool one = G == 1;
+  double prev_sum = a;  // thread 0: the block sum the next phase reads
+  if (threadIdx.x == 0) bc = one ? (0.0 + b) / (0.0 + c) : grid_sum(psy) / grid_sum(pyy);
   __syncthreads();
   const double gamma = bc;  // <s,y>/<y,y> of the newest pair (H0 scaling)
 
   // first loop, newest -> oldest: alpha_k = rho_k <s_k, q>;  q -= alpha_k y_k
   for (int k = 0; k < A.count; ++k) {
     __syncthreads();
-    if (threadIdx.x == 0) bc = A.rho[k] * grid_sum(rot + (p % 3) * kVecBlocks);
+    if (threadIdx.x == 0) bc = A.rho[k] * (one ? 0.0 + prev_sum : grid_sum(rot + (p % 3) * kVecBlocks));
     __syncthreads();
     alpha[k] = bc;
     const bool last = k + 1 == A.count;
@@ -229,13 +266,14 @@ __device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
     }
     acc = block_sum256(acc, sh);
     ++p;
-    if (threadIdx.x == 0) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
-    grid.sync();
+    prev_sum = acc;
+    if (threadIdx.x == 0 && !one) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
+    grid_barrier(grid);
   }
   // second loop, oldest -> newest: beta = rho_k <y_k, q>;  q += (alpha_k - beta) s_k
   for (int k = A.count - 1; k >= 0; --k) {
     __syncthreads();
-    if (threadIdx.x == 0) bc = A.rho[k] * grid_sum(rot + (p % 3) * kVecBlocks);
+    if (threadIdx.x == 0) bc = A.rho[k] * (one ? 0.0 + prev_sum : grid_sum(rot + (p % 3) * kVecBlocks));
     __syncthreads();
     const double coef = alpha[k] - bc;
     const double* s = A.S + (int64_t)A.idx[k] * n;
@@ -252,13 +290,16 @@ __device__ __forceinline__ void two_loop_body(const TwoLoopArgs& A) {
     }
     acc = block_sum256(acc, sh);
     ++p;
-    if (threadIdx.x == 0) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
-    grid.sync();
+    prev_sum = acc;
+    if (threadIdx.x == 0 && !one) rot[(p % 3) * kVecBlocks + blockIdx.x] = acc;
+    grid_barrier(grid);
   }
-  (void)G;
 }
 
-__global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) { two_loop_body(A); }
+__global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
+  pdl_wait();  // (one-block grids are plain launches with programmatic serialization)
+  two_loop_body(A);
+}
 
 // Device-driven variant for the graph-resident L-BFGS (ffm_min.cuh): the
 // pair count, ring slots (newest first) and rho come from device memory.
@@ -278,6 +319,7 @@ struct TwoLoopDevArgs {
 };
 
 __global__ void __launch_bounds__(kVecThreads) two_loop_dev_kernel(TwoLoopDevArgs D) {
+  pdl_wait();
   const int count = *D.count;
   if (count == 0) {
     const double gn = *D.gn;
@@ -316,6 +358,7 @@ static int two_loop_grid(int64_t n) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, two_loop_dev_kernel, kVecThreads, 0);
   if (per_sm2 < per_sm) per_sm = per_sm2;
   int blocks = sms * (per_sm < 2 ? per_sm : 2);
+  if (n <= kSmallVecN) return 1;  // one block: plain launch, block barriers only
   const int64_t need = (n + kVecThreads - 1) / kVecThreads;
   if (blocks > need) blocks = (int)need;
   if (blocks > kVecBlocks) blocks = kVecBlocks;
@@ -341,8 +384,12 @@ cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const do
   a.part = scratch;
   void* args[] = {&a};
   count_launch();
-  return cudaLaunchCooperativeKernel((void*)two_loop_kernel, two_loop_grid(n), kVecThreads,
-                                     args, 0, st);
+  const int grid = two_loop_grid(n);
+  if (grid == 1) {
+    launch_k(two_loop_kernel, 1, kVecThreads, 0, st, a);
+    return cudaGetLastError();
+  }
+  return cudaLaunchCooperativeKernel((void*)two_loop_kernel, grid, kVecThreads, args, 0, st);
 }
 
 cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* idx,
@@ -352,8 +399,13 @@ cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* id
   TwoLoopDevArgs d{n, count, idx, rho, gn, S, Y, g, q, scratch};
   void* args[] = {&d};
   count_launch();
-  return cudaLaunchCooperativeKernel((void*)two_loop_dev_kernel, two_loop_grid(n), kVecThreads,
-                                     args, 0, st);
+  const int grid = two_loop_grid(n);
+  if (grid == 1) {
+    launch_k(two_loop_dev_kernel, 1, kVecThreads, 0, st, d);
+    return cudaGetLastError();
+  }
+  return cudaLaunchCooperativeKernel((void*)two_loop_dev_kernel, grid, kVecThreads, args, 0,
+                                     st);
 }
 
 }  // namespace ffm
