@@ -1429,7 +1429,7 @@ int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls)
   MinState* S = L->S;
   const int method = L->cfg.method;
   if (method == kMethodLbfgs)
-    FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, &S->count, S->idx_nf, S->rho_nf, &S->gn,
+    FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, L->cfg.m, &S->count, S->idx_nf, S->rho_nf, &S->gn,
                                        L->ring_s, L->ring_y, L->g, L->d, L->scratch, st));
   if (method != kMethodSd) {  // L-BFGS: d = two-loop direction; CG: d = p
     const double* xs[1] = {L->d};
@@ -1761,6 +1761,7 @@ int lbfgs_build(ffm_lbfgs* L) {
   // attributes are set on first launch)
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, L->cap[0]));
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->gnew, L->en, L->stw, L->cap[0]));
+  FFM_CUDA(two_loop_small_prepare());
   FFM_CUDA(cudaStreamSynchronize(L->cap[0]));
   MinState* S = L->S;
   const long long before = g_launch_count.load();

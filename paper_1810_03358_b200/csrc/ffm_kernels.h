@@ -194,10 +194,12 @@ cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const do
                                   const double* S, const double* Y, const double* g,
                                   double* q, double* scratch, cudaStream_t st);
 // the same with count / slots / rho / |g| read from device memory
-cudaError_t launch_lbfgs_two_loop_dev(int64_t n, const int* count, const int* idx,
+// m: the ring capacity (sizes the short-vector variant's shared staging)
+cudaError_t launch_lbfgs_two_loop_dev(int64_t n, int m, const int* count, const int* idx,
                                       const double* rho, const double* gn, const double* S,
                                       const double* Y, const double* g, double* q,
                                       double* scratch, cudaStream_t st);
+cudaError_t two_loop_small_prepare();  // once, outside graph capture
 
 // ---- device-resident L-BFGS controllers (ffm_minimize.cu, state in ffm_min.cuh) ----
 struct MinState;
