@@ -2,7 +2,8 @@
 library built with -DFFM_MIN_STAMPS (tools/build_lib_variant.sh mstamps
 -DFFM_MIN_STAMPS).  Tags: 1 it_begin, 2 min_dir, 3 ls_init, 4 fused
 evaluation start, 10 its P1 start, 11 its P2 start, 5 its pass end, 7
-ls_post, 8 commit, 9 it_end.
+ls_post, 8 commit, 9 it_end, 12/13 around the fused kernel's probe
+controller, 14 after its loop barrier, 20/21 two-loop kernel start/end, 22 one-block dots.
 usage: FFMIN_B200_LIB=... python tools/lbfgs_timeline.py [N] [iters]"""
 import collections
 import ctypes as C
@@ -26,14 +27,14 @@ lbfgs(o, s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
       stop=StopCriteria(max_iterations=2, gradient_norm_rtol=1e-6))
 lib = N.load()
 buf = torch.zeros(1 + 2 * 200000, dtype=torch.int64, device="cuda")
-for f in ("ffm_debug_min_clock_minimize", "ffm_debug_min_clock_small"):
+for f in ("ffm_debug_min_clock_minimize", "ffm_debug_min_clock_small", "ffm_debug_min_clock_vec"):
     getattr(lib, f).argtypes = [C.c_void_p]
     assert getattr(lib, f)(C.c_void_p(buf.data_ptr())) == 0
 torch.cuda.synchronize()
 res = lbfgs(o, s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
             stop=StopCriteria(max_iterations=it, gradient_norm_rtol=1e-6))
 torch.cuda.synchronize()
-for f in ("ffm_debug_min_clock_minimize", "ffm_debug_min_clock_small"):
+for f in ("ffm_debug_min_clock_minimize", "ffm_debug_min_clock_small", "ffm_debug_min_clock_vec"):
     getattr(lib, f)(None)
 b = buf.cpu().numpy()
 k = int(b[0])
