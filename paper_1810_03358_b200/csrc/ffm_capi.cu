@@ -81,6 +81,7 @@ struct Work {
   double* epart = nullptr; // [batch][nunits][3]
   int e_batch = 0;
   double* term_e = nullptr;  // [batch][nterm_e]
+  int64_t* term_st = nullptr;  // [term blocks * 4 warps][4]: tiny systems' term status slots
   int te_batch = 0;
   double* term_f = nullptr;  // [nslots][3]
   double* escratch = nullptr;  // split energy reduction: [kMaxEnergyParts][3] + counter
@@ -146,7 +147,7 @@ struct ffm_system {
   // row sharding (ffm_system_set_shard): units u with u % nranks == rank
   int rank = 0, nranks = 1;
   // fused small-system evaluation: cooperative grid per [precision][grad], 0 = not sized yet
-  int small_grid[2][2] = {{0, 0}, {0, 0}};
+  int small_grid[2][2][2] = {};  // [precision][grad][kernel variant (small_fromx)]
   unsigned long long* phase_clock = nullptr;  // ffm_debug_phase_clock (tuning aid)
   int* d_unit_list = nullptr;
   std::vector<char> unit_live;  // host: slot holds a real unit (build_units)
@@ -210,7 +211,7 @@ void free_all(ffm_system* s) {
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
   for (auto& w : s->w) {
     void* wp[] = {w.pos, w.ipos, w.bbox, w.ipart, w.jpart, w.epart, w.term_e, w.term_f,
-                  w.escratch};
+                  w.escratch, w.term_st};
     for (void* p : wp)
       if (p) cudaFree(p);
   }
@@ -487,8 +488,10 @@ int build_terms(ffm_system* s, int64_t nbond, const int64_t* bidx, const double*
   for (auto& w : s->w) {
     if (w.term_e) cudaFree(w.term_e);
     if (w.term_f) cudaFree(w.term_f);
+    if (w.term_st) cudaFree(w.term_st);
     w.term_e = nullptr;
     w.term_f = nullptr;
+    w.term_st = nullptr;
     w.te_batch = 0;
   }
   return FFM_OK;
@@ -551,14 +554,16 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
   struct Bump {
     ffm_system* s;
     Work* w;
-    void* p[8];
+    void* p[9];
     Bump(ffm_system* s_, Work* w_) : s(s_), w(w_) {
-      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox};
-      for (int i = 0; i < 8; ++i) p[i] = q[i];
+      void* q[9] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox,
+                    w->term_st};
+      for (int i = 0; i < 9; ++i) p[i] = q[i];
     }
     ~Bump() {
-      void* q[8] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox};
-      for (int i = 0; i < 8; ++i)
+      void* q[9] = {w->pos, w->ipos, w->ipart, w->jpart, w->epart, w->term_e, w->term_f, w->bbox,
+                    w->term_st};
+      for (int i = 0; i < 9; ++i)
         if (q[i] != p[i]) {
           drop_graphs(s);
           break;
@@ -623,6 +628,11 @@ int ensure_work(ffm_system* s, int prec, int batch, bool grad) {
     if (cudaMalloc(&w.term_e, (size_t)batch * ne * sizeof(double)) != cudaSuccess)
       return fail(FFM_ENOMEM, "cudaMalloc failed for term energies");
     w.te_batch = batch;
+  }
+  if (!w.term_st) {
+    const size_t nw = (size_t)std::max(1, term_blocks(s->tp)) * kTermSlotsPerBlock;
+    if (cudaMalloc(&w.term_st, nw * 4 * sizeof(int64_t)) != cudaSuccess)
+      return fail(FFM_ENOMEM, "cudaMalloc failed for term status slots");
   }
   if (grad && !w.term_f) {
     const size_t nsl = std::max(1, s->tp.nslots);
@@ -990,7 +1000,7 @@ int ffm_debug_phase_clock(ffm_system_t* s, void* clock_d, int* grids) {
   if (!s || !grids) return fail(FFM_EINVAL, "NULL argument");
   s->phase_clock = static_cast<unsigned long long*>(clock_d);
   for (int p = 0; p < 2; ++p)
-    for (int g = 0; g < 2; ++g) grids[2 * p + g] = s->small_grid[p][g];
+    for (int g = 0; g < 2; ++g) grids[2 * p + g] = s->small_grid[p][g][0] ? s->small_grid[p][g][0] : s->small_grid[p][g][1];
   return FFM_OK;
 }
 
@@ -1036,7 +1046,7 @@ static int issue_small(ffm_system* s, int precision, bool grad, const double* co
   *launched = false;
   Work& w = s->w[precision];
   const bool f64 = precision == FFM_F64;
-  int& grid = s->small_grid[precision][grad ? 1 : 0];
+  int* grid_slot = s->small_grid[precision][grad ? 1 : 0];  // [variant], picked once a is filled
   SmallEvalArgs a;
   a.plan = s->plan;
   a.tp = s->tp;
@@ -1052,6 +1062,7 @@ static int issue_small(ffm_system* s, int precision, bool grad, const double* co
   a.epart = w.epart;
   a.term_part = w.term_e;
   a.term_f = w.term_f;
+  a.term_st = w.term_st;
   a.trow_ptr = s->d_trow_ptr;
   a.tcol_ptr = s->d_tcol_ptr;
   a.tcol_idx = s->d_tcol_idx;
@@ -1070,6 +1081,7 @@ static int issue_small(ffm_system* s, int precision, bool grad, const double* co
   a.trial_h = trial_h;
   a.ls_state = ls_state;
   a.ls_loop = ls_loop;
+  int& grid = grid_slot[small_fromx(a, f64) ? 1 : 0];
   if (grid == 0) grid = small_eval_grid(a, f64, grad, s->device);
   if (grid <= 0) return FFM_OK;
   FFM_CUDA(launch_small_eval(a, f64, grad, grid, st));

@@ -201,6 +201,16 @@ template <typename T> struct Vec2T;
 template <> struct Vec2T<float> { using type = float2; };
 template <> struct Vec2T<double> { using type = double2; };
 
+// Coordinates of an evaluation: x itself, or a line-search trial point
+// x + h r formed on the fly with the same fma as the trial buffer's
+// (ffm_small.cu P0), so every reader sees the same doubles.
+struct CoordSrc {
+  const double* x;
+  const double* r;  // null: plain coordinates
+  double h;
+  __device__ __forceinline__ double at(int64_t q) const { return r ? fma(h, r[q], x[q]) : x[q]; }
+};
+
 // Status words written by the kernels (device int64[kStatusWords]).
 enum StatusSlot : int {
   kStNbBadI = 0,      // first coincident nonbonded pair (i, j), -1 clean

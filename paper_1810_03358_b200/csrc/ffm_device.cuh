@@ -8,6 +8,7 @@
 // 130-140) see the same roundoff as the reference's CPU arithmetic.
 #pragma once
 #include <cfloat>
+#include <climits>
 #include "ffm_plan.cuh"
 
 namespace ffm {
@@ -74,6 +75,9 @@ struct P3 {
   double x, y, z;
 };
 __device__ __forceinline__ P3 ld3(const double* c, int i) { return {c[3 * i], c[3 * i + 1], c[3 * i + 2]}; }
+__device__ __forceinline__ P3 ld3(const CoordSrc& cs, int i) {
+  return {cs.at(3 * (int64_t)i), cs.at(3 * (int64_t)i + 1), cs.at(3 * (int64_t)i + 2)};
+}
 __device__ __forceinline__ P3 sub(P3 a, P3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
 __device__ __forceinline__ double dot(P3 a, P3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 __device__ __forceinline__ P3 cross(P3 a, P3 b) {
@@ -208,22 +212,31 @@ __device__ __forceinline__ int term_block_count(const TermPlanDev& tp) {
   return (tot + kTermThreads - 1) / kTermThreads;
 }
 
-__device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
-                                           const double* __restrict__ coords,
+// One virtual block of kTermThreads bonded / scaled-pair terms.  Status:
+// with warp_slots null the degenerate-term indices go straight into the
+// status words (amin; the caller reset them beforehand); else each warp
+// writes its own four words -- the first degenerate bond, angle and
+// dihedral (kSentinel: none) and a scaled-pair coincidence flag -- to
+// warp_slots[4 (kTermThreads / 32 vb + warp) ..], folded into the status
+// words after a barrier (status_from_term_slots), so no reset has to
+// precede the block (the fused small evaluation without a packing pass).
+__device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad, CoordSrc cs,
                                            double* __restrict__ term_part,
                                            double* __restrict__ term_f,
                                            int64_t* __restrict__ status, int b, int vb, int nvb,
-                                           double (*sh)[kTermThreads / 32]) {
-  coords += (size_t)b * tp.n * 3;
+                                           double (*sh)[kTermThreads / 32],
+                                           int64_t* __restrict__ warp_slots = nullptr) {
+  cs.x += (size_t)b * tp.n * 3;
   status += (size_t)b * kStWords;
   double e5[5] = {0.0, 0.0, 0.0, 0.0, 0.0};  // stretch, bend, torsion, coulomb, vdw
+  int bad_b = INT_MAX, bad_a = INT_MAX, bad_d = INT_MAX, bad_nb = 0;
   int t = vb * kTermThreads + threadIdx.x;
   if (t < tp.nbond) {
     const int i = tp.bond_idx[2 * t], j = tp.bond_idx[2 * t + 1];
     double e = 0.0;
     P3 gi = {0, 0, 0};
-    if (!bond_term(ld3(coords, i), ld3(coords, j), tp.bond_K[t], tp.bond_r0[t], grad, &e, &gi))
-      amin(status + kStBond, t);
+    if (!bond_term(ld3(cs, i), ld3(cs, j), tp.bond_K[t], tp.bond_r0[t], grad, &e, &gi))
+      bad_b = t;
     e5[0] = e;
     if (grad) {
       st3(term_f + 3 * (2 * t), gi);
@@ -233,9 +246,9 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
     const int i = tp.ang_idx[3 * t], j = tp.ang_idx[3 * t + 1], k = tp.ang_idx[3 * t + 2];
     double e = 0.0;
     P3 gi = {0, 0, 0}, gk = {0, 0, 0};
-    if (!angle_term(ld3(coords, i), ld3(coords, j), ld3(coords, k), tp.ang_K[t], tp.ang_t0[t],
-                    grad, &e, &gi, &gk)) {
-      amin(status + kStAngle, t);
+    if (!angle_term(ld3(cs, i), ld3(cs, j), ld3(cs, k), tp.ang_K[t], tp.ang_t0[t], grad, &e,
+                    &gi, &gk)) {
+      bad_a = t;
       e = 0.0;
       gi = gk = {0, 0, 0};
     }
@@ -250,9 +263,9 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
     const int* id = tp.dih_idx + 4 * t;
     double e = 0.0;
     P3 g[4] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-    if (!dihedral_term(ld3(coords, id[0]), ld3(coords, id[1]), ld3(coords, id[2]),
-                       ld3(coords, id[3]), tp.dih_V + 4 * t, grad, &e, g)) {
-      amin(status + kStDihedral, t);
+    if (!dihedral_term(ld3(cs, id[0]), ld3(cs, id[1]), ld3(cs, id[2]), ld3(cs, id[3]),
+                       tp.dih_V + 4 * t, grad, &e, g)) {
+      bad_d = t;
       e = 0.0;
       g[0] = g[1] = g[2] = g[3] = {0, 0, 0};
     }
@@ -265,10 +278,10 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
     const int i = tp.sc_idx[2 * t], j = tp.sc_idx[2 * t + 1];
     double ec, ev;
     P3 gi;
-    if (!scaled_pair(ld3(coords, i), ld3(coords, j), tp.q[i], tp.q[j], tp.sigma[i],
-                     tp.sigma[j], tp.eps[i], tp.eps[j], tp.sc_s[t], tp.has_cutoff != 0,
-                     tp.cutoff, grad, &ec, &ev, &gi))
-      status[kStNbSuspect] = 1;
+    if (!scaled_pair(ld3(cs, i), ld3(cs, j), tp.q[i], tp.q[j], tp.sigma[i], tp.sigma[j],
+                     tp.eps[i], tp.eps[j], tp.sc_s[t], tp.has_cutoff != 0, tp.cutoff, grad, &ec,
+                     &ev, &gi))
+      bad_nb = 1;
     e5[3] = ec;
     e5[4] = ev;
     if (grad) {
@@ -278,6 +291,24 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
     }
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp_slots) {
+    const unsigned mb = __reduce_min_sync(0xffffffffu, (unsigned)bad_b);
+    const unsigned ma = __reduce_min_sync(0xffffffffu, (unsigned)bad_a);
+    const unsigned md = __reduce_min_sync(0xffffffffu, (unsigned)bad_d);
+    const bool fl = __any_sync(0xffffffffu, bad_nb);
+    if (lane == 0) {
+      int64_t* w = warp_slots + 4 * ((size_t)vb * (kTermThreads / 32) + warp);
+      w[0] = mb == (unsigned)INT_MAX ? kSentinel : (int64_t)mb;
+      w[1] = ma == (unsigned)INT_MAX ? kSentinel : (int64_t)ma;
+      w[2] = md == (unsigned)INT_MAX ? kSentinel : (int64_t)md;
+      w[3] = fl ? 1 : 0;
+    }
+  } else {
+    if (bad_b != INT_MAX) amin(status + kStBond, bad_b);
+    if (bad_a != INT_MAX) amin(status + kStAngle, bad_a);
+    if (bad_d != INT_MAX) amin(status + kStDihedral, bad_d);
+    if (bad_nb) status[kStNbSuspect] = 1;
+  }
 #pragma unroll
   for (int c = 0; c < 5; ++c) {
     double v = e5[c];
@@ -291,6 +322,50 @@ __device__ __forceinline__ void term_block(const TermPlanDev& tp, bool grad,
     term_part[((size_t)b * nvb + vb) * 5 + threadIdx.x] = v;
   }
   __syncthreads();  // sh is reused by the next virtual block
+}
+
+// The status words from the term blocks' warp slots (block-uniform: the
+// threads scan shares of the slots, thread 0 writes when `write`); returns
+// the scaled-pair coincidence flag to every thread.  st: the status words
+// to fill (global or a shared copy).
+__device__ __forceinline__ int status_from_term_slots(const int64_t* __restrict__ slots,
+                                                      int nwarps, int64_t* st, bool write,
+                                                      int64_t (*sh)[kTermThreads / 32]) {
+  int64_t mb = kSentinel, ma = kSentinel, md = kSentinel;
+  int fl = 0;
+  for (int k = threadIdx.x; k < nwarps; k += blockDim.x) {
+    const int64_t* w = slots + 4 * (size_t)k;
+    mb = min(mb, w[0]);
+    ma = min(ma, w[1]);
+    md = min(md, w[2]);
+    fl |= w[3] != 0;
+  }
+  fl = __syncthreads_or(fl);
+  if (!write) return fl;
+  for (int o = 16; o > 0; o >>= 1) {
+    mb = min(mb, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mb, o));
+    ma = min(ma, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)ma, o));
+    md = min(md, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)md, o));
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    sh[0][warp] = mb;
+    sh[1][warp] = ma;
+    sh[2][warp] = md;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      mb = min(mb, sh[0][w]);
+      ma = min(ma, sh[1][w]);
+      md = min(md, sh[2][w]);
+    }
+    st[kStBond] = mb;
+    st[kStAngle] = ma;
+    st[kStDihedral] = md;
+  }
+  __syncthreads();
+  return fl;
 }
 
 // ---------------------------------------------------------- gradient gather

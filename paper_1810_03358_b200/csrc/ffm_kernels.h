@@ -128,6 +128,8 @@ cudaError_t launch_farfield(const TermPlanDev& tp, const double* coords, const i
 // One cooperative launch = pack + term blocks + pair tiles + gather +
 // reduction (+ finder when flagged) for a tile-mode system evaluated whole
 // (batch 1, unsharded, all terms), same bits as the kernel chain.
+// term status slots per term block (one per warp of its kTermThreads)
+constexpr int kTermSlotsPerBlock = 4;
 struct SmallEvalArgs {
   NbPlanDev plan;
   TermPlanDev tp;
@@ -143,6 +145,7 @@ struct SmallEvalArgs {
   double* epart;
   double* term_part;
   double* term_f;
+  int64_t* term_st;  // [nterm_blocks * kTermSlotsPerBlock][4] term status slots (tiny systems)
   const int* trow_ptr;
   const int* tcol_ptr;
   const int* tcol_idx;
@@ -166,8 +169,10 @@ struct SmallEvalArgs {
   struct MinState* ls_state;
   cudaGraphConditionalHandle ls_loop;
 };
-// grid size (co-resident CTAs, at most what the work needs); 0 on error
+// grid size (co-resident CTAs, at most what the work needs) of the kernel
+// variant this call selects (small_fromx); 0 on error
 int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device);
+bool small_fromx(const SmallEvalArgs& a, bool fp64);
 cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int grid,
                               cudaStream_t st);
 

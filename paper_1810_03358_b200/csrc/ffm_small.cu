@@ -18,6 +18,7 @@
 // Compiled with -fmad=false like ffm_terms.cu (the bonded terms need it; the
 // pair tile arithmetic is explicit and flag-independent).
 #include <algorithm>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -32,8 +33,14 @@ namespace cg = cooperative_groups;
 
 constexpr int kSmallThreads = 128;  // = kTermThreads = kRedThreads = 4 tile warps
 static_assert(kSmallThreads == kTermThreads && kSmallThreads == kRedThreads, "block shape");
+static_assert(kTermSlotsPerBlock == kTermThreads / 32, "term status slots: one per warp");
 
-template <typename T, bool GRAD, bool CUTOFF>
+// FROMX (tiny systems, small_fromx): no packing pass and no barrier after
+// P0 -- the pair tiles read positions and charges straight from the
+// coordinates, line-search trial points are formed on the fly by every
+// reader with the trial buffer's fma, and the term blocks leave their status
+// in per-warp slots folded after P1; the same arithmetic, so the same bits.
+template <typename T, bool GRAD, bool CUTOFF, bool FROMX>
 __global__ void __launch_bounds__(kSmallThreads)
 small_eval_kernel(SmallEvalArgs a) {
   using V4 = typename Vec4T<T>::type;
@@ -45,6 +52,7 @@ small_eval_kernel(SmallEvalArgs a) {
   __shared__ MinState ms;  // the probe controller's copy of the driver state
   __shared__ int64_t st_s[kStWords];
   __shared__ double en_s[5];  // stretch, bend, torsion, coulomb, vdw
+  __shared__ int64_t shs[3][kTermThreads / 32];
   cg::grid_group grid = cg::this_grid();
   const NbPlanDev& plan = a.plan;
   const int n = plan.n;
@@ -76,15 +84,34 @@ small_eval_kernel(SmallEvalArgs a) {
     // the axpby of the host-driven loop, into the trial buffer)
     const double* coords = a.trial_out ? a.trial_out : a.coords;
     const double th = a.trial_out ? *(volatile const double*)a.trial_h : 0.0;
-    for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs) {
-      if (a.trial_out && k < n)
-        for (int c = 0; c < 3; ++c) {
-          const int64_t q = 3 * k + c;
-          a.trial_out[q] = fma(th, a.trial_r[q], 1.0 * a.trial_x[q]);
-        }
-      pack_item<T>(k, n, plan.np, 1, coords, a.qt, pos, ipos, a.status);
+    // FROMX readers form x_t themselves; the others read the trial buffer
+    const CoordSrc cs = FROMX && a.trial_out ? CoordSrc{a.trial_x, a.trial_r, th}
+                                             : CoordSrc{coords, nullptr, 0.0};
+    if constexpr (FROMX) {
+      if (gt == 0) {
+        int64_t* st = a.status;
+        st[kStNbBadI] = -1;
+        st[kStNbBadJ] = -1;
+        st[kStBond] = kSentinel;
+        st[kStAngle] = kSentinel;
+        st[kStDihedral] = kSentinel;
+        st[kStNbSuspect] = 0;
+        st[kStNbKey] = kSentinel;
+        st[kStCount] = 0;
+      }
+      if (a.trial_out)
+        for (int64_t q = gt; q < 3 * (int64_t)n; q += gs) a.trial_out[q] = cs.at(q);
+    } else {
+      for (int64_t k = gt; k < (n > 1 ? n : 1); k += gs) {
+        if (a.trial_out && k < n)
+          for (int c = 0; c < 3; ++c) {
+            const int64_t q = 3 * k + c;
+            a.trial_out[q] = fma(th, a.trial_r[q], 1.0 * a.trial_x[q]);
+          }
+        pack_item<T>(k, n, plan.np, 1, coords, a.qt, pos, ipos, a.status);
+      }
+      grid.sync();
     }
-    grid.sync();
     stamp(1);
     FFM_MSTAMP(10);
 
@@ -97,11 +124,12 @@ small_eval_kernel(SmallEvalArgs a) {
     const int nitems = plan.nlaunch + a.nterm_blocks;
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
       if (it < plan.nlaunch)
-        tile_cta<T, GRAD, CUTOFF>(plan, pos, static_cast<const V2*>(a.lj), ipos,
-                                  static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it, 0, tsm);
+        tile_cta<T, GRAD, CUTOFF, FROMX>(plan, pos, static_cast<const V2*>(a.lj), ipos,
+                                         static_cast<const T*>(a.ilj), ipart, jpart, a.epart, it,
+                                         0, tsm, cs, a.qt);
       else
-        term_block(a.tp, GRAD, coords, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
-                   a.nterm_blocks, sh);
+        term_block(a.tp, GRAD, cs, a.term_part, a.term_f, a.status, 0, it - plan.nlaunch,
+                   a.nterm_blocks, sh, FROMX ? a.term_st : nullptr);
     }
     __syncthreads();
     stamp(2);
@@ -115,13 +143,16 @@ small_eval_kernel(SmallEvalArgs a) {
     // thread tests its tiles without an early exit, so its partial loads go
     // out together (the early-exit scan was ~ntiles / 128 dependent L2 round
     // trips per CTA: 6.7 us of the 3000-atom evaluation)
-    int bad = *(volatile const int64_t*)(a.status + kStNbSuspect) != 0;
+    int bad = FROMX ? 0 : *(volatile const int64_t*)(a.status + kStNbSuspect) != 0;
 #pragma unroll 8
     for (int t = threadIdx.x; t < plan.ntiles; t += kSmallThreads) {
       const double* e = a.epart + 3 * (size_t)t;
       bad |= !isfinite(e[0]) | !isfinite(e[1]) | (e[2] < kRmin * kRmin);
     }
-    const int suspect = __syncthreads_or(bad);
+    int suspect = __syncthreads_or(bad);
+    if constexpr (FROMX)  // the term blocks' slots (the last CTA also writes the status words)
+      suspect |= status_from_term_slots(a.term_st, a.nterm_blocks * kTermSlotsPerBlock, a.status,
+                                        blockIdx.x == gridDim.x - 1, shs);
     if (GRAD)  // 32-atom groups, the same 4-warp split as the chain's gather
       for (int g = blockIdx.x; g < ((n + 31) >> 5); g += gridDim.x)
         gather_group<T, kGatherWarpsTiles>(g, n, plan.S, plan.nb, nullptr, a.trow_ptr, a.tcol_ptr,
@@ -135,6 +166,14 @@ small_eval_kernel(SmallEvalArgs a) {
     stamp(4);
     if (suspect) {  // P3 (uniform across the grid)
       grid.sync();
+      if constexpr (FROMX) {  // the finder reads packed positions: pack them now
+        for (int64_t i = gt; i < n; i += gs) {
+          V4 p;
+          atom_record<T>(cs, a.qt, n, (int)i, p.x, p.y, p.z, p.w);
+          pos[i] = p;
+        }
+        grid.sync();
+      }
       for (int64_t i = gt; i < n; i += gs)
         finder_row<T>((int)i, n, pos, a.sp_ptr, a.sp_j, a.sp_s, a.status);
       grid.sync();
@@ -178,25 +217,48 @@ small_eval_kernel(SmallEvalArgs a) {
 }
 
 template <typename T, bool GRAD, bool CUTOFF>
-static void* small_kernel_ptr() {
-  return reinterpret_cast<void*>(&small_eval_kernel<T, GRAD, CUTOFF>);
+static void* small_kernel_ptr(bool fromx) {
+  return fromx ? reinterpret_cast<void*>(&small_eval_kernel<T, GRAD, CUTOFF, true>)
+               : reinterpret_cast<void*>(&small_eval_kernel<T, GRAD, CUTOFF, false>);
 }
 
-static void* small_kernel(bool fp64, bool grad, bool cut) {
+static void* small_kernel(bool fp64, bool grad, bool cut, bool fromx) {
   if (fp64) {
-    if (grad) return cut ? small_kernel_ptr<double, true, true>() : small_kernel_ptr<double, true, false>();
-    return cut ? small_kernel_ptr<double, false, true>() : small_kernel_ptr<double, false, false>();
+    if (grad) return cut ? small_kernel_ptr<double, true, true>(fromx) : small_kernel_ptr<double, true, false>(fromx);
+    return cut ? small_kernel_ptr<double, false, true>(fromx) : small_kernel_ptr<double, false, false>(fromx);
   }
-  if (grad) return cut ? small_kernel_ptr<float, true, true>() : small_kernel_ptr<float, true, false>();
-  return cut ? small_kernel_ptr<float, false, true>() : small_kernel_ptr<float, false, false>();
+  if (grad) return cut ? small_kernel_ptr<float, true, true>(fromx) : small_kernel_ptr<float, true, false>(fromx);
+  return cut ? small_kernel_ptr<float, false, true>(fromx) : small_kernel_ptr<float, false, false>(fromx);
+}
+
+// The FROMX variant (small_eval_kernel) where it measured faster (one B200,
+// profiles/r02_small_tile_loads.log): FP32 evaluations up to 1500 atoms
+// (500 atoms 16.5 -> 14.6 us, 1500 18.1 -> 16.9 us) and line-search trials
+// in both precisions (FP64 L-BFGS, 500 atoms 0.179 -> 0.174 ms per
+// iteration); a single FP64 evaluation keeps the packing pass (500 atoms
+// 13.1 vs 14.6 us).
+#ifndef FFM_SMALL_FROMX_MAXN
+#define FFM_SMALL_FROMX_MAXN 1500
+#endif
+bool small_fromx(const SmallEvalArgs& a, bool fp64) {
+  static const int maxn = [] {
+    const char* f = getenv("FFM_SMALL_FROMX_MAXN");  // tuning aid
+    return f ? atoi(f) : FFM_SMALL_FROMX_MAXN;
+  }();
+  static const bool f64_all = [] {
+    const char* f = getenv("FFM_SMALL_FROMX_F64");  // tuning aid: FP64 single evaluations too
+    return f && atoi(f) != 0;
+  }();
+  return a.plan.n <= maxn && a.term_st != nullptr && (!fp64 || f64_all || a.ls_state != nullptr);
 }
 
 int small_eval_grid(const SmallEvalArgs& a, bool fp64, bool grad, int device) {
   const bool cut = a.plan.has_cutoff != 0;
   int sms = 0, per_sm = 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel(fp64, grad, cut),
-                                                    kSmallThreads, 0) != cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+          &per_sm, small_kernel(fp64, grad, cut, small_fromx(a, fp64)), kSmallThreads, 0) !=
+          cudaSuccess)
     return 0;
   int64_t want = 1;
   want = std::max<int64_t>(want, (int64_t)a.plan.nlaunch + a.nterm_blocks);
@@ -210,7 +272,7 @@ cudaError_t launch_small_eval(const SmallEvalArgs& a, bool fp64, bool grad, int 
   SmallEvalArgs args = a;
   void* params[] = {&args};
   count_launch();
-  return cudaLaunchCooperativeKernel(small_kernel(fp64, grad, a.plan.has_cutoff != 0),
+  return cudaLaunchCooperativeKernel(small_kernel(fp64, grad, a.plan.has_cutoff != 0, small_fromx(a, fp64)),
                                      dim3(grid), dim3(kSmallThreads), params, 0, st);
 }
 

@@ -94,7 +94,8 @@ terms_kernel(TermPlanDev tp, bool grad, const double* __restrict__ coords,
   pdl_wait();
   pdl_launch_dependents();
   __shared__ double sh[5][kTermThreads / 32];
-  term_block(tp, grad, coords, term_part, term_f, status, blockIdx.y, blockIdx.x, gridDim.x, sh);
+  term_block(tp, grad, CoordSrc{coords, nullptr, 0.0}, term_part, term_f, status, blockIdx.y,
+             blockIdx.x, gridDim.x, sh);
 }
 
 int term_blocks(const TermPlanDev& tp) {

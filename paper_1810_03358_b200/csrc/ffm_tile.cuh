@@ -450,16 +450,38 @@ __device__ __forceinline__ bool tile_diag_mask(int ib, int jb, int lane, uint32_
   return masked;
 }
 
+// The pair record of atom a straight from the evaluation's coordinates:
+// the values the packing pass writes (pack_item / pad_kernel)
+template <typename T>
+__device__ __forceinline__ void atom_record(const CoordSrc& cs, const double* __restrict__ qt,
+                                            int n, int a, T& x, T& y, T& z, T& w) {
+  if (a < n) {
+    x = T(cs.at(3 * (int64_t)a));
+    y = T(cs.at(3 * (int64_t)a + 1));
+    z = T(cs.at(3 * (int64_t)a + 2));
+    w = T(qt[a]);
+  } else {
+    x = T(1.0e4 + 10.0 * (double)(a - n));
+    y = T(1.0e4);
+    z = T(1.0e4);
+    w = T(0);
+  }
+}
+
 // tile_cta evaluates launch slot `slot` of batch entry bidx with the whole
-// CTA (kTileWarps warps; block-uniform call, contains __syncthreads)
-template <typename T, bool GRAD, bool CUTOFF>
+// CTA (kTileWarps warps; block-uniform call, contains __syncthreads).
+// FROMX: positions and charges come straight from the coordinates (cs, qt)
+// instead of the packed records pos / ipos (the fused evaluation of tiny
+// systems, which so skips its packing pass and the barrier after it).
+template <typename T, bool GRAD, bool CUTOFF, bool FROMX = false>
 __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
                                          const typename Vec4T<T>::type* __restrict__ pos,
                                          const typename Vec2T<T>::type* __restrict__ lj,
                                          const T* __restrict__ ipos, const T* __restrict__ ilj,
                                          T* __restrict__ ipart, T* __restrict__ jpart,
                                          double* __restrict__ epart, int slot, int bidx,
-                                         TileSmem<T>& sm) {
+                                         TileSmem<T>& sm, CoordSrc cs = {nullptr, nullptr, 0.0},
+                                         const double* __restrict__ qt = nullptr) {
   using P = Pk<T>;
   using V = typename P::V;
   using V4 = typename Vec4T<T>::type;
@@ -477,7 +499,9 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
   ipos += (size_t)bidx * 4 * plan.np;
   const int64_t half = plan.np >> 1;
   if (q == 0) {
-    V4 p = pos[jb + lane];
+    V4 p;
+    if constexpr (FROMX) atom_record<T>(cs, qt, plan.n, jb + lane, p.x, p.y, p.z, p.w);
+    else p = pos[jb + lane];
     p.x = -p.x;
     p.y = -p.y;
     p.z = -p.z;
@@ -494,10 +518,21 @@ __device__ __forceinline__ void tile_cta(const NbPlanDev& plan,
 #pragma unroll
   for (int pp = 0; pp < 2; ++pp) {
     const int64_t r = (int64_t)kk * 64 + pp * 32 + lane;
-    xi[pp] = ld_pair<T>(ipos, r);
-    yi[pp] = ld_pair<T>(ipos, half + r);
-    zi[pp] = ld_pair<T>(ipos, 2 * half + r);
-    qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+    if constexpr (FROMX) {  // atoms (128 kk + 64 pp + lane, + 32): ipos_index's pair
+      T x0, y0, z0, w0, x1, y1, z1, w1;
+      const int a0 = ib + 64 * pp + lane;
+      atom_record<T>(cs, qt, plan.n, a0, x0, y0, z0, w0);
+      atom_record<T>(cs, qt, plan.n, a0 + 32, x1, y1, z1, w1);
+      xi[pp] = P::make(x0, x1);
+      yi[pp] = P::make(y0, y1);
+      zi[pp] = P::make(z0, z1);
+      qi[pp] = P::make(w0, w1);
+    } else {
+      xi[pp] = ld_pair<T>(ipos, r);
+      yi[pp] = ld_pair<T>(ipos, half + r);
+      zi[pp] = ld_pair<T>(ipos, 2 * half + r);
+      qi[pp] = ld_pair<T>(ipos, 3 * half + r);
+    }
     ai[pp] = ld_pair<T>(ilj, r);
     bi[pp] = ld_pair<T>(ilj, half + r);
   }
