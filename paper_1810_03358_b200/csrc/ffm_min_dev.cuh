@@ -237,7 +237,8 @@ __device__ inline void ls_step(MinState* S, const double* en, const int64_t* stw
     }
   }
   S->ls_more = more ? 1 : 0;
-  cudaGraphSetConditional(hloop, more ? 1u : 0u);
+  // the loop condition is 1 from ls_init on: only its end needs a write
+  if (!more) cudaGraphSetConditional(hloop, 0u);
 }
 
 }  // namespace mindev
