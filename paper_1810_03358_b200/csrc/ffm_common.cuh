@@ -221,7 +221,6 @@ enum StatusSlot : int {
   kStNbSuspect = 5,   // set when the pair sweep saw a possible coincidence
   kStNbKey = 6,       // scratch: min (i * n + j) over coincident pairs
   kStCount = 7,       // scratch, 0 between evaluations: the finder's finished-block counter
-                      // (kernel chain) / a tile saw a possible coincidence (fused small evaluation)
   kStWords = 8
 };
 
