@@ -241,14 +241,11 @@ static void* small_kernel(bool fp64, bool grad, bool cut, bool fromx) {
 #define FFM_SMALL_FROMX_MAXN 1500
 #endif
 bool small_fromx(const SmallEvalArgs& a, bool fp64) {
-  static const int maxn = [] {
-    const char* f = getenv("FFM_SMALL_FROMX_MAXN");  // tuning aid
-    return f ? atoi(f) : FFM_SMALL_FROMX_MAXN;
-  }();
-  static const bool f64_all = [] {
-    const char* f = getenv("FFM_SMALL_FROMX_F64");  // tuning aid: FP64 single evaluations too
-    return f && atoi(f) != 0;
-  }();
+  // tuning / test overrides, read per call (a launch is captured once per graph)
+  const char* fm = getenv("FFM_SMALL_FROMX_MAXN");
+  const int maxn = fm ? atoi(fm) : FFM_SMALL_FROMX_MAXN;
+  const char* ff = getenv("FFM_SMALL_FROMX_F64");  // FP64 single evaluations too
+  const bool f64_all = ff && atoi(ff) != 0;
   return a.plan.n <= maxn && a.term_st != nullptr && (!fp64 || f64_all || a.ls_state != nullptr);
 }
 

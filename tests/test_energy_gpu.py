@@ -484,18 +484,26 @@ def test_tiny_and_block_edge_systems(n):
         assert np.max(np.abs(np.ravel(g) - np.ravel(g_ref))) <= gt * gmax
 
 
+@pytest.mark.parametrize("fromx", ["default", "forced", "off"])
 @pytest.mark.parametrize("name", ["chain10", "cloud24", "cloud24c7", "chain200", "chain12cut",
                                   "globule1500", "coincident", "collinear", "explicit8"])
-def test_fused_small_evaluation_equals_kernel_chain(golden, name):
+def test_fused_small_evaluation_equals_kernel_chain(golden, name, fromx, monkeypatch):
     """Small (tile-mode) systems evaluate in one cooperative launch
     (ffm_small.cu) running the same per-item bodies as the kernel chain:
     energies, gradient and status words must be bit-identical, in both
-    precisions, with and without the gradient, error cases included."""
+    precisions, with and without the gradient, error cases included -- for
+    both kernel variants (fromx: the variant without the packing pass, as
+    chosen by size, forced for every size and precision, or never)."""
     import torch
 
     from paper_1810_03358_b200 import _native as N
     from paper_1810_03358_b200.engine import engine_for
 
+    if fromx == "forced":
+        monkeypatch.setenv("FFM_SMALL_FROMX_MAXN", "1000000")
+        monkeypatch.setenv("FFM_SMALL_FROMX_F64", "1")
+    elif fromx == "off":
+        monkeypatch.setenv("FFM_SMALL_FROMX_MAXN", "0")
     s = golden_system(golden, name)
     eng = engine_for(s.topology)
     c = torch.from_numpy(np.ascontiguousarray(s.coords)).cuda()
