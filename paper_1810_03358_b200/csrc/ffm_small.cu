@@ -74,6 +74,17 @@ small_eval_kernel(SmallEvalArgs a) {
   };
   stamp(0);
   FFM_MSTAMP(4);
+  // the probe controller (the last CTA, every pass) works on a shared-memory
+  // copy of the driver state, read once per launch: its scalar logic is a
+  // chain of dependent reads and writes (~4 us per probe as L2 round trips);
+  // nothing else writes the state during the launch, and every pass writes
+  // the copy back for the other CTAs (h_trial, ls_more) and the graph
+  constexpr int kW = (int)(sizeof(MinState) / sizeof(unsigned long long));
+  static_assert(sizeof(MinState) % sizeof(unsigned long long) == 0, "MinState words");
+  unsigned long long* gw = reinterpret_cast<unsigned long long*>(a.ls_state);
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(&ms);
+  if (a.ls_state && blockIdx.x == gridDim.x - 1)
+    for (int w = threadIdx.x; w < kW; w += kSmallThreads) sw[w] = gw[w];  // (synced below)
 
   // a line-search trial repeats the whole evaluation for every probe the
   // controller asks for (one launch per search instead of one per probe:
@@ -183,24 +194,17 @@ small_eval_kernel(SmallEvalArgs a) {
     // line-search trial, runs the probe controller (ffm_min_dev.cuh)
     FFM_MSTAMP_LAST(12);
     if (blockIdx.x == gridDim.x - 1) {
-      // the probe controller works on a shared-memory copy of the driver
-      // state: its scalar logic is a chain of dependent reads and writes,
-      // ~4 us per probe as L2 round trips, one copy in and out instead
-      constexpr int kW = (int)(sizeof(MinState) / sizeof(unsigned long long));
-      static_assert(sizeof(MinState) % sizeof(unsigned long long) == 0, "MinState words");
-      unsigned long long* gw = reinterpret_cast<unsigned long long*>(a.ls_state);
-      unsigned long long* sw = reinterpret_cast<unsigned long long*>(&ms);
       // (the status words and energies likewise: every input is read in one
       // round trip, the outputs written back together)
-      if (a.ls_state)
-        for (int w = threadIdx.x; w < kW; w += kSmallThreads) sw[w] = gw[w];
       if (threadIdx.x < kStWords) st_s[threadIdx.x] = a.status[threadIdx.x];
       else if (threadIdx.x < kStWords + 5) en_s[threadIdx.x - kStWords] = a.energies[threadIdx.x - kStWords];
       __syncthreads();
+      FFM_MSTAMP_LAST(15);
       if (threadIdx.x == 0) {
         finalize_entry(n, st_s);
         if (a.ls_state) mindev::ls_step(&ms, en_s, st_s, a.ls_loop);
       }
+      FFM_MSTAMP_LAST(16);
       __syncthreads();
       if (a.ls_state)
         for (int w = threadIdx.x; w < kW; w += kSmallThreads) gw[w] = sw[w];
