@@ -1727,6 +1727,12 @@ int cap_accept(ffm_lbfgs* L, cudaStream_t st) {
   FFM_CUDA(launch_axpby(L->n, nullptr, 1.0, 1.0, L->x, &S->res_h, 0.0, L->r, L->xn, st));
   FFM_TRYR(issue_eval(L->sys, L->prec, FFM_ENERGY | FFM_GRAD, L->xn, L->gnew, L->en, L->stw,
                       st));
+  if (L->cfg.method == kMethodLbfgs && L->n <= kAcceptSmallN) {
+    // short vectors: the whole tail below in one launch (same bits)
+    FFM_CUDA(launch_lbfgs_accept_small(S, L->n, L->stw, L->xn, L->gnew, L->x, L->g, L->st, L->yt,
+                                       L->ring_s, L->ring_y, L->rec, st));
+    return FFM_OK;
+  }
   const double* gs[1] = {L->gnew};
   FFM_CUDA(launch_dots(L->n, 1, gs, gs, L->scratch, &S->gg, st));
   FFM_CUDA(launch_min_acc_check(S, L->stw, st));

@@ -275,6 +275,12 @@ cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const 
                              double* ring_s, double* ring_y, const double* x_new,
                              const double* g_new, double* x, double* g, cudaStream_t st);
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st);
+// the L-BFGS acceptance tail of a short vector in one launch (n <= kAcceptSmallN)
+constexpr int64_t kAcceptSmallN = 3072;  // (2000 atoms: one block measured slower than the chain)
+cudaError_t launch_lbfgs_accept_small(MinState* S, int64_t n, const int64_t* stw,
+                                      const double* x_new, const double* g_new, double* x,
+                                      double* g, double* s_tmp, double* y_tmp, double* ring_s,
+                                      double* ring_y, double* rec, cudaStream_t st);
 cudaError_t launch_min_it_end(MinState* S, cudaGraphConditionalHandle hout, cudaStream_t st);
 
 }  // namespace ffm

@@ -198,9 +198,7 @@ __global__ void min_ls_post_kernel(MinState* S, double* rec, cudaGraphConditiona
 }
 
 // after the gradient at x_new and <g_new, g_new>
-__global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
-  pdl_wait();
-  pdl_launch_dependents();
+__device__ inline void acc_check(MinState* S, const int64_t* stw) {
   S->gcalls++;
   if (bad_status(stw, true)) {
     set_err(S, kMinErrEval, stw, true);
@@ -209,11 +207,14 @@ __global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
   if (!isfinite(S->res_f) || !isfinite(S->gg)) set_err(S, kMinErrDiverged, nullptr, true);
 }
 
-// after <s,y>, <s,s>, <y,y>: LbfgsMemory._commit
-__global__ void min_commit_kernel(MinState* S) {
+__global__ void min_acc_check_kernel(MinState* S, const int64_t* stw) {
   pdl_wait();
-  FFM_MSTAMP(8);
   pdl_launch_dependents();
+  acc_check(S, stw);
+}
+
+// after <s,y>, <s,s>, <y,y>: LbfgsMemory._commit
+__device__ inline void commit(MinState* S) {
   S->store_slot = -1;
   if (S->err) return;
   const double sy = S->sy, ss = S->ss, yy = S->yy;
@@ -238,6 +239,13 @@ __global__ void min_commit_kernel(MinState* S) {
     S->rho_nf[q] = S->rho[S->count - 1 - q];
   }
   S->store_slot = slot;
+}
+
+__global__ void min_commit_kernel(MinState* S) {
+  pdl_wait();
+  FFM_MSTAMP(8);
+  pdl_launch_dependents();
+  commit(S);
 }
 
 __global__ void min_store_kernel(const MinState* S, int64_t n, const double* __restrict__ s_tmp,
@@ -765,9 +773,7 @@ __global__ void wig_record_kernel(MinState* S, double* rec) {
   S->nrec++;
 }
 
-__global__ void min_iter_end_kernel(MinState* S, double* rec) {
-  pdl_wait();
-  pdl_launch_dependents();
+__device__ inline void iter_end(MinState* S, double* rec) {
   if (S->err) return;
   S->f = S->res_f;
   S->gn = sqrt(S->gg);
@@ -778,6 +784,100 @@ __global__ void min_iter_end_kernel(MinState* S, double* rec) {
     S->status = kMinConverged;
     S->done = 1;
   }
+}
+
+__global__ void min_iter_end_kernel(MinState* S, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
+  iter_end(S, rec);
+}
+
+// The L-BFGS acceptance tail of a short vector (n <= kAcceptSmallN) as one
+// block: <g+,g+>, the acceptance checks, s = x+ - x, y = g+ - g, <s,y>,
+// <s,s>, <y,y>, the memory commit, the ring store and the iteration record
+// -- eight graph nodes in one, each step with the arithmetic and reduction
+// order of its own kernel (axpby_kernel, dots_small_kernel: one block,
+// per-thread strides of 256, then the block sum), so the same bits.  The
+// scalar steps run on a shared copy of the driver state.
+constexpr int kAcceptThreads = 256;
+__device__ __forceinline__ double block_sum_accept(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kAcceptThreads / 32; ++w) t += sh[w];
+  __syncthreads();
+  return t;  // thread 0
+}
+
+__global__ void __launch_bounds__(kAcceptThreads)
+lbfgs_accept_small_kernel(MinState* S, int64_t n, const int64_t* __restrict__ stw,
+                          const double* __restrict__ x_new, const double* __restrict__ g_new,
+                          double* __restrict__ x, double* __restrict__ g, double* __restrict__ st,
+                          double* __restrict__ yt, double* __restrict__ ring_s,
+                          double* __restrict__ ring_y, double* rec) {
+  pdl_wait();
+  pdl_launch_dependents();
+  __shared__ MinState ms;
+  __shared__ double sh[kAcceptThreads / 32];
+  constexpr int kW = (int)(sizeof(MinState) / sizeof(unsigned long long));
+  unsigned long long* gw = reinterpret_cast<unsigned long long*>(S);
+  unsigned long long* sw = reinterpret_cast<unsigned long long*>(&ms);
+  const int t = threadIdx.x;
+  for (int w = t; w < kW; w += kAcceptThreads) sw[w] = gw[w];
+  // <g+, g+> (launch_dots, one product)
+  double acc = 0.0;
+  for (int64_t i = t; i < n; i += kAcceptThreads) acc = fma(g_new[i], g_new[i], acc);
+  acc = block_sum_accept(acc, sh);  // (its barriers also publish ms)
+  if (t == 0) {
+    ms.gg = acc;
+    acc_check(&ms, stw);
+  }
+  // s = x+ - x, y = g+ - g (axpby_kernel: v = 1 x+; v = fma(-1, x, v); z = 1 v)
+  for (int64_t i = t; i < n; i += kAcceptThreads) {
+    double v = 1.0 * x_new[i];
+    v = fma(-1.0, x[i], v);
+    st[i] = 1.0 * v;
+    double w = 1.0 * g_new[i];
+    w = fma(-1.0, g[i], w);
+    yt[i] = 1.0 * w;
+  }
+  __syncthreads();
+  // <s,y>, <s,s>, <y,y>
+  const double* xa[3] = {st, st, yt};
+  const double* ya[3] = {yt, st, yt};
+  double d3[3];
+  for (int q = 0; q < 3; ++q) {
+    double a = 0.0;
+    for (int64_t i = t; i < n; i += kAcceptThreads) a = fma(xa[q][i], ya[q][i], a);
+    d3[q] = block_sum_accept(a, sh);
+  }
+  __shared__ int slot_s, err_s;
+  if (t == 0) {
+    ms.sy = d3[0];
+    ms.ss = d3[1];
+    ms.yy = d3[2];
+    commit(&ms);
+    slot_s = ms.store_slot;
+    err_s = ms.err;
+  }
+  __syncthreads();
+  // the ring store and x <- x+, g <- g+ (min_store_kernel)
+  if (!err_s) {
+    const int slot = slot_s;
+    for (int64_t i = t; i < n; i += kAcceptThreads) {
+      if (slot >= 0) {
+        ring_s[(int64_t)slot * n + i] = st[i];
+        ring_y[(int64_t)slot * n + i] = yt[i];
+      }
+      x[i] = x_new[i];
+      g[i] = g_new[i];
+    }
+  }
+  if (t == 0) iter_end(&ms, rec);
+  __syncthreads();
+  for (int w = t; w < kW; w += kAcceptThreads) gw[w] = sw[w];
 }
 
 __global__ void min_it_end_kernel(MinState* S, cudaGraphConditionalHandle hout) {
@@ -898,6 +998,15 @@ cudaError_t launch_mom_post(MinState* S, const double* en, const int64_t* stw, d
 cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_check_kernel, S); }
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(min_iter_end_kernel, S, rec);
+}
+cudaError_t launch_lbfgs_accept_small(MinState* S, int64_t n, const int64_t* stw,
+                                      const double* x_new, const double* g_new, double* x,
+                                      double* g, double* s_tmp, double* y_tmp, double* ring_s,
+                                      double* ring_y, double* rec, cudaStream_t st) {
+  count_launch();
+  launch_k(lbfgs_accept_small_kernel, 1, kAcceptThreads, 0, st, S, n, stw, x_new, g_new, x, g,
+           s_tmp, y_tmp, ring_s, ring_y, rec);
+  return cudaGetLastError();
 }
 cudaError_t launch_min_it_end(MinState* S, cudaGraphConditionalHandle hout, cudaStream_t st) {
   FFM_ONE(min_it_end_kernel, S, hout);
