@@ -1440,6 +1440,13 @@ int add_conditional(cudaStream_t st, cudaGraphConditionalHandle h,
 int cap_direction(ffm_lbfgs* L, cudaStream_t st, cudaGraphConditionalHandle hls) {
   MinState* S = L->S;
   const int method = L->cfg.method;
+  if (method == kMethodLbfgs && lbfgs_dir_small_applies(L->n, L->cfg.m)) {
+    // short vectors: the direction, its norm and the search's r and slope
+    // in one launch (the line search below then skips its axpby and dot)
+    FFM_CUDA(launch_lbfgs_dir_small(S, L->n, L->cfg.m, L->d, L->r, L->ring_s, L->ring_y, L->g, hls,
+                                    st));
+    return FFM_OK;
+  }
   if (method == kMethodLbfgs)
     FFM_CUDA(launch_lbfgs_two_loop_dev(L->n, L->cfg.m, &S->count, S->idx_nf, S->rho_nf, &S->gn,
                                        L->ring_s, L->ring_y, L->g, L->d, L->scratch, st));
@@ -1780,6 +1787,7 @@ int lbfgs_build(ffm_lbfgs* L) {
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, L->cap[0]));
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->gnew, L->en, L->stw, L->cap[0]));
   FFM_CUDA(two_loop_small_prepare());
+  FFM_CUDA(lbfgs_dir_small_prepare());
   FFM_CUDA(cudaStreamSynchronize(L->cap[0]));
   MinState* S = L->S;
   const long long before = g_launch_count.load();
@@ -1842,13 +1850,18 @@ int lbfgs_build(ffm_lbfgs* L) {
     {  // line search
       FFM_GC(cudaGraphConditionalHandleCreate(&hloop, bls, 0, 0));
       FFM_GC(cudaStreamBeginCaptureToGraph(c2, bls, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-      if (L->cfg.method == kMethodSd || L->cfg.method == kMethodFgm)  // r = (1 / |g|) (-g)
-        FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, -1.0, L->g, nullptr, 0.0, nullptr, L->r, c2));
-      else
-        FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
-      const double* gs[1] = {L->g};
-      const double* rs[1] = {L->r};
-      FFM_GC(launch_dots(L->n, 1, gs, rs, L->scratch, &S->slope, c2));
+      const bool dir_fused = L->cfg.method == kMethodLbfgs && lbfgs_dir_small_applies(L->n, L->cfg.m);
+      if (dir_fused) {
+        // r and the slope came with the direction (lbfgs_dir_small_kernel)
+      } else {
+        if (L->cfg.method == kMethodSd || L->cfg.method == kMethodFgm)  // r = (1 / |g|) (-g)
+          FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, -1.0, L->g, nullptr, 0.0, nullptr, L->r, c2));
+        else
+          FFM_GC(launch_axpby(L->n, &S->inv_dn, 0.0, 1.0, L->d, nullptr, 0.0, nullptr, L->r, c2));
+        const double* gs[1] = {L->g};
+        const double* rs[1] = {L->r};
+        FFM_GC(launch_dots(L->n, 1, gs, rs, L->scratch, &S->slope, c2));
+      }
       FFM_GC(launch_min_ls_init(S, hloop, c2));
       FFM_G(add_conditional(c2, hloop, cudaGraphCondTypeWhile, &bloop));
       FFM_GC(cudaStreamBeginCaptureToGraph(c3, bloop, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));

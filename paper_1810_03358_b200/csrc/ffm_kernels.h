@@ -275,6 +275,13 @@ cudaError_t launch_min_store(MinState* S, int64_t n, const double* s_tmp, const 
                              double* ring_s, double* ring_y, const double* x_new,
                              const double* g_new, double* x, double* g, cudaStream_t st);
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st);
+// the L-BFGS direction of a short vector in one launch (two-loop, <d,d>,
+// min_dir, r = d / |d|, <g,r>); _prepare once outside graph capture
+bool lbfgs_dir_small_applies(int64_t n, int m);
+cudaError_t lbfgs_dir_small_prepare();
+cudaError_t launch_lbfgs_dir_small(MinState* S, int64_t n, int m, double* d, double* r,
+                                   const double* S_ring, const double* Y_ring, const double* g,
+                                   cudaGraphConditionalHandle hls, cudaStream_t st);
 // the L-BFGS acceptance tail of a short vector in one launch (n <= kAcceptSmallN)
 constexpr int64_t kAcceptSmallN = 3072;  // (2000 atoms: one block measured slower than the chain)
 cudaError_t launch_lbfgs_accept_small(MinState* S, int64_t n, const int64_t* stw,

@@ -13,6 +13,7 @@
 // This file is compiled with -fmad=false: every product and sum rounds
 // separately, as in the reference's Python float arithmetic.
 #include "ffm_min_dev.cuh"
+#include "ffm_two_loop.cuh"
 
 namespace ffm {
 
@@ -792,6 +793,64 @@ __global__ void min_iter_end_kernel(MinState* S, double* rec) {
   iter_end(S, rec);
 }
 
+// The L-BFGS direction of a short vector (n <= 256 kTwoLoopSmallE) as one
+// block: the two-loop d (two_loop_small_body, written to D.q), <d, d>, the
+// min_dir step (|d|, 1 / |d|, the line-search condition) and, when the
+// search runs, r = d / |d| and its slope <g, r> -- five graph nodes (the
+// two-loop, two dot launches, min_dir, the search's axpby) in one, each
+// step with the arithmetic and reduction order of its own kernel: the same
+// bits.
+__global__ void __launch_bounds__(kTwoLoopThreads)
+lbfgs_dir_small_kernel(MinState* S, TwoLoopDevArgs D, double* __restrict__ r,
+                       cudaGraphConditionalHandle hls) {
+  pdl_wait();
+  pdl_launch_dependents();
+  extern __shared__ double ring[];
+  __shared__ double sh2[kTwoLoopThreads / 32];
+  __shared__ double inv_s;
+  __shared__ int go_s;
+  const int t = threadIdx.x;
+  const int n = (int)D.n;
+  double q[kTwoLoopSmallE];
+  two_loop_small_body(D, ring, q);
+  double acc = 0.0;  // <d, d> (dots_small_kernel order)
+#pragma unroll
+  for (int e = 0; e < kTwoLoopSmallE; ++e)
+    if (t + e * kTwoLoopThreads < n) acc = fma(q[e], q[e], acc);
+  acc = two_loop_block_sum(acc, sh2);
+  if (t == 0) {  // min_dir_kernel, L-BFGS branch
+    S->dd = acc;
+    const double dn = sqrt(S->dd);
+    S->dn = dn;
+    int go = 1;
+    if (dn == 0.0) {
+      S->status = kMinConverged;
+      S->done = 1;
+      go = 0;
+    } else {
+      S->inv_dn = 1.0 / dn;  // ops.div(d, dn) = lincomb(1 / dn, d)
+    }
+    cudaGraphSetConditional(hls, go ? 1u : 0u);
+    inv_s = go ? S->inv_dn : 0.0;
+    go_s = go;
+  }
+  __syncthreads();
+  if (!go_s) return;
+  // r = (1 / |d|) d (axpby_kernel: v = a x; z = 1 v) and <g, r>
+  double sl = 0.0;
+#pragma unroll
+  for (int e = 0; e < kTwoLoopSmallE; ++e) {
+    const int i = t + e * kTwoLoopThreads;
+    if (i < n) {
+      const double v = 1.0 * (inv_s * q[e]);
+      r[i] = v;
+      sl = fma(D.g[i], v, sl);
+    }
+  }
+  sl = two_loop_block_sum(sl, sh2);
+  if (t == 0) S->slope = sl;
+}
+
 // The L-BFGS acceptance tail of a short vector (n <= kAcceptSmallN) as one
 // block: <g+,g+>, the acceptance checks, s = x+ - x, y = g+ - g, <s,y>,
 // <s,s>, <y,y>, the memory commit, the ring store and the iteration record
@@ -999,6 +1058,25 @@ cudaError_t launch_min_cg_check(MinState* S, cudaStream_t st) { FFM_ONE(min_cg_c
 cudaError_t launch_min_iter_end(MinState* S, double* rec, cudaStream_t st) {
   FFM_ONE(min_iter_end_kernel, S, rec);
 }
+constexpr size_t kDirSmallSmem = 200 * 1024;
+bool lbfgs_dir_small_applies(int64_t n, int m) {
+  return n <= (int64_t)kTwoLoopSmallE * kTwoLoopThreads && m <= kMaxLbfgsPairs &&
+         (size_t)2 * m * n * sizeof(double) <= kDirSmallSmem;
+}
+cudaError_t lbfgs_dir_small_prepare() {
+  return cudaFuncSetAttribute(lbfgs_dir_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)kDirSmallSmem);
+}
+cudaError_t launch_lbfgs_dir_small(MinState* S, int64_t n, int m, double* d, double* r,
+                                   const double* S_ring, const double* Y_ring, const double* g,
+                                   cudaGraphConditionalHandle hls, cudaStream_t st) {
+  TwoLoopDevArgs D{n, &S->count, S->idx_nf, S->rho_nf, &S->gn, S_ring, Y_ring, g, d, nullptr};
+  count_launch();
+  launch_k(lbfgs_dir_small_kernel, 1, kTwoLoopThreads, (size_t)2 * m * n * sizeof(double), st, S,
+           D, r, hls);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_lbfgs_accept_small(MinState* S, int64_t n, const int64_t* stw,
                                       const double* x_new, const double* g_new, double* x,
                                       double* g, double* s_tmp, double* y_tmp, double* ring_s,

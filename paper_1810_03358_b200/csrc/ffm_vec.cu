@@ -11,6 +11,7 @@
 
 #include "../../include/ffmin_b200.h"
 #include "ffm_kernels.h"
+#include "ffm_two_loop.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -303,22 +304,10 @@ __global__ void __launch_bounds__(kVecThreads) two_loop_kernel(TwoLoopArgs A) {
 }
 
 // Device-driven variant for the graph-resident L-BFGS (ffm_min.cuh): the
-// pair count, ring slots (newest first) and rho come from device memory.
-// count = 0 gives the normalised antigradient of lbfgs_direction
-// (ffmin/optimizers/lbfgs.py:53-58): d = (1 / |g|) (-g), or -g when |g| = 0.
-struct TwoLoopDevArgs {
-  int64_t n;
-  const int* count;
-  const int* idx;
-  const double* rho;
-  const double* gn;
-  const double* S;
-  const double* Y;
-  const double* g;
-  double* q;
-  double* part;
-};
-
+// pair count, ring slots (newest first) and rho come from device memory
+// (TwoLoopDevArgs, ffm_two_loop.cuh).  count = 0 gives the normalised
+// antigradient of lbfgs_direction (ffmin/optimizers/lbfgs.py:53-58):
+// d = (1 / |g|) (-g), or -g when |g| = 0.
 __global__ void __launch_bounds__(kVecThreads) two_loop_dev_kernel(TwoLoopDevArgs D) {
   pdl_wait();
   FFM_MSTAMP(20);
@@ -395,116 +384,17 @@ cudaError_t launch_lbfgs_two_loop(int64_t n, int count, const int* idx, const do
   return cudaLaunchCooperativeKernel((void*)two_loop_kernel, grid, kVecThreads, args, 0, st);
 }
 
-// Short vectors (one-block grids): the same recursion with the ring pairs
-// staged in shared memory once and q in registers, so its 2 m + 1 dependent
-// phases cost block reductions instead of L2 round trips (500 atoms: 19 ->
-// 9 us per direction, tools/lbfgs_timeline.py).  Element order, fma sequence and reductions are two_loop_body's on
-// one block: the same bits.
-constexpr int kTwoLoopSmallE = 8;  // elements per thread: n <= 2048
+// Short vectors (one-block grids): the recursion with the ring pairs staged
+// in shared memory and q in registers (ffm_two_loop.cuh; 500 atoms: 19 ->
+// 9 us per direction, tools/lbfgs_timeline.py).
 constexpr size_t kTwoLoopSmallSmem = 200 * 1024;
 
 __global__ void __launch_bounds__(kVecThreads) two_loop_dev_small_kernel(TwoLoopDevArgs D) {
   pdl_wait();
   FFM_MSTAMP(20);
-  extern __shared__ double ring[];  // [count][n] s rows, then [count][n] y rows, newest first
-  __shared__ double sh[kVecThreads / 32];
-  __shared__ double bc;
-  __shared__ double alpha[kMaxLbfgsPairs], rho[kMaxLbfgsPairs];
-  const int count = *D.count;
-  const int n = (int)D.n;
-  const int t = threadIdx.x;
-  if (count == 0) {
-    const double gn = *D.gn;
-    const double inv = 1.0 / gn;
-    for (int i = t; i < n; i += kVecThreads) {
-      const double v = -D.g[i];
-      D.q[i] = gn == 0.0 ? v : inv * v;
-    }
-    return;
-  }
-  double* sS = ring;
-  double* sY = ring + (size_t)count * n;
-  for (int k = 0; k < count; ++k) {
-    const double* s = D.S + (int64_t)D.idx[k] * n;
-    const double* y = D.Y + (int64_t)D.idx[k] * n;
-    for (int i = t; i < n; i += kVecThreads) {
-      sS[(size_t)k * n + i] = s[i];
-      sY[(size_t)k * n + i] = y[i];
-    }
-  }
-  if (t < count) rho[t] = D.rho[t];
+  extern __shared__ double ring[];
   double q[kTwoLoopSmallE];
-#pragma unroll
-  for (int e = 0; e < kTwoLoopSmallE; ++e) {
-    const int i = t + e * kVecThreads;
-    q[e] = i < n ? D.g[i] : 0.0;
-  }
-  __syncthreads();
-  double a = 0.0, b = 0.0, c = 0.0;
-#pragma unroll
-  for (int e = 0; e < kTwoLoopSmallE; ++e) {
-    const int i = t + e * kVecThreads;
-    if (i < n) {
-      a = fma(sS[i], q[e], a);
-      b = fma(sS[i], sY[i], b);
-      c = fma(sY[i], sY[i], c);
-    }
-  }
-  a = block_sum256(a, sh);
-  b = block_sum256(b, sh);
-  c = block_sum256(c, sh);
-  double prev_sum = a;
-  if (t == 0) bc = (0.0 + b) / (0.0 + c);
-  __syncthreads();
-  const double gamma = bc;
-  for (int k = 0; k < count; ++k) {
-    __syncthreads();
-    if (t == 0) alpha[k] = bc = rho[k] * (0.0 + prev_sum);
-    __syncthreads();
-    const double al = bc;
-    const bool last = k + 1 == count;
-    const double* y = sY + (size_t)k * n;
-    const double* w = last ? sY + (size_t)(count - 1) * n : sS + (size_t)(k + 1) * n;
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < kTwoLoopSmallE; ++e) {
-      const int i = t + e * kVecThreads;
-      if (i < n) {
-        double v = fma(-al, y[i], q[e]);
-        if (last) v *= gamma;
-        q[e] = v;
-        acc = fma(w[i], v, acc);
-      }
-    }
-    prev_sum = block_sum256(acc, sh);
-  }
-  for (int k = count - 1; k >= 0; --k) {
-    __syncthreads();
-    if (t == 0) bc = rho[k] * (0.0 + prev_sum);
-    __syncthreads();
-    const double coef = alpha[k] - bc;
-    const double* s = sS + (size_t)k * n;
-    if (k == 0) {
-#pragma unroll
-      for (int e = 0; e < kTwoLoopSmallE; ++e) {
-        const int i = t + e * kVecThreads;
-        if (i < n) D.q[i] = -fma(coef, s[i], q[e]);
-      }
-      break;
-    }
-    const double* y2 = sY + (size_t)(k - 1) * n;
-    double acc = 0.0;
-#pragma unroll
-    for (int e = 0; e < kTwoLoopSmallE; ++e) {
-      const int i = t + e * kVecThreads;
-      if (i < n) {
-        const double v = fma(coef, s[i], q[e]);
-        q[e] = v;
-        acc = fma(y2[i], v, acc);
-      }
-    }
-    prev_sum = block_sum256(acc, sh);
-  }
+  two_loop_small_body(D, ring, q);
   FFM_MSTAMP(21);
 }
 
