@@ -28,6 +28,18 @@ struct TwoLoopDevArgs {
   double* part;
 };
 
+// the block sum in every thread with one barrier: warp sums to sh (a buffer
+// the previous call did not use), then every thread adds the eight of them
+// in the same order as two_loop_block_sum's thread 0 -- the same bits
+__device__ __forceinline__ double two_loop_allreduce(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < kTwoLoopThreads / 32; ++w) s += sh[w];
+  return s;
+}
+
 __device__ __forceinline__ double two_loop_block_sum(double v, double* sh) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
@@ -44,9 +56,7 @@ __device__ __forceinline__ double two_loop_block_sum(double v, double* sh) {
 // antigradient (lbfgs.py:53-58), d = (1 / |g|) (-g), or -g when |g| = 0.
 __device__ __forceinline__ void two_loop_small_body(const TwoLoopDevArgs& D, double* ring,
                                                     double (&q)[kTwoLoopSmallE]) {
-  __shared__ double sh[kTwoLoopThreads / 32];
-  __shared__ double bc;
-  __shared__ double alpha[kMaxLbfgsPairs], rho[kMaxLbfgsPairs];
+  __shared__ double rho[kMaxLbfgsPairs], alpha[kMaxLbfgsPairs];
   const int count = *D.count;
   const int n = (int)D.n;
   const int t = threadIdx.x;
@@ -92,18 +102,23 @@ __device__ __forceinline__ void two_loop_small_body(const TwoLoopDevArgs& D, dou
       c = fma(sY[i], sY[i], c);
     }
   }
-  a = two_loop_block_sum(a, sh);
-  b = two_loop_block_sum(b, sh);
-  c = two_loop_block_sum(c, sh);
+  // (sums on alternating buffers: one barrier per phase, every thread holds
+  // the sum, the scalars computed redundantly in each thread)
+  __shared__ double shb[2][kTwoLoopThreads / 32];
+  int pb = 0;
+  a = two_loop_allreduce(a, shb[pb]);
+  pb ^= 1;
+  b = two_loop_allreduce(b, shb[pb]);
+  pb ^= 1;
+  c = two_loop_allreduce(c, shb[pb]);
+  pb ^= 1;
   double prev_sum = a;
-  if (t == 0) bc = (0.0 + b) / (0.0 + c);
-  __syncthreads();
-  const double gamma = bc;
+  const double gamma = (0.0 + b) / (0.0 + c);
   for (int k = 0; k < count; ++k) {
-    __syncthreads();
-    if (t == 0) alpha[k] = bc = rho[k] * (0.0 + prev_sum);
-    __syncthreads();
-    const double al = bc;
+    // (explicit roundings: no contraction whatever the unit's -fmad, as in
+    // the kernels whose bits this reproduces)
+    const double al = __dmul_rn(rho[k], 0.0 + prev_sum);
+    if (t == 0) alpha[k] = al;  // (read in the second loop, after barriers)
     const bool last = k + 1 == count;
     const double* y = sY + (size_t)k * n;
     const double* w = last ? sY + (size_t)(count - 1) * n : sS + (size_t)(k + 1) * n;
@@ -118,13 +133,11 @@ __device__ __forceinline__ void two_loop_small_body(const TwoLoopDevArgs& D, dou
         acc = fma(w[i], v, acc);
       }
     }
-    prev_sum = two_loop_block_sum(acc, sh);
+    prev_sum = two_loop_allreduce(acc, shb[pb]);
+    pb ^= 1;
   }
   for (int k = count - 1; k >= 0; --k) {
-    __syncthreads();
-    if (t == 0) bc = rho[k] * (0.0 + prev_sum);
-    __syncthreads();
-    const double coef = alpha[k] - bc;
+    const double coef = __dsub_rn(alpha[k], __dmul_rn(rho[k], 0.0 + prev_sum));
     const double* s = sS + (size_t)k * n;
     if (k == 0) {
 #pragma unroll
@@ -148,7 +161,8 @@ __device__ __forceinline__ void two_loop_small_body(const TwoLoopDevArgs& D, dou
         acc = fma(y2[i], v, acc);
       }
     }
-    prev_sum = two_loop_block_sum(acc, sh);
+    prev_sum = two_loop_allreduce(acc, shb[pb]);
+    pb ^= 1;
   }
 }
 
