@@ -6,6 +6,7 @@
 // order, so every dot product -- and therefore every optimiser trace -- is
 // bit-identical run to run.
 #include <cmath>
+#include <cstdlib>
 
 #include <cooperative_groups.h>
 
@@ -354,6 +355,14 @@ static int two_loop_grid(int64_t n) {
   const int64_t need = (n + kVecThreads - 1) / kVecThreads;
   if (blocks > need) blocks = (int)need;
   if (blocks > kVecBlocks) blocks = kVecBlocks;
+  // at most 64 blocks: the 2 m + 1 grid-wide phases are latency-bound (grid
+  // barrier, every block summing every partial), not bandwidth-bound
+  // (tools/lbfgs_launches.py, FP64 L-BFGS per iteration, blocks 118 -> 64:
+  // 10k atoms 0.924 -> 0.905 ms, 30k 5.10 -> 5.01 ms; 100k unchanged)
+  int cap = 64;
+  if (const char* f = getenv("FFM_TWOLOOP_BLOCKS"))  // tuning aid
+    if (atoi(f) > 0) cap = atoi(f);
+  if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
   return blocks;
 }
