@@ -22,7 +22,7 @@ from paper_1810_03358_b200.synth import make_globule_system  # noqa: E402
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 500
 it = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 s = make_globule_system(n, seed=1)
-o = MolecularOracle(s)
+o = MolecularOracle(s, np.float32 if os.environ.get("PREC") == "f32" else np.float64)
 lbfgs(o, s.coords.ravel(), m=5, linesearch=make_linesearch("par"),
       stop=StopCriteria(max_iterations=2, gradient_norm_rtol=1e-6))
 lib = N.load()
