@@ -233,6 +233,28 @@ def test_graph_lbfgs_equals_host_driven_loop(golden, monkeypatch, case):
     assert (oa.value_calls, oa.grad_calls) == (ob.value_calls, ob.grad_calls)
 
 
+@pytest.mark.parametrize("natoms,m", [(682, 5), (683, 5), (1024, 5), (1025, 3), (1500, 7),
+                                     (2048, 5), (2049, 5)])
+def test_graph_lbfgs_equals_host_loop_at_size_boundaries(monkeypatch, natoms, m):
+    """Bit-identical graph-resident and host-driven L-BFGS on both sides of
+    the short-vector thresholds: the fused direction (n <= 2048, shared-memory
+    ring), the fused acceptance tail (n <= 3072), the fused evaluation without
+    its packing pass (<= 1500 atoms) and the one-block two-loop (n <= 6144)."""
+    from paper_1810_03358_b200.optimizers import StopCriteria
+    from paper_1810_03358_b200.synth import make_globule_system
+
+    s = make_globule_system(natoms, seed=natoms % 13)
+    stop = StopCriteria(max_iterations=12, gradient_norm_rtol=0.0)
+    a, oa = _run_lbfgs(s, True, monkeypatch, "par", m, stop)
+    b, ob = _run_lbfgs(s, False, monkeypatch, "par", m, stop)
+    ra = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in a.trace.records]
+    rb = [(r.iteration, r.f, r.grad_norm, r.step, r.value_calls, r.grad_calls, r.best_f)
+          for r in b.trace.records]
+    assert ra == rb
+    assert a.status == b.status and np.array_equal(a.x, b.x)
+
+
 def test_graph_lbfgs_budgets(golden, monkeypatch):
     """Iteration and oracle-call budgets stop the graph run where the host
     loop stops."""
