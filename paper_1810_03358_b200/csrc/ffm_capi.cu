@@ -153,6 +153,11 @@ struct ffm_system {
   std::vector<char> unit_live;  // host: slot holds a real unit (build_units)
   // small-system tile mode (NbPlanDev::ntiles > 0)
   int4* d_tiles = nullptr;
+  // atom-delta scratch (launch_atom_delta's multi-block candidates)
+  double* dl_part = nullptr;
+  long long* dl_bad = nullptr;
+  unsigned* dl_cnt = nullptr;
+  int64_t dl_cap = 0;
   int* d_tile_list = nullptr;
   int* d_trow_ptr = nullptr;  // [np/128 + 1] tiles of each i-sub-block (contiguous)
   int* d_tcol_ptr = nullptr;  // [np/32 + 1] tiles of each j-block ...
@@ -209,6 +214,8 @@ void free_all(ffm_system* s) {
   if (s->ev_join) cudaEventDestroy(s->ev_join);
   if (s->ev_nb0) cudaEventDestroy(s->ev_nb0);
   if (s->ev_nb1) cudaEventDestroy(s->ev_nb1);
+  for (void* p : {(void*)s->dl_part, (void*)s->dl_bad, (void*)s->dl_cnt})
+    if (p) cudaFree(p);
   for (auto& w : s->w) {
     void* wp[] = {w.pos, w.ipos, w.bbox, w.ipart, w.jpart, w.epart, w.term_e, w.term_f,
                   w.escratch, w.term_st};
@@ -1307,6 +1314,47 @@ int ffm_atom_delta(ffm_system_t* s, const double* coords_d, int64_t ncand,
                             stream);
 }
 
+}  // extern "C"
+
+// candidates below this count are split over delta_blocks(n) blocks each
+// (a few probes of a large system would otherwise run on a few SMs); larger
+// batches fill the GPU with one block per candidate
+constexpr int64_t kDeltaSplitMax = 148;
+
+// atom-delta scratch for up to ncand split candidates (outside graph capture)
+static int ensure_delta_scratch(ffm_system* s, int64_t ncand) {
+  if (ncand >= kDeltaSplitMax || ncand <= s->dl_cap) return FFM_OK;
+  FFM_CUDA(cudaDeviceSynchronize());
+  for (void* p : {(void*)s->dl_part, (void*)s->dl_bad, (void*)s->dl_cnt})
+    if (p) cudaFree(p);
+  s->dl_part = nullptr;
+  s->dl_bad = nullptr;
+  s->dl_cnt = nullptr;
+  s->dl_cap = 0;
+  const int64_t cap = kDeltaSplitMax;
+  const size_t nb = (size_t)delta_blocks(s->plan.n);
+  if (cudaMalloc(&s->dl_part, cap * nb * 6 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&s->dl_bad, cap * nb * 3 * sizeof(long long)) != cudaSuccess ||
+      cudaMalloc(&s->dl_cnt, cap * sizeof(unsigned)) != cudaSuccess)
+    return fail(FFM_ENOMEM, "cudaMalloc failed for the atom-delta scratch");
+  FFM_CUDA(cudaMemset(s->dl_cnt, 0, cap * sizeof(unsigned)));
+  FFM_CUDA(cudaDeviceSynchronize());
+  s->dl_cap = cap;
+  return FFM_OK;
+}
+
+static cudaError_t issue_atom_delta(ffm_system* s, const double* coords, int ncand,
+                                    const int* atoms, const double* newpos, double lin,
+                                    double* out, int64_t* status, cudaStream_t st) {
+  const bool split = ncand < kDeltaSplitMax && ncand <= s->dl_cap;
+  return launch_atom_delta(s->tp, coords, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s, s->d_aterm_ptr,
+                           s->d_aterm_idx, ncand, atoms, newpos, lin, out, status,
+                           split ? s->dl_part : nullptr, split ? s->dl_bad : nullptr,
+                           split ? s->dl_cnt : nullptr, st);
+}
+
+extern "C" {
+
 int ffm_atom_delta_lin(ffm_system_t* s, const double* coords_d, int64_t ncand,
                        const int32_t* atoms_d, const double* newpos_d, double lin_cutoff,
                        double* out_d, int64_t* status_d, void* stream) {
@@ -1318,10 +1366,10 @@ int ffm_atom_delta_lin(ffm_system_t* s, const double* coords_d, int64_t ncand,
   if (!coords_d || !atoms_d || !newpos_d || !out_d || !status_d)
     return fail(FFM_EINVAL, "NULL argument");
   DeviceGuard guard(s->device);
-  FFM_CUDA(launch_atom_delta(s->tp, coords_d, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s,
-                             s->d_aterm_ptr, s->d_aterm_idx, (int)ncand, atoms_d, newpos_d,
-                             lin_cutoff > 0.0 ? lin_cutoff : 0.0, out_d, status_d,
-                             static_cast<cudaStream_t>(stream)));
+  FFM_TRYR(ensure_delta_scratch(s, ncand));
+  FFM_CUDA(issue_atom_delta(s, coords_d, (int)ncand, atoms_d, newpos_d,
+                            lin_cutoff > 0.0 ? lin_cutoff : 0.0, out_d, status_d,
+                            static_cast<cudaStream_t>(stream)));
   return FFM_OK;
 }
 
@@ -1677,8 +1725,7 @@ int cap_wiggle(ffm_lbfgs* L, cudaStream_t st, cudaStream_t c3, cudaGraph_t bdir)
   const double lin = L->cfg.wig_cutoff;
   auto delta = [&](int k, const int* atoms, const double* newpos, double lc, double* out,
                    int64_t* stw, cudaStream_t q) {
-    return launch_atom_delta(s->tp, L->x, s->d_fsp_ptr, s->d_fsp_j, s->d_fsp_s, s->d_aterm_ptr,
-                             s->d_aterm_idx, k, atoms, newpos, lc, out, stw, q);
+    return issue_atom_delta(s, L->x, k, atoms, newpos, lc, out, stw, q);
   };
   FFM_CUDA(launch_wig_prep(S, L->x, b.atoms6, b.newpos6, st));
   FFM_CUDA(delta(6, b.atoms6, b.newpos6, lin, b.out6, b.st6, st));
@@ -1787,6 +1834,7 @@ int lbfgs_build(ffm_lbfgs* L) {
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY, L->x, nullptr, L->en, L->stw, L->cap[0]));
   FFM_TRYR(issue_eval(s, L->prec, FFM_ENERGY | FFM_GRAD, L->x, L->gnew, L->en, L->stw, L->cap[0]));
   FFM_CUDA(two_loop_small_prepare());
+  if (L->cfg.method == kMethodWiggle) FFM_TRYR(ensure_delta_scratch(s, 6));
   FFM_CUDA(lbfgs_dir_small_prepare());
   FFM_CUDA(cudaStreamSynchronize(L->cap[0]));
   MinState* S = L->S;

@@ -115,7 +115,12 @@ cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
                               const int* aterm_ptr, const int* aterm_idx, int ncand,
                               const int* atoms, const double* newpos, double lin_cutoff,
-                              double* out, int64_t* status, cudaStream_t st);
+                              double* out, int64_t* status, double* part, long long* part_bad,
+                              unsigned* count, cudaStream_t st);
+// blocks per candidate of launch_atom_delta (with scratch: part [ncand *
+// blocks][6], part_bad [ncand * blocks][3], count [ncand] zeroed; null part:
+// one block per candidate)
+int delta_blocks(int n);
 
 // far-field linearisation of one atom: e0_coef[4] = (E_far, dE/dx, dE/dy,
 // dE/dz), near_mask[n], bad = first coincident far partner or -1

@@ -301,20 +301,32 @@ __device__ __forceinline__ P3 pick(const double* c, int atom, P3 np, int i) {
   return i == atom ? np : ld3(c, i);
 }
 
-// one block per candidate move.  Nonbonded part restates
+// delta_blocks(n) blocks per candidate move (the partner range split
+// between them, the first also takes the bonded terms; the last block to
+// finish adds the blocks' partial sums in block order: deterministic).
+// One block per candidate left the FP64 pair arithmetic of a 10k-atom
+// system on 6 SMs (71 us per wiggle probe launch).  Nonbonded part restates
 // ffmin/kernels.py:419-454 (_loop_nb_atom_delta), bonded parts 457-593.
+int delta_blocks(int n) {
+  const int b = (n + 511) / 512;  // ~2 partners per thread
+  return b < 1 ? 1 : (b > 32 ? 32 : b);
+}
+
 __global__ void __launch_bounds__(kDeltaThreads)
 atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
                   const int* __restrict__ fsp_ptr, const int* __restrict__ fsp_j,
                   const double* __restrict__ fsp_s, const int* __restrict__ aterm_ptr,
                   const int* __restrict__ aterm_idx, const int* __restrict__ atoms,
                   const double* __restrict__ newpos, double lin_cutoff,
-                  double* __restrict__ out, int64_t* __restrict__ status) {
+                  double* __restrict__ out, int64_t* __restrict__ status, int nblk,
+                  double* __restrict__ part, long long* __restrict__ part_bad,
+                  unsigned* __restrict__ count) {
   pdl_wait();
   pdl_launch_dependents();
   __shared__ double sh[32];
   __shared__ long long bad[3];
-  const int k = blockIdx.x;
+  __shared__ bool last_s;
+  const int k = blockIdx.x / nblk, blk = blockIdx.x - k * nblk;
   const int a = atoms[k];
   const P3 np = {newpos[3 * k], newpos[3 * k + 1], newpos[3 * k + 2]};
   const P3 ca = ld3(coords, a);
@@ -324,7 +336,7 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
   const bool lin = lin_cutoff > 0.0;
   const P3 dl = sub(np, ca);
   double dec = 0.0, dev = 0.0, far = 0.0;
-  for (int j = threadIdx.x; j < tp.n; j += kDeltaThreads) {
+  for (int j = blk * kDeltaThreads + threadIdx.x; j < tp.n; j += nblk * kDeltaThreads) {
     if (j == a) continue;
     // binary search of the (short, sorted) special row of atom a
     double s = 1.0;
@@ -393,7 +405,7 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
   }
   // bonded terms touching the atom
   double db = 0.0, da = 0.0, dd = 0.0;
-  for (int q = aterm_ptr[a] + threadIdx.x; q < aterm_ptr[a + 1]; q += kDeltaThreads) {
+  for (int q = aterm_ptr[a] + threadIdx.x; blk == 0 && q < aterm_ptr[a + 1]; q += kDeltaThreads) {
     int t = aterm_idx[q];
     if (t < tp.nbond) {
       const int i = tp.bond_idx[2 * t], j = tp.bond_idx[2 * t + 1];
@@ -440,17 +452,49 @@ atom_delta_kernel(TermPlanDev tp, const double* __restrict__ coords,
   da = tree_sum(da, sh);
   dd = tree_sum(dd, sh);
   far = tree_sum(far, sh);
+  double v[6] = {dec, dev, db, da, dd, far};
+  long long bv[3] = {bad[0], bad[1], bad[2]};
+  if (nblk > 1) {  // partials of this block; the last block of the candidate adds them
+    if (threadIdx.x == 0) {
+      double* p = part + 6 * ((size_t)k * nblk + blk);
+      for (int q = 0; q < 6; ++q) p[q] = v[q];
+      long long* pb = part_bad + 3 * ((size_t)k * nblk + blk);
+      for (int q = 0; q < 3; ++q) pb[q] = bv[q];
+      __threadfence();
+      last_s = atomicAdd(count + k, 1u) == (unsigned)(nblk - 1);
+    }
+    __syncthreads();
+    if (!last_s) return;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      for (int q = 0; q < 6; ++q) {
+        double acc = 0.0;
+        for (int b2 = 0; b2 < nblk; ++b2)
+          acc += __ldcg(part + 6 * ((size_t)k * nblk + b2) + q);
+        v[q] = acc;
+      }
+      for (int q = 0; q < 3; ++q) {
+        long long m = kSentinel;
+        for (int b2 = 0; b2 < nblk; ++b2) {
+          const long long x = __ldcg(part_bad + 3 * ((size_t)k * nblk + b2) + q);
+          m = x < m ? x : m;
+        }
+        bv[q] = m;
+      }
+      count[k] = 0;  // ready for the next launch
+    }
+  }
   if (threadIdx.x == 0) {
     const int w = lin ? 6 : 5;
     double* o = out + w * (size_t)k;
-    o[0] = dec;
-    o[1] = dev;
-    o[2] = db;
-    o[3] = da;
-    o[4] = dd;
-    if (lin) o[5] = far;
+    o[0] = v[0];
+    o[1] = v[1];
+    o[2] = v[2];
+    o[3] = v[3];
+    o[4] = v[4];
+    if (lin) o[5] = v[5];
     int64_t* s = status + 3 * (size_t)k;
-    for (int q = 0; q < 3; ++q) s[q] = bad[q] == kSentinel ? -1 : (int64_t)bad[q];
+    for (int q = 0; q < 3; ++q) s[q] = bv[q] == kSentinel ? -1 : (int64_t)bv[q];
   }
 }
 
@@ -458,11 +502,13 @@ cudaError_t launch_atom_delta(const TermPlanDev& tp, const double* coords,
                               const int* fsp_ptr, const int* fsp_j, const double* fsp_s,
                               const int* aterm_ptr, const int* aterm_idx, int ncand,
                               const int* atoms, const double* newpos, double lin_cutoff,
-                              double* out, int64_t* status, cudaStream_t st) {
+                              double* out, int64_t* status, double* part,
+                              long long* part_bad, unsigned* count, cudaStream_t st) {
   if (ncand <= 0) return cudaSuccess;
-  count_launch(), launch_k(atom_delta_kernel, ncand, kDeltaThreads, 0, st, tp, coords, fsp_ptr, fsp_j, fsp_s,
-                                                     aterm_ptr, aterm_idx, atoms, newpos, lin_cutoff,
-                                                     out, status);
+  const int nblk = part ? delta_blocks(tp.n) : 1;
+  count_launch(), launch_k(atom_delta_kernel, ncand * nblk, kDeltaThreads, 0, st, tp, coords,
+                           fsp_ptr, fsp_j, fsp_s, aterm_ptr, aterm_idx, atoms, newpos, lin_cutoff,
+                           out, status, nblk, part, part_bad, count);
   return cudaGetLastError();
 }
 
