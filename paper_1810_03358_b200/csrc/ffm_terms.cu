@@ -307,9 +307,15 @@ __device__ __forceinline__ P3 pick(const double* c, int atom, P3 np, int i) {
 // One block per candidate left the FP64 pair arithmetic of a 10k-atom
 // system on 6 SMs (71 us per wiggle probe launch).  Nonbonded part restates
 // ffmin/kernels.py:419-454 (_loop_nb_atom_delta), bonded parts 457-593.
+#ifndef FFM_DELTA_PARTNERS
+#define FFM_DELTA_PARTNERS 512  // partners per block (tuning aid)
+#endif
+#ifndef FFM_DELTA_MAXBLK
+#define FFM_DELTA_MAXBLK 32
+#endif
 int delta_blocks(int n) {
-  const int b = (n + 511) / 512;  // ~2 partners per thread
-  return b < 1 ? 1 : (b > 32 ? 32 : b);
+  const int b = (n + FFM_DELTA_PARTNERS - 1) / FFM_DELTA_PARTNERS;
+  return b < 1 ? 1 : (b > FFM_DELTA_MAXBLK ? FFM_DELTA_MAXBLK : b);
 }
 
 __global__ void __launch_bounds__(kDeltaThreads)
