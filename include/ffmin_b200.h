@@ -164,7 +164,12 @@ int ffm_eval_batch(ffm_system_t* sys, int precision, int64_t batch, const double
  * (ffmin/energy.py:284-313, exact_delta_atom_move): atoms_d[k] moves to
  * newpos_d[k][3].  out_d[k][5] = (coulomb, vdw, stretch, bend, torsion)
  * deltas, status_d[k][3] = (first coincident partner j, first degenerate
- * angle row, first degenerate dihedral row), -1 when clean. */
+ * angle row, first degenerate dihedral row), -1 when clean.  Batches of
+ * fewer than 148 candidates split each candidate's partners over several
+ * blocks and add the partial sums in a fixed order (deterministic; sums of
+ * the same terms in another order than a larger batch's, so the two agree
+ * to rounding).  Not reentrant across streams for such batches (one
+ * scratch per system). */
 int ffm_atom_delta(ffm_system_t* sys, const double* coords_d, int64_t ncand,
                    const int32_t* atoms_d, const double* newpos_d, double* out_d,
                    int64_t* status_d, void* stream);
