@@ -41,7 +41,7 @@ def main():
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         print(f"rep {rep}: {dt * 1e3:.1f} ms total, {dt / iters * 1e3:.3f} ms/it, "
-              f"graph init {t_init[-1] * 1e3:.1f} ms, f={res.f:.6f}, "
+              f"graph init {(t_init[-1] if t_init else 0.0) * 1e3:.1f} ms, f={res.f:.6f}, "
               f"calls={res.trace.records[-1].value_calls}", flush=True)
     print("PDL", os.environ.get("FFM_PDL", "default"))
 
